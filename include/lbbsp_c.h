@@ -1,0 +1,329 @@
+/*
+ * lbbsp_c.h -- C-ABI boundary of the B200-native LB-BSP iteration hot path.
+ *
+ * The reference (arxiv 1806.02508, /root/reference/proj) has no FFI: its API is
+ * the C++ headers under core/include/lbbsp/. Every entry point below names the
+ * reference function it replaces (file:line, relative to /root/reference/proj).
+ * A reference-side caller binds these symbols with ctypes / a C++ shim
+ * (include/lbbsp_b200.hpp) -- see INTEGRATION.md.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. `d_` prefixes are DEVICE pointers, `h_`
+ *     prefixes HOST pointers. Streams are passed as `void*` (cudaStream_t).
+ *   - Every call returns an int status (LBBSP_OK == 0). The message of the
+ *     last failure on this thread is `lbbsp_last_error()`, worded like the
+ *     reference exception text (e.g. "gpu_allocate: budget 100 below total
+ *     saturation minimum 150", batch_sizer.cpp:37-42).
+ *   - Device-side precondition failures are written to a device status word
+ *     (lbbsp_dev_status) and surfaced by the host-pointer variants, which
+ *     synchronise; the device-pointer variants never synchronise.
+ *   - There is no CPU fallback: without a CUDA device every compute entry
+ *     point returns LBBSP_CUDA.
+ */
+#ifndef LBBSP_C_H
+#define LBBSP_C_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (map to the reference exception types) --- */
+#define LBBSP_OK 0
+#define LBBSP_INVALID_ARGUMENT (-1) /* std::invalid_argument */
+#define LBBSP_OUT_OF_RANGE (-2)     /* std::out_of_range     */
+#define LBBSP_RUNTIME (-3)          /* std::runtime_error    */
+#define LBBSP_LOGIC (-4)            /* std::logic_error      */
+#define LBBSP_CUDA (-5)
+#define LBBSP_NCCL (-6)
+
+const char* lbbsp_last_error(void);
+int lbbsp_version(void);
+/* number of CUDA devices visible to the library; 0 on a CPU-only host */
+int lbbsp_device_count(void);
+
+/* Device status word written by kernels when a precondition fails. */
+typedef struct {
+  int code;   /* 0 ok, else one of the status codes above            */
+  int what;   /* which check failed (LBBSP_E_* below)                */
+  int64_t a;  /* numeric payload for the message                     */
+  int64_t b;
+} lbbsp_dev_status;
+
+enum {
+  LBBSP_E_NONE = 0,
+  LBBSP_E_CPU_NO_WORKERS = 1,      /* "cpu_allocate: no workers"                  */
+  LBBSP_E_CPU_BUDGET = 2,          /* "cpu_allocate: budget a below worker count b"*/
+  LBBSP_E_CPU_SPEED = 3,           /* "cpu_allocate: speeds must be > 0"          */
+  LBBSP_E_CPU_MIN1 = 4,            /* "cpu_allocate: cannot enforce minimum batch"*/
+  LBBSP_E_GPU_NO_WORKERS = 10,
+  LBBSP_E_GPU_SLOPE = 11,
+  LBBSP_E_GPU_BASE = 12,
+  LBBSP_E_GPU_BOUNDS = 13,
+  LBBSP_E_GPU_COMM = 14,
+  LBBSP_E_GPU_BELOW = 15,          /* "budget a below total saturation minimum b" */
+  LBBSP_E_GPU_ABOVE = 16,          /* "budget a above total memory capacity b"    */
+  LBBSP_E_GPU_REPAIR = 17,
+  LBBSP_E_GPU_OOM = 18,            /* gpu_compute_time: batch above oom point     */
+  LBBSP_E_GRAD_EMPTY = 20,
+  LBBSP_E_GRAD_INDEX = 21,
+  LBBSP_E_AGG_BATCH = 22
+};
+
+/* ======================================================================== */
+/* Batch-size solver (K1/K2)                                                */
+/* ======================================================================== */
+
+/* GpuProfile, batch_sizer.hpp:10-15 */
+typedef struct {
+  double sec_per_sample;
+  double base_time_s;
+  int saturation_point;
+  int oom_point;
+} lbbsp_gpu_profile;
+
+/* clamp_speed_floor (batch_sizer.cpp:12-14) + cpu_allocate (batch_sizer.cpp:54-99)
+ * as ONE single-block kernel. speed_floor <= 0 disables the clamp (plain
+ * cpu_allocate). Device pointers, stream-ordered, no host sync. */
+int lbbsp_solve_prop(const double* d_speeds, int n, int budget, double speed_floor,
+                     int* d_sizes, lbbsp_dev_status* d_status, void* stream);
+
+/* gpu_allocate (batch_sizer.cpp:101-199), single-block kernel. */
+int lbbsp_solve_gpu(const lbbsp_gpu_profile* d_profiles, const double* d_comm, int n,
+                    int budget, int* d_sizes, lbbsp_dev_status* d_status, void* stream);
+
+/* Host-pointer variants (synchronous): same kernels, reference error text. */
+int lbbsp_cpu_allocate(const double* h_speeds, int n, int budget, int* h_sizes);
+int lbbsp_gpu_allocate(const lbbsp_gpu_profile* h_profiles, const double* h_comm, int n,
+                       int budget, int* h_sizes);
+
+/* ======================================================================== */
+/* Speed predictor (K3-K5)                                                  */
+/* ======================================================================== */
+
+enum { LBBSP_PRED_MEMORYLESS = 0, LBBSP_PRED_EMA = 1, LBBSP_PRED_NARX = 2, LBBSP_PRED_PERFECT = 3 };
+
+/* NarxModel (predictor.hpp:49-67) without the unbounded training_loss log. */
+typedef struct {
+  double input_weights[8];
+  double hidden_bias;
+  double output_weight;
+  double output_bias;
+  double speed_mean, speed_stddev;
+  double cpu_mean, cpu_stddev;
+  double mem_mean, mem_stddev;
+} lbbsp_narx_model;
+
+/* NarxTrainConfig (predictor.hpp:69-75) */
+typedef struct {
+  double step;
+  int max_epochs;
+  double early_stop_delta;
+  int early_stop_patience;
+  int min_history;
+} lbbsp_narx_train_cfg;
+
+/* NarxTrainReport (predictor.hpp:84-88) */
+typedef struct {
+  int ran;
+  int epochs;
+  double final_loss;
+} lbbsp_narx_report;
+
+/* narx_init (predictor.cpp:35-44), computed on the host (setup, not hot path). */
+int lbbsp_narx_init(uint64_t seed, lbbsp_narx_model* out);
+
+/* ema (predictor.cpp:18-25) over a host series, evaluated by the device kernel. */
+int lbbsp_ema(const double* h_series, int len, double alpha, double* h_out);
+
+/* narx_predict (predictor.cpp:147-153). windows most-recent-first. */
+int lbbsp_narx_predict(const lbbsp_narx_model* h_model, const double h_speeds[2],
+                       const double h_cpu[3], const double h_mem[3], double floor,
+                       double* h_out);
+
+/* narx_train_online (predictor.cpp:155-196) over one host history.
+ * h_loss_log (optional, may be NULL) receives one entry per accepted epoch
+ * (NarxModel::training_loss), capacity max_epochs. Bit-exact fp64 kernel. */
+int lbbsp_narx_train_online(lbbsp_narx_model* h_model, const double* h_speed,
+                            const double* h_cpu, const double* h_mem, int len,
+                            const lbbsp_narx_train_cfg* cfg, lbbsp_narx_report* h_report,
+                            double* h_loss_log);
+
+/* PredictorConfig (predictor.hpp:107-114) */
+typedef struct {
+  int kind;
+  double alpha;
+  int warmup_iterations;
+  double speed_floor;
+  lbbsp_narx_train_cfg train; /* train.min_history is forced to warmup (predictor.cpp:264) */
+} lbbsp_predictor_cfg;
+
+/* A bank of per-worker SpeedPredictors (predictor.hpp:118-136) whose
+ * histories (SpeedHistory, predictor.hpp:15-26) live in device memory. */
+typedef struct lbbsp_predictor lbbsp_predictor;
+
+/* seeds[i] is the per-worker predictor seed (cluster_sim.cpp:295 uses
+ * mix_seed(seed, 0x9ced1c70, i)); NULL initial models => narx_init(seeds[i]). */
+int lbbsp_predictor_create(const lbbsp_predictor_cfg* cfg, int n_workers, int max_history,
+                           const uint64_t* h_seeds, const lbbsp_narx_model* h_initial,
+                           lbbsp_predictor** out);
+int lbbsp_predictor_destroy(lbbsp_predictor* p);
+/* SpeedHistory::push for every worker (cluster_sim.cpp:309-313). */
+int lbbsp_predictor_observe(lbbsp_predictor* p, const double* d_v, const double* d_c,
+                            const double* d_m, void* stream);
+/* SpeedPredictor::predict for every worker (predictor.cpp:271-292), batched. */
+int lbbsp_predictor_predict(lbbsp_predictor* p, const double* d_c_now, const double* d_m_now,
+                            double* d_v_pred, void* stream);
+/* train_rotation (cluster_sim.cpp:315-324): trains ceil(n/2) models from the
+ * device-resident cursor, one CTA per model, and advances the cursor. */
+int lbbsp_predictor_train_rotation(lbbsp_predictor* p, void* stream);
+/* Train every model (predictor_series_rmse replays / C4 sweep). */
+int lbbsp_predictor_train_all(lbbsp_predictor* p, void* stream);
+int lbbsp_predictor_get_models(lbbsp_predictor* p, lbbsp_narx_model* h_models);
+int lbbsp_predictor_history_len(lbbsp_predictor* p, int* h_len);
+
+/* ======================================================================== */
+/* Workload: reference logistic-regression worker (K6-K10), fp64            */
+/* ======================================================================== */
+
+/* sample_stream (cluster_sim.cpp:302-307): B draws of
+ * mt19937_64(mix_seed(seed, 0x57e3a9, k)) mapped by Rng::uniform_int(0, N-1). */
+int lbbsp_sample_stream(uint64_t seed, int64_t iteration, int budget, int dataset_size,
+                        int* d_indices, void* stream);
+
+/* Dataset (sgd.hpp:15-21) resident on device, SoA features [N][d] + labels. */
+typedef struct lbbsp_lr_data lbbsp_lr_data;
+/* generate_dataset (sgd.cpp:39-57) */
+int lbbsp_lr_data_create(uint64_t seed, int n, int d, double noise, lbbsp_lr_data** out);
+/* Upload an explicit dataset (row-major features[n*d], labels[n]). */
+int lbbsp_lr_data_upload(const double* h_features, const double* h_labels, int n, int d,
+                         lbbsp_lr_data** out);
+int lbbsp_lr_data_destroy(lbbsp_lr_data* data);
+int lbbsp_lr_data_dim(const lbbsp_lr_data* data, int* n, int* d);
+
+/* batch_gradient (sgd.cpp:72-90) for n_seg contiguous segments of d_idx:
+ * segment i = d_idx[off_i : off_i + d_sizes[i]], off_i = prefix sum.
+ * d_grads receives n_seg x d per-worker MEAN gradients (Gradient::values). */
+int lbbsp_lr_worker_grads(const lbbsp_lr_data* data, const double* d_params,
+                          const int* d_idx, const int* d_sizes, int n_seg, double* d_grads,
+                          lbbsp_dev_status* d_status, void* stream);
+
+/* aggregate_weighted (coordination.cpp:52-68) when weighted != 0, else
+ * aggregate_naive (coordination.cpp:39-50), fused with apply_update
+ * (sgd.cpp:92-99): params -= lr * agg. d_agg (optional) receives the aggregate,
+ * d_norm (optional) its l2 norm (cluster_sim.cpp:203-207). */
+int lbbsp_aggregate_apply(const double* d_grads, const int* d_sizes, int n_seg, int dim,
+                          int weighted, double lr, double* d_params, double* d_agg,
+                          double* d_norm, lbbsp_dev_status* d_status, void* stream);
+
+/* loss (sgd.cpp:65-70) over the whole device dataset. */
+int lbbsp_lr_loss(const lbbsp_lr_data* data, const double* d_params, double* d_loss,
+                  void* stream);
+
+/* Host-pointer convenience variants for the reference-shaped API. */
+int lbbsp_batch_gradient(const lbbsp_lr_data* data, const double* h_params,
+                         const int* h_indices, int count, double* h_grad);
+int lbbsp_loss(const lbbsp_lr_data* data, const double* h_params, double* h_loss);
+/* aggregate over n host gradients of dimension dim with batch sizes */
+int lbbsp_aggregate(const double* h_grads, const int* h_sizes, int n, int dim, int weighted,
+                    double* h_out);
+
+/* ======================================================================== */
+/* Fused iteration driver (A1 step_sync, cluster_sim.cpp:349-469)           */
+/* ======================================================================== */
+
+enum { LBBSP_SCHEME_BSP = 0, LBBSP_SCHEME_ASP = 1, LBBSP_SCHEME_SSP = 2, LBBSP_SCHEME_LBBSP = 3 };
+enum {
+  LBBSP_DYN_STATIC = 0,
+  LBBSP_DYN_STRAGGLER = 1,
+  LBBSP_DYN_BENCHMARK = 2
+};
+enum {
+  LBBSP_PRESET_NONE = -1,
+  LBBSP_PRESET_HOMO = 0,
+  LBBSP_PRESET_HETERO_L2 = 1,
+  LBBSP_PRESET_HETERO_L3 = 2,
+  LBBSP_PRESET_HETERO_L2_STATIC = 3,
+  LBBSP_PRESET_HETERO_L3_STATIC = 4
+};
+
+/* StragglerSpec, cluster_sim.hpp:43-48 */
+typedef struct {
+  double on_probability;
+  double cpu_consumed;
+  double mem_consumed;
+  int period;
+} lbbsp_straggler;
+
+#define LBBSP_MAX_WORKERS 1024
+
+/* SimConfig (cluster_sim.hpp:165-180) flattened, plus the worker/dynamics
+ * description that SimConfig carries in WorkerProfile/DynamicsConfig. */
+typedef struct {
+  int scheme;             /* LBBSP_SCHEME_BSP | LBBSP_SCHEME_LBBSP                  */
+  int n_workers;
+  int total_budget;
+  int preset;             /* LBBSP_PRESET_*, NONE => use dynamics below         */
+  double base_speed;      /* WorkerProfile::base_speed (CPU kind)                 */
+  int dynamics;           /* LBBSP_DYN_* when preset == NONE                     */
+  const double* static_cpu;              /* [n] or NULL (1.0)                    */
+  const double* static_mem;              /* [n] or NULL (1.0)                    */
+  const lbbsp_straggler* stragglers;     /* [n] for LBBSP_DYN_STRAGGLER          */
+  /* BenchmarkTraceConfig, cluster_sim.hpp:76-83 */
+  int bench_iterations, bench_regime_length;
+  double bench_high_lo, bench_high_hi, bench_low_lo, bench_low_hi;
+  double bench_spike_mult, bench_spike_prob;
+  /* predictor */
+  lbbsp_predictor_cfg predictor;
+  /* GPU-kind cluster (gpu_mode): profiles[n] != NULL switches every worker to Gpu */
+  const lbbsp_gpu_profile* gpu_profiles;
+  /* CommModel per worker: tm = base_comm_s * factor(k) */
+  double base_comm_s;
+  int bw_worker;          /* -1: none; else BandwidthEvent on that worker         */
+  int64_t bw_at_iteration;
+  double bw_factor;
+  /* SimConfig scalars */
+  double learning_rate;
+  uint64_t dataset_seed;
+  int dataset_size;
+  int dataset_dim;
+  double dataset_noise;
+  double convergence_loss;
+  int convergence_consecutive;
+  int64_t max_updates;
+  uint64_t seed;
+} lbbsp_sim_cfg;
+
+/* IterationRecord (cluster_sim.hpp:149-155) + WorkerIterationStats (:139-147),
+ * flattened: per-iteration scalars and [n] per-worker arrays. */
+typedef struct {
+  int64_t k;
+  double grad_norm;
+  double loss;
+  double wall_s;
+} lbbsp_iter_scalars;
+
+typedef struct lbbsp_sim lbbsp_sim;
+
+int lbbsp_sim_create(const lbbsp_sim_cfg* cfg, lbbsp_sim** out);
+int lbbsp_sim_destroy(lbbsp_sim* sim);
+/* Run up to `iterations` LB-BSP/BSP barrier rounds with no host round trip
+ * (the convergence stop of check_stop, cluster_sim.cpp:326-334, is evaluated
+ * on device and turns the remaining rounds into no-ops). */
+int lbbsp_sim_run(lbbsp_sim* sim, int iterations, void* stream);
+/* Copy out the records produced so far (blocking). Arrays are [rows] and
+ * [rows*n]; params is [rows*d] (the record_params trajectory). Any pointer
+ * may be NULL. Returns the row count in *rows. */
+int lbbsp_sim_records(lbbsp_sim* sim, int max_rows, int* rows, lbbsp_iter_scalars* scalars,
+                      int* batch, double* tp, double* tm, double* wait, double* v_pred,
+                      double* v_actual, double* params);
+int lbbsp_sim_status(lbbsp_sim* sim, int* done, int* converged);
+/* Number of CUDA kernels one iteration launches (captured graph nodes). */
+int lbbsp_sim_launches_per_iteration(lbbsp_sim* sim, int* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LBBSP_C_H */

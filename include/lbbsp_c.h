@@ -51,6 +51,10 @@ typedef struct {
   int64_t b;
 } lbbsp_dev_status;
 
+/* Formats a device status word copied back to the host into
+ * lbbsp_last_error() (reference wording) and returns its code. */
+int lbbsp_check_status(const lbbsp_dev_status* h_status);
+
 enum {
   LBBSP_E_NONE = 0,
   LBBSP_E_CPU_NO_WORKERS = 1,      /* "cpu_allocate: no workers"                  */

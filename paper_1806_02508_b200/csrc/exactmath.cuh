@@ -1,0 +1,175 @@
+// exactmath.cuh -- device arithmetic that reproduces the reference's fp64
+// results bit-for-bit.
+//
+// The reference core is built for baseline x86-64 (SSE2, no FMA),
+// so every product and sum is individually rounded. nvcc would otherwise
+// contract a*b+c into DFMA; the _rn intrinsics below are never contracted.
+// The one place the reference DOES see fused ops is glibc's tanh -> expm1
+// IFUNC, which selects __expm1_fma on FMA hosts; glibc_tanh() restates that
+// exact dataflow (validated against host libm by the oracle restatement
+// orc_tanh_glibc_fma and on device by tests/test_gpu_predictor.py).
+#pragma once
+#include <cstdint>
+
+namespace lbbsp {
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+__device__ __forceinline__ uint32_t hi_word(double x) {
+  return static_cast<uint32_t>(__double2hiint(x));
+}
+__device__ __forceinline__ uint32_t lo_word(double x) {
+  return static_cast<uint32_t>(__double2loint(x));
+}
+__device__ __forceinline__ double with_hi(double x, uint32_t hi) {
+  return __hiloint2double(static_cast<int>(hi), __double2loint(x));
+}
+
+// glibc 2.39 __expm1_fma (fdlibm s_expm1.c compiled with -mfma); constants
+// read from libm's .rodata (see oracle/lbbsp_oracle.c orc_expm1_glibc_fma).
+__device__ __forceinline__ double glibc_expm1(double x) {
+  const double o_threshold = 0x1.62e42fefa39efp+9, ln2_hi = 0x1.62e42fee00000p-1,
+               ln2_lo = 0x1.a39ef35793c76p-33, invln2 = 0x1.71547652b82fep+0;
+  const double Q1 = -0x1.11111111110f4p-5, Q2 = 0x1.a01a019fe5585p-10,
+               Q3 = -0x1.4ce199eaadbb7p-14, Q4 = 0x1.0cfca86e65239p-18,
+               Q5 = -0x1.afdb76e09c32dp-23;
+  uint32_t hx = hi_word(x);
+  const uint32_t xsb = hx & 0x80000000u;
+  hx &= 0x7fffffffu;
+  double hi, lo, c = 0.0, t;
+  int k;
+  if (hx >= 0x4043687Au) {
+    if (hx >= 0x40862E42u) {
+      if (hx >= 0x7ff00000u) {
+        if (((hx & 0xfffffu) | lo_word(x)) != 0) return dadd(x, x);
+        return xsb == 0 ? x : -1.0;
+      }
+      if (x > o_threshold) return __int_as_float(0x7f800000);  // +inf
+    }
+    if (xsb != 0) return -1.0;  // tiny - one rounds to -1
+  }
+  if (hx > 0x3fd62e42u) {
+    if (hx < 0x3FF0A2B2u) {
+      if (xsb == 0) {
+        hi = dsub(x, ln2_hi);
+        lo = ln2_lo;
+        k = 1;
+      } else {
+        hi = dadd(x, ln2_hi);
+        lo = -ln2_lo;
+        k = -1;
+      }
+    } else {
+      k = static_cast<int>(dadd(dmul(invln2, x), xsb == 0 ? 0.5 : -0.5));
+      t = static_cast<double>(k);
+      hi = dfma(-t, ln2_hi, x);
+      lo = dmul(t, ln2_lo);
+    }
+    x = dsub(hi, lo);
+    c = dsub(dsub(hi, x), lo);
+  } else if (hx < 0x3c900000u) {
+    return x;  // |x| < 2^-54 (inexact flag only)
+  } else {
+    k = 0;
+  }
+  const double hfx = dmul(x, 0.5);
+  const double hxs = dmul(x, hfx);
+  const double R1 = dfma(hxs, Q1, 1.0);
+  const double R2 = dfma(hxs, Q3, Q2);
+  const double R3 = dfma(hxs, Q5, Q4);
+  const double h2 = dmul(hxs, hxs);
+  const double h4 = dmul(h2, h2);
+  const double r1 = dfma(h4, R3, dfma(h2, R2, R1));
+  t = dfma(-r1, hfx, 3.0);
+  double e = dmul(ddiv(dsub(r1, t), dfma(-x, t, 6.0)), hxs);
+  if (k == 0) return dsub(x, dfma(e, x, -hxs));
+  e = dfma(dsub(e, c), x, -c);
+  e = dsub(e, hxs);
+  if (k == -1) return dfma(0.5, dsub(x, e), -0.5);
+  if (k == 1) {
+    if (x < -0.25) return dmul(dsub(e, dadd(x, 0.5)), -2.0);
+    return dfma(dsub(x, e), 2.0, 1.0);
+  }
+  double y;
+  if (k <= -2 || k > 56) {
+    y = dsub(1.0, dsub(e, x));
+    y = with_hi(y, hi_word(y) + (static_cast<uint32_t>(k) << 20));
+    return dsub(y, 1.0);
+  }
+  if (k < 20) {
+    t = __hiloint2double(static_cast<int>(0x3ff00000u - (0x200000u >> k)), 0);
+    y = dsub(t, dsub(e, x));
+  } else {
+    t = __hiloint2double(static_cast<int>(static_cast<uint32_t>(0x3ff - k) << 20), 0);
+    y = dadd(dsub(x, dadd(e, t)), 1.0);
+  }
+  return with_hi(y, hi_word(y) + (static_cast<uint32_t>(k) << 20));
+}
+
+// glibc 2.39 tanh (sysdeps/ieee754/dbl-64/s_tanh.c; no FMA in tanh itself).
+__device__ __forceinline__ double glibc_tanh(double x) {
+  const uint32_t jx = hi_word(x), ix = jx & 0x7fffffffu;
+  if (ix >= 0x7ff00000u) {
+    if (jx & 0x80000000u) return dsub(ddiv(1.0, x), 1.0);
+    return dadd(ddiv(1.0, x), 1.0);
+  }
+  double z;
+  if (ix < 0x40360000u) {
+    if ((ix | lo_word(x)) == 0) return x;
+    if (ix < 0x3c800000u) return dmul(x, dadd(1.0, x));
+    const double ax = fabs(x);
+    if (ix >= 0x3ff00000u) {
+      const double t = glibc_expm1(dadd(ax, ax));
+      z = dsub(1.0, ddiv(2.0, dadd(t, 2.0)));
+    } else {
+      const double t = glibc_expm1(dmul(-2.0, ax));
+      z = ddiv(-t, dadd(t, 2.0));
+    }
+  } else {
+    z = 1.0;  // one - tiny
+  }
+  return (jx & 0x80000000u) ? -z : z;
+}
+
+// ---- rng.hpp:9-42 ----------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t a, uint64_t b) {
+  return mix64(a ^ mix64(b));
+}
+__host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t a, uint64_t b, uint64_t c) {
+  return mix_seed(mix_seed(a, b), c);
+}
+
+__device__ __forceinline__ uint64_t mt64_temper(uint64_t x) {
+  x ^= (x >> 29) & 0x5555555555555555ull;
+  x ^= (x << 17) & 0x71D67FFFEDA60000ull;
+  x ^= (x << 37) & 0xFFF7EEE000000000ull;
+  x ^= (x >> 43);
+  return x;
+}
+
+__device__ __forceinline__ uint64_t mt64_twist_one(uint64_t cur, uint64_t next, uint64_t far) {
+  const uint64_t x = (cur & 0xFFFFFFFF80000000ull) | (next & 0x7FFFFFFFull);
+  return far ^ (x >> 1) ^ ((x & 1ull) ? 0xB5026F5AA96619E9ull : 0ull);
+}
+
+// Rng::uniform() then uniform_int(lo, lo+range-1) (rng.hpp:31,36-38)
+__device__ __forceinline__ int uniform_int_from(uint64_t u, int lo, int range) {
+  const double f = dmul(static_cast<double>(u >> 11), 0x1.0p-53);
+  return lo + static_cast<int>(dmul(f, static_cast<double>(range)));
+}
+
+__device__ __forceinline__ double uniform_from(uint64_t u) {
+  return dmul(static_cast<double>(u >> 11), 0x1.0p-53);
+}
+
+}  // namespace lbbsp

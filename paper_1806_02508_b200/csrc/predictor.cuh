@@ -1,0 +1,251 @@
+// predictor.cuh -- K3/K4/K5: the speed predictor on device.
+//
+//   ema state update            : ema / predict_ema / predict_comm_ema
+//                                 (predictor.cpp:18-33), incremental but with
+//                                 the same operation sequence as the refold
+//   narx_predict_d              : standardize + forward + denorm + floor
+//                                 (predictor.cpp:52-69, 147-153)
+//   predictor_predict_d         : SpeedPredictor::predict (predictor.cpp:271-292)
+//   narx_train_block            : narx_train_online (predictor.cpp:155-196),
+//                                 one CTA per model, fp64, bit-exact
+#pragma once
+#include "common.cuh"
+#include "exactmath.cuh"
+
+namespace lbbsp {
+
+__device__ __forceinline__ double narx_forward_d(const double* w /*11*/, const double* z) {
+  double a = w[8];  // hidden_bias
+  for (int j = 0; j < 8; ++j) a = dadd(a, dmul(w[j], z[j]));
+  const double h = glibc_tanh(a);
+  return dadd(dmul(w[9], h), w[10]);
+}
+
+__device__ __forceinline__ void model_weights(const lbbsp_narx_model& m, double* w) {
+  for (int j = 0; j < 8; ++j) w[j] = m.input_weights[j];
+  w[8] = m.hidden_bias;
+  w[9] = m.output_weight;
+  w[10] = m.output_bias;
+}
+
+// narx_predict, predictor.cpp:147-153
+__device__ inline double narx_predict_d(const lbbsp_narx_model& m, double v0, double v1, double c0,
+                                 double c1, double c2, double m0, double m1, double m2,
+                                 double floor_) {
+  double z[8], w[11];
+  z[0] = ddiv(dsub(v0, m.speed_mean), m.speed_stddev);
+  z[1] = ddiv(dsub(v1, m.speed_mean), m.speed_stddev);
+  z[2] = ddiv(dsub(c0, m.cpu_mean), m.cpu_stddev);
+  z[3] = ddiv(dsub(c1, m.cpu_mean), m.cpu_stddev);
+  z[4] = ddiv(dsub(c2, m.cpu_mean), m.cpu_stddev);
+  z[5] = ddiv(dsub(m0, m.mem_mean), m.mem_stddev);
+  z[6] = ddiv(dsub(m1, m.mem_mean), m.mem_stddev);
+  z[7] = ddiv(dsub(m2, m.mem_mean), m.mem_stddev);
+  model_weights(m, w);
+  const double v = dadd(m.speed_mean, dmul(m.speed_stddev, narx_forward_d(w, z)));
+  return v > floor_ ? v : floor_;
+}
+
+// SpeedPredictor::predict (predictor.cpp:271-292) for worker w; requires len >= 1.
+__device__ inline double predictor_predict_d(const PredDev& P, int w, int len, double c_now,
+                                      double m_now) {
+  const double* v = P.hv + static_cast<size_t>(w) * P.max_hist;
+  switch (P.kind) {
+    case LBBSP_PRED_MEMORYLESS:
+      return v[len - 1];
+    case LBBSP_PRED_NARX:
+      if (len >= P.warmup && len >= 2) {
+        const double* c = P.hc + static_cast<size_t>(w) * P.max_hist;
+        const double* m = P.hm + static_cast<size_t>(w) * P.max_hist;
+        return narx_predict_d(P.models[w], v[len - 1], v[len - 2], c_now, c[len - 1], c[len - 2],
+                              m_now, m[len - 1], m[len - 2], P.floor);
+      }
+      return P.ema[w];
+    default:  // Ema, Perfect
+      return P.ema[w];
+  }
+}
+
+// SpeedHistory::push + comm_obs push (cluster_sim.cpp:309-313) with the
+// incremental EMA states. `len` is the length BEFORE the push.
+__device__ inline void observe_d(const PredDev& P, int w, int len, double v, double c, double m,
+                          double tm) {
+  const size_t o = static_cast<size_t>(w) * P.max_hist + len;
+  if (len < P.max_hist) {
+    P.hv[o] = v;
+    P.hc[o] = c;
+    P.hm[o] = m;
+  }
+  const double a = P.alpha, oma = dsub(1.0, P.alpha);
+  // ema_0 = x_0, ema_k = alpha*x_k + (1-alpha)*ema_{k-1}  (predictor.cpp:22-23)
+  P.ema[w] = len == 0 ? v : dadd(dmul(a, v), dmul(oma, P.ema[w]));
+  // lagged comm EMA covers comm_obs[0..len-1] after this push
+  if (len == 1)
+    P.comm_ema_lag[w] = P.comm_last[w];
+  else if (len > 1)
+    P.comm_ema_lag[w] = dadd(dmul(a, P.comm_last[w]), dmul(oma, P.comm_ema_lag[w]));
+  P.comm_last[w] = tm;
+}
+
+// Bytes of per-sample scratch a training call needs (13 doubles per sample).
+__host__ __device__ __forceinline__ size_t narx_train_scratch_bytes(int len) {
+  const int cnt = len > 2 ? len - 2 : 1;
+  return static_cast<size_t>(cnt) * 13 * sizeof(double);
+}
+
+struct NarxTrainSmem {
+  double w[11], g[11], trial[11], sc[6];
+  double val;
+  double current;
+  int stall, epochs, stop;
+};
+
+// E[i] = (forward(wt, z_i) - t_i)^2 in parallel, then the reference's
+// left-to-right sum (predictor.cpp:104-107) by thread 0.
+__device__ inline double block_mse(const double* wt, const double* Z, const double* T, double* E,
+                            int cnt, NarxTrainSmem* s) {
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    double z[8];
+    for (int j = 0; j < 8; ++j) z[j] = Z[static_cast<size_t>(j) * cnt + i];
+    const double e = dsub(narx_forward_d(wt, z), T[i]);
+    E[i] = dmul(e, e);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double total = 0.0;
+    for (int i = 0; i < cnt; ++i) total = dadd(total, E[i]);
+    s->val = ddiv(total, static_cast<double>(cnt));
+  }
+  __syncthreads();
+  return s->val;
+}
+
+// narx_train_online (predictor.cpp:155-196) for one model with history
+// (v, c, m)[0..L). buf: 13*(L-2) doubles (shared or global).
+__device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, const double* c,
+                                 const double* m, int L, const lbbsp_narx_train_cfg cfg,
+                                 lbbsp_narx_report* rep, double* loss_log, int loss_cap,
+                                 double* buf, NarxTrainSmem* s) {
+  const int tid = threadIdx.x;
+  const int minh = cfg.min_history > 3 ? cfg.min_history : 3;
+  if (L < minh) {
+    if (tid == 0 && rep) *rep = lbbsp_narx_report{0, 0, 0.0};
+    return;
+  }
+  // fit_scaler x3 (predictor.cpp:71-82), one sequential thread per series
+  if (tid == 0 || tid == 32 || tid == 64) {
+    const int which = tid / 32;
+    const double* xs = which == 0 ? v : (which == 1 ? c : m);
+    double sum = 0.0;
+    for (int i = 0; i < L; ++i) sum = dadd(sum, xs[i]);
+    const double mean = ddiv(sum, static_cast<double>(L));
+    double var = 0.0;
+    for (int i = 0; i < L; ++i) {
+      const double d = dsub(xs[i], mean);
+      var = dadd(var, dmul(d, d));
+    }
+    var = ddiv(var, static_cast<double>(L));
+    s->sc[2 * which] = mean;
+    s->sc[2 * which + 1] = var > 1e-18 ? __dsqrt_rn(var) : 1.0;
+  }
+  if (tid == 96) {
+    model_weights(*gm, s->w);
+    s->stall = 0;
+    s->epochs = 0;
+    s->stop = 0;
+  }
+  __syncthreads();
+  const int cnt = L - 2;
+  double* Z = buf;                              // [8][cnt]
+  double* T = Z + static_cast<size_t>(8) * cnt;  // [cnt]
+  double* H = T + cnt;
+  double* DY = H + cnt;
+  double* DZ = DY + cnt;
+  double* E = DZ + cnt;
+  const double mv = s->sc[0], sv = s->sc[1], mc = s->sc[2], scd = s->sc[3], mm = s->sc[4],
+               sm = s->sc[5];
+  // build_training_set (predictor.cpp:89-100)
+  for (int i = tid; i < cnt; i += blockDim.x) {
+    const int t = i + 2;
+    Z[0 * cnt + i] = ddiv(dsub(v[t - 1], mv), sv);
+    Z[1 * cnt + i] = ddiv(dsub(v[t - 2], mv), sv);
+    Z[2 * cnt + i] = ddiv(dsub(c[t], mc), scd);
+    Z[3 * cnt + i] = ddiv(dsub(c[t - 1], mc), scd);
+    Z[4 * cnt + i] = ddiv(dsub(c[t - 2], mc), scd);
+    Z[5 * cnt + i] = ddiv(dsub(m[t], mm), sm);
+    Z[6 * cnt + i] = ddiv(dsub(m[t - 1], mm), sm);
+    Z[7 * cnt + i] = ddiv(dsub(m[t - 2], mm), sm);
+    T[i] = ddiv(dsub(v[t], mv), sv);
+  }
+  __syncthreads();
+  double current = block_mse(s->w, Z, T, E, cnt, s);
+  const double scale = ddiv(2.0, static_cast<double>(cnt));
+  for (int epoch = 0; epoch < cfg.max_epochs; ++epoch) {
+    // loss_gradient (predictor.cpp:118-134): per-sample terms in parallel ...
+    for (int i = tid; i < cnt; i += blockDim.x) {
+      double a = s->w[8];
+      for (int j = 0; j < 8; ++j) a = dadd(a, dmul(s->w[j], Z[static_cast<size_t>(j) * cnt + i]));
+      const double h = glibc_tanh(a);
+      const double y = dadd(dmul(s->w[9], h), s->w[10]);
+      const double dy = dmul(scale, dsub(y, T[i]));
+      H[i] = h;
+      DY[i] = dy;
+      DZ[i] = dmul(dmul(dy, s->w[9]), dsub(1.0, dmul(h, h)));
+    }
+    __syncthreads();
+    // ... and each of the 11 accumulators summed left to right by its own thread
+    if (tid < 11) {
+      double acc = 0.0;
+      if (tid < 8) {
+        const double* zj = Z + static_cast<size_t>(tid) * cnt;
+        for (int i = 0; i < cnt; ++i) acc = dadd(acc, dmul(DZ[i], zj[i]));
+      } else if (tid == 8) {
+        for (int i = 0; i < cnt; ++i) acc = dadd(acc, DZ[i]);
+      } else if (tid == 9) {
+        for (int i = 0; i < cnt; ++i) acc = dadd(acc, dmul(DY[i], H[i]));
+      } else {
+        for (int i = 0; i < cnt; ++i) acc = dadd(acc, DY[i]);
+      }
+      s->g[tid] = acc;
+    }
+    __syncthreads();
+    double step = cfg.step;
+    if (tid < 11) s->trial[tid] = dsub(s->w[tid], dmul(step, s->g[tid]));  // apply_step :136-143
+    __syncthreads();
+    double next = block_mse(s->trial, Z, T, E, cnt, s);
+    int halvings = 0;
+    while (next > current && halvings < 20) {
+      step = dmul(step, 0.5);
+      if (tid < 11) s->trial[tid] = dsub(s->w[tid], dmul(step, s->g[tid]));
+      __syncthreads();
+      next = block_mse(s->trial, Z, T, E, cnt, s);
+      ++halvings;
+    }
+    if (next > current) break;  // no descent direction left (:182)
+    if (tid < 11) s->w[tid] = s->trial[tid];
+    if (tid == 0) {
+      if (loss_log && s->epochs < loss_cap) loss_log[s->epochs] = next;
+      s->epochs += 1;
+      s->stall = dsub(current, next) < cfg.early_stop_delta ? s->stall + 1 : 0;
+    }
+    __syncthreads();
+    current = next;
+    if (s->stall >= cfg.early_stop_patience) break;
+  }
+  if (tid == 0) {
+    if (rep) *rep = lbbsp_narx_report{1, s->epochs, current};
+    for (int j = 0; j < 8; ++j) gm->input_weights[j] = s->w[j];
+    gm->hidden_bias = s->w[8];
+    gm->output_weight = s->w[9];
+    gm->output_bias = s->w[10];
+    gm->speed_mean = mv;
+    gm->speed_stddev = sv;
+    gm->cpu_mean = mc;
+    gm->cpu_stddev = scd;
+    gm->mem_mean = mm;
+    gm->mem_stddev = sm;
+  }
+  __syncthreads();
+}
+
+}  // namespace lbbsp

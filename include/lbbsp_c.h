@@ -326,6 +326,27 @@ int lbbsp_sim_status(lbbsp_sim* sim, int* done, int* converged);
 /* Number of CUDA kernels one iteration launches (captured graph nodes). */
 int lbbsp_sim_launches_per_iteration(lbbsp_sim* sim, int* launches);
 
+/* ======================================================================== */
+/* Gradient engine building block: tcgen05/TMA bf16 GEMM (K7, north_star 1) */
+/* ======================================================================== */
+
+/* C[M,N] = epilogue(A * B^T) with bf16 operands, fp32 accumulation in TMEM.
+ *   A: a_mn ? [K][M] : [M][K];  B: b_mn ? [K][N] : [N][K] (dense bf16 rows)
+ *   epilogue: 0 C_f32 = acc; 1 C_bf16 = relu(acc + bias); 2 C_bf16 = acc + bias;
+ *             3 C_bf16 = acc * (aux > 0)  (aux = bf16 [M][N])
+ *   mode 0 (rows): worker g owns rows [r0_g, r1_g) of M (ragged, masked);
+ *   mode 1 (k-split): worker g owns K range [r0_g, r1_g) and writes its fp32
+ *   partial to C + g*M*N (the segmented reduction sums them).
+ *   Worker g runs on CTAs [cta0_g, cta0_g + ctan_g) -- its SM cap.
+ *   d_timing (optional) [n_groups][2] u64 {min start, max end} globaltimer ns.
+ * Replaces the per-worker batch_gradient loop (sgd.cpp:72-90,
+ * cluster_sim.cpp:422-431) for the dense-layer workloads. */
+int lbbsp_gemm_bf16(const void* d_a, const void* d_b, void* d_c, int M, int N, int K, int a_mn,
+                    int b_mn, int epilogue, const float* d_bias, const void* d_aux, int mode,
+                    int n_groups, const int* d_group_r0, const int* d_group_r1,
+                    const int* d_group_cta0, const int* d_group_ctan, int ctas,
+                    unsigned long long* d_timing, int bn, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

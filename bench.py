@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""LB-BSP iteration benchmark (driver contract).
+
+Workload (BASELINE.json configs[1], "C2"): MLP 784-256-10 (bf16 GEMM operands,
+fp32 master weights), 8 emulated workers per B200 each confined to a CTA
+partition (its SM cap) driven by a recorded, iteration-indexed straggler trace
+(the reference's make_benchmark_series, seed 3), global batch 4096 per GPU,
+LB-BSP with the NARX predictor (warm-up 50), full-dataset loss every round.
+A step = one LB-BSP round (plan, sample, forward/backward of every worker,
+Eq.-7 aggregation, update, loss, observe, NARX training) -- all on device.
+N>1: one process per GPU, weak scaling (8 workers and 4096 samples per GPU),
+gradients summed with ncclAllReduce, measured speeds with ncclAllGather.
+
+The same line reports the BSP and no-straggler-ideal rounds on the same trace.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "LB-BSP samples/sec & iter time vs BSP at 1/2/4/8 B200 (injected stragglers)"
+DIMS = [784, 256, 10]
+WORKERS_PER_GPU = 8
+BATCH_PER_GPU = 4096
+WARMUP_NARX = 50
+TRACE_SEED = 3
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=60)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU arms (oracle port: MLP restatement + reference predictor/solver)
+# ---------------------------------------------------------------------------
+def cpu_measure(n_workers, batch, max_rounds, budget_s):
+    """Times the CPU path of the C2 round on host cores. The reference has no
+    MLP: the round is the fp64 restatement (oracle/mlp_oracle.py)
+    and the batch sizes come from the reference's own predictor + solver
+    (oracle/_ref replay driver over the trace speeds, timed per round).
+    Returns (seconds per round, rounds timed, threads)."""
+    import numpy as np
+
+    from oracle import mlp_oracle as MO
+    from oracle import oracle as O
+    from paper_1806_02508_b200 import abi
+
+    chk = O.reference() if O.reference_available() else O.restatement()
+    orc = O.restatement()
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, (1000, DIMS[0])).astype(np.float32)
+    y = rng.integers(0, DIMS[-1], 1000)
+    params = [(rng.uniform(-0.03, 0.03, (DIMS[l + 1], DIMS[l])), np.zeros(DIMS[l + 1]))
+              for l in range(len(DIMS) - 1)]
+    R = WARMUP_NARX + max_rounds
+    # the reference's make_benchmark_series per worker (Dynamics 'benchmark')
+    trace = [np.zeros((n_workers, R)) for _ in range(3)]
+    for i in range(n_workers):
+        c, m, x3 = chk.benchmark_series(chk.mix_seed(TRACE_SEED, 0xbe7c, i), R)
+        trace[0][i], trace[1][i], trace[2][i] = c, m, x3
+    pcfg = abi.PredictorConfig.default(abi.PRED_NARX, warmup_iterations=WARMUP_NARX)
+    seeds = [chk.mix_seed(1, 0x9ced1c70, i) for i in range(n_workers)]
+    v = 10.0 * trace[0].T * trace[2].T  # effective_speed(base 10) * speed_mult
+    t0 = time.perf_counter()
+    sizes, _ = chk.replay_cpu(pcfg, seeds, batch, v, trace[0].T, trace[1].T)
+    t_plan = (time.perf_counter() - t0) / R
+    t0 = time.perf_counter()
+    done = 0
+    for k in range(WARMUP_NARX, R):
+        stream = orc.sample_stream(1, k, batch, 1000)
+        params, _ = MO.lbbsp_round(params, x, y, stream, sizes[k].tolist(), 0.05)
+        MO.full_loss(params, x, y)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    t_round = (time.perf_counter() - t0) / done + t_plan
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count() or 1
+    return t_round, done, threads
+
+
+def cpu_baseline(budget_s=12.0):
+    t_round, done, threads = cpu_measure(WORKERS_PER_GPU, BATCH_PER_GPU, 200, budget_s)
+    return {"value": BATCH_PER_GPU / t_round, "unit": "samples/s", "cores": threads,
+            "kind": "port",
+            "sample": f"{done} rounds of the C2 workload (8 workers, B=4096, MLP 784-256-10) in "
+                      f"fp64 numpy (oracle/mlp_oracle.py) + the reference predictor/solver "
+                      f"(oracle/_ref replay, {WARMUP_NARX + 200} rounds amortised)"}
+
+
+def reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    t_round, done, threads = cpu_measure(WORKERS_PER_GPU, BATCH_PER_GPU,
+                                         max(args.steps, 20), 30.0)
+    value = BATCH_PER_GPU / t_round
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": done, "warmup": WARMUP_NARX, "ms_per_step": t_round * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": "C2: MLP 784-256-10, 8 workers, global batch 4096, "
+                                   "benchmark-series straggler trace, LB-BSP + NARX",
+                       "parallelism": "cpu"},
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
+                             "sample": f"{done} rounds of the C2 round on host cores: fp64 numpy "
+                                       f"restatement + reference predictor/solver (oracle/_ref)"},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+class Clocks:
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.path = os.path.join("/tmp", f"lbbsp_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+            self.f.close()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4)
+                          if len(r) > 3 + j and r[3 + j].strip().lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1806_02508_b200.mlp import MlpEngine, benchmark_trace, constant_trace
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+    n_total = WORKERS_PER_GPU * world
+    B = BATCH_PER_GPU * world
+    e2e_steps = min(args.steps, 50)
+    iters = args.warmup + args.steps + e2e_steps + 8
+    trace = benchmark_trace(n_total, iters, seed=TRACE_SEED)
+
+    def make(scheme, tr):
+        eng = MlpEngine(dims=DIMS, global_batch=B, n_workers_local=WORKERS_PER_GPU, world=world,
+                        rank=rank, scheme=scheme, predictor="narx",
+                        warmup_iterations=WARMUP_NARX, learning_rate=0.05, seed=1,
+                        max_iterations=iters + 4, trace=tr)
+        if world > 1:
+            uid = [MlpEngine.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            eng.init_comm(uid[0])
+        return eng
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2 (126 MB)
+
+    def timed(eng, steps, warmup, phases=False):
+        st = torch.cuda.ExternalStream(eng.stream)
+        eng.run(warmup)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        total = 0.0
+        ph = None
+        for _ in range(steps):
+            with torch.cuda.stream(st):
+                flush.zero_()  # L2 flush between steps, outside the timed events
+                s = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                s.record(st)
+            eng.run(1)
+            with torch.cuda.stream(st):
+                e.record(st)
+            e.synchronize()
+            total += s.elapsed_time(e)
+            if phases:
+                p = eng.phase_times()
+                ph = p if ph is None else ph + p
+        torch.cuda.synchronize()
+        if world > 1:
+            t = torch.tensor([total], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total = float(t.item())
+            dist.barrier()
+        return total / steps, (ph / steps if ph is not None else None)
+
+    # ---- main arm: LB-BSP under the recorded trace ----
+    eng = make("lb-bsp", trace)
+    with Clocks(local) as clk:
+        ms_lb, phases = timed(eng, args.steps, args.warmup, phases=True)
+    rec = eng.records()
+    launches = eng.launches_per_iteration()
+    gemm_flops, _ = eng.work()
+
+    # ---- e2e through the C-ABI with host buffers (pinned), per-step H2D/D2H ----
+    x_host, y_host = eng.dataset()
+    xb = torch.from_numpy(x_host).to(torch.bfloat16).pin_memory()
+    yb = torch.from_numpy(y_host.astype(np.int32)).pin_memory()
+    out_sizes = torch.zeros(n_total, dtype=torch.int32).pin_memory()
+    out_loss = torch.zeros(1, dtype=torch.float64).pin_memory()
+    st = torch.cuda.ExternalStream(eng.stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record(st)
+    for _ in range(e2e_steps):
+        eng.load_data_async(xb.data_ptr(), yb.data_ptr())
+        eng.run(1)
+        eng.read_result_async(out_sizes.data_ptr(), out_loss.data_ptr())
+    e.record(st)
+    e.synchronize()
+    e2e_ms = s.elapsed_time(e) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = xb.numel() * 2 + yb.numel() * 4
+    d2h = n_total * 4 + 8
+    del eng
+
+    # ---- BSP and no-straggler ideal on the same trace / config ----
+    eng_b = make("bsp", trace)
+    ms_bsp, _ = timed(eng_b, args.steps, args.warmup)
+    del eng_b
+    eng_i = make("lb-bsp", constant_trace(n_total, iters))
+    ms_ideal, _ = timed(eng_i, args.steps, args.warmup)
+    del eng_i
+
+    # ---- roofline of the dominant tensor-core kernel (forward GEMM phase) ----
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak_tf = peaks.get("bf16_tflops", 1590.0)
+    peak_src = "measured" if "bf16_tflops" in peaks else "fallback"
+    # per-worker phase list: [fwd L0, head, bias L0, dW L0] for 784-256-10
+    fwd_flops = 2.0 * BATCH_PER_GPU * DIMS[0] * DIMS[1]
+    ph_fwd = float(phases[0]) if phases is not None and len(phases) else 0.0
+    ph_dw = float(phases[3]) if phases is not None and len(phases) > 3 else 0.0
+    achieved = fwd_flops / ph_fwd / 1e12 if ph_fwd > 0 else 0.0
+
+    if rank == 0:
+        clocks = clk.summary()
+        value = B / (ms_lb * 1e-3)
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_lb,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": "C2: MLP 784-256-10, 8 emulated workers per GPU under "
+                                   "trace-driven SM caps, global batch 4096 per GPU, LB-BSP + "
+                                   "NARX (warm-up 50), full-dataset loss every round",
+                       "global_batch": B, "workers": n_total,
+                       "parallelism": f"dp{n_total} (emulated {WORKERS_PER_GPU}/GPU)",
+                       "trace": "make_benchmark_series seed 3, iteration-indexed",
+                       "l2": "256 MB buffer zeroed between timed steps, outside the events"},
+            "bsp": {"value": B / (ms_bsp * 1e-3), "ms_per_step": ms_bsp},
+            "ideal_no_straggler": {"value": B / (ms_ideal * 1e-3), "ms_per_step": ms_ideal},
+            "lbbsp_over_bsp": ms_bsp / ms_lb,
+            "lbbsp_over_ideal_time": ms_lb / ms_ideal,
+            "phase_ms": [round(float(x) * 1e3, 4) for x in (phases if phases is not None else [])],
+            "roofline": {"bound": "tensor", "kernel": "fwd GEMM 4096x256x784 (tcgen05, per-worker "
+                                                      "partitions)",
+                         "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf if peak_tf else None,
+                         "peak_source": peak_src, "traffic": None,
+                         "note": "C2 GEMMs are latency-bound (SURVEY 8(d)); see profiles/ for "
+                                 "the C3 tensor-bound numbers"},
+            "gpu_launches": launches * args.steps,
+            "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "clocks": clocks,
+            "rounds_recorded": rec["rows"],
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline()
+            except Exception as ex:  # noqa: BLE001
+                line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -72,7 +72,8 @@ enum {
   LBBSP_E_GPU_OOM = 18,            /* gpu_compute_time: batch above oom point     */
   LBBSP_E_GRAD_EMPTY = 20,
   LBBSP_E_GRAD_INDEX = 21,
-  LBBSP_E_AGG_BATCH = 22
+  LBBSP_E_AGG_BATCH = 22,
+  LBBSP_E_MLP_CAPACITY = 30        /* "mlp: round a exceeds max_iterations b"      */
 };
 
 /* ======================================================================== */
@@ -308,6 +309,13 @@ typedef struct {
   double wall_s;
 } lbbsp_iter_scalars;
 
+/* make_benchmark_series (cluster_sim.cpp:41-64) with the given
+ * BenchmarkTraceConfig: the recorded-trace generator behind the "benchmark"
+ * dynamics (A2). Host arrays of length iterations. */
+int lbbsp_benchmark_series(uint64_t seed, int iterations, int regime_length, double high_lo,
+                           double high_hi, double low_lo, double low_hi, double spike_mult,
+                           double spike_prob, double* h_cpu, double* h_mem, double* h_mult);
+
 typedef struct lbbsp_sim lbbsp_sim;
 
 int lbbsp_sim_create(const lbbsp_sim_cfg* cfg, lbbsp_sim** out);
@@ -346,6 +354,77 @@ int lbbsp_gemm_bf16(const void* d_a, const void* d_b, void* d_c, int M, int N, i
                     int n_groups, const int* d_group_r0, const int* d_group_r1,
                     const int* d_group_cta0, const int* d_group_ctan, int ctas,
                     unsigned long long* d_timing, int bn, void* stream);
+
+/* ======================================================================== */
+/* MLP gradient engine with emulated / sharded workers (C1-C5)               */
+/* ======================================================================== */
+
+#define LBBSP_MLP_MAX_LAYERS 8
+
+/* One LB-BSP iteration of data-parallel MLP training on this GPU. Workers are
+ * either emulated on this GPU (n_workers_local > 1: each gets a CTA partition
+ * = SM cap driven by the trace) or one per GPU (n_workers_local == 1, ranks
+ * exchange gradients with ncclAllReduce and speeds with ncclAllGather).
+ * The workload generalises the reference's logistic regression
+ * (sgd.cpp:32-99) to an MLP with softmax-CE; sample stream, contiguous
+ * chunking, Eq.-7 weighting and the update follow cluster_sim.cpp:422-439. */
+typedef struct {
+  int n_layers;                       /* number of Linear layers            */
+  int dims[LBBSP_MLP_MAX_LAYERS + 1]; /* dims[0] input .. dims[n_layers] out */
+  int n_workers_total;
+  int n_workers_local;
+  int rank, world;
+  int global_batch;                   /* B over all workers                  */
+  int scheme;                         /* LBBSP_SCHEME_BSP | _LBBSP           */
+  int static_sizes;                   /* 1: h_static_sizes every round        */
+  const int* h_static_sizes;          /* [n_workers_total] (static-proportional) */
+  lbbsp_predictor_cfg predictor;
+  double learning_rate;
+  uint64_t seed;                      /* sample stream + predictor seeds     */
+  uint64_t dataset_seed;
+  int dataset_size;
+  int loss_every;                     /* full-dataset loss cadence (1 = every round) */
+  int sm_budget;                      /* SMs this rank's workers may use (0 = all) */
+  /* straggler trace, iteration-indexed: availability a = min(1, c*mult) of
+   * each worker's nominal SM share; [n_workers_total][trace_len], host */
+  const double* h_trace_c;
+  const double* h_trace_m;
+  const double* h_trace_mult;
+  int trace_len;
+  const double* h_worker_share;       /* [n_workers_total] nominal share of its GPU (NULL: 1/n_local) */
+  int max_iterations;                 /* record capacity                     */
+} lbbsp_mlp_cfg;
+
+typedef struct lbbsp_mlp lbbsp_mlp;
+
+int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out);
+int lbbsp_mlp_destroy(lbbsp_mlp* m);
+/* NCCL plumbing for world > 1: rank 0 gets an id, every rank inits with it. */
+int lbbsp_nccl_unique_id(unsigned char h_id[128]);
+int lbbsp_mlp_init_comm(lbbsp_mlp* m, const unsigned char h_id[128]);
+/* Run `iterations` LB-BSP rounds on the engine stream (no host sync). */
+int lbbsp_mlp_run(lbbsp_mlp* m, int iterations);
+void* lbbsp_mlp_stream(lbbsp_mlp* m);
+/* Records of the rounds run so far (blocking): [rows][n_total] arrays. */
+int lbbsp_mlp_records(lbbsp_mlp* m, int max_rows, int* rows, int* sizes, double* v_pred,
+                      double* v_obs, int* caps, double* t_worker, double* loss);
+/* Copy the fp32 master parameters (flat, per layer W [out][in] then b [out],
+ * each segment padded to 64 elements) and the offsets of each segment. */
+int lbbsp_mlp_params(lbbsp_mlp* m, float* h_params, long long* h_offsets, long long* n_params);
+int lbbsp_mlp_set_params(lbbsp_mlp* m, const float* h_params);
+int lbbsp_mlp_dataset(lbbsp_mlp* m, void* h_x_bf16, int* h_labels);
+int lbbsp_mlp_launches_per_iteration(lbbsp_mlp* m, int* launches);
+/* End-to-end plumbing on the engine stream (async, pinned host buffers):
+ * replace the resident dataset with host rows ([dataset_size][dims[0]] bf16 +
+ * labels) before a round, and read back the newest round's record
+ * (sizes [n_total] ints, then loss) after it. */
+int lbbsp_mlp_load_data_async(lbbsp_mlp* m, const void* h_x_bf16, const int* h_labels);
+int lbbsp_mlp_read_result_async(lbbsp_mlp* m, int* h_sizes, double* h_loss);
+/* Mean per-phase device time of the rounds run so far: phase p of the last
+ * round as {min start, max end} over workers (globaltimer ns); n_phases out. */
+int lbbsp_mlp_phase_times(lbbsp_mlp* m, double* h_phase_ns, int* n_phases);
+/* algorithmic work of one round on this rank: GEMM flops, reduction bytes */
+int lbbsp_mlp_work(lbbsp_mlp* m, double* gemm_flops, double* reduce_bytes);
 
 #ifdef __cplusplus
 }

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "exactmath.cuh"
+#include "host.cuh"
 #include "kernels.cuh"
 #include "predictor.cuh"
 
@@ -68,6 +69,9 @@ static int status_error(const lbbsp_dev_status& st) {
       return set_error(st.code, "batch_gradient: sample index out of range");
     case LBBSP_E_AGG_BATCH:
       return set_error(st.code, "aggregate_weighted: batch size must be >= 1");
+    case LBBSP_E_MLP_CAPACITY:
+      return set_error(st.code, "mlp: round %lld exceeds max_iterations %lld", (long long)st.a,
+                       (long long)st.b);
     default: return set_error(st.code, "lbbsp: device status %d/%d", st.code, st.what);
   }
 }
@@ -270,23 +274,6 @@ extern "C" int lbbsp_narx_train_online(lbbsp_narx_model* h_model, const double* 
 // ===========================================================================
 // predictor bank
 // ===========================================================================
-struct lbbsp_predictor {
-  PredDev dev{};
-  std::vector<void*> allocs;
-  ~lbbsp_predictor() {
-    for (void* p : allocs) cudaFree(p);
-  }
-  template <typename T>
-  cudaError_t alloc(T** p, size_t count) {
-    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1));
-    if (e == cudaSuccess) {
-      allocs.push_back(*p);
-      cudaMemset(*p, 0, sizeof(T) * (count ? count : 1));
-    }
-    return e;
-  }
-};
-
 namespace lbbsp {
 // Builds a device predictor bank; used by lbbsp_predictor_create and the sim.
 static int make_pred(lbbsp_predictor* P, const lbbsp_predictor_cfg* cfg, int n, int max_hist,
@@ -577,6 +564,25 @@ static void host_benchmark_series(uint64_t seed, const lbbsp_sim_cfg& c, double*
   }
 }
 }  // namespace lbbsp
+
+extern "C" int lbbsp_benchmark_series(uint64_t seed, int iterations, int regime_length,
+                                      double high_lo, double high_hi, double low_lo, double low_hi,
+                                      double spike_mult, double spike_prob, double* h_cpu,
+                                      double* h_mem, double* h_mult) {
+  if (iterations < 1 || regime_length < 1)
+    return set_error(LBBSP_INVALID_ARGUMENT, "benchmark series: need iterations, regime >= 1");
+  lbbsp_sim_cfg c{};
+  c.bench_iterations = iterations;
+  c.bench_regime_length = regime_length;
+  c.bench_high_lo = high_lo;
+  c.bench_high_hi = high_hi;
+  c.bench_low_lo = low_lo;
+  c.bench_low_hi = low_hi;
+  c.bench_spike_mult = spike_mult;
+  c.bench_spike_prob = spike_prob;
+  host_benchmark_series(seed, c, h_cpu, h_mem, h_mult);
+  return LBBSP_OK;
+}
 
 extern "C" int lbbsp_sim_create(const lbbsp_sim_cfg* cfg, lbbsp_sim** out) {
   LBBSP_REQUIRE_DEVICE();

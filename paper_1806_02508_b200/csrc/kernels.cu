@@ -189,6 +189,15 @@ __global__ void __launch_bounds__(kTrainThreads) pred_train_kernel(PredDev P, in
                    buf, &s);
 }
 
+cudaError_t launch_pred_train_from(const PredDev& P, const int* first_slot, cudaStream_t s) {
+  if (P.kind != LBBSP_PRED_NARX) return cudaSuccess;
+  const size_t smem = train_smem_bytes(P.max_hist);
+  cudaFuncSetAttribute(pred_train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(kTrainSmemCap));
+  pred_train_kernel<<<(P.n + 1) / 2, kTrainThreads, smem, s>>>(P, 1, nullptr, first_slot, smem);
+  return cudaGetLastError();
+}
+
 __global__ void pred_cursor_kernel(PredDev P) {
   if (threadIdx.x == 0) *P.cursor = (*P.cursor + (P.n + 1) / 2) % P.n;
 }

@@ -1,0 +1,1125 @@
+// mlp.cu -- the data-parallel MLP gradient engine of the LB-BSP iteration
+// (north_star (1)-(4) on one or more B200s) and its C-ABI.
+//
+// One round (cluster_sim.cpp:349-469 with the simulated timing replaced by
+// measured per-worker compute time under SM caps):
+//   plan        P1-P4  trace -> SM caps, predictor -> v_pred, solver -> b_i
+//   gather      P6     stream rows -> X, labels, Eq.6/7 row scales
+//   fwd GEMMs   P7     per-worker CTA partitions, ragged rows masked
+//   head        P7     softmax-CE + dlogits (+ small last layer on CUDA cores)
+//   bwd         P7     bias-grad column sums, dW (k-split per worker), dX
+//   reduce      P8     segmented reduction of worker partials (+ ncclAllReduce)
+//   apply       P8     w -= lr g, bf16 copies
+//   loss        P9     full-dataset loss (forward only)
+//   observe     P10    measured t_p -> v (+ ncclAllGather), push histories
+//   train       P10    NARX train_rotation
+#include <cuda_bf16.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+#include "exactmath.cuh"
+#include "gemm.cuh"
+#include "host.cuh"
+#include "kernels.cuh"
+#include "mlp_kernels.cuh"
+#include "predictor.cuh"
+#include "solver.cuh"
+
+namespace lbbsp {
+
+cudaError_t launch_pred_train_from(const PredDev& P, const int* first_slot, cudaStream_t s);
+
+// NCCL is resolved at run time (dlopen of libnccl.so.2): inside a PyTorch
+// process this binds the NCCL build torch already loaded instead of forcing
+// a second, older copy into the process.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static const NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+      api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+      api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+      api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
+      api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
+      api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    }
+  }
+  return api.AllReduce ? &api : nullptr;
+}
+
+namespace mlp {
+
+using bf16 = __nv_bfloat16;
+constexpr int kMaxPhases = 3 * LBBSP_MLP_MAX_LAYERS + 4;
+
+// ---------------------------------------------------------------------------
+// setup kernels (run once)
+// ---------------------------------------------------------------------------
+__global__ void init_x_kernel(bf16* x, long long count, uint64_t seed) {
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < count; i += 256ll * gridDim.x)
+    x[i] = __float2bfloat16_rn(hash_uniform(seed, static_cast<uint64_t>(i), -1.f, 1.f));
+}
+
+// labels = argmax_c(W* x + U[-0.1, 0.1]) with a seeded teacher W* (the
+// multi-class generalisation of generate_dataset, sgd.cpp:32-57); large
+// heads draw hashed labels.
+__global__ void teacher_labels_kernel(const bf16* x, int* y, int d, int d_out, uint64_t seed) {
+  __shared__ float acc[32];
+  const int i = blockIdx.x;
+  if (d_out > 32) {
+    if (threadIdx.x == 0) y[i] = static_cast<int>(hash64(seed ^ (0x1abe1ull + i)) % d_out);
+    return;
+  }
+  if (threadIdx.x < 32) acc[threadIdx.x] = 0.f;
+  __syncthreads();
+  for (int c = 0; c < d_out; ++c) {
+    float s = 0.f;
+    for (int j = threadIdx.x; j < d; j += blockDim.x)
+      s += hash_uniform(seed ^ 0x5e9a7a70ull, static_cast<uint64_t>(c) * d + j, -1.f, 1.f) *
+           __bfloat162float(x[static_cast<long long>(i) * d + j]);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&acc[c], s);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int best = 0;
+    float bv = -1e30f;
+    for (int c = 0; c < d_out; ++c) {
+      const float v = acc[c] + hash_uniform(seed ^ 0xda7a5e7ull, static_cast<uint64_t>(i) * d_out + c, -0.1f, 0.1f);
+      if (v > bv) { bv = v; best = c; }
+    }
+    y[i] = best;
+  }
+}
+
+__global__ void init_params_kernel(float* p, bf16* pb, long long off_w, long long off_b, int dout,
+                                   int din, uint64_t seed) {
+  const float s = rsqrtf(static_cast<float>(din));
+  const long long nw = static_cast<long long>(dout) * din;
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < nw; i += 256ll * gridDim.x) {
+    const float w = hash_uniform(seed, static_cast<uint64_t>(off_w + i), -s, s);
+    p[off_w + i] = w;
+    pb[off_w + i] = __float2bfloat16_rn(w);
+  }
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < dout; i += 256ll * gridDim.x) {
+    p[off_b + i] = 0.f;
+    pb[off_b + i] = __float2bfloat16_rn(0.f);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// iteration state (device-resident) shared by the small kernels
+// ---------------------------------------------------------------------------
+struct PlanDev {
+  int n_total, n_local, rank, B_total, scheme, static_sizes, sm_budget, trace_len;
+  const int* static_sizes_d;
+  const double* trace_c;
+  const double* trace_m;
+  const double* trace_mult;
+  const double* share;  // [n_total]
+  PredDev pred;
+  long long* k;
+  int* rows;
+  int max_rows;
+  int* sizes_all;      // [n_total]
+  int* r0;             // [n_local]
+  int* r1;
+  int* cta0;
+  int* ctan;
+  int* local_rows;     // scalar
+  int* stream_off;     // scalar
+  double* c_now;       // [n_total]
+  double* m_now;
+  double* v_pred;
+  unsigned long long* timing;  // [kMaxPhases][n_local][2]
+  double* v_obs_local;  // [n_local]
+  double* v_obs_all;    // [n_total]
+  double* loss_acc;
+  int N_data;
+  int loss_on;
+  int* train_first;
+  int* rec_sizes;
+  double* rec_vpred;
+  double* rec_vobs;
+  int* rec_caps;
+  double* rec_t;
+  double* rec_loss;
+  lbbsp_dev_status* status;
+};
+
+// P1-P4: trace -> caps, predictor -> v_pred, solver -> sizes, local slice
+__global__ void __launch_bounds__(256) plan_kernel(PlanDev D) {
+  __shared__ SolverSmem sm;
+  __shared__ double rem[LBBSP_MAX_WORKERS];
+  __shared__ double avail[LBBSP_MAX_WORKERS];
+  const int tid = threadIdx.x, n = D.n_total;
+  const long long k = *D.k;
+  const int len = min(*D.pred.len, D.pred.max_hist);
+  if (k >= D.max_rows && tid == 0)
+    set_status(D.status, LBBSP_RUNTIME, LBBSP_E_MLP_CAPACITY, k, D.max_rows);
+  const long long ti = k < D.trace_len - 1 ? k : D.trace_len - 1;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const size_t o = static_cast<size_t>(i) * D.trace_len + ti;
+    const double c = D.trace_c[o], m = D.trace_m[o], mult = D.trace_mult[o];
+    D.c_now[i] = c;
+    D.m_now[i] = m;
+    const double a = dmul(c, mult);
+    avail[i] = a < 1.0 ? a : 1.0;
+    D.v_pred[i] = len >= 1 ? predictor_predict_d(D.pred, i, len, c, m) : 0.0;
+  }
+  __syncthreads();
+  int code = 0;
+  if (D.static_sizes) {
+    for (int i = tid; i < n; i += blockDim.x) D.sizes_all[i] = D.static_sizes_d[i];
+  } else if (D.scheme == LBBSP_SCHEME_LBBSP && k > 0) {
+    code = block_cpu_allocate(D.v_pred, n, D.B_total, D.pred.floor, D.sizes_all, rem, &sm, D.status);
+  } else {
+    for (int i = tid; i < n; i += blockDim.x)
+      D.sizes_all[i] = D.B_total / n + (i < D.B_total % n ? 1 : 0);  // equal_split
+  }
+  __syncthreads();
+  if (code) return;
+  if (tid == 0) {
+    const int first = D.rank * D.n_local;
+    int off = 0;
+    for (int i = 0; i < first; ++i) off += D.sizes_all[i];
+    *D.stream_off = off;
+    int r = 0, c0 = 0;
+    for (int i = 0; i < D.n_local; ++i) {
+      const int w = first + i;
+      D.r0[i] = r;
+      r += D.sizes_all[w];
+      D.r1[i] = r;
+      const double share = D.share[w];
+      int cap = static_cast<int>(floor(static_cast<double>(D.sm_budget) * share * avail[w]));
+      cap = cap < 1 ? 1 : cap;
+      if (c0 + cap > D.sm_budget) cap = D.sm_budget - c0 > 0 ? D.sm_budget - c0 : 1;
+      D.cta0[i] = c0;
+      D.ctan[i] = cap;
+      c0 += cap;
+    }
+    *D.local_rows = r;
+    *D.loss_acc = 0.0;
+  }
+  for (int i = tid; i < kMaxPhases * D.n_local; i += blockDim.x) {
+    D.timing[2 * i] = ~0ull;
+    D.timing[2 * i + 1] = 0ull;
+  }
+  __syncthreads();
+  const int row = *D.rows;
+  if (row < D.max_rows) {
+    for (int i = tid; i < n; i += blockDim.x) {
+      D.rec_sizes[static_cast<size_t>(row) * n + i] = D.sizes_all[i];
+      D.rec_vpred[static_cast<size_t>(row) * n + i] = D.v_pred[i];
+    }
+    for (int i = tid; i < D.n_local; i += blockDim.x)
+      D.rec_caps[static_cast<size_t>(row) * n + D.rank * D.n_local + i] = D.ctan[i];
+  }
+}
+
+// P6: X[r] = data[stream[off + r]], labels, row scale (Eq. 7: 1/B; Eq. 6: 1/(n b_i))
+__global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const bf16* data_x,
+                              const int* data_y, int d0, bf16* X, int* y, float* row_scale) {
+  const long long k = min(*D.k, static_cast<long long>(D.max_rows - 1));  // capacity-guarded
+  const int rows = *D.local_rows, off = *D.stream_off;
+  const int* idx = streams + static_cast<size_t>(k) * B_total + off;
+  const int vec = d0 / 8;  // 16-byte chunks per row
+  const long long total = static_cast<long long>(rows) * vec;
+  for (long long t = blockIdx.x * 256ll + threadIdx.x; t < total; t += 256ll * gridDim.x) {
+    const int r = static_cast<int>(t / vec), v = static_cast<int>(t % vec);
+    const int src = idx[r];
+    reinterpret_cast<uint4*>(X)[static_cast<long long>(r) * vec + v] =
+        reinterpret_cast<const uint4*>(data_x)[static_cast<long long>(src) * vec + v];
+  }
+  for (int r = blockIdx.x * 256 + threadIdx.x; r < rows; r += 256 * gridDim.x) {
+    y[r] = data_y[idx[r]];
+    float s;
+    if (D.scheme == LBBSP_SCHEME_LBBSP) {
+      s = 1.0f / static_cast<float>(B_total);
+    } else {
+      int g = 0;
+      while (g + 1 < D.n_local && r >= D.r1[g]) ++g;
+      s = 1.0f / (static_cast<float>(D.n_total) *
+                  static_cast<float>(D.sizes_all[D.rank * D.n_local + g]));
+    }
+    row_scale[r] = s;
+  }
+}
+
+__device__ __forceinline__ void phase_begin(unsigned long long* timing, int g) {
+  if (timing && threadIdx.x == 0) atomicMin(&timing[2 * g], static_cast<unsigned long long>(gtimer()));
+}
+__device__ __forceinline__ void phase_end(unsigned long long* timing, int g) {
+  if (timing && threadIdx.x == 0) atomicMax(&timing[2 * g + 1], static_cast<unsigned long long>(gtimer()));
+}
+
+// Last layer with a small output (d_out <= 16) on CUDA cores, one warp per
+// row: logits, softmax-CE (warp shuffles), dlogits * row scale, per-worker dW
+// and db partials, dH = dlogits W through ReLU(H).
+template <int DOUT, int NK>
+__global__ void __launch_bounds__(256) head_small_kernel(
+    Groups G, int rows_total, const bf16* __restrict__ H, const float* __restrict__ W,
+    const float* __restrict__ bias, const int* __restrict__ y, const float* __restrict__ row_scale,
+    bf16* dH, float* slab, long long slab_stride, long long off_w, long long off_b,
+    double* loss_acc, unsigned long long* timing) {
+  constexpr int DH = 32 * NK;
+  __shared__ float sW[DOUT][DH];
+  __shared__ float sG[DOUT][DH];
+  __shared__ float sGb[DOUT];
+  int g, cta_in, cta_cnt;
+  if (!my_group(G, &g, &cta_in, &cta_cnt)) return;
+  phase_begin(timing, g);
+  for (int i = threadIdx.x; i < DOUT * DH; i += blockDim.x) {
+    sW[i / DH][i % DH] = W[i];
+    sG[i / DH][i % DH] = 0.f;
+  }
+  if (threadIdx.x < DOUT) sGb[threadIdx.x] = 0.f;
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  const int r0 = G.n ? G.r0[g] : 0, r1 = G.n ? G.r1[g] : rows_total;
+  float acc[DOUT][NK];
+  float accb[DOUT];
+#pragma unroll
+  for (int c = 0; c < DOUT; ++c) {
+    accb[c] = 0.f;
+#pragma unroll
+    for (int t = 0; t < NK; ++t) acc[c][t] = 0.f;
+  }
+  double lsum = 0.0;
+  for (int r = r0 + cta_in * nw + warp; r < r1; r += cta_cnt * nw) {
+    float h[NK];
+#pragma unroll
+    for (int t = 0; t < NK; ++t) h[t] = __bfloat162float(H[static_cast<long long>(r) * DH + lane + 32 * t]);
+    float logit[DOUT];
+#pragma unroll
+    for (int c = 0; c < DOUT; ++c) {
+      float s = 0.f;
+#pragma unroll
+      for (int t = 0; t < NK; ++t) s += h[t] * sW[c][lane + 32 * t];
+      logit[c] = warp_sum(s) + bias[c];
+    }
+    float mx = logit[0];
+#pragma unroll
+    for (int c = 1; c < DOUT; ++c) mx = fmaxf(mx, logit[c]);
+    float se = 0.f, p[DOUT];
+#pragma unroll
+    for (int c = 0; c < DOUT; ++c) {
+      p[c] = __expf(logit[c] - mx);
+      se += p[c];
+    }
+    const int yr = y[r];
+    float ly = 0.f;
+#pragma unroll
+    for (int c = 0; c < DOUT; ++c) ly = c == yr ? logit[c] : ly;
+    if (lane == 0) lsum += static_cast<double>(logf(se) + mx - ly);
+    if (dH) {
+      const float inv = 1.f / se, sc = row_scale[r];
+      float dl[DOUT];
+#pragma unroll
+      for (int c = 0; c < DOUT; ++c) {
+        dl[c] = (p[c] * inv - (c == yr ? 1.f : 0.f)) * sc;
+        accb[c] += dl[c];
+#pragma unroll
+        for (int t = 0; t < NK; ++t) acc[c][t] += dl[c] * h[t];
+      }
+#pragma unroll
+      for (int t = 0; t < NK; ++t) {
+        float d = 0.f;
+#pragma unroll
+        for (int c = 0; c < DOUT; ++c) d += dl[c] * sW[c][lane + 32 * t];
+        dH[static_cast<long long>(r) * DH + lane + 32 * t] = __float2bfloat16_rn(h[t] > 0.f ? d : 0.f);
+      }
+    }
+  }
+  if (loss_acc && lane == 0 && lsum != 0.0) atomicAdd(loss_acc, lsum);
+  if (dH) {
+#pragma unroll
+    for (int c = 0; c < DOUT; ++c) {
+#pragma unroll
+      for (int t = 0; t < NK; ++t) atomicAdd(&sG[c][lane + 32 * t], acc[c][t]);
+      if (lane == 0) atomicAdd(&sGb[c], accb[c]);
+    }
+    __syncthreads();
+    float* gs = slab + static_cast<long long>(g) * slab_stride;
+    for (int i = threadIdx.x; i < DOUT * DH; i += blockDim.x) atomicAdd(&gs[off_w + i], sG[i / DH][i % DH]);
+    if (threadIdx.x < DOUT) atomicAdd(&gs[off_b + threadIdx.x], sGb[threadIdx.x]);
+  }
+  __syncthreads();
+  phase_end(timing, g);
+}
+
+// Large softmax-CE head: one warp per row over bf16 logits [rows][n_out]
+// (n_out % 256 == 0): loss and dZ = (softmax - onehot) * row_scale.
+__global__ void __launch_bounds__(256) softmax_ce_kernel(
+    Groups G, int rows_total, const bf16* __restrict__ logits, int n_out,
+    const int* __restrict__ y, const float* __restrict__ row_scale, bf16* dZ, double* loss_acc,
+    unsigned long long* timing) {
+  int g, cta_in, cta_cnt;
+  if (!my_group(G, &g, &cta_in, &cta_cnt)) return;
+  phase_begin(timing, g);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  const int r0 = G.n ? G.r0[g] : 0, r1 = G.n ? G.r1[g] : rows_total;
+  double lsum = 0.0;
+  for (int r = r0 + cta_in * nw + warp; r < r1; r += cta_cnt * nw) {
+    const uint4* row = reinterpret_cast<const uint4*>(logits + static_cast<long long>(r) * n_out);
+    const int nv = n_out / 8;
+    float mx = -1e30f;
+    for (int v = lane; v < nv; v += 32) {
+      const uint4 q = row[v];
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(b2[j]);
+        mx = fmaxf(mx, fmaxf(f.x, f.y));
+      }
+    }
+    mx = warp_max(mx);
+    float se = 0.f;
+    for (int v = lane; v < nv; v += 32) {
+      const uint4 q = row[v];
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(b2[j]);
+        se += __expf(f.x - mx) + __expf(f.y - mx);
+      }
+    }
+    se = warp_sum(se);
+    const int yr = y[r];
+    const float ly = __bfloat162float(logits[static_cast<long long>(r) * n_out + yr]);
+    if (lane == 0) lsum += static_cast<double>(logf(se) + mx - ly);
+    if (dZ) {
+      const float inv = 1.f / se, sc = row_scale[r];
+      uint4* out = reinterpret_cast<uint4*>(dZ + static_cast<long long>(r) * n_out);
+      for (int v = lane; v < nv; v += 32) {
+        const uint4 q = row[v];
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+        uint4 o;
+        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(b2[j]);
+          const int c = v * 8 + 2 * j;
+          const float a = (__expf(f.x - mx) * inv - (c == yr ? 1.f : 0.f)) * sc;
+          const float b = (__expf(f.y - mx) * inv - (c + 1 == yr ? 1.f : 0.f)) * sc;
+          o2[j] = __floats2bfloat162_rn(a, b);
+        }
+        out[v] = o;
+      }
+    }
+  }
+  if (loss_acc && lane == 0 && lsum != 0.0) atomicAdd(loss_acc, lsum);
+  __syncthreads();
+  phase_end(timing, g);
+}
+
+// db partial of worker g = column sums of dZ over its rows (N % 8 == 0)
+__global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __restrict__ dZ, int N,
+                                                        float* slab, long long slab_stride,
+                                                        long long off_b, unsigned long long* timing) {
+  int g, cta_in, cta_cnt;
+  if (!my_group(G, &g, &cta_in, &cta_cnt)) return;
+  phase_begin(timing, g);
+  const int r0 = G.r0[g], r1 = G.r1[g];
+  const int nv = N / 8;
+  float* gs = slab + static_cast<long long>(g) * slab_stride + off_b;
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r = r0 + cta_in; r < r1; r += cta_cnt) {
+      const uint4 q = reinterpret_cast<const uint4*>(dZ + static_cast<long long>(r) * N)[v];
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(b2[j]);
+        a[2 * j] += f.x;
+        a[2 * j + 1] += f.y;
+      }
+    }
+    if (r0 + cta_in < r1)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) atomicAdd(&gs[v * 8 + j], a[j]);
+  }
+  __syncthreads();
+  phase_end(timing, g);
+}
+
+// Segmented reduction of the worker partial slabs + SGD apply (K8+K9), HBM-
+// bound: reads (n+1) P fp32, writes P fp32 + P bf16. `apply` == 0 only
+// reduces into grad (the allreduce then runs on grad).
+__global__ void __launch_bounds__(256) reduce_apply_kernel(const float* __restrict__ partial, int n,
+                                                           long long P, float* grad, float* params,
+                                                           bf16* pb, float lr, int apply) {
+  const long long nv = P / 4;
+  for (long long v = blockIdx.x * 256ll + threadIdx.x; v < nv; v += 256ll * gridDim.x) {
+    float4 s = reinterpret_cast<const float4*>(partial)[v];
+    for (int g = 1; g < n; ++g) {
+      const float4 q = reinterpret_cast<const float4*>(partial + g * P)[v];
+      s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
+    }
+    if (!apply) {
+      reinterpret_cast<float4*>(grad)[v] = s;
+      continue;
+    }
+    float4 w = reinterpret_cast<float4*>(params)[v];
+    w.x -= lr * s.x; w.y -= lr * s.y; w.z -= lr * s.z; w.w -= lr * s.w;
+    reinterpret_cast<float4*>(params)[v] = w;
+    __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(pb) + 2 * v;
+    o[0] = __floats2bfloat162_rn(w.x, w.y);
+    o[1] = __floats2bfloat162_rn(w.z, w.w);
+  }
+}
+
+// zero the partial regions that are accumulated with atomics (biases, head)
+__global__ void zero_regions_kernel(float* slab, long long slab_stride, int n_slabs,
+                                    const long long* reg_off, const long long* reg_len, int n_reg) {
+  for (int s = 0; s < n_slabs; ++s)
+    for (int r = 0; r < n_reg; ++r) {
+      float* p = slab + s * slab_stride + reg_off[r];
+      for (long long i = blockIdx.x * 256ll + threadIdx.x; i < reg_len[r]; i += 256ll * gridDim.x) p[i] = 0.f;
+    }
+}
+
+// measured per-worker compute time -> realised speed b_i / t_i
+__global__ void speed_kernel(PlanDev D, int n_phases) {
+  const int i = threadIdx.x;
+  if (i >= D.n_local) return;
+  double t = 0.0;
+  for (int p = 0; p < n_phases; ++p) {
+    const unsigned long long s = D.timing[2 * (p * D.n_local + i)], e = D.timing[2 * (p * D.n_local + i) + 1];
+    if (s != ~0ull && e > s) t += static_cast<double>(e - s) * 1e-9;
+  }
+  const int w = D.rank * D.n_local + i;
+  const double b = static_cast<double>(D.sizes_all[w]);
+  D.v_obs_local[i] = t > 0.0 ? b / t : b;
+  const int row = *D.rows;
+  if (row < D.max_rows) D.rec_t[static_cast<size_t>(row) * D.n_total + w] = t;
+}
+
+// P10: push every worker's (v, c, m) (cluster_sim.cpp:309-313), advance round
+__global__ void observe_kernel(PlanDev D) {
+  const int len = *D.pred.len;
+  const int row = *D.rows;
+  for (int i = threadIdx.x; i < D.n_total; i += blockDim.x) {
+    observe_d(D.pred, i, len, D.v_obs_all[i], D.c_now[i], D.m_now[i], 0.0);
+    if (row < D.max_rows) D.rec_vobs[static_cast<size_t>(row) * D.n_total + i] = D.v_obs_all[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *D.pred.len = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
+    *D.train_first = *D.pred.cursor;
+    *D.pred.cursor = (*D.pred.cursor + (D.n_total + 1) / 2) % D.n_total;
+    if (row < D.max_rows)
+      D.rec_loss[row] = D.loss_on ? *D.loss_acc / static_cast<double>(D.N_data) : -1.0;
+    *D.rows = row + 1;
+    *D.k += 1;
+  }
+}
+
+}  // namespace mlp
+}  // namespace lbbsp
+
+// ===========================================================================
+// host engine
+// ===========================================================================
+using namespace lbbsp;
+using namespace lbbsp::mlp;
+
+struct lbbsp_mlp {
+  lbbsp_mlp_cfg cfg{};
+  int L = 0;
+  std::vector<int> dims;
+  int n_local = 1, n_total = 1, B_total = 0, B_cap = 0, N_data = 0, max_rows = 0;
+  bool small_head = false;
+  long long P = 0;
+  std::vector<long long> off_w, off_b;
+  std::vector<void*> allocs;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  ncclComm_t comm = nullptr;
+  int launches = 0;
+  // device buffers
+  bf16 *data_x = nullptr, *X = nullptr, *pb = nullptr, *logits = nullptr, *dlogits = nullptr;
+  int *data_y = nullptr, *y = nullptr, *streams = nullptr;
+  float *params = nullptr, *grad = nullptr, *partial = nullptr, *row_scale = nullptr;
+  std::vector<bf16*> H, dZ;           // H[l]: output of layer l (l < L-1); dZ[l] grad wrt layer-l output
+  std::vector<bf16*> Hd;               // full-dataset forward buffers
+  bf16* logits_d = nullptr;
+  long long* reg_off = nullptr;
+  long long* reg_len = nullptr;
+  int n_reg = 0;
+  PlanDev D{};
+  lbbsp_predictor pred;
+  std::vector<GemmPlan> fwd, dx, dw, fwd_d;
+  int n_phases = 0;
+  double gemm_flops = 0.0, reduce_bytes = 0.0;
+  double* result = nullptr;
+
+  ~lbbsp_mlp() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (comm && nccl_api()) nccl_api()->CommDestroy(comm);
+    if (stream) cudaStreamDestroy(stream);
+    for (void* p : allocs) cudaFree(p);
+  }
+  template <typename T>
+  cudaError_t alloc(T** p, size_t count) {
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1));
+    if (e == cudaSuccess) {
+      allocs.push_back(*p);
+      e = cudaMemset(*p, 0, sizeof(T) * (count ? count : 1));
+    }
+    return e;
+  }
+  template <typename T>
+  cudaError_t upload(T** dst, const T* src, size_t count) {
+    cudaError_t e = alloc(dst, count);
+    if (e == cudaSuccess && count) e = cudaMemcpy(*dst, src, sizeof(T) * count, cudaMemcpyHostToDevice);
+    return e;
+  }
+
+  Groups groups() const {
+    Groups G;
+    G.n = n_local;
+    G.r0 = D.r0;
+    G.r1 = D.r1;
+    G.cta0 = D.cta0;
+    G.ctan = D.ctan;
+    return G;
+  }
+  unsigned long long* phase_slot(int p) { return D.timing + 2ll * p * n_local; }
+
+  int enqueue_iteration(cudaStream_t s);
+};
+
+namespace {
+
+// grouped GEMM launch helper
+int launch_grouped(lbbsp_mlp* m, GemmPlan& p, int mode, unsigned long long* timing, cudaStream_t s) {
+  p.args.mode = mode;
+  p.args.n_groups = m->n_local;
+  p.args.g_r0 = m->D.r0;
+  p.args.g_r1 = m->D.r1;
+  p.args.g_cta0 = m->D.cta0;
+  p.args.g_ctan = m->D.ctan;
+  p.args.timing = timing;
+  p.ctas = m->D.sm_budget;
+  return gemm_launch(p, s);
+}
+
+}  // namespace
+
+int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
+  const Groups G = groups();
+  int nl = 0, ph = 0;
+  const int sms = D.sm_budget;
+  plan_kernel<<<1, 256, 0, s>>>(D);
+  ++nl;
+  zero_regions_kernel<<<32, 256, 0, s>>>(partial, P, n_local, reg_off, reg_len, n_reg);
+  ++nl;
+  gather_kernel<<<sms, 256, 0, s>>>(D, streams, B_total, data_x, data_y, dims[0], X, y, row_scale);
+  ++nl;
+  // ---- forward (per-worker partitions) ----
+  const int Lg = small_head ? L - 1 : L;  // layers on the tensor-core GEMM
+  for (int l = 0; l < Lg; ++l) {
+    int rc = launch_grouped(this, fwd[l], tc::kRows, phase_slot(ph++), s);
+    if (rc) return rc;
+    ++nl;
+  }
+  // ---- head ----
+  const int hl = L - 1;  // last layer index
+  if (small_head) {
+    const bf16* Hin = L >= 2 ? H[L - 2] : X;
+    head_small_kernel<10, 8><<<sms, 256, 0, s>>>(G, 0, Hin, params + off_w[hl], params + off_b[hl], y,
+                                                  row_scale, dZ[L - 2], partial, P, off_w[hl],
+                                                  off_b[hl], nullptr, phase_slot(ph++));
+  } else {
+    softmax_ce_kernel<<<sms, 256, 0, s>>>(G, 0, logits, dims[L], y, row_scale, dZ[L - 1], nullptr,
+                                          phase_slot(ph++));
+  }
+  ++nl;
+  // ---- backward ----
+  for (int l = Lg - 1; l >= 0; --l) {
+    bias_grad_kernel<<<sms, 256, 0, s>>>(G, dZ[l], dims[l + 1], partial, P, off_b[l], phase_slot(ph++));
+    ++nl;
+    int rc = launch_grouped(this, dw[l], tc::kKSplit, phase_slot(ph++), s);
+    if (rc) return rc;
+    ++nl;
+    if (l > 0) {
+      rc = launch_grouped(this, dx[l], tc::kRows, phase_slot(ph++), s);
+      if (rc) return rc;
+      ++nl;
+    }
+  }
+  n_phases = ph;
+  // ---- aggregate + apply ----
+  const float lr = static_cast<float>(cfg.learning_rate);
+  if (cfg.world > 1) {
+    reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 0);
+    ++nl;
+    if (nccl_api()->AllReduce(grad, grad, static_cast<size_t>(P), ncclFloat, ncclSum, comm, s) != ncclSuccess)
+      return set_error(LBBSP_NCCL, "ncclAllReduce failed");
+    ++nl;
+    reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(grad, 1, P, grad, params, pb, lr, 1);
+    ++nl;
+  } else {
+    reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 1);
+    ++nl;
+  }
+  // ---- full-dataset loss (step_sync P9, cluster_sim.cpp:445) ----
+  if (D.loss_on) {
+    for (int l = 0; l < Lg; ++l) {
+      fwd_d[l].ctas = std::min(fwd_d[l].ctas, sms);
+      int rc = gemm_launch(fwd_d[l], s);
+      if (rc) return rc;
+      ++nl;
+    }
+    Groups none{};
+    none.n = 0;
+    if (small_head) {
+      const bf16* Hin = L >= 2 ? Hd[L - 2] : data_x;
+      head_small_kernel<10, 8><<<sms, 256, 0, s>>>(none, N_data, Hin, params + off_w[hl],
+                                                    params + off_b[hl], data_y, nullptr, nullptr,
+                                                    nullptr, 0, 0, 0, D.loss_acc, nullptr);
+    } else {
+      softmax_ce_kernel<<<sms, 256, 0, s>>>(none, N_data, logits_d, dims[L], data_y, nullptr, nullptr,
+                                            D.loss_acc, nullptr);
+    }
+    ++nl;
+  }
+  // ---- observe (measured speeds) + NARX training ----
+  speed_kernel<<<1, 32 * ((n_local + 31) / 32), 0, s>>>(D, n_phases);
+  ++nl;
+  if (cfg.world > 1) {
+    if (nccl_api()->AllGather(D.v_obs_local, D.v_obs_all, static_cast<size_t>(n_local), ncclDouble, comm, s) !=
+        ncclSuccess)
+      return set_error(LBBSP_NCCL, "ncclAllGather failed");
+    ++nl;
+  }
+  observe_kernel<<<1, 256, 0, s>>>(D);
+  ++nl;
+  if (pred.dev.kind == LBBSP_PRED_NARX) {
+    LBBSP_CUDA_CHECK(launch_pred_train_from(pred.dev, D.train_first, s));
+    ++nl;
+  }
+  LBBSP_CUDA_CHECK(cudaGetLastError());
+  launches = nl;
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return set_error(LBBSP_CUDA, "lbbsp: no CUDA device (the B200 path has no CPU fallback)");
+  }
+  const lbbsp_mlp_cfg& c = *cfg;
+  if (c.n_layers < 1 || c.n_layers > LBBSP_MLP_MAX_LAYERS)
+    return set_error(LBBSP_INVALID_ARGUMENT, "mlp: n_layers must be in [1, %d]", LBBSP_MLP_MAX_LAYERS);
+  if (c.n_workers_local < 1 || c.world < 1 || c.n_workers_total != c.n_workers_local * c.world)
+    return set_error(LBBSP_INVALID_ARGUMENT, "mlp: n_workers_total must equal n_workers_local * world");
+  if (c.n_workers_total > LBBSP_MAX_WORKERS)
+    return set_error(LBBSP_INVALID_ARGUMENT, "mlp: at most %d workers", LBBSP_MAX_WORKERS);
+  if (c.global_batch < c.n_workers_total)
+    return set_error(LBBSP_INVALID_ARGUMENT, "simulation: total_budget below worker count");
+  if (c.scheme != LBBSP_SCHEME_LBBSP && c.global_batch % c.n_workers_total != 0)
+    return set_error(LBBSP_INVALID_ARGUMENT,
+                     "simulation: bsp/asp/ssp need total_budget divisible by workers");
+  if (c.trace_len < 1 || !c.h_trace_c || !c.h_trace_m || !c.h_trace_mult)
+    return set_error(LBBSP_INVALID_ARGUMENT, "mlp: a straggler trace is required");
+  const int L = c.n_layers;
+  const bool small_head = c.dims[L] <= 16;
+  if (small_head && (c.dims[L] != 10 || L < 2 || c.dims[L - 1] != 256))
+    return set_error(LBBSP_INVALID_ARGUMENT, "mlp: small heads support the 256->10 classifier");
+  for (int l = 0; l <= L; ++l)
+    if (c.dims[l] % 8 != 0 && !(small_head && l == L))
+      return set_error(LBBSP_INVALID_ARGUMENT, "mlp: layer widths must be multiples of 8");
+  if (!small_head && c.dims[L] % 256 != 0)
+    return set_error(LBBSP_INVALID_ARGUMENT, "mlp: softmax head width must be a multiple of 256");
+
+  auto M = std::make_unique<lbbsp_mlp>();
+  lbbsp_mlp& m = *M;
+  m.cfg = c;
+  m.L = L;
+  m.dims.assign(c.dims, c.dims + L + 1);
+  m.n_local = c.n_workers_local;
+  m.n_total = c.n_workers_total;
+  m.B_total = c.global_batch;
+  m.B_cap = c.global_batch;  // a rank can be handed (almost) the whole batch
+  m.N_data = c.dataset_size;
+  m.small_head = small_head;
+  m.max_rows = c.max_iterations > 0 ? c.max_iterations : 1;
+  LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking));
+
+  // flat parameter layout, 64-element aligned segments
+  auto pad = [](long long x) { return (x + 63) / 64 * 64; };
+  long long P = 0;
+  for (int l = 0; l < L; ++l) {
+    m.off_w.push_back(P);
+    P += pad(static_cast<long long>(c.dims[l + 1]) * c.dims[l]);
+    m.off_b.push_back(P);
+    P += pad(c.dims[l + 1]);
+  }
+  m.P = P;
+  const int d0 = c.dims[0];
+  LBBSP_CUDA_CHECK(m.alloc(&m.params, P));
+  LBBSP_CUDA_CHECK(m.alloc(&m.pb, P));
+  LBBSP_CUDA_CHECK(m.alloc(&m.grad, P));
+  if (m.n_local > 1 || c.world > 1)
+    LBBSP_CUDA_CHECK(m.alloc(&m.partial, static_cast<size_t>(P) * m.n_local));
+  else
+    m.partial = m.grad;  // one worker: the dW GEMM writes the gradient directly
+  LBBSP_CUDA_CHECK(m.alloc(&m.data_x, static_cast<size_t>(m.N_data) * d0));
+  LBBSP_CUDA_CHECK(m.alloc(&m.data_y, m.N_data));
+  LBBSP_CUDA_CHECK(m.alloc(&m.X, static_cast<size_t>(m.B_cap) * d0));
+  LBBSP_CUDA_CHECK(m.alloc(&m.y, m.B_cap));
+  LBBSP_CUDA_CHECK(m.alloc(&m.row_scale, m.B_cap));
+  m.H.assign(L, nullptr);
+  m.dZ.assign(L, nullptr);
+  m.Hd.assign(L, nullptr);
+  for (int l = 0; l < L; ++l) {
+    if (l < L - 1) {
+      LBBSP_CUDA_CHECK(m.alloc(&m.H[l], static_cast<size_t>(m.B_cap) * c.dims[l + 1]));
+      LBBSP_CUDA_CHECK(m.alloc(&m.Hd[l], static_cast<size_t>(m.N_data) * c.dims[l + 1]));
+    }
+    if (!(small_head && l == L - 1))
+      LBBSP_CUDA_CHECK(m.alloc(&m.dZ[l], static_cast<size_t>(m.B_cap) * c.dims[l + 1]));
+  }
+  if (!small_head) {
+    LBBSP_CUDA_CHECK(m.alloc(&m.logits, static_cast<size_t>(m.B_cap) * c.dims[L]));
+    LBBSP_CUDA_CHECK(m.alloc(&m.logits_d, static_cast<size_t>(m.N_data) * c.dims[L]));
+  }
+  // atomic-accumulated partial regions: all biases (+ the small head's W)
+  std::vector<long long> ro, rl;
+  for (int l = 0; l < L; ++l) {
+    ro.push_back(m.off_b[l]);
+    rl.push_back(c.dims[l + 1]);
+  }
+  if (small_head) {
+    ro.push_back(m.off_w[L - 1]);
+    rl.push_back(static_cast<long long>(c.dims[L]) * c.dims[L - 1]);
+  }
+  m.n_reg = static_cast<int>(ro.size());
+  LBBSP_CUDA_CHECK(m.upload(&m.reg_off, ro.data(), ro.size()));
+  LBBSP_CUDA_CHECK(m.upload(&m.reg_len, rl.data(), rl.size()));
+
+  // dataset + parameters (setup-time device generators)
+  init_x_kernel<<<512, 256>>>(m.data_x, static_cast<long long>(m.N_data) * d0, c.dataset_seed);
+  teacher_labels_kernel<<<m.N_data, 256>>>(m.data_x, m.data_y, d0, c.dims[L], c.dataset_seed);
+  for (int l = 0; l < L; ++l)
+    init_params_kernel<<<512, 256>>>(m.params, m.pb, m.off_w[l], m.off_b[l], c.dims[l + 1], c.dims[l],
+                                     c.seed ^ (0x9a4c0ull + l));
+  LBBSP_CUDA_CHECK(cudaGetLastError());
+
+  // sample streams for every round (cluster_sim.cpp:302-307)
+  const size_t R = static_cast<size_t>(m.max_rows);
+  LBBSP_CUDA_CHECK(m.alloc(&m.streams, R * m.B_total));
+  LBBSP_CUDA_CHECK(launch_sample_streams(c.seed, 0, static_cast<int>(R), m.B_total, m.N_data, m.streams,
+                                         nullptr));
+
+  // plan state
+  PlanDev& D = m.D;
+  const int n = m.n_total;
+  D.n_total = n;
+  D.n_local = m.n_local;
+  D.rank = c.rank;
+  D.B_total = m.B_total;
+  D.scheme = c.scheme;
+  D.static_sizes = c.static_sizes;
+  int sms = num_sms();
+  D.sm_budget = c.sm_budget > 0 && c.sm_budget < sms ? c.sm_budget : sms;
+  D.trace_len = c.trace_len;
+  const size_t TL = static_cast<size_t>(n) * c.trace_len;
+  double *tc_ = nullptr, *tm_ = nullptr, *tx_ = nullptr, *sh = nullptr;
+  LBBSP_CUDA_CHECK(m.upload(&tc_, c.h_trace_c, TL));
+  LBBSP_CUDA_CHECK(m.upload(&tm_, c.h_trace_m, TL));
+  LBBSP_CUDA_CHECK(m.upload(&tx_, c.h_trace_mult, TL));
+  D.trace_c = tc_;
+  D.trace_m = tm_;
+  D.trace_mult = tx_;
+  std::vector<double> share(n, 1.0 / m.n_local);
+  if (c.h_worker_share) share.assign(c.h_worker_share, c.h_worker_share + n);
+  LBBSP_CUDA_CHECK(m.upload(&sh, share.data(), share.size()));
+  D.share = sh;
+  if (c.static_sizes) {
+    int* ss = nullptr;
+    LBBSP_CUDA_CHECK(m.upload(&ss, c.h_static_sizes, n));
+    D.static_sizes_d = ss;
+  }
+  LBBSP_CUDA_CHECK(m.alloc(&D.k, 1));
+  LBBSP_CUDA_CHECK(m.alloc(&D.rows, 1));
+  D.max_rows = m.max_rows;
+  LBBSP_CUDA_CHECK(m.alloc(&D.sizes_all, n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.r0, m.n_local));
+  LBBSP_CUDA_CHECK(m.alloc(&D.r1, m.n_local));
+  LBBSP_CUDA_CHECK(m.alloc(&D.cta0, m.n_local));
+  LBBSP_CUDA_CHECK(m.alloc(&D.ctan, m.n_local));
+  LBBSP_CUDA_CHECK(m.alloc(&D.local_rows, 1));
+  LBBSP_CUDA_CHECK(m.alloc(&D.stream_off, 1));
+  LBBSP_CUDA_CHECK(m.alloc(&D.c_now, n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.m_now, n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.v_pred, n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.timing, 2ull * kMaxPhases * m.n_local));
+  LBBSP_CUDA_CHECK(m.alloc(&D.v_obs_local, m.n_local));
+  if (c.world > 1)
+    LBBSP_CUDA_CHECK(m.alloc(&D.v_obs_all, n));
+  else
+    D.v_obs_all = D.v_obs_local;
+  LBBSP_CUDA_CHECK(m.alloc(&D.loss_acc, 1));
+  D.N_data = m.N_data;
+  D.loss_on = c.loss_every > 0 ? 1 : 0;
+  LBBSP_CUDA_CHECK(m.alloc(&D.train_first, 1));
+  LBBSP_CUDA_CHECK(m.alloc(&D.rec_sizes, R * n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.rec_vpred, R * n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.rec_vobs, R * n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.rec_caps, R * n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.rec_t, R * n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.rec_loss, R));
+  LBBSP_CUDA_CHECK(m.alloc(&D.status, 1));
+
+  // predictor bank over all workers (replicated on every rank)
+  {
+    std::vector<uint64_t> seeds(n);
+    for (int i = 0; i < n; ++i) seeds[i] = mix_seed(c.seed, 0x9ced1c70ull, static_cast<uint64_t>(i));
+    lbbsp_predictor* tmp = nullptr;
+    lbbsp_predictor_cfg pc = c.predictor;
+    pc.train.min_history = pc.warmup_iterations;
+    int rc = lbbsp_predictor_create(&pc, n, m.max_rows, seeds.data(), nullptr, &tmp);
+    if (rc) return rc;
+    // adopt the bank's allocations
+    m.pred.dev = tmp->dev;
+    m.pred.allocs.swap(tmp->allocs);
+    delete tmp;
+    D.pred = m.pred.dev;
+  }
+
+  // GEMM plans (tensor maps on the fixed buffers)
+  const int Lg = small_head ? L - 1 : L;
+  m.fwd.resize(Lg);
+  m.dx.resize(Lg);
+  m.dw.resize(Lg);
+  m.fwd_d.resize(Lg);
+  double flops = 0.0;
+  for (int l = 0; l < Lg; ++l) {
+    const int din = c.dims[l], dout = c.dims[l + 1];
+    const bf16* Ain = l == 0 ? m.X : m.H[l - 1];
+    const bf16* Ain_d = l == 0 ? m.data_x : m.Hd[l - 1];
+    const bool last = (l == L - 1);
+    const int bn = dout >= 256 ? 256 : 128;
+    const int epi = last ? tc::kEpiBiasBf16 : tc::kEpiBiasReluBf16;
+    int rc = gemm_plan(&m.fwd[l], Ain, m.pb + m.off_w[l], m.B_cap, dout, din, false, false, bn, epi);
+    if (rc) return rc;
+    m.fwd[l].args.c_bf16 = last ? m.logits : m.H[l];
+    m.fwd[l].args.ldc = dout;
+    m.fwd[l].args.bias = m.params + m.off_b[l];
+    rc = gemm_plan(&m.fwd_d[l], Ain_d, m.pb + m.off_w[l], m.N_data, dout, din, false, false, bn, epi);
+    if (rc) return rc;
+    m.fwd_d[l].args.c_bf16 = last ? m.logits_d : m.Hd[l];
+    m.fwd_d[l].args.ldc = dout;
+    m.fwd_d[l].args.bias = m.params + m.off_b[l];
+    // dW_l = dZ_l^T A_l : M=dout, N=din, K=rows ; A = dZ_l [rows][dout] MN-major, B = A_l [rows][din] MN-major
+    const int bn_w = din >= 256 ? 256 : 128;
+    rc = gemm_plan(&m.dw[l], m.dZ[l], Ain, dout, din, m.B_cap, true, true, bn_w, tc::kEpiF32);
+    if (rc) return rc;
+    m.dw[l].args.c_f32 = m.partial + m.off_w[l];
+    m.dw[l].args.ldc = din;
+    m.dw[l].args.group_stride = P;
+    if (l > 0) {
+      // dZ_{l-1} = (dZ_l W_l) * (H_{l-1} > 0): A = dZ_l [rows][dout] K-major, B = W_l [dout][din] = [K][N] MN-major
+      rc = gemm_plan(&m.dx[l], m.dZ[l], m.pb + m.off_w[l], m.B_cap, din, dout, false, true, bn_w,
+                     tc::kEpiDReluBf16);
+      if (rc) return rc;
+      m.dx[l].args.c_bf16 = m.dZ[l - 1];
+      m.dx[l].args.ldc = din;
+      m.dx[l].args.aux = m.H[l - 1];
+      m.dx[l].args.ld_aux = din;
+    }
+    flops += 2.0 * m.B_total / c.world * din * dout * (l > 0 ? 3.0 : 2.0);
+  }
+  if (small_head) flops += 2.0 * m.B_total / c.world * c.dims[L - 1] * c.dims[L] * 3.0;
+  m.gemm_flops = flops;
+  m.reduce_bytes = (m.n_local + 1.0) * P * 4.0 + P * 4.0 + P * 2.0;
+  LBBSP_CUDA_CHECK(cudaDeviceSynchronize());
+  *out = M.release();
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_mlp_destroy(lbbsp_mlp* m) {
+  delete m;
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_nccl_unique_id(unsigned char h_id[128]) {
+  const NcclApi* api = nccl_api();
+  if (!api) return set_error(LBBSP_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  if (api->GetUniqueId(&id) != ncclSuccess) return set_error(LBBSP_NCCL, "ncclGetUniqueId failed");
+  std::memcpy(h_id, id.internal, 128);
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_mlp_init_comm(lbbsp_mlp* m, const unsigned char h_id[128]) {
+  if (m->cfg.world <= 1) return LBBSP_OK;
+  const NcclApi* api = nccl_api();
+  if (!api) return set_error(LBBSP_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  std::memcpy(id.internal, h_id, 128);
+  ncclResult_t r = api->CommInitRank(&m->comm, m->cfg.world, id, m->cfg.rank);
+  if (r != ncclSuccess) return set_error(LBBSP_NCCL, "ncclCommInitRank: %s", api->GetErrorString(r));
+  return LBBSP_OK;
+}
+
+extern "C" void* lbbsp_mlp_stream(lbbsp_mlp* m) { return m->stream; }
+
+extern "C" int lbbsp_mlp_run(lbbsp_mlp* m, int iterations) {
+  if (m->cfg.world > 1 && !m->comm)
+    return set_error(LBBSP_NCCL, "mlp: world > 1 needs lbbsp_mlp_init_comm first");
+  if (!m->exec) {
+    LBBSP_CUDA_CHECK(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = m->enqueue_iteration(m->stream);
+    cudaError_t e2 = cudaStreamEndCapture(m->stream, &m->graph);
+    if (rc) return rc;
+    LBBSP_CUDA_CHECK(e2);
+    LBBSP_CUDA_CHECK(cudaGraphInstantiate(&m->exec, m->graph, 0));
+  }
+  for (int i = 0; i < iterations; ++i) LBBSP_CUDA_CHECK(cudaGraphLaunch(m->exec, m->stream));
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_mlp_records(lbbsp_mlp* m, int max_rows, int* rows, int* sizes, double* v_pred,
+                                 double* v_obs, int* caps, double* t_worker, double* loss) {
+  LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->stream));
+  int r = 0;
+  LBBSP_CUDA_CHECK(cudaMemcpy(&r, m->D.rows, sizeof(int), cudaMemcpyDeviceToHost));
+  r = std::min(std::min(r, max_rows), m->max_rows);
+  *rows = r;
+  const size_t n = m->n_total;
+  auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    return (dst && bytes) ? cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost) : cudaSuccess;
+  };
+  LBBSP_CUDA_CHECK(cp(sizes, m->D.rec_sizes, sizeof(int) * r * n));
+  LBBSP_CUDA_CHECK(cp(v_pred, m->D.rec_vpred, sizeof(double) * r * n));
+  LBBSP_CUDA_CHECK(cp(v_obs, m->D.rec_vobs, sizeof(double) * r * n));
+  LBBSP_CUDA_CHECK(cp(caps, m->D.rec_caps, sizeof(int) * r * n));
+  LBBSP_CUDA_CHECK(cp(t_worker, m->D.rec_t, sizeof(double) * r * n));
+  LBBSP_CUDA_CHECK(cp(loss, m->D.rec_loss, sizeof(double) * r));
+  lbbsp_dev_status st{};
+  LBBSP_CUDA_CHECK(cudaMemcpy(&st, m->D.status, sizeof st, cudaMemcpyDeviceToHost));
+  if (st.code) return lbbsp_check_status(&st);
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_mlp_params(lbbsp_mlp* m, float* h_params, long long* h_offsets,
+                                long long* n_params) {
+  LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->stream));
+  if (n_params) *n_params = m->P;
+  if (h_offsets)
+    for (int l = 0; l < m->L; ++l) {
+      h_offsets[2 * l] = m->off_w[l];
+      h_offsets[2 * l + 1] = m->off_b[l];
+    }
+  if (h_params) LBBSP_CUDA_CHECK(cudaMemcpy(h_params, m->params, sizeof(float) * m->P, cudaMemcpyDeviceToHost));
+  return LBBSP_OK;
+}
+
+namespace {
+__global__ void to_bf16_kernel(const float* p, __nv_bfloat16* pb, long long n) {
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x) pb[i] = __float2bfloat16_rn(p[i]);
+}
+}  // namespace
+
+extern "C" int lbbsp_mlp_set_params(lbbsp_mlp* m, const float* h_params) {
+  LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->stream));
+  LBBSP_CUDA_CHECK(cudaMemcpy(m->params, h_params, sizeof(float) * m->P, cudaMemcpyHostToDevice));
+  to_bf16_kernel<<<256, 256, 0, m->stream>>>(m->params, m->pb, m->P);
+  LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->stream));
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_mlp_dataset(lbbsp_mlp* m, void* h_x_bf16, int* h_labels) {
+  LBBSP_CUDA_CHECK(cudaDeviceSynchronize());
+  if (h_x_bf16)
+    LBBSP_CUDA_CHECK(cudaMemcpy(h_x_bf16, m->data_x, sizeof(bf16) * m->N_data * m->dims[0], cudaMemcpyDeviceToHost));
+  if (h_labels) LBBSP_CUDA_CHECK(cudaMemcpy(h_labels, m->data_y, sizeof(int) * m->N_data, cudaMemcpyDeviceToHost));
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_mlp_launches_per_iteration(lbbsp_mlp* m, int* launches) {
+  *launches = m->launches;
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_mlp_load_data_async(lbbsp_mlp* m, const void* h_x_bf16, const int* h_labels) {
+  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_x, h_x_bf16, sizeof(bf16) * m->N_data * m->dims[0],
+                                   cudaMemcpyHostToDevice, m->stream));
+  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_y, h_labels, sizeof(int) * m->N_data,
+                                   cudaMemcpyHostToDevice, m->stream));
+  return LBBSP_OK;
+}
+
+namespace {
+__global__ void last_row_kernel(const int* rows, const int* rec_sizes, const double* rec_loss, int n,
+                                int* out_sizes, double* out_loss) {
+  const int r = *rows - 1;
+  if (r < 0) return;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out_sizes[i] = rec_sizes[static_cast<size_t>(r) * n + i];
+  if (threadIdx.x == 0) *out_loss = rec_loss[r];
+}
+}  // namespace
+
+extern "C" int lbbsp_mlp_read_result_async(lbbsp_mlp* m, int* h_sizes, double* h_loss) {
+  if (!m->result) {
+    LBBSP_CUDA_CHECK(m->alloc(&m->result, m->n_total + 2));
+  }
+  int* rs = reinterpret_cast<int*>(m->result);
+  double* rl = m->result + (m->n_total + 1) / 2 + 1;
+  last_row_kernel<<<1, 256, 0, m->stream>>>(m->D.rows, m->D.rec_sizes, m->D.rec_loss, m->n_total, rs, rl);
+  LBBSP_CUDA_CHECK(cudaMemcpyAsync(h_sizes, rs, sizeof(int) * m->n_total, cudaMemcpyDeviceToHost, m->stream));
+  LBBSP_CUDA_CHECK(cudaMemcpyAsync(h_loss, rl, sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_mlp_phase_times(lbbsp_mlp* m, double* h_phase_ns, int* n_phases) {
+  LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->stream));
+  std::vector<unsigned long long> t(2ull * kMaxPhases * m->n_local);
+  LBBSP_CUDA_CHECK(cudaMemcpy(t.data(), m->D.timing, sizeof(unsigned long long) * t.size(),
+                              cudaMemcpyDeviceToHost));
+  *n_phases = m->n_phases;
+  for (int p = 0; p < m->n_phases; ++p) {
+    unsigned long long s = ~0ull, e = 0;
+    for (int i = 0; i < m->n_local; ++i) {
+      s = std::min(s, t[2 * (p * m->n_local + i)]);
+      e = std::max(e, t[2 * (p * m->n_local + i) + 1]);
+    }
+    h_phase_ns[p] = (s != ~0ull && e > s) ? static_cast<double>(e - s) : 0.0;
+  }
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_mlp_work(lbbsp_mlp* m, double* gemm_flops, double* reduce_bytes) {
+  if (gemm_flops) *gemm_flops = m->gemm_flops;
+  if (reduce_bytes) *reduce_bytes = m->reduce_bytes;
+  return LBBSP_OK;
+}

@@ -1,0 +1,96 @@
+"""MLP gradient engine (emulated workers under SM caps) vs the fp64 restatement
+(oracle/mlp_oracle.py) and the allocation replay oracle.
+
+Bars:
+  * batch sizes of every round: BIT-EXACT vs replaying the measured speed
+    stream through the reference predictor + solver (oracle/_ref when built,
+    else the restatement);
+  * parameter update of a round: relative L2 error of the update <= 2e-2
+    (bf16 GEMM operands and activations, fp32 accumulation; fp64 oracle);
+  * full-dataset loss: within 1e-2 relative of the fp64 restatement.
+"""
+import numpy as np
+import pytest
+
+from oracle import mlp_oracle as MO
+from paper_1806_02508_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine(**kw):
+    from paper_1806_02508_b200.mlp import MlpEngine
+    return MlpEngine(**kw)
+
+
+def _checker():
+    from oracle import oracle as O
+    return O.reference() if O.reference_available() else O.restatement()
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("dims,B,n", [([784, 256, 10], 4096, 8), ([512, 512, 512, 256], 1024, 4)])
+def test_one_round_matches_restatement(orc, dims, B, n):
+    """One round vs (a) the bf16-aware restatement (same rounding points:
+    relative L2 error of each update <= 2e-3) and (b) the pure fp64
+    restatement (<= 1e-1: bf16 activations/gradients through up to 3 layers,
+    with cancellation in the batch sums)."""
+    eng = _engine(dims=dims, global_batch=B, n_workers_local=n, predictor="ema",
+                  learning_rate=0.05, max_iterations=4, seed=5)
+    p0 = eng.params()
+    x, y = eng.dataset()
+    eng.run(1)
+    rec = eng.records()
+    sizes = rec["sizes"][0].tolist()
+    assert sizes == [B // n + (i < B % n) for i in range(n)]  # round 0 = equal split
+    stream = orc.sample_stream(5, 0, B, 1000)
+    got = eng.params()
+    exp_q, _ = MO.lbbsp_round_bf16(p0, x, y, stream, sizes, 0.05)
+    exp_f, _ = MO.lbbsp_round(p0, x, y, stream, sizes, 0.05)
+    for l, ((W0, b0), (W1, b1)) in enumerate(zip(p0, got)):
+        dW = W1.astype(np.float64) - W0
+        db = b1.astype(np.float64) - b0
+        assert rel(dW, exp_q[l][0] - W0) < 2e-3, (l, rel(dW, exp_q[l][0] - W0))
+        assert rel(db, exp_q[l][1] - b0) < 2e-3, (l, rel(db, exp_q[l][1] - b0))
+        assert rel(dW, exp_f[l][0] - W0) < 1e-1, (l, rel(dW, exp_f[l][0] - W0))
+    loss_ref = MO.full_loss(got, x, y)
+    assert abs(rec["loss"][0] - loss_ref) <= 1e-2 * loss_ref
+
+
+def test_allocations_bit_exact_vs_replayed_reference(orc):
+    """Measured mode: the device predictor+solver sizes every round; replaying
+    the device's observed (v, c, m) stream through the reference gives the
+    same sizes bit-for-bit (north_star: bit-exact batch allocation)."""
+    from paper_1806_02508_b200.mlp import benchmark_trace
+    n, B, iters = 8, 4096, 120
+    trace = benchmark_trace(n, iters, seed=3)
+    eng = _engine(dims=[784, 256, 10], global_batch=B, n_workers_local=n, predictor="narx",
+                  warmup_iterations=50, max_iterations=iters, trace=trace, seed=1)
+    eng.run(iters)
+    rec = eng.records()
+    assert rec["rows"] == iters
+    assert (rec["sizes"].sum(axis=1) == B).all()
+    chk = _checker()
+    pcfg = abi.PredictorConfig.default(abi.PRED_NARX, warmup_iterations=50)
+    seeds = [chk.mix_seed(1, 0x9ced1c70, i) for i in range(n)]
+    c, m = trace[0][:, :iters].T, trace[1][:, :iters].T
+    sizes, vpred = chk.replay_cpu(pcfg, seeds, B, rec["v_obs"], c, m)
+    assert sizes.tolist() == rec["sizes"].tolist()
+    assert np.array_equal(vpred, rec["v_pred"])
+
+
+def test_lbbsp_balances_stragglers_and_loss_falls():
+    from paper_1806_02508_b200.mlp import constant_trace
+    n, B, iters = 8, 4096, 40
+    avail = [1.0, 1.0, 1.0, 1.0, 0.5, 0.5, 0.25, 0.25]
+    trace = constant_trace(n, iters, avail)
+    eng = _engine(dims=[784, 256, 10], global_batch=B, n_workers_local=n, predictor="ema",
+                  max_iterations=iters, trace=trace, learning_rate=0.1)
+    eng.run(iters)
+    rec = eng.records()
+    last = rec["sizes"][-1]
+    assert last[0] > last[6]            # the fast worker gets more samples
+    assert rec["loss"][-1] < rec["loss"][0]

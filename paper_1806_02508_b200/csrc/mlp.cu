@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -221,6 +222,10 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D) {
       c0 += cap;
     }
     *D.local_rows = r;
+    // the previous round's full-dataset loss (computed beside its observe branch)
+    const int prev = *D.rows - 1;
+    if (prev >= 0 && prev < D.max_rows)
+      D.rec_loss[prev] = D.loss_on ? *D.loss_acc / static_cast<double>(D.N_data) : -1.0;
     *D.loss_acc = 0.0;
   }
   for (int i = tid; i < kMaxPhases * D.n_local; i += blockDim.x) {
@@ -241,7 +246,16 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D) {
 
 // P6: X[r] = data[stream[off + r]], labels, row scale (Eq. 7: 1/B; Eq. 6: 1/(n b_i))
 __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const bf16* data_x,
-                              const int* data_y, int d0, bf16* X, int* y, float* row_scale) {
+                              const int* data_y, int d0, bf16* X, int* y, float* row_scale,
+                              float* slab, long long slab_stride, const long long* reg_off,
+                              const long long* reg_len, int n_reg) {
+  // zero the partial regions accumulated with atomics (biases, small head)
+  for (int sl = 0; sl < D.n_local; ++sl)
+    for (int rg = 0; rg < n_reg; ++rg) {
+      float* p = slab + sl * slab_stride + reg_off[rg];
+      for (long long i = blockIdx.x * 256ll + threadIdx.x; i < reg_len[rg]; i += 256ll * gridDim.x)
+        p[i] = 0.f;
+    }
   const long long k = min(*D.k, static_cast<long long>(D.max_rows - 1));  // capacity-guarded
   const int rows = *D.local_rows, off = *D.stream_off;
   const int* idx = streams + static_cast<size_t>(k) * B_total + off;
@@ -277,30 +291,30 @@ __device__ __forceinline__ void phase_end(unsigned long long* timing, int g) {
 
 // Last layer with a small output (d_out <= 16) on CUDA cores, one warp per
 // row: logits, softmax-CE (warp shuffles), dlogits * row scale, per-worker dW
-// and db partials, dH = dlogits W through ReLU(H).
+// and db partials of this layer, dH = dlogits W through ReLU(H), and the
+// previous layer's bias gradient (column sums of dH) -- fused, so the 256-wide
+// hidden layer needs no separate bias-reduction pass.
 template <int DOUT, int NK>
 __global__ void __launch_bounds__(256) head_small_kernel(
     Groups G, int rows_total, const bf16* __restrict__ H, const float* __restrict__ W,
     const float* __restrict__ bias, const int* __restrict__ y, const float* __restrict__ row_scale,
     bf16* dH, float* slab, long long slab_stride, long long off_w, long long off_b,
-    double* loss_acc, unsigned long long* timing) {
+    long long off_b_prev, double* loss_acc, unsigned long long* timing) {
   constexpr int DH = 32 * NK;
   __shared__ float sW[DOUT][DH];
-  __shared__ float sG[DOUT][DH];
-  __shared__ float sGb[DOUT];
+  __shared__ float sG[DOUT * DH + DOUT + DH];
   int g, cta_in, cta_cnt;
   if (!my_group(G, &g, &cta_in, &cta_cnt)) return;
   phase_begin(timing, g);
-  for (int i = threadIdx.x; i < DOUT * DH; i += blockDim.x) {
-    sW[i / DH][i % DH] = W[i];
-    sG[i / DH][i % DH] = 0.f;
-  }
-  if (threadIdx.x < DOUT) sGb[threadIdx.x] = 0.f;
+  for (int i = threadIdx.x; i < DOUT * DH; i += blockDim.x) sW[i / DH][i % DH] = W[i];
   __syncthreads();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   const int r0 = G.n ? G.r0[g] : 0, r1 = G.n ? G.r1[g] : rows_total;
   float acc[DOUT][NK];
   float accb[DOUT];
+  float accd[NK];
+#pragma unroll
+  for (int t = 0; t < NK; ++t) accd[t] = 0.f;
 #pragma unroll
   for (int c = 0; c < DOUT; ++c) {
     accb[c] = 0.f;
@@ -315,10 +329,10 @@ __global__ void __launch_bounds__(256) head_small_kernel(
     float logit[DOUT];
 #pragma unroll
     for (int c = 0; c < DOUT; ++c) {
-      float s = 0.f;
+      float sacc = 0.f;
 #pragma unroll
-      for (int t = 0; t < NK; ++t) s += h[t] * sW[c][lane + 32 * t];
-      logit[c] = warp_sum(s) + bias[c];
+      for (int t = 0; t < NK; ++t) sacc += h[t] * sW[c][lane + 32 * t];
+      logit[c] = warp_sum(sacc) + bias[c];
     }
     float mx = logit[0];
 #pragma unroll
@@ -349,22 +363,40 @@ __global__ void __launch_bounds__(256) head_small_kernel(
         float d = 0.f;
 #pragma unroll
         for (int c = 0; c < DOUT; ++c) d += dl[c] * sW[c][lane + 32 * t];
-        dH[static_cast<long long>(r) * DH + lane + 32 * t] = __float2bfloat16_rn(h[t] > 0.f ? d : 0.f);
+        const bf16 q = __float2bfloat16_rn(h[t] > 0.f ? d : 0.f);
+        dH[static_cast<long long>(r) * DH + lane + 32 * t] = q;
+        accd[t] += __bfloat162float(q);
       }
     }
   }
   if (loss_acc && lane == 0 && lsum != 0.0) atomicAdd(loss_acc, lsum);
   if (dH) {
+    // deterministic cross-warp reduction (one warp at a time), then one
+    // global atomic per value per CTA into the worker's partial slab
+    for (int w = 0; w < nw; ++w) {
+      if (warp == w) {
 #pragma unroll
-    for (int c = 0; c < DOUT; ++c) {
+        for (int c = 0; c < DOUT; ++c) {
 #pragma unroll
-      for (int t = 0; t < NK; ++t) atomicAdd(&sG[c][lane + 32 * t], acc[c][t]);
-      if (lane == 0) atomicAdd(&sGb[c], accb[c]);
+          for (int t = 0; t < NK; ++t) {
+            float* q = &sG[c * DH + lane + 32 * t];
+            *q = (w == 0 ? 0.f : *q) + acc[c][t];
+          }
+          if (lane == 0) sG[DOUT * DH + c] = (w == 0 ? 0.f : sG[DOUT * DH + c]) + accb[c];
+        }
+#pragma unroll
+        for (int t = 0; t < NK; ++t) {
+          float* q = &sG[DOUT * DH + DOUT + lane + 32 * t];
+          *q = (w == 0 ? 0.f : *q) + accd[t];
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
     float* gs = slab + static_cast<long long>(g) * slab_stride;
-    for (int i = threadIdx.x; i < DOUT * DH; i += blockDim.x) atomicAdd(&gs[off_w + i], sG[i / DH][i % DH]);
-    if (threadIdx.x < DOUT) atomicAdd(&gs[off_b + threadIdx.x], sGb[threadIdx.x]);
+    for (int i = threadIdx.x; i < DOUT * DH; i += blockDim.x) atomicAdd(&gs[off_w + i], sG[i]);
+    if (threadIdx.x < DOUT) atomicAdd(&gs[off_b + threadIdx.x], sG[DOUT * DH + threadIdx.x]);
+    for (int i = threadIdx.x; i < DH; i += blockDim.x)
+      atomicAdd(&gs[off_b_prev + i], sG[DOUT * DH + DOUT + i]);
   }
   __syncthreads();
   phase_end(timing, g);
@@ -518,7 +550,23 @@ __global__ void speed_kernel(PlanDev D, int n_phases) {
 }
 
 // P10: push every worker's (v, c, m) (cluster_sim.cpp:309-313), advance round
-__global__ void observe_kernel(PlanDev D) {
+__global__ void observe_kernel(PlanDev D, int fused_speed_phases) {
+  if (fused_speed_phases > 0) {  // single rank: measured speeds computed here
+    const int i = threadIdx.x;
+    if (i < D.n_local) {
+      double t = 0.0;
+      for (int p = 0; p < fused_speed_phases; ++p) {
+        const unsigned long long s0 = D.timing[2 * (p * D.n_local + i)], e0 = D.timing[2 * (p * D.n_local + i) + 1];
+        if (s0 != ~0ull && e0 > s0) t += static_cast<double>(e0 - s0) * 1e-9;
+      }
+      const int w = D.rank * D.n_local + i;
+      const double b = static_cast<double>(D.sizes_all[w]);
+      D.v_obs_local[i] = t > 0.0 ? b / t : b;
+      const int rw = *D.rows;
+      if (rw < D.max_rows) D.rec_t[static_cast<size_t>(rw) * D.n_total + w] = t;
+    }
+    __syncthreads();
+  }
   const int len = *D.pred.len;
   const int row = *D.rows;
   for (int i = threadIdx.x; i < D.n_total; i += blockDim.x) {
@@ -530,8 +578,6 @@ __global__ void observe_kernel(PlanDev D) {
     *D.pred.len = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
     *D.train_first = *D.pred.cursor;
     *D.pred.cursor = (*D.pred.cursor + (D.n_total + 1) / 2) % D.n_total;
-    if (row < D.max_rows)
-      D.rec_loss[row] = D.loss_on ? *D.loss_acc / static_cast<double>(D.N_data) : -1.0;
     *D.rows = row + 1;
     *D.k += 1;
   }
@@ -556,6 +602,8 @@ struct lbbsp_mlp {
   std::vector<long long> off_w, off_b;
   std::vector<void*> allocs;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   ncclComm_t comm = nullptr;
@@ -582,6 +630,9 @@ struct lbbsp_mlp {
     if (graph) cudaGraphDestroy(graph);
     if (comm && nccl_api()) nccl_api()->CommDestroy(comm);
     if (stream) cudaStreamDestroy(stream);
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     for (void* p : allocs) cudaFree(p);
   }
   template <typename T>
@@ -637,9 +688,8 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   const int sms = D.sm_budget;
   plan_kernel<<<1, 256, 0, s>>>(D);
   ++nl;
-  zero_regions_kernel<<<32, 256, 0, s>>>(partial, P, n_local, reg_off, reg_len, n_reg);
-  ++nl;
-  gather_kernel<<<sms, 256, 0, s>>>(D, streams, B_total, data_x, data_y, dims[0], X, y, row_scale);
+  gather_kernel<<<sms, 256, 0, s>>>(D, streams, B_total, data_x, data_y, dims[0], X, y, row_scale,
+                                     partial, P, reg_off, reg_len, n_reg);
   ++nl;
   // ---- forward (per-worker partitions) ----
   const int Lg = small_head ? L - 1 : L;  // layers on the tensor-core GEMM
@@ -654,7 +704,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     const bf16* Hin = L >= 2 ? H[L - 2] : X;
     head_small_kernel<10, 8><<<sms, 256, 0, s>>>(G, 0, Hin, params + off_w[hl], params + off_b[hl], y,
                                                   row_scale, dZ[L - 2], partial, P, off_w[hl],
-                                                  off_b[hl], nullptr, phase_slot(ph++));
+                                                  off_b[hl], off_b[L - 2], nullptr, phase_slot(ph++));
   } else {
     softmax_ce_kernel<<<sms, 256, 0, s>>>(G, 0, logits, dims[L], y, row_scale, dZ[L - 1], nullptr,
                                           phase_slot(ph++));
@@ -662,8 +712,10 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   ++nl;
   // ---- backward ----
   for (int l = Lg - 1; l >= 0; --l) {
-    bias_grad_kernel<<<sms, 256, 0, s>>>(G, dZ[l], dims[l + 1], partial, P, off_b[l], phase_slot(ph++));
-    ++nl;
+    if (!(small_head && l == L - 2)) {  // the small head already summed this bias gradient
+      bias_grad_kernel<<<sms, 256, 0, s>>>(G, dZ[l], dims[l + 1], partial, P, off_b[l], phase_slot(ph++));
+      ++nl;
+    }
     int rc = launch_grouped(this, dw[l], tc::kKSplit, phase_slot(ph++), s);
     if (rc) return rc;
     ++nl;
@@ -674,6 +726,33 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     }
   }
   n_phases = ph;
+  // Single rank: fork -- the loss branch (apply, full-dataset forward) runs
+  // beside the observe branch (measured speeds, history push, NARX training);
+  // both join before the next round's plan. step_sync computes the loss
+  // (cluster_sim.cpp:445) and trains (:464) independently of each other.
+  const bool fork = cfg.world == 1 && !getenv("LBBSP_NO_FORK");
+  cudaStream_t so = s;
+  if (fork) {
+    LBBSP_CUDA_CHECK(cudaEventRecord(ev_fork, s));
+    LBBSP_CUDA_CHECK(cudaStreamWaitEvent(side, ev_fork, 0));
+    so = side;
+  }
+  // ---- observe branch ----
+  if (cfg.world > 1) {
+    speed_kernel<<<1, 32 * ((n_local + 31) / 32), 0, s>>>(D, n_phases);
+    ++nl;
+    if (nccl_api()->AllGather(D.v_obs_local, D.v_obs_all, static_cast<size_t>(n_local), ncclDouble, comm, s) !=
+        ncclSuccess)
+      return set_error(LBBSP_NCCL, "ncclAllGather failed");
+    observe_kernel<<<1, 256, 0, s>>>(D, 0);
+  } else {
+    observe_kernel<<<1, 256, 0, so>>>(D, n_phases);
+  }
+  ++nl;
+  if (pred.dev.kind == LBBSP_PRED_NARX) {
+    LBBSP_CUDA_CHECK(launch_pred_train_from(pred.dev, D.train_first, so));
+    ++nl;
+  }
   // ---- aggregate + apply ----
   const float lr = static_cast<float>(cfg.learning_rate);
   if (cfg.world > 1) {
@@ -681,7 +760,6 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     ++nl;
     if (nccl_api()->AllReduce(grad, grad, static_cast<size_t>(P), ncclFloat, ncclSum, comm, s) != ncclSuccess)
       return set_error(LBBSP_NCCL, "ncclAllReduce failed");
-    ++nl;
     reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(grad, 1, P, grad, params, pb, lr, 1);
     ++nl;
   } else {
@@ -702,27 +780,16 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
       const bf16* Hin = L >= 2 ? Hd[L - 2] : data_x;
       head_small_kernel<10, 8><<<sms, 256, 0, s>>>(none, N_data, Hin, params + off_w[hl],
                                                     params + off_b[hl], data_y, nullptr, nullptr,
-                                                    nullptr, 0, 0, 0, D.loss_acc, nullptr);
+                                                    nullptr, 0, 0, 0, 0, D.loss_acc, nullptr);
     } else {
       softmax_ce_kernel<<<sms, 256, 0, s>>>(none, N_data, logits_d, dims[L], data_y, nullptr, nullptr,
                                             D.loss_acc, nullptr);
     }
     ++nl;
   }
-  // ---- observe (measured speeds) + NARX training ----
-  speed_kernel<<<1, 32 * ((n_local + 31) / 32), 0, s>>>(D, n_phases);
-  ++nl;
-  if (cfg.world > 1) {
-    if (nccl_api()->AllGather(D.v_obs_local, D.v_obs_all, static_cast<size_t>(n_local), ncclDouble, comm, s) !=
-        ncclSuccess)
-      return set_error(LBBSP_NCCL, "ncclAllGather failed");
-    ++nl;
-  }
-  observe_kernel<<<1, 256, 0, s>>>(D);
-  ++nl;
-  if (pred.dev.kind == LBBSP_PRED_NARX) {
-    LBBSP_CUDA_CHECK(launch_pred_train_from(pred.dev, D.train_first, s));
-    ++nl;
+  if (fork) {
+    LBBSP_CUDA_CHECK(cudaEventRecord(ev_join, side));
+    LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_join, 0));
   }
   LBBSP_CUDA_CHECK(cudaGetLastError());
   launches = nl;
@@ -772,6 +839,9 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   m.small_head = small_head;
   m.max_rows = c.max_iterations > 0 ? c.max_iterations : 1;
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking));
+  LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.side, cudaStreamNonBlocking));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_fork, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_join, cudaEventDisableTiming));
 
   // flat parameter layout, 64-element aligned segments
   auto pad = [](long long x) { return (x + 63) / 64 * 64; };
@@ -927,7 +997,16 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     const bf16* Ain = l == 0 ? m.X : m.H[l - 1];
     const bf16* Ain_d = l == 0 ? m.data_x : m.Hd[l - 1];
     const bool last = (l == L - 1);
-    const int bn = dout >= 256 ? 256 : 128;
+    // wide tiles (BN=256) unless a worker's share of tiles would leave most of
+    // its CTA partition idle (the emulated-worker C2 shapes)
+    const double rows_per_worker = static_cast<double>(m.B_total) / c.world / m.n_local;
+    const int ctas_per_worker = std::max(1, D.sm_budget / m.n_local);
+    auto pick_bn = [&](double mrows, int ncols) {
+      if (ncols < 256) return 128;
+      const double tiles256 = std::ceil(mrows / 128.0) * std::ceil(ncols / 256.0);
+      return tiles256 * 2 < ctas_per_worker ? 128 : 256;
+    };
+    const int bn = pick_bn(rows_per_worker, dout);
     const int epi = last ? tc::kEpiBiasBf16 : tc::kEpiBiasReluBf16;
     int rc = gemm_plan(&m.fwd[l], Ain, m.pb + m.off_w[l], m.B_cap, dout, din, false, false, bn, epi);
     if (rc) return rc;
@@ -940,7 +1019,8 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     m.fwd_d[l].args.ldc = dout;
     m.fwd_d[l].args.bias = m.params + m.off_b[l];
     // dW_l = dZ_l^T A_l : M=dout, N=din, K=rows ; A = dZ_l [rows][dout] MN-major, B = A_l [rows][din] MN-major
-    const int bn_w = din >= 256 ? 256 : 128;
+    const int bn_w = pick_bn(static_cast<double>(dout), din);
+    const int bn_x = pick_bn(rows_per_worker, din);
     rc = gemm_plan(&m.dw[l], m.dZ[l], Ain, dout, din, m.B_cap, true, true, bn_w, tc::kEpiF32);
     if (rc) return rc;
     m.dw[l].args.c_f32 = m.partial + m.off_w[l];
@@ -948,7 +1028,7 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     m.dw[l].args.group_stride = P;
     if (l > 0) {
       // dZ_{l-1} = (dZ_l W_l) * (H_{l-1} > 0): A = dZ_l [rows][dout] K-major, B = W_l [dout][din] = [K][N] MN-major
-      rc = gemm_plan(&m.dx[l], m.dZ[l], m.pb + m.off_w[l], m.B_cap, din, dout, false, true, bn_w,
+      rc = gemm_plan(&m.dx[l], m.dZ[l], m.pb + m.off_w[l], m.B_cap, din, dout, false, true, bn_x,
                      tc::kEpiDReluBf16);
       if (rc) return rc;
       m.dx[l].args.c_bf16 = m.dZ[l - 1];
@@ -1025,6 +1105,11 @@ extern "C" int lbbsp_mlp_records(lbbsp_mlp* m, int max_rows, int* rows, int* siz
   LBBSP_CUDA_CHECK(cp(caps, m->D.rec_caps, sizeof(int) * r * n));
   LBBSP_CUDA_CHECK(cp(t_worker, m->D.rec_t, sizeof(double) * r * n));
   LBBSP_CUDA_CHECK(cp(loss, m->D.rec_loss, sizeof(double) * r));
+  if (loss && r > 0) {  // the newest round's loss is still in the accumulator
+    double acc = 0.0;
+    LBBSP_CUDA_CHECK(cudaMemcpy(&acc, m->D.loss_acc, sizeof(double), cudaMemcpyDeviceToHost));
+    loss[r - 1] = m->D.loss_on ? acc / static_cast<double>(m->N_data) : -1.0;
+  }
   lbbsp_dev_status st{};
   LBBSP_CUDA_CHECK(cudaMemcpy(&st, m->D.status, sizeof st, cudaMemcpyDeviceToHost));
   if (st.code) return lbbsp_check_status(&st);
@@ -1080,12 +1165,12 @@ extern "C" int lbbsp_mlp_load_data_async(lbbsp_mlp* m, const void* h_x_bf16, con
 }
 
 namespace {
-__global__ void last_row_kernel(const int* rows, const int* rec_sizes, const double* rec_loss, int n,
-                                int* out_sizes, double* out_loss) {
+__global__ void last_row_kernel(const int* rows, const int* rec_sizes, const double* loss_acc,
+                                int n_data, int n, int* out_sizes, double* out_loss) {
   const int r = *rows - 1;
   if (r < 0) return;
   for (int i = threadIdx.x; i < n; i += blockDim.x) out_sizes[i] = rec_sizes[static_cast<size_t>(r) * n + i];
-  if (threadIdx.x == 0) *out_loss = rec_loss[r];
+  if (threadIdx.x == 0) *out_loss = *loss_acc / static_cast<double>(n_data);
 }
 }  // namespace
 
@@ -1095,7 +1180,8 @@ extern "C" int lbbsp_mlp_read_result_async(lbbsp_mlp* m, int* h_sizes, double* h
   }
   int* rs = reinterpret_cast<int*>(m->result);
   double* rl = m->result + (m->n_total + 1) / 2 + 1;
-  last_row_kernel<<<1, 256, 0, m->stream>>>(m->D.rows, m->D.rec_sizes, m->D.rec_loss, m->n_total, rs, rl);
+  last_row_kernel<<<1, 256, 0, m->stream>>>(m->D.rows, m->D.rec_sizes, m->D.loss_acc, m->N_data,
+                                            m->n_total, rs, rl);
   LBBSP_CUDA_CHECK(cudaMemcpyAsync(h_sizes, rs, sizeof(int) * m->n_total, cudaMemcpyDeviceToHost, m->stream));
   LBBSP_CUDA_CHECK(cudaMemcpyAsync(h_loss, rl, sizeof(double), cudaMemcpyDeviceToHost, m->stream));
   return LBBSP_OK;

@@ -94,38 +94,72 @@ __host__ __device__ __forceinline__ size_t narx_train_scratch_bytes(int len) {
 }
 
 struct NarxTrainSmem {
-  double w[11], g[11], trial[11], sc[6];
+  double w[11], g[11], gs[11], trial[11], sc[6];
   double val;
-  double current;
   int stall, epochs, stop;
 };
 
-// E[i] = (forward(wt, z_i) - t_i)^2 in parallel, then the reference's
-// left-to-right sum (predictor.cpp:104-107) by thread 0.
-__device__ inline double block_mse(const double* wt, const double* Z, const double* T, double* E,
-                            int cnt, NarxTrainSmem* s) {
+// One evaluation of the training objective at weights wt, fused with the
+// gradient at wt (predictor.cpp:102-134). Per-sample terms are computed in
+// parallel; then, concurrently in two warps, thread 0 folds the squared errors
+// left to right (mse, :104-107) and threads 32..42 fold the 11 gradient
+// accumulators left to right (loss_gradient, :121-132). The gradient is
+// speculative: it is exactly the next epoch's loss_gradient(model) whenever
+// the trial is accepted (same weights, same per-sample operations, same
+// order), and is discarded otherwise.
+__device__ inline double block_eval(const double* wt, const double* Z, const double* T, double* E,
+                                    double* H, double* DY, double* DZ, int cnt, double scale,
+                                    double* gout, NarxTrainSmem* s) {
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-    double z[8];
-    for (int j = 0; j < 8; ++j) z[j] = Z[static_cast<size_t>(j) * cnt + i];
-    const double e = dsub(narx_forward_d(wt, z), T[i]);
+    double a = wt[8];
+    for (int j = 0; j < 8; ++j) a = dadd(a, dmul(wt[j], Z[static_cast<size_t>(j) * cnt + i]));
+    const double h = glibc_tanh(a);
+    const double y = dadd(dmul(wt[9], h), wt[10]);
+    const double e = dsub(y, T[i]);
     E[i] = dmul(e, e);
+    const double dy = dmul(scale, e);
+    H[i] = h;
+    DY[i] = dy;
+    DZ[i] = dmul(dmul(dy, wt[9]), dsub(1.0, dmul(h, h)));
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
     double total = 0.0;
-    for (int i = 0; i < cnt; ++i) total = dadd(total, E[i]);
+    int i = 0;
+    for (; i + 4 <= cnt; i += 4) {
+      const double e0 = E[i], e1 = E[i + 1], e2 = E[i + 2], e3 = E[i + 3];
+      total = dadd(dadd(dadd(dadd(total, e0), e1), e2), e3);
+    }
+    for (; i < cnt; ++i) total = dadd(total, E[i]);
     s->val = ddiv(total, static_cast<double>(cnt));
+  } else if (tid >= 32 && tid < 43) {
+    const int k = tid - 32;
+    double acc = 0.0;
+    if (k < 8) {
+      const double* zj = Z + static_cast<size_t>(k) * cnt;
+      for (int i = 0; i < cnt; ++i) acc = dadd(acc, dmul(DZ[i], zj[i]));
+    } else if (k == 8) {
+      for (int i = 0; i < cnt; ++i) acc = dadd(acc, DZ[i]);
+    } else if (k == 9) {
+      for (int i = 0; i < cnt; ++i) acc = dadd(acc, dmul(DY[i], H[i]));
+    } else {
+      for (int i = 0; i < cnt; ++i) acc = dadd(acc, DY[i]);
+    }
+    gout[k] = acc;
   }
   __syncthreads();
   return s->val;
 }
 
 // narx_train_online (predictor.cpp:155-196) for one model with history
-// (v, c, m)[0..L). buf: 13*(L-2) doubles (shared or global).
+// (v, c, m)[0..L). buf: 13*(L-2) doubles (shared or global). Bit-exact: every
+// value the reference computes is computed with the same operations in the
+// same order; only independent work is overlapped.
 __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, const double* c,
-                                 const double* m, int L, const lbbsp_narx_train_cfg cfg,
-                                 lbbsp_narx_report* rep, double* loss_log, int loss_cap,
-                                 double* buf, NarxTrainSmem* s) {
+                                        const double* m, int L, const lbbsp_narx_train_cfg cfg,
+                                        lbbsp_narx_report* rep, double* loss_log, int loss_cap,
+                                        double* buf, NarxTrainSmem* s) {
   const int tid = threadIdx.x;
   const int minh = cfg.min_history > 3 ? cfg.min_history : 3;
   if (L < minh) {
@@ -178,51 +212,27 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
     T[i] = ddiv(dsub(v[t], mv), sv);
   }
   __syncthreads();
-  double current = block_mse(s->w, Z, T, E, cnt, s);
   const double scale = ddiv(2.0, static_cast<double>(cnt));
+  // current = mse(model) (:165), and loss_gradient(model) of epoch 0
+  double current = block_eval(s->w, Z, T, E, H, DY, DZ, cnt, scale, s->g, s);
   for (int epoch = 0; epoch < cfg.max_epochs; ++epoch) {
-    // loss_gradient (predictor.cpp:118-134): per-sample terms in parallel ...
-    for (int i = tid; i < cnt; i += blockDim.x) {
-      double a = s->w[8];
-      for (int j = 0; j < 8; ++j) a = dadd(a, dmul(s->w[j], Z[static_cast<size_t>(j) * cnt + i]));
-      const double h = glibc_tanh(a);
-      const double y = dadd(dmul(s->w[9], h), s->w[10]);
-      const double dy = dmul(scale, dsub(y, T[i]));
-      H[i] = h;
-      DY[i] = dy;
-      DZ[i] = dmul(dmul(dy, s->w[9]), dsub(1.0, dmul(h, h)));
-    }
-    __syncthreads();
-    // ... and each of the 11 accumulators summed left to right by its own thread
-    if (tid < 11) {
-      double acc = 0.0;
-      if (tid < 8) {
-        const double* zj = Z + static_cast<size_t>(tid) * cnt;
-        for (int i = 0; i < cnt; ++i) acc = dadd(acc, dmul(DZ[i], zj[i]));
-      } else if (tid == 8) {
-        for (int i = 0; i < cnt; ++i) acc = dadd(acc, DZ[i]);
-      } else if (tid == 9) {
-        for (int i = 0; i < cnt; ++i) acc = dadd(acc, dmul(DY[i], H[i]));
-      } else {
-        for (int i = 0; i < cnt; ++i) acc = dadd(acc, DY[i]);
-      }
-      s->g[tid] = acc;
-    }
-    __syncthreads();
     double step = cfg.step;
     if (tid < 11) s->trial[tid] = dsub(s->w[tid], dmul(step, s->g[tid]));  // apply_step :136-143
     __syncthreads();
-    double next = block_mse(s->trial, Z, T, E, cnt, s);
+    double next = block_eval(s->trial, Z, T, E, H, DY, DZ, cnt, scale, s->gs, s);
     int halvings = 0;
     while (next > current && halvings < 20) {
       step = dmul(step, 0.5);
       if (tid < 11) s->trial[tid] = dsub(s->w[tid], dmul(step, s->g[tid]));
       __syncthreads();
-      next = block_mse(s->trial, Z, T, E, cnt, s);
+      next = block_eval(s->trial, Z, T, E, H, DY, DZ, cnt, scale, s->gs, s);
       ++halvings;
     }
     if (next > current) break;  // no descent direction left (:182)
-    if (tid < 11) s->w[tid] = s->trial[tid];
+    if (tid < 11) {
+      s->w[tid] = s->trial[tid];
+      s->g[tid] = s->gs[tid];  // loss_gradient at the accepted weights
+    }
     if (tid == 0) {
       if (loss_log && s->epochs < loss_cap) loss_log[s->epochs] = next;
       s->epochs += 1;

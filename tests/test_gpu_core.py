@@ -265,3 +265,14 @@ def test_bsp_lbbsp_share_parameter_trajectory(lb):
     rl = lb.Simulation(scheme="lb-bsp", **base).run()
     assert (rl.batch != 128).any()
     np.testing.assert_allclose(rb.params, rl.params, rtol=1e-9, atol=1e-9)
+
+
+def test_reference_signature_cpp_shim(lb):
+    """include/lbbsp_b200.hpp (reference signatures + exception types) against
+    the reference's known answers, as a compiled C++ program."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "test_shim")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASS" in r.stdout

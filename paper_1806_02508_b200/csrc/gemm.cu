@@ -76,6 +76,26 @@ static int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs
   return LBBSP_OK;
 }
 
+template <int BN, bool A_MN, bool B_MN, int EPI>
+static int launch_t2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int ctas,
+                     cudaStream_t s) {
+  constexpr int STAGES = BN == 256 ? 6 : 8;
+  constexpr size_t smem = tc::gemm2_smem_bytes<BN, STAGES>();
+  auto kern = tc::gemm_bf16_tc2_kernel<BN, A_MN, B_MN, EPI, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = true;
+  }
+  kern<<<ctas, tc::kGemmThreads, smem, s>>>(ta, tb, a);
+  LBBSP_CUDA_CHECK(cudaGetLastError());
+  return LBBSP_OK;
+}
+
+#define LBBSP_GEMM2_CASE(BN_, AMN, BMN, EPI_)                                          \
+  if (bn == BN_ && a_mn == AMN && b_mn == BMN && epi == EPI_)                          \
+    return launch_t2<BN_, AMN, BMN, EPI_>(p.ta, p.tb, p.args, ctas, s);
+
 #define LBBSP_GEMM_CASE(BN_, AMN, BMN, EPI_)                                           \
   if (bn == BN_ && a_mn == AMN && b_mn == BMN && epi == EPI_)                          \
     return launch_t<BN_, AMN, BMN, EPI_>(p.ta, p.tb, p.args, ctas, s);
@@ -84,6 +104,18 @@ int gemm_launch(const GemmPlan& p, cudaStream_t s) {
   const int bn = p.bn, epi = p.args_epi;
   const bool a_mn = p.a_mn, b_mn = p.b_mn;
   int ctas = p.ctas;
+  if (p.pair) {
+    ctas &= ~1;
+    if (ctas < 2) ctas = 2;
+    LBBSP_GEMM2_CASE(256, false, false, tc::kEpiBiasReluBf16)
+    LBBSP_GEMM2_CASE(256, false, false, tc::kEpiBiasBf16)
+    LBBSP_GEMM2_CASE(256, false, false, tc::kEpiF32)
+    LBBSP_GEMM2_CASE(256, false, true, tc::kEpiDReluBf16)
+    LBBSP_GEMM2_CASE(256, false, true, tc::kEpiF32)
+    LBBSP_GEMM2_CASE(256, true, true, tc::kEpiF32)
+    return set_error(LBBSP_INVALID_ARGUMENT, "gemm: unsupported pair variant bn=%d a_mn=%d b_mn=%d epi=%d",
+                     bn, (int)a_mn, (int)b_mn, epi);
+  }
   // forward / hidden layers
   LBBSP_GEMM_CASE(256, false, false, tc::kEpiBiasReluBf16)
   LBBSP_GEMM_CASE(128, false, false, tc::kEpiBiasReluBf16)
@@ -107,14 +139,17 @@ int gemm_launch(const GemmPlan& p, cudaStream_t s) {
 
 // A: a_mn ? [K][M] : [M][K];  B: b_mn ? [K][N] : [N][K]  (bf16, dense rows)
 int gemm_plan(GemmPlan* p, const void* A, const void* B, int M, int N, int K, bool a_mn, bool b_mn,
-              int bn, int epi) {
+              int bn, int epi, bool pair) {
   p->a_mn = a_mn;
   p->b_mn = b_mn;
   p->bn = bn;
   p->args_epi = epi;
+  p->pair = pair;
   int rc = a_mn ? make_tmap_bf16(&p->ta, A, M, K, M, 64) : make_tmap_bf16(&p->ta, A, K, M, K, 128);
   if (rc) return rc;
-  rc = b_mn ? make_tmap_bf16(&p->tb, B, N, K, N, 64) : make_tmap_bf16(&p->tb, B, K, N, K, bn);
+  // a CTA pair stages bn/2 rows of B per CTA
+  rc = b_mn ? make_tmap_bf16(&p->tb, B, N, K, N, 64)
+            : make_tmap_bf16(&p->tb, B, K, N, K, pair ? bn / 2 : bn);
   if (rc) return rc;
   GemmArgs& a = p->args;
   a = GemmArgs{};
@@ -125,6 +160,10 @@ int gemm_plan(GemmPlan* p, const void* A, const void* B, int M, int N, int K, bo
   a.ldc = N;
   const int tiles = ((M + tc::kBM - 1) / tc::kBM) * ((N + bn - 1) / bn);
   p->ctas = tiles < num_sms() ? tiles : num_sms();
+  if (pair) {  // one 256-row tile per CTA pair
+    const int tiles2 = ((M + 2 * tc::kBM - 1) / (2 * tc::kBM)) * ((N + bn - 1) / bn);
+    p->ctas = 2 * (tiles2 < num_sms() / 2 ? tiles2 : num_sms() / 2);
+  }
   return LBBSP_OK;
 }
 
@@ -139,8 +178,11 @@ extern "C" int lbbsp_gemm_bf16(const void* d_a, const void* d_b, void* d_c, int 
                                const int* d_group_ctan, int ctas, unsigned long long* d_timing,
                                int bn, void* stream) {
   GemmPlan p;
+  // bn < 0 selects the CTA-pair kernel (256 x |bn| tiles, ungrouped problems)
+  const bool pair = bn < 0 && n_groups == 0;
+  if (bn < 0) bn = -bn;
   if (bn != 128 && bn != 256) bn = N > 128 ? 256 : 128;
-  int rc = gemm_plan(&p, d_a, d_b, M, N, K, a_mn != 0, b_mn != 0, bn, epilogue);
+  int rc = gemm_plan(&p, d_a, d_b, M, N, K, a_mn != 0, b_mn != 0, bn, epilogue, pair);
   if (rc) return rc;
   tc::GemmArgs& a = p.args;
   a.mode = mode;
@@ -158,6 +200,6 @@ extern "C" int lbbsp_gemm_bf16(const void* d_a, const void* d_b, void* d_c, int 
   a.bias = d_bias;
   a.aux = static_cast<const __nv_bfloat16*>(d_aux);
   a.ld_aux = N;
-  if (n_groups > 0 || ctas > 0) p.ctas = ctas > 0 ? ctas : num_sms();
+  if (!pair && (n_groups > 0 || ctas > 0)) p.ctas = ctas > 0 ? ctas : num_sms();
   return gemm_launch(p, static_cast<cudaStream_t>(stream));
 }

@@ -533,6 +533,23 @@ __global__ void zero_regions_kernel(float* slab, long long slab_stride, int n_sl
     }
 }
 
+// One worker per GPU: zero rows [rows, roundup64(rows)) of every dZ buffer so
+// the CTA-pair dW GEMM can read whole 64-row K blocks; record the rounded end.
+__global__ void zero_dz_tail_kernel(PlanDev D, bf16** dz, const int* widths, int n_layers,
+                                    int* dz_end, int cap) {
+  const int rows = *D.local_rows;
+  int end = (rows + 63) / 64 * 64;
+  end = end < cap ? end : cap;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *dz_end = end;
+  for (int l = 0; l < n_layers; ++l) {
+    if (!dz[l]) continue;
+    const long long n = static_cast<long long>(end - rows) * widths[l];
+    bf16* p = dz[l] + static_cast<long long>(rows) * widths[l];
+    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x)
+      p[i] = __float2bfloat16_rn(0.f);
+  }
+}
+
 // measured per-worker compute time -> realised speed b_i / t_i
 __global__ void speed_kernel(PlanDev D, int n_phases) {
   const int i = threadIdx.x;
@@ -624,6 +641,10 @@ struct lbbsp_mlp {
   int n_phases = 0;
   double gemm_flops = 0.0, reduce_bytes = 0.0;
   double* result = nullptr;
+  int* dz_end = nullptr;  // [1] local rows rounded up to 64 (one-worker k-split)
+  bool use_pair = false;  // one worker per GPU: CTA-pair GEMMs
+  bf16** dz_ptrs = nullptr;
+  int* dz_widths = nullptr;
 
   ~lbbsp_mlp() {
     if (exec) cudaGraphExecDestroy(exec);
@@ -670,9 +691,14 @@ namespace {
 // grouped GEMM launch helper
 int launch_grouped(lbbsp_mlp* m, GemmPlan& p, int mode, unsigned long long* timing, cudaStream_t s) {
   p.args.mode = mode;
+  if (p.pair && mode == tc::kKSplit) {
+    // k-split over [0, rows) rounded up to the 64-row block (rows past the
+    // worker's end are zero in dZ, see zero_dz_tail_kernel)
+    p.args.g_r1 = m->dz_end;
+  }
   p.args.n_groups = m->n_local;
   p.args.g_r0 = m->D.r0;
-  p.args.g_r1 = m->D.r1;
+  if (!(p.pair && mode == tc::kKSplit)) p.args.g_r1 = m->D.r1;
   p.args.g_cta0 = m->D.cta0;
   p.args.g_ctan = m->D.ctan;
   p.args.timing = timing;
@@ -691,6 +717,10 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   gather_kernel<<<sms, 256, 0, s>>>(D, streams, B_total, data_x, data_y, dims[0], X, y, row_scale,
                                      partial, P, reg_off, reg_len, n_reg);
   ++nl;
+  if (use_pair) {
+    zero_dz_tail_kernel<<<8, 256, 0, s>>>(D, dz_ptrs, dz_widths, L, dz_end, B_cap);
+    ++nl;
+  }
   // ---- forward (per-worker partitions) ----
   const int Lg = small_head ? L - 1 : L;  // layers on the tensor-core GEMM
   for (int l = 0; l < Lg; ++l) {
@@ -769,7 +799,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   // ---- full-dataset loss (step_sync P9, cluster_sim.cpp:445) ----
   if (D.loss_on) {
     for (int l = 0; l < Lg; ++l) {
-      fwd_d[l].ctas = std::min(fwd_d[l].ctas, sms);
+      fwd_d[l].ctas = std::min(fwd_d[l].ctas, sms) & ~1;
       int rc = gemm_launch(fwd_d[l], s);
       if (rc) return rc;
       ++nl;
@@ -985,8 +1015,23 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     D.pred = m.pred.dev;
   }
 
-  // GEMM plans (tensor maps on the fixed buffers)
+  // GEMM plans (tensor maps on the fixed buffers). One worker per GPU with
+  // wide layers runs the CTA-pair kernel (256-row UMMA tiles).
   const int Lg = small_head ? L - 1 : L;
+  m.use_pair = m.n_local == 1 && !small_head && !getenv("LBBSP_NO_PAIR");
+  for (int l = 0; l <= L && m.use_pair; ++l)
+    if (c.dims[l] < 256) m.use_pair = false;
+  if (m.use_pair) {
+    LBBSP_CUDA_CHECK(m.alloc(&m.dz_end, 1));
+    std::vector<bf16*> zp(L, nullptr);
+    std::vector<int> zw(L, 0);
+    for (int l = 0; l < L; ++l) {
+      zp[l] = m.dZ[l];
+      zw[l] = c.dims[l + 1];
+    }
+    LBBSP_CUDA_CHECK(m.upload(&m.dz_ptrs, zp.data(), zp.size()));
+    LBBSP_CUDA_CHECK(m.upload(&m.dz_widths, zw.data(), zw.size()));
+  }
   m.fwd.resize(Lg);
   m.dx.resize(Lg);
   m.dw.resize(Lg);
@@ -1008,12 +1053,15 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     };
     const int bn = pick_bn(rows_per_worker, dout);
     const int epi = last ? tc::kEpiBiasBf16 : tc::kEpiBiasReluBf16;
-    int rc = gemm_plan(&m.fwd[l], Ain, m.pb + m.off_w[l], m.B_cap, dout, din, false, false, bn, epi);
+    const bool pr = m.use_pair;
+    int rc = gemm_plan(&m.fwd[l], Ain, m.pb + m.off_w[l], m.B_cap, dout, din, false, false,
+                       pr ? 256 : bn, epi, pr);
     if (rc) return rc;
     m.fwd[l].args.c_bf16 = last ? m.logits : m.H[l];
     m.fwd[l].args.ldc = dout;
     m.fwd[l].args.bias = m.params + m.off_b[l];
-    rc = gemm_plan(&m.fwd_d[l], Ain_d, m.pb + m.off_w[l], m.N_data, dout, din, false, false, bn, epi);
+    rc = gemm_plan(&m.fwd_d[l], Ain_d, m.pb + m.off_w[l], m.N_data, dout, din, false, false,
+                   pr ? 256 : bn, epi, pr);
     if (rc) return rc;
     m.fwd_d[l].args.c_bf16 = last ? m.logits_d : m.Hd[l];
     m.fwd_d[l].args.ldc = dout;
@@ -1021,15 +1069,16 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     // dW_l = dZ_l^T A_l : M=dout, N=din, K=rows ; A = dZ_l [rows][dout] MN-major, B = A_l [rows][din] MN-major
     const int bn_w = pick_bn(static_cast<double>(dout), din);
     const int bn_x = pick_bn(rows_per_worker, din);
-    rc = gemm_plan(&m.dw[l], m.dZ[l], Ain, dout, din, m.B_cap, true, true, bn_w, tc::kEpiF32);
+    rc = gemm_plan(&m.dw[l], m.dZ[l], Ain, dout, din, m.B_cap, true, true, pr ? 256 : bn_w,
+                   tc::kEpiF32, pr);
     if (rc) return rc;
     m.dw[l].args.c_f32 = m.partial + m.off_w[l];
     m.dw[l].args.ldc = din;
     m.dw[l].args.group_stride = P;
     if (l > 0) {
       // dZ_{l-1} = (dZ_l W_l) * (H_{l-1} > 0): A = dZ_l [rows][dout] K-major, B = W_l [dout][din] = [K][N] MN-major
-      rc = gemm_plan(&m.dx[l], m.dZ[l], m.pb + m.off_w[l], m.B_cap, din, dout, false, true, bn_x,
-                     tc::kEpiDReluBf16);
+      rc = gemm_plan(&m.dx[l], m.dZ[l], m.pb + m.off_w[l], m.B_cap, din, dout, false, true,
+                     pr ? 256 : bn_x, tc::kEpiDReluBf16, pr);
       if (rc) return rc;
       m.dx[l].args.c_bf16 = m.dZ[l - 1];
       m.dx[l].args.ldc = din;

@@ -18,7 +18,7 @@ cases = {
 }
 flop = 2.0 * M * N * K
 for name, fn in cases.items():
-    for bn in (128, 256):
+    for bn in (128, 256, -256):
         for _ in range(3): fn(bn)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(); s.record()

@@ -113,3 +113,27 @@ def test_gemm_ragged_worker_groups():
         refg = dY[a:b].float().t() @ X[a:b].float()
         err = (parts[gi] - refg).abs().max().item()
         assert err <= 1e-3 * max(1.0, refg.abs().max().item()), (gi, err)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (512, 512, 1024), (1000, 784, 320), (2048, 4096, 512)])
+@pytest.mark.parametrize("a_mn,b_mn,epi", [(False, False, 0), (False, True, 0), (True, True, 0),
+                                           (False, False, 1), (False, True, 3)])
+def test_gemm_cta_pair(M, N, K, a_mn, b_mn, epi):
+    """CTA-pair (tcgen05.mma.cta_group::2, 256-row tiles) variant."""
+    import torch
+    A = mk((K, M) if a_mn else (M, K), 11)
+    B = mk((K, N) if b_mn else (N, K), 12)
+    Af = (A.float().t() if a_mn else A.float())
+    Bf = (B.float() if b_mn else B.float().t())
+    ref = Af @ Bf
+    bias = aux = None
+    if epi == 1:
+        bias = torch.linspace(-0.5, 0.5, N, device="cuda")
+        ref = torch.relu(ref + bias)
+    if epi == 3:
+        aux = mk((M, N), 13)
+        ref = ref * (aux.float() > 0)
+    out = run_gemm(A, B, M, N, K, a_mn, b_mn, epi, bias=bias, aux=aux, bn=-256)
+    tol = 1e-3 if epi == 0 else 2 ** -7
+    err = (out.float() - ref).abs().max().item()
+    assert err <= tol * max(1.0, ref.abs().max().item()), err

@@ -32,7 +32,8 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-@pytest.mark.parametrize("dims,B,n", [([784, 256, 10], 4096, 8), ([512, 512, 512, 256], 1024, 4)])
+@pytest.mark.parametrize("dims,B,n", [([784, 256, 10], 4096, 8), ([512, 512, 512, 256], 1024, 4),
+                                    ([512, 512, 512, 256], 1000, 1)])
 def test_one_round_matches_restatement(orc, dims, B, n):
     """One round vs (a) the bf16-aware restatement (same rounding points:
     relative L2 error of each update <= 2e-3) and (b) the pure fp64

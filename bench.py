@@ -179,6 +179,53 @@ class Clocks:
                 "samples": len(rows)}
 
 
+def c3_straggler_demo(steps, warmup):
+    """BASELINE configs[2] shape on one GPU: wide MLP 4x(4096x4096) bf16, two
+    workers, worker 1 capped to half its SMs (a 2x straggler, the 'one
+    injected 2x straggler'), global batch 4096 (2048 per worker nominal).
+    Measures LB-BSP vs BSP vs the no-straggler ideal on compute-bound work,
+    and the tcgen05 GEMM throughput of the worker phases."""
+    import torch
+
+    from paper_1806_02508_b200.mlp import MlpEngine, constant_trace
+
+    dims = [4096] * 5
+    n, B = 2, 4096
+    iters = warmup + steps + 4
+    out = {}
+    for name, scheme, avail in (("lbbsp", "lb-bsp", [1.0, 0.5]), ("bsp", "bsp", [1.0, 0.5]),
+                                ("ideal", "lb-bsp", [1.0, 1.0])):
+        eng = MlpEngine(dims=dims, global_batch=B, n_workers_local=n, scheme=scheme,
+                        predictor="ema", max_iterations=iters, trace=constant_trace(n, iters, avail),
+                        learning_rate=0.01)
+        st = torch.cuda.ExternalStream(eng.stream)
+        eng.run(warmup)
+        torch.cuda.synchronize()
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record(st)
+        eng.run(steps)
+        e.record(st)
+        e.synchronize()
+        ms = s.elapsed_time(e) / steps
+        rec = eng.records()
+        ph = eng.phase_times()
+        flops, _ = eng.work()
+        out[name] = {"ms_per_step": ms, "samples_per_s": B / (ms * 1e-3),
+                     "sizes_last": rec["sizes"][-1].tolist(), "caps_last": rec["caps"][-1].tolist(),
+                     "worker_ms_last": [round(float(t) * 1e3, 4) for t in rec["t_worker"][-1]],
+                     "gemm_tflops_in_worker_phases": flops / (float(rec["t_worker"][-1].max()) * 1e12)}
+        del eng
+    out["lbbsp_over_bsp_speedup"] = out["bsp"]["ms_per_step"] / out["lbbsp"]["ms_per_step"]
+    out["lbbsp_over_ideal_time"] = out["lbbsp"]["ms_per_step"] / out["ideal"]["ms_per_step"]
+    # capacity-aware ideal (SURVEY 8(d)): perfect balance over the SMs left = 1.5x no-straggler
+    cap = (74 + 37) / 148.0
+    out["lbbsp_over_capacity_ideal"] = out["lbbsp"]["ms_per_step"] / (out["ideal"]["ms_per_step"] / cap)
+    out["workload"] = ("C3 shape on 1 GPU: MLP 4096x4 (bf16, fp32 accum), 2 workers (worker 1 = 2x "
+                       "straggler: half its SM share), global batch 4096, EMA predictor")
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -286,6 +333,14 @@ def main():
     ms_ideal, _ = timed(eng_i, args.steps, args.warmup)
     del eng_i
 
+    # ---- C3-shape straggler demonstration (compute-bound) ----
+    c3 = None
+    if world == 1 and not os.environ.get("LBBSP_BENCH_NO_C3"):
+        try:
+            c3 = c3_straggler_demo(steps=min(args.steps, 30), warmup=8)
+        except Exception as ex:  # noqa: BLE001
+            c3 = {"error": str(ex)[:300]}
+
     # ---- roofline of the dominant tensor-core kernel (forward GEMM phase) ----
     peaks = {}
     try:
@@ -333,6 +388,8 @@ def main():
             "clocks": clocks,
             "rounds_recorded": rec["rows"],
         }
+        if c3 is not None:
+            line["c3_straggler_1gpu"] = c3
         if world == 1 and not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline()

@@ -335,6 +335,31 @@ int lbbsp_sim_status(lbbsp_sim* sim, int* done, int* converged);
 int lbbsp_sim_launches_per_iteration(lbbsp_sim* sim, int* launches);
 
 /* ======================================================================== */
+/* C4: NARX at sweep scale -- delay d, hidden H, W models, fp32 CUDA cores   */
+/* ======================================================================== */
+
+/* Generalised NarxModel (predictor.hpp:49-67) with lags d (inputs 3d+2) and H
+ * tanh units; params per model: W1[H][3d+2] | b1[H] | w2[H] | b2 | 6 scalers. */
+int lbbsp_narxg_param_count(int delay, int hidden);
+/* narx_init (predictor.cpp:35-44) generalised, same draw order (host). */
+int lbbsp_narxg_init(uint64_t seed, int delay, int hidden, float* h_params);
+/* narx_train_online (predictor.cpp:155-196) for W models at once, one CTA per
+ * model; histories d_v/d_c/d_m are [W][L]; fixed_epochs > 0 disables the
+ * early stop (throughput mode). d_epochs [W], d_loss [W] outputs;
+ * d_scratch: lbbsp_narx_sweep_scratch_floats(...) floats. */
+int lbbsp_narx_sweep_train(int W, int L, int delay, int hidden, const double* d_v,
+                           const double* d_c, const double* d_m, float* d_params,
+                           const lbbsp_narx_train_cfg* cfg, int fixed_epochs, int* d_epochs,
+                           float* d_loss, float* d_scratch, void* stream);
+long long lbbsp_narx_sweep_scratch_floats(int W, int L, int delay, int hidden);
+/* narx_predict (predictor.cpp:147-153) for W models (histories [W][L], the
+ * current exogenous values c_now/m_now [W]). */
+int lbbsp_narx_sweep_predict(int W, int L, int delay, int hidden, const double* d_v,
+                             const double* d_c, const double* d_m, const double* d_c_now,
+                             const double* d_m_now, const float* d_params, double floor,
+                             double* d_out, void* stream);
+
+/* ======================================================================== */
 /* Gradient engine building block: tcgen05/TMA bf16 GEMM (K7, north_star 1) */
 /* ======================================================================== */
 

@@ -1127,3 +1127,139 @@ int orc_replay_cpu(const lbbsp_predictor_cfg* pc, const uint64_t* seeds, int n, 
   free(W); free(equal); free(vp);
   return st;
 }
+
+/* ---------------------------------------------------------------------- */
+/* Generalised NARX (delay d, hidden h) -- the C4 sweep shape. Restates     */
+/* predictor.cpp:35-196 with the lag structure and width as parameters:     */
+/* inputs {v_{t-1..t-d}, c_{t..t-d}, m_{t..t-d}} (I = 3d+2), h tanh units,   */
+/* one linear output. Parameter layout (double[P], P = h*I + 2h + 1 + 6):    */
+/*   W1[h][I] | b1[h] | w2[h] | b2 | speed_mean, speed_std, cpu_mean,        */
+/*   cpu_std, mem_mean, mem_std.                                             */
+/* At (d, h) = (2, 1) every operation and its order equals the reference,    */
+/* so results are bit-identical (tests/test_oracle.py pins that).            */
+/* ---------------------------------------------------------------------- */
+int orc_narxg_param_count(int d, int h) { return h * (3 * d + 2) + 2 * h + 1 + 6; }
+
+/* narx_init generalised (predictor.cpp:35-44): same draw order */
+void orc_narxg_init(uint64_t seed, int d, int h, double* p) {
+  const int I = 3 * d + 2;
+  mt64 g;
+  mt64_seed(&g, orc_mix_seed2(seed, 0x9a4c0ull));
+  for (int j = 0; j < h * I; ++j) p[j] = rng_uniform2(&g, -0.3, 0.3);
+  for (int j = 0; j < h; ++j) p[h * I + j] = rng_uniform2(&g, -0.1, 0.1);
+  for (int j = 0; j < h; ++j) p[h * I + h + j] = rng_uniform2(&g, -0.3, 0.3);
+  p[h * I + 2 * h] = 0.0;
+  double* sc = p + h * I + 2 * h + 1;
+  sc[0] = 0.0; sc[1] = 1.0; sc[2] = 0.0; sc[3] = 1.0; sc[4] = 0.0; sc[5] = 1.0;
+}
+
+static double narxg_fwd(const double* p, int I, int h, const double* x, double* hid) {
+  double y = 0.0;
+  for (int j = 0; j < h; ++j) {
+    double a = p[h * I + j];                       /* hidden bias */
+    for (int i = 0; i < I; ++i) a += p[j * I + i] * x[i];
+    const double t = tanh(a);
+    if (hid) hid[j] = t;
+    y += p[h * I + h + j] * t;                     /* output weight */
+  }
+  return y + p[h * I + 2 * h];                     /* output bias */
+}
+
+static void narxg_inputs(const double* sc, int d, const double* v, const double* c,
+                         const double* m, int t, double* x) {
+  for (int l = 0; l < d; ++l) x[l] = (v[t - 1 - l] - sc[0]) / sc[1];
+  for (int l = 0; l <= d; ++l) x[d + l] = (c[t - l] - sc[2]) / sc[3];
+  for (int l = 0; l <= d; ++l) x[2 * d + 1 + l] = (m[t - l] - sc[4]) / sc[5];
+}
+
+/* narx_predict generalised (predictor.cpp:147-153); windows most recent first */
+double orc_narxg_predict(const double* p, int d, int h, const double* vlags, const double* cwin,
+                         const double* mwin, double floor_) {
+  const int I = 3 * d + 2;
+  const double* sc = p + h * I + 2 * h + 1;
+  double x[256];
+  for (int l = 0; l < d; ++l) x[l] = (vlags[l] - sc[0]) / sc[1];
+  for (int l = 0; l <= d; ++l) x[d + l] = (cwin[l] - sc[2]) / sc[3];
+  for (int l = 0; l <= d; ++l) x[2 * d + 1 + l] = (mwin[l] - sc[4]) / sc[5];
+  const double out = sc[0] + sc[1] * narxg_fwd(p, I, h, x, NULL);
+  return out > floor_ ? out : floor_;
+}
+
+/* narx_train_online generalised (predictor.cpp:155-196). fixed_epochs > 0
+ * disables the early stop (throughput mode of the C4 sweep). */
+int orc_narxg_train(double* p, int d, int h, const double* v, const double* c, const double* m,
+                    int len, const lbbsp_narx_train_cfg* cfg, int fixed_epochs,
+                    lbbsp_narx_report* rep, double* loss_log, int loss_cap) {
+  const int I = 3 * d + 2, P = h * I + 2 * h + 1;
+  rep->ran = 0; rep->epochs = 0; rep->final_loss = 0.0;
+  const int minh = cfg->min_history > d + 1 ? cfg->min_history : d + 1;
+  if (len < minh) return 0;
+  double* sc = p + P;
+  fit_scaler(v, len, &sc[0], &sc[1]);
+  fit_scaler(c, len, &sc[2], &sc[3]);
+  fit_scaler(m, len, &sc[4], &sc[5]);
+  const int cnt = len - d;
+  double* Z = (double*)malloc(sizeof(double) * (size_t)I * cnt);
+  double* T = (double*)malloc(sizeof(double) * (size_t)cnt);
+  for (int t = d; t < len; ++t) {
+    narxg_inputs(sc, d, v, c, m, t, Z + (size_t)I * (t - d));
+    T[t - d] = (v[t] - sc[0]) / sc[1];
+  }
+  double* w = (double*)malloc(sizeof(double) * P);
+  double* g = (double*)malloc(sizeof(double) * P);
+  double* tr = (double*)malloc(sizeof(double) * P);
+  double* hid = (double*)malloc(sizeof(double) * h);
+  memcpy(w, p, sizeof(double) * P);
+#define NARXG_MSE(wt, out)                                               \
+  do {                                                                   \
+    double tot_ = 0.0;                                                   \
+    for (int i_ = 0; i_ < cnt; ++i_) {                                   \
+      const double e_ = narxg_fwd(wt, I, h, Z + (size_t)I * i_, NULL) - T[i_]; \
+      tot_ += e_ * e_;                                                   \
+    }                                                                    \
+    out = tot_ / (double)cnt;                                            \
+  } while (0)
+  double current;
+  NARXG_MSE(w, current);
+  int stall = 0;
+  rep->ran = 1;
+  const int max_ep = fixed_epochs > 0 ? fixed_epochs : cfg->max_epochs;
+  for (int epoch = 0; epoch < max_ep; ++epoch) {
+    for (int k = 0; k < P; ++k) g[k] = 0.0;
+    const double scale = 2.0 / (double)cnt;
+    for (int i = 0; i < cnt; ++i) {
+      const double* x = Z + (size_t)I * i;
+      const double y = narxg_fwd(w, I, h, x, hid);
+      const double dy = scale * (y - T[i]);
+      for (int j = 0; j < h; ++j) {
+        g[h * I + h + j] += dy * hid[j];                  /* output weight */
+        if (j == 0) g[h * I + 2 * h] += dy;                /* output bias   */
+        const double dz = dy * w[h * I + h + j] * (1.0 - hid[j] * hid[j]);
+        for (int q = 0; q < I; ++q) g[j * I + q] += dz * x[q];
+        g[h * I + j] += dz;                                /* hidden bias   */
+      }
+    }
+    double step = cfg->step, next;
+    for (int k = 0; k < P; ++k) tr[k] = w[k] - step * g[k];
+    NARXG_MSE(tr, next);
+    int halvings = 0;
+    while (next > current && halvings < 20) {
+      step *= 0.5;
+      for (int k = 0; k < P; ++k) tr[k] = w[k] - step * g[k];
+      NARXG_MSE(tr, next);
+      ++halvings;
+    }
+    if (next > current) break;
+    memcpy(w, tr, sizeof(double) * P);
+    if (loss_log && rep->epochs < loss_cap) loss_log[rep->epochs] = next;
+    ++rep->epochs;
+    stall = (current - next < cfg->early_stop_delta) ? stall + 1 : 0;
+    current = next;
+    if (fixed_epochs <= 0 && stall >= cfg->early_stop_patience) break;
+  }
+#undef NARXG_MSE
+  rep->final_loss = current;
+  memcpy(p, w, sizeof(double) * P);
+  free(Z); free(T); free(w); free(g); free(tr); free(hid);
+  return 0;
+}

@@ -217,6 +217,34 @@ class RestatementChecker(CpuChecker):
     def tanh_port(self, x):
         return self.lib.orc_tanh_glibc_fma(float(x))
 
+    # -- generalised NARX (delay d, hidden h), the C4 sweep shape -------------
+    def narxg_param_count(self, d, h):
+        return self.lib.orc_narxg_param_count(C.c_int(d), C.c_int(h))
+
+    def narxg_init(self, seed, d, h):
+        p = np.zeros(self.narxg_param_count(d, h))
+        self.lib.orc_narxg_init(C.c_uint64(seed), C.c_int(d), C.c_int(h), p.ctypes.data_as(_dp))
+        return p
+
+    def narxg_train(self, params, d, h, speed, cpu, mem, cfg, fixed_epochs=0):
+        """mutates params in place; returns (report, loss_log)"""
+        v, vp = _d(speed); c, cp = _d(cpu); m, mp = _d(mem)
+        rep = abi.NarxReport()
+        cap = max(cfg.max_epochs, fixed_epochs, 1)
+        log = np.zeros(cap)
+        assert params.dtype == np.float64 and params.flags.c_contiguous
+        self._check(self.lib.orc_narxg_train(params.ctypes.data_as(_dp), C.c_int(d), C.c_int(h), vp,
+                                             cp, mp, C.c_int(len(v)), C.byref(cfg),
+                                             C.c_int(fixed_epochs), C.byref(rep),
+                                             log.ctypes.data_as(_dp), C.c_int(cap)))
+        return rep, log[:rep.epochs].copy()
+
+    def narxg_predict(self, params, d, h, vlags, cwin, mwin, floor=1e-3):
+        v, vp = _d(vlags); c, cp = _d(cwin); m, mp = _d(mwin)
+        self.lib.orc_narxg_predict.restype = C.c_double
+        return self.lib.orc_narxg_predict(params.ctypes.data_as(_dp), C.c_int(d), C.c_int(h), vp, cp,
+                                          mp, C.c_double(floor))
+
 
 _cache = {}
 

@@ -124,27 +124,45 @@ __device__ inline double block_eval(const double* wt, const double* Z, const dou
   }
   __syncthreads();
   const int tid = threadIdx.x;
+  // left-to-right folds; loads are hoisted 8 at a time so only the dependent
+  // DADD chain is on the critical path (the fold order is unchanged)
   if (tid == 0) {
     double total = 0.0;
     int i = 0;
-    for (; i + 4 <= cnt; i += 4) {
-      const double e0 = E[i], e1 = E[i + 1], e2 = E[i + 2], e3 = E[i + 3];
-      total = dadd(dadd(dadd(dadd(total, e0), e1), e2), e3);
+    for (; i + 8 <= cnt; i += 8) {
+      double e[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) e[q] = E[i + q];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) total = dadd(total, e[q]);
     }
     for (; i < cnt; ++i) total = dadd(total, E[i]);
     s->val = ddiv(total, static_cast<double>(cnt));
   } else if (tid >= 32 && tid < 43) {
     const int k = tid - 32;
+    // term_i = a_i * b_i (or a_i alone), folded left to right
+    const double* a = k < 8 ? DZ : (k == 8 ? DZ : DY);
+    const double* b = k < 8 ? Z + static_cast<size_t>(k) * cnt : (k == 9 ? H : nullptr);
     double acc = 0.0;
-    if (k < 8) {
-      const double* zj = Z + static_cast<size_t>(k) * cnt;
-      for (int i = 0; i < cnt; ++i) acc = dadd(acc, dmul(DZ[i], zj[i]));
-    } else if (k == 8) {
-      for (int i = 0; i < cnt; ++i) acc = dadd(acc, DZ[i]);
-    } else if (k == 9) {
-      for (int i = 0; i < cnt; ++i) acc = dadd(acc, dmul(DY[i], H[i]));
+    int i = 0;
+    if (b) {
+      for (; i + 8 <= cnt; i += 8) {
+        double t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = dmul(a[i + q], b[i + q]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc = dadd(acc, t[q]);
+      }
+      for (; i < cnt; ++i) acc = dadd(acc, dmul(a[i], b[i]));
     } else {
-      for (int i = 0; i < cnt; ++i) acc = dadd(acc, DY[i]);
+      for (; i + 8 <= cnt; i += 8) {
+        double t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = a[i + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc = dadd(acc, t[q]);
+      }
+      for (; i < cnt; ++i) acc = dadd(acc, a[i]);
     }
     gout[k] = acc;
   }

@@ -143,3 +143,25 @@ def test_replay_driver_vs_reference(orc, ref):
         s2, v2 = ref.replay_cpu(p, seeds, 1024, v, c, m)
         assert s1.tolist() == s2.tolist()
         assert bits_equal(v1, v2)
+
+
+def test_generalised_narx_reduces_to_reference_at_delay2_hidden1(orc, golden):
+    """the (delay, hidden) generalisation used for the C4 sweep
+    must reproduce the reference bit-for-bit at (2, 1) before it is trusted."""
+    for case in golden("predictor")["narx_train"]:
+        seed_model = fromhex(case["model_in"])
+        p = np.zeros(orc.narxg_param_count(2, 1))
+        p[:8] = seed_model[:8]
+        p[8], p[9], p[10] = seed_model[8], seed_model[9], seed_model[10]
+        p[11:] = [0.0, 1.0, 0.0, 1.0, 0.0, 1.0]
+        cfg = abi.NarxTrainConfig.default(min_history=case["min_history"])
+        rep, log = orc.narxg_train(p, 2, 1, fromhex(case["v"]), fromhex(case["c"]),
+                                   fromhex(case["m"]), cfg)
+        assert rep.epochs == case["epochs"], case["name"]
+        out = fromhex(case["model_out"])
+        assert bits_equal(p, out), case["name"]
+        assert bits_equal(log, fromhex(case["loss_log"])), case["name"]
+    # narx_init draw order
+    m = orc.narx_init(31)
+    p = orc.narxg_init(31, 2, 1)
+    assert bits_equal(p[:11], m.weights())

@@ -38,6 +38,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=60)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="c2", choices=["c2", "c3"],
+                    help="c2 (default, BASELINE configs[1]) or c3 (configs[2]: 4096x4 MLP, one "
+                         "worker per GPU, one injected 2x straggler)")
     return ap.parse_args()
 
 
@@ -226,10 +229,107 @@ def c3_straggler_demo(steps, warmup):
     return out
 
 
+def main_c3(args):
+    """BASELINE configs[2]: wide MLP 4x(4096x4096) bf16, one worker per GPU,
+    2048 samples per GPU (16384 at 8 GPUs), the last GPU capped to half its
+    SMs (one injected 2x straggler). LB-BSP vs BSP vs no-straggler ideal."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1806_02508_b200.mlp import MlpEngine, constant_trace
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+    dims = [4096] * 5
+    B = 2048 * world
+    iters = args.warmup + args.steps + 8
+    avail = [1.0] * world
+    if world > 1:
+        avail[-1] = 0.5
+
+    def make(scheme, av):
+        eng = MlpEngine(dims=dims, global_batch=B, n_workers_local=1, world=world, rank=rank,
+                        scheme=scheme, predictor="ema", learning_rate=0.01, seed=1,
+                        max_iterations=iters, trace=constant_trace(world, iters, av))
+        if world > 1:
+            uid = [MlpEngine.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            eng.init_comm(uid[0])
+        return eng
+
+    def timed(eng):
+        st = torch.cuda.ExternalStream(eng.stream)
+        eng.run(args.warmup)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record(st)
+        eng.run(args.steps)
+        e.record(st)
+        e.synchronize()
+        ms = s.elapsed_time(e) / args.steps
+        if world > 1:
+            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    out = {}
+    for name, scheme, av in (("lbbsp", "lb-bsp", avail), ("bsp", "bsp", avail),
+                             ("ideal", "lb-bsp", [1.0] * world)):
+        eng = make(scheme, av)
+        ms = timed(eng)
+        rec = eng.records()
+        flops, _ = eng.work()
+        out[name] = {"ms_per_step": ms, "sizes_last": rec["sizes"][-1].tolist(),
+                     "worker_ms_last": [round(float(t) * 1e3, 4) for t in rec["t_worker"][-1]],
+                     "gemm_flops_per_round_this_rank": flops}
+        del eng
+    if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        sust = peaks.get("bf16_tflops_sustained", 1400.0)
+        lb = out["lbbsp"]
+        # GEMM throughput of the fastest (uncapped) worker's phases
+        wt = min(t for t in out["ideal"]["worker_ms_last"] if t > 0) * 1e-3
+        achieved = 2.0 * 2048 * 4096 * 4096 * 11 / wt / 1e12
+        cap = (world - 0.5) / world if world > 1 else 1.0
+        line = {"metric": METRIC, "value": B / (lb["ms_per_step"] * 1e-3), "unit": "samples/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": lb["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": "C3: MLP 4x(4096x4096) bf16, one worker per GPU, 2048 "
+                                       "samples per GPU, last GPU = 2x straggler (half SMs), "
+                                       "LB-BSP + EMA", "global_batch": B,
+                           "parallelism": f"dp{world}"},
+                "bsp": out["bsp"], "ideal_no_straggler": out["ideal"], "lbbsp": lb,
+                "lbbsp_over_bsp_speedup": out["bsp"]["ms_per_step"] / lb["ms_per_step"],
+                "lbbsp_over_capacity_ideal": lb["ms_per_step"] / (out["ideal"]["ms_per_step"] / cap),
+                "roofline": {"bound": "tensor", "kernel": "worker GEMM phases (11 GEMMs, CTA-pair "
+                                                          "tcgen05)",
+                             "achieved": achieved, "peak": sust, "unit": "TFLOP/s",
+                             "frac": achieved / sust, "peak_source": "measured (sustained)",
+                             "traffic": None}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.config == "c3":
+        return main_c3(args)
     import numpy as np
     import torch
     import torch.distributed as dist

@@ -620,7 +620,9 @@ struct lbbsp_mlp {
   std::vector<void*> allocs;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_speed = nullptr, ev_comm = nullptr;
+  cudaEvent_t ev_layer[LBBSP_MLP_MAX_LAYERS] = {};
+  cudaStream_t comm_stream = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   ncclComm_t comm = nullptr;
@@ -654,6 +656,11 @@ struct lbbsp_mlp {
     if (side) cudaStreamDestroy(side);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_speed) cudaEventDestroy(ev_speed);
+    if (ev_comm) cudaEventDestroy(ev_comm);
+    for (auto& e : ev_layer)
+      if (e) cudaEventDestroy(e);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     for (void* p : allocs) cudaFree(p);
   }
   template <typename T>
@@ -741,6 +748,12 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   }
   ++nl;
   // ---- backward ----
+  // One worker per GPU on several GPUs: each layer's gradient segment
+  // (W_l | b_l, contiguous in the flat layout) is all-reduced in place on the
+  // comm stream as soon as its dW/db are final, overlapping the rest of the
+  // backward pass (bucketed allreduce); the speed all-gather follows on the
+  // same stream, so the communicator sees one fixed order on every rank.
+  const bool bucketed = cfg.world > 1 && n_local == 1 && !small_head;
   for (int l = Lg - 1; l >= 0; --l) {
     if (!(small_head && l == L - 2)) {  // the small head already summed this bias gradient
       bias_grad_kernel<<<sms, 256, 0, s>>>(G, dZ[l], dims[l + 1], partial, P, off_b[l], phase_slot(ph++));
@@ -749,6 +762,14 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     int rc = launch_grouped(this, dw[l], tc::kKSplit, phase_slot(ph++), s);
     if (rc) return rc;
     ++nl;
+    if (bucketed) {
+      const long long seg0 = off_w[l], seg1 = l + 1 < L ? off_w[l + 1] : P;
+      LBBSP_CUDA_CHECK(cudaEventRecord(ev_layer[l], s));
+      LBBSP_CUDA_CHECK(cudaStreamWaitEvent(comm_stream, ev_layer[l], 0));
+      if (nccl_api()->AllReduce(partial + seg0, partial + seg0, static_cast<size_t>(seg1 - seg0),
+                                ncclFloat, ncclSum, comm, comm_stream) != ncclSuccess)
+        return set_error(LBBSP_NCCL, "ncclAllReduce (bucket %d) failed", l);
+    }
     if (l > 0) {
       rc = launch_grouped(this, dx[l], tc::kRows, phase_slot(ph++), s);
       if (rc) return rc;
@@ -756,11 +777,35 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     }
   }
   n_phases = ph;
-  // Single rank: fork -- the loss branch (apply, full-dataset forward) runs
-  // beside the observe branch (measured speeds, history push, NARX training);
-  // both join before the next round's plan. step_sync computes the loss
-  // (cluster_sim.cpp:445) and trains (:464) independently of each other.
-  const bool fork = cfg.world == 1 && !getenv("LBBSP_NO_FORK");
+  // measured speeds; on several GPUs all-gathered (after the gradient buckets)
+  const float lr = static_cast<float>(cfg.learning_rate);
+  if (cfg.world > 1) {
+    speed_kernel<<<1, 32 * ((n_local + 31) / 32), 0, s>>>(D, n_phases);
+    ++nl;
+    if (bucketed) {
+      LBBSP_CUDA_CHECK(cudaEventRecord(ev_speed, s));
+      LBBSP_CUDA_CHECK(cudaStreamWaitEvent(comm_stream, ev_speed, 0));
+      if (nccl_api()->AllGather(D.v_obs_local, D.v_obs_all, static_cast<size_t>(n_local), ncclDouble,
+                                comm, comm_stream) != ncclSuccess)
+        return set_error(LBBSP_NCCL, "ncclAllGather failed");
+      LBBSP_CUDA_CHECK(cudaEventRecord(ev_comm, comm_stream));
+      LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_comm, 0));
+    } else {
+      reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 0);
+      ++nl;
+      if (nccl_api()->AllReduce(grad, grad, static_cast<size_t>(P), ncclFloat, ncclSum, comm, s) !=
+          ncclSuccess)
+        return set_error(LBBSP_NCCL, "ncclAllReduce failed");
+      if (nccl_api()->AllGather(D.v_obs_local, D.v_obs_all, static_cast<size_t>(n_local), ncclDouble,
+                                comm, s) != ncclSuccess)
+        return set_error(LBBSP_NCCL, "ncclAllGather failed");
+    }
+  }
+  // Fork -- the loss branch (apply, full-dataset forward) runs beside the
+  // observe branch (history push, NARX training); both join before the next
+  // round's plan. step_sync computes the loss (cluster_sim.cpp:445) and trains
+  // (:464) independently of each other.
+  const bool fork = !getenv("LBBSP_NO_FORK");
   cudaStream_t so = s;
   if (fork) {
     LBBSP_CUDA_CHECK(cudaEventRecord(ev_fork, s));
@@ -768,34 +813,19 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     so = side;
   }
   // ---- observe branch ----
-  if (cfg.world > 1) {
-    speed_kernel<<<1, 32 * ((n_local + 31) / 32), 0, s>>>(D, n_phases);
-    ++nl;
-    if (nccl_api()->AllGather(D.v_obs_local, D.v_obs_all, static_cast<size_t>(n_local), ncclDouble, comm, s) !=
-        ncclSuccess)
-      return set_error(LBBSP_NCCL, "ncclAllGather failed");
-    observe_kernel<<<1, 256, 0, s>>>(D, 0);
-  } else {
-    observe_kernel<<<1, 256, 0, so>>>(D, n_phases);
-  }
+  observe_kernel<<<1, 256, 0, so>>>(D, cfg.world > 1 ? 0 : n_phases);
   ++nl;
   if (pred.dev.kind == LBBSP_PRED_NARX) {
     LBBSP_CUDA_CHECK(launch_pred_train_from(pred.dev, D.train_first, so));
     ++nl;
   }
   // ---- aggregate + apply ----
-  const float lr = static_cast<float>(cfg.learning_rate);
-  if (cfg.world > 1) {
-    reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 0);
-    ++nl;
-    if (nccl_api()->AllReduce(grad, grad, static_cast<size_t>(P), ncclFloat, ncclSum, comm, s) != ncclSuccess)
-      return set_error(LBBSP_NCCL, "ncclAllReduce failed");
+  if (cfg.world > 1 && !bucketed) {
     reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(grad, 1, P, grad, params, pb, lr, 1);
-    ++nl;
   } else {
     reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 1);
-    ++nl;
   }
+  ++nl;
   // ---- full-dataset loss (step_sync P9, cluster_sim.cpp:445) ----
   if (D.loss_on) {
     for (int l = 0; l < Lg; ++l) {
@@ -872,6 +902,10 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.side, cudaStreamNonBlocking));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_fork, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_join, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_speed, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_comm, cudaEventDisableTiming));
+  for (auto& e : m.ev_layer) LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.comm_stream, cudaStreamNonBlocking));
 
   // flat parameter layout, 64-element aligned segments
   auto pad = [](long long x) { return (x + 63) / 64 * 64; };

@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=60)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="c2", choices=["c2", "c3"],
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"],
                     help="c2 (default, BASELINE configs[1]) or c3 (configs[2]: 4096x4 MLP, one "
                          "worker per GPU, one injected 2x straggler)")
     return ap.parse_args()
@@ -324,12 +324,98 @@ def main_c3(args):
     return 0
 
 
+def main_c5(args):
+    """BASELINE configs[4]: time-varying interference trace over the rounds at
+    N GPUs, BSP vs static-proportional vs LB-BSP (+ NARX). Model: the C3 MLP
+    with 2048 samples per GPU (weak scaling), one worker per GPU whose SM
+    availability follows its make_benchmark_series trace (iteration-indexed).
+    Static-proportional = one cpu_allocate from the profiled mean availability,
+    never re-solved (not a reference scheme)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1806_02508_b200 import lbbsp
+    from paper_1806_02508_b200.mlp import MlpEngine, benchmark_trace
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+    dims = [4096] * 5
+    B = 2048 * world
+    rounds = args.steps
+    iters = rounds + 8
+    trace = benchmark_trace(world, iters, seed=TRACE_SEED)
+    mean_avail = np.minimum(1.0, trace[0] * trace[2]).mean(axis=1)
+    static = lbbsp.cpu_allocate(mean_avail.tolist(), B).sizes
+
+    def make(scheme, static_sizes=None, predictor="narx"):
+        eng = MlpEngine(dims=dims, global_batch=B, n_workers_local=1, world=world, rank=rank,
+                        scheme=scheme, predictor=predictor, warmup_iterations=WARMUP_NARX,
+                        learning_rate=0.01, seed=1, max_iterations=iters, trace=trace,
+                        static_sizes=static_sizes)
+        if world > 1:
+            uid = [MlpEngine.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            eng.init_comm(uid[0])
+        return eng
+
+    out = {}
+    for name, kw in (("bsp", dict(scheme="bsp")), ("static_proportional",
+                                                   dict(scheme="lb-bsp", static_sizes=static)),
+                     ("lbbsp_narx", dict(scheme="lb-bsp"))):
+        eng = make(**kw)
+        st = torch.cuda.ExternalStream(eng.stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record(st)
+        eng.run(rounds)
+        e.record(st)
+        e.synchronize()
+        ms = s.elapsed_time(e) / rounds
+        if world > 1:
+            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        rec = eng.records()
+        out[name] = {"ms_per_round": ms, "samples_per_s": B / (ms * 1e-3),
+                     "final_loss": float(rec["loss"][rec["rows"] - 1]),
+                     "sizes_last": rec["sizes"][-1].tolist()}
+        del eng
+    if rank == 0:
+        lb = out["lbbsp_narx"]
+        line = {"metric": METRIC, "value": lb["samples_per_s"], "unit": "samples/s",
+                "n_gpus": world, "steps": rounds, "warmup": 0, "ms_per_step": lb["ms_per_round"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic",
+                "config": {"workload": "C5: MLP 4x(4096x4096) bf16, one worker per GPU, 2048 "
+                                       "samples per GPU, per-GPU time-varying SM availability "
+                                       "(make_benchmark_series seed 3), all rounds timed "
+                                       "including the NARX warm-up", "global_batch": B,
+                           "parallelism": f"dp{world}", "static_sizes": static},
+                "schemes": out,
+                "lbbsp_over_bsp_speedup": out["bsp"]["ms_per_round"] / lb["ms_per_round"],
+                "lbbsp_over_static_speedup": out["static_proportional"]["ms_per_round"] /
+                lb["ms_per_round"]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
     if args.config == "c3":
         return main_c3(args)
+    if args.config == "c5":
+        return main_c5(args)
     import numpy as np
     import torch
     import torch.distributed as dist

@@ -37,6 +37,7 @@ extern "C" {
 #define LBBSP_LOGIC (-4)            /* std::logic_error      */
 #define LBBSP_CUDA (-5)
 #define LBBSP_NCCL (-6)
+#define LBBSP_CONFIG (-7)           /* lbbsp::ConfigError (scenario.hpp:13-15), a runtime_error */
 
 const char* lbbsp_last_error(void);
 int lbbsp_version(void);
@@ -242,7 +243,8 @@ enum { LBBSP_SCHEME_BSP = 0, LBBSP_SCHEME_ASP = 1, LBBSP_SCHEME_SSP = 2, LBBSP_S
 enum {
   LBBSP_DYN_STATIC = 0,
   LBBSP_DYN_STRAGGLER = 1,
-  LBBSP_DYN_BENCHMARK = 2
+  LBBSP_DYN_BENCHMARK = 2,
+  LBBSP_DYN_TRACE = 3     /* recorded resource traces (cluster_sim.cpp:110-115) */
 };
 enum {
   LBBSP_PRESET_NONE = -1,
@@ -298,6 +300,17 @@ typedef struct {
   int convergence_consecutive;
   int64_t max_updates;
   uint64_t seed;
+  /* DynamicsKind::Trace (cluster_sim.cpp:110-115): worker i follows the
+   * step-interpolated trace (trace_at, trace.cpp:137-143) made of points
+   * [trace_offsets[i], trace_offsets[i+1]) of the three arrays, looked up at
+   * the simulated clock (the sum of the previous rounds' walls). */
+  const int* trace_offsets;   /* [n+1] */
+  const double* trace_t;
+  const double* trace_cpu;
+  const double* trace_mem;
+  /* PredictorConfig::initial_weights (predictor.cpp:264-269): NULL or "" =>
+   * narx_init(mix_seed(seed, 0x9ced1c70, i)); else load_narx_csv(path) */
+  const char* narx_weights_path;
 } lbbsp_sim_cfg;
 
 /* IterationRecord (cluster_sim.hpp:149-155) + WorkerIterationStats (:139-147),
@@ -333,6 +346,134 @@ int lbbsp_sim_records(lbbsp_sim* sim, int max_rows, int* rows, lbbsp_iter_scalar
 int lbbsp_sim_status(lbbsp_sim* sim, int* done, int* converged);
 /* Number of CUDA kernels one iteration launches (captured graph nodes). */
 int lbbsp_sim_launches_per_iteration(lbbsp_sim* sim, int* launches);
+
+/* ======================================================================== */
+/* Records, metrics and exporters                      */
+/* ======================================================================== */
+
+/* A host view of a record stream: [rows] scalars, [rows*n] per-worker rows. */
+typedef struct {
+  int rows;
+  int n;
+  const lbbsp_iter_scalars* scalars;
+  const int* batch;
+  const double* tp;
+  const double* tm;
+  const double* wait;
+  const double* v_pred;
+  const double* v_actual;
+} lbbsp_records_view;
+
+/* Metrics (cluster_sim.hpp:157-163) */
+typedef struct {
+  int64_t updates_to_convergence;
+  double mean_per_update_time;
+  double wastage;
+  double predictor_rmse;
+  int converged;
+} lbbsp_metrics;
+
+/* compute_metrics (cluster_sim.cpp:217-245). round9 != 0 first rounds every
+ * real to 9 significant digits as the exporter does (round_records,
+ * scenario.cpp:66-88), giving the metrics.json numbers. Host. */
+int lbbsp_compute_metrics(const lbbsp_records_view* rec, int converged, int rmse_from_iteration,
+                          int round9, lbbsp_metrics* out);
+/* Simulation::run's metrics (cluster_sim.cpp:638) computed on device from the
+ * device-resident records: per-row terms in parallel, the reference's
+ * sequential folds by one thread. */
+int lbbsp_sim_metrics(lbbsp_sim* sim, int rmse_from_iteration, lbbsp_metrics* out);
+/* write_records_csv (scenario.cpp:306-342): byte-identical records.csv. */
+int lbbsp_write_records_csv(const lbbsp_records_view* rec, const char* path);
+/* write_metrics_json (scenario.cpp:344-358): byte-identical metrics.json. */
+int lbbsp_write_metrics_json(const lbbsp_metrics* m, double convergence_loss,
+                             int convergence_consecutive, int warmup_iterations, const char* path);
+
+/* ======================================================================== */
+/* Recorded resource traces (trace.hpp:11-38)           */
+/* ======================================================================== */
+
+typedef struct lbbsp_traces lbbsp_traces;
+
+/* parse_trace (trace.cpp:54-97): machine_id,t_offset_s,cpu_avail,mem_avail. */
+int lbbsp_trace_parse(const char* path, lbbsp_traces** out);
+/* In-memory traces: trace i = points [offsets[i], offsets[i+1]). */
+int lbbsp_trace_create(int n_traces, const char* const* machine_ids, const int* offsets,
+                       const double* t, const double* cpu, const double* mem,
+                       lbbsp_traces** out);
+int lbbsp_trace_destroy(lbbsp_traces* tr);
+int lbbsp_trace_count(const lbbsp_traces* tr, int* n_traces);
+/* machine id (valid until destroy), point count, ResourceTrace::mean_cpu */
+int lbbsp_trace_info(const lbbsp_traces* tr, int i, const char** machine_id, int* points,
+                     double* mean_cpu);
+int lbbsp_trace_points(const lbbsp_traces* tr, int i, double* t, double* cpu, double* mem);
+/* write_trace (trace.cpp:99-107) */
+int lbbsp_trace_write(const lbbsp_traces* tr, const char* path);
+/* map_traces (trace.cpp:109-135): one trace index per worker. */
+int lbbsp_trace_map(const lbbsp_traces* tr, int workers, uint64_t seed, int* assignment);
+/* trace_at (trace.cpp:137-143) */
+int lbbsp_trace_at(const lbbsp_traces* tr, int i, double time_s, double* cpu, double* mem);
+
+/* load_narx_csv / save_narx_csv (predictor.cpp:198-243) */
+int lbbsp_narx_load_csv(const char* path, lbbsp_narx_model* out);
+int lbbsp_narx_save_csv(const lbbsp_narx_model* m, const char* path);
+
+/* ======================================================================== */
+/* Scenario JSON and the CLI entry points (scenario.hpp:13-91, 8(f) rank 3) */
+/* ======================================================================== */
+
+typedef struct lbbsp_scenario lbbsp_scenario;
+
+/* ScenarioConfig scalars (scenario.hpp:33-64) */
+typedef struct {
+  char name[256];           /* config file stem */
+  int scheme;               /* LBBSP_SCHEME_* */
+  int staleness_threshold;
+  int workers;
+  int total_budget;
+  int predictor;            /* LBBSP_PRED_* */
+  double alpha;
+  int warmup_iterations;
+  double speed_floor;
+  double base_speed;
+  double base_comm_s;
+  double learning_rate;
+  double convergence_loss;
+  int convergence_consecutive;
+  int64_t max_iterations;
+  uint64_t seed;
+  int paired_sim;
+} lbbsp_scenario_info;
+
+/* load_scenario + validate_scenario (scenario.cpp:92-217): strict keys,
+ * reference ConfigError wording (LBBSP_CONFIG). */
+int lbbsp_scenario_load(const char* path, lbbsp_scenario** out);
+int lbbsp_scenario_destroy(lbbsp_scenario* s);
+/* the CLI's --seed override (cfg.seed = seed before build_sim_config) */
+int lbbsp_scenario_set_seed(lbbsp_scenario* s, uint64_t seed);
+int lbbsp_scenario_get_info(const lbbsp_scenario* s, lbbsp_scenario_info* info);
+/* build_sim_config (scenario.cpp:219-294): presets, traces (parse_trace +
+ * map_traces), GPU groups and the bandwidth drop resolved into a
+ * lbbsp_sim_cfg whose arrays the scenario owns (valid until destroy or the
+ * next set_seed). ASP/SSP scenarios are rejected (out of scope). */
+int lbbsp_scenario_sim_cfg(lbbsp_scenario* s, const lbbsp_sim_cfg** cfg);
+
+/* predictor_series_rmse (cluster_sim.cpp:645-672) on device: one predictor
+ * replayed over a benchmark series (h_cpu/h_mem/h_mult [len]), predicting
+ * then observing then training every step, one CTA. */
+int lbbsp_predictor_series_rmse(int kind, const lbbsp_predictor_cfg* base, const double* h_cpu,
+                                const double* h_mem, const double* h_mult, int len,
+                                double base_speed, uint64_t seed, int measure_from,
+                                double* rmse);
+
+/* cmd_run / cmd_compare / cmd_predict_bench (scenario.cpp:369-481) with every
+ * simulation executed by the device driver. Return the CLI exit status
+ * (0 ok, 1 error; the error is printed to stderr as "lbbsp run: <what>" and
+ * kept in lbbsp_last_error()). has_seed selects the --seed override. */
+int lbbsp_cmd_run(const char* config, const char* out_dir, int has_seed, uint64_t seed);
+int lbbsp_cmd_compare(const char* const* configs, int n_configs, const char* out_dir,
+                      int has_seed, uint64_t seed);
+int lbbsp_cmd_predict_bench(const char* config, const char* out_dir, int has_seed,
+                            uint64_t seed);
 
 /* ======================================================================== */
 /* C4: NARX at sweep scale -- delay d, hidden H, W models, fp32 CUDA cores   */

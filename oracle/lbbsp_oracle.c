@@ -725,10 +725,58 @@ typedef struct {
   double* phase;                   /* [n] */
   int bench_len;
   double *bcpu, *bmem, *bmult;     /* [n*bench_len] */
+  const int* trace_off;            /* [n+1] (Trace) */
+  const double *trace_t, *trace_c, *trace_m;
 } dynamics;
 
+/* load_narx_csv, predictor.cpp:215-243: "name,value" rows, any order. */
+int orc_narx_load_csv(const char* path, lbbsp_narx_model* out) {
+  static const char* names[17] = {"input_weight_0", "input_weight_1", "input_weight_2",
+                                  "input_weight_3", "input_weight_4", "input_weight_5",
+                                  "input_weight_6", "input_weight_7", "hidden_bias",
+                                  "output_weight",  "output_bias",    "speed_mean",
+                                  "speed_stddev",   "cpu_mean",       "cpu_stddev",
+                                  "mem_mean",       "mem_stddev"};
+  double vals[17];
+  int have[17] = {0};
+  FILE* f = fopen(path, "r");
+  if (!f) return err(LBBSP_RUNTIME, "load_narx_csv: cannot open %s", path);
+  char line[512];
+  while (fgets(line, sizeof line, f)) {
+    size_t L = strlen(line);
+    if (L && line[L - 1] == '\n') line[--L] = 0;
+    if (!L) continue;
+    char* comma = strchr(line, ',');
+    if (!comma) {
+      fclose(f);
+      return err(LBBSP_RUNTIME, "load_narx_csv: malformed row '%s'", line);
+    }
+    *comma = 0;
+    for (int j = 0; j < 17; ++j)
+      if (!strcmp(line, names[j])) {
+        vals[j] = strtod(comma + 1, NULL);
+        have[j] = 1;
+      }
+  }
+  fclose(f);
+  for (int j = 0; j < 17; ++j)
+    if (!have[j]) return err(LBBSP_RUNTIME, "load_narx_csv: missing parameter '%s'", names[j]);
+  for (int j = 0; j < 8; ++j) out->input_weights[j] = vals[j];
+  out->hidden_bias = vals[8];
+  out->output_weight = vals[9];
+  out->output_bias = vals[10];
+  out->speed_mean = vals[11];
+  out->speed_stddev = vals[12];
+  out->cpu_mean = vals[13];
+  out->cpu_stddev = vals[14];
+  out->mem_mean = vals[15];
+  out->mem_stddev = vals[16];
+  return LBBSP_OK;
+}
+
 /* Dynamics::at, cluster_sim.cpp:77-118 -> (cpu, mem, mult) */
-static void dyn_at(const dynamics* D, int w, int64_t k, double* c, double* m, double* mult) {
+static void dyn_at(const dynamics* D, int w, int64_t k, double now, double* c, double* m,
+                   double* mult) {
   *c = 1.0;
   *m = 1.0;
   *mult = 1.0;
@@ -755,6 +803,16 @@ static void dyn_at(const dynamics* D, int w, int64_t k, double* c, double* m, do
       *c = D->bcpu[(size_t)w * D->bench_len + idx];
       *m = D->bmem[(size_t)w * D->bench_len + idx];
       *mult = D->bmult[(size_t)w * D->bench_len + idx];
+      return;
+    }
+    case LBBSP_DYN_TRACE: { /* trace_at, trace.cpp:137-143: latest point at or before now */
+      const int lo = D->trace_off[w], hi = D->trace_off[w + 1];
+      int p = lo;
+      for (int q = lo; q < hi; ++q)
+        if (D->trace_t[q] <= now) p = q;
+        else break;
+      *c = D->trace_c[p];
+      *m = D->trace_m[p];
       return;
     }
   }
@@ -905,6 +963,10 @@ int orc_sim_run(const lbbsp_sim_cfg* c, int max_rows, int* rows, lbbsp_iter_scal
     D.static_cpu = (double*)c->static_cpu;
     D.static_mem = (double*)c->static_mem;
     D.strag = (lbbsp_straggler*)c->stragglers;
+    D.trace_off = c->trace_offsets;
+    D.trace_t = c->trace_t;
+    D.trace_c = c->trace_cpu;
+    D.trace_m = c->trace_mem;
   }
   D.phase = (double*)malloc(sizeof(double) * (size_t)n); /* Dynamics ctor, cluster_sim.cpp:66-75 */
   for (int i = 0; i < n; ++i) {
@@ -925,13 +987,26 @@ int orc_sim_run(const lbbsp_sim_cfg* c, int max_rows, int* rows, lbbsp_iter_scal
   }
 
   const int64_t cap = c->max_updates > 0 ? c->max_updates : 1;
+  lbbsp_narx_model initial; /* PredictorConfig::initial_weights (predictor.cpp:265-266) */
+  const int have_initial = c->narx_weights_path && c->narx_weights_path[0];
+  if (have_initial) {
+    st = orc_narx_load_csv(c->narx_weights_path, &initial);
+    if (st) {
+      free(equal); free(feat); free(lab); free(params);
+      free(D.phase); free(D.bcpu); free(D.bmem); free(D.bmult); free(pre_cpu); free(pre_strag);
+      return st;
+    }
+  }
   worker_rt* W = (worker_rt*)calloc((size_t)n, sizeof(worker_rt));
   for (int i = 0; i < n; ++i) {
     W[i].v = (double*)malloc(sizeof(double) * (size_t)cap);
     W[i].c = (double*)malloc(sizeof(double) * (size_t)cap);
     W[i].m = (double*)malloc(sizeof(double) * (size_t)cap);
     W[i].comm = (double*)malloc(sizeof(double) * (size_t)cap);
-    orc_narx_init(orc_mix_seed3(c->seed, 0x9ced1c70ull, (uint64_t)i), &W[i].model);
+    if (have_initial)
+      W[i].model = initial;
+    else
+      orc_narx_init(orc_mix_seed3(c->seed, 0x9ced1c70ull, (uint64_t)i), &W[i].model);
   }
   double *rc = malloc(sizeof(double) * n), *rm = malloc(sizeof(double) * n), *rmult = malloc(sizeof(double) * n);
   double *vact = malloc(sizeof(double) * n), *vpred = malloc(sizeof(double) * n);
@@ -941,11 +1016,12 @@ int orc_sim_run(const lbbsp_sim_cfg* c, int max_rows, int* rows, lbbsp_iter_scal
   double* grads = malloc(sizeof(double) * (size_t)n * d);
   double* agg = malloc(sizeof(double) * (size_t)d);
   int below = 0, converged = 0, count = 0, cursor = 0;
+  double now = 0.0; /* Simulation::now_ */
 
   for (int64_t k = 0;; ++k) {
     /* P1-P3 (:355-367) */
     for (int i = 0; i < n; ++i) {
-      dyn_at(&D, i, k, &rc[i], &rm[i], &rmult[i]);
+      dyn_at(&D, i, k, now, &rc[i], &rm[i], &rmult[i]);
       vact[i] = 0.0;
       vpred[i] = 0.0;
       if (!gpu_mode) {
@@ -1056,6 +1132,7 @@ int orc_sim_run(const lbbsp_sim_cfg* c, int max_rows, int* rows, lbbsp_iter_scal
       for (int j = 0; j < bud; ++j) predictor_train(&c->predictor, &W[(cursor + j) % n]);
       cursor = (cursor + bud) % n;
     }
+    now += wall; /* :466 */
     /* check_stop (:326-334) */
     below = lossv < c->convergence_loss ? below + 1 : 0;
     if (below >= c->convergence_consecutive) {

@@ -199,6 +199,56 @@ class CpuChecker:
         return sizes, vpred
 
 
+    # -- scenario / CLI (reference build only: scenario.cpp, trace.cpp) -----------
+    def cmd_run(self, config, out_dir, seed=None):
+        f = self._fn("cmd_run")
+        f.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_uint64]
+        return f(str(config).encode(), str(out_dir).encode(), int(seed is not None),
+                 int(seed or 0))
+
+    def cmd_compare(self, configs, out_dir, seed=None):
+        f = self._fn("cmd_compare")
+        f.argtypes = [C.POINTER(C.c_char_p), C.c_int, C.c_char_p, C.c_int, C.c_uint64]
+        arr = (C.c_char_p * len(configs))(*[str(c).encode() for c in configs])
+        return f(arr, len(configs), str(out_dir).encode(), int(seed is not None), int(seed or 0))
+
+    def cmd_predict_bench(self, config, out_dir, seed=None):
+        f = self._fn("cmd_predict_bench")
+        f.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_uint64]
+        return f(str(config).encode(), str(out_dir).encode(), int(seed is not None),
+                 int(seed or 0))
+
+    def scenario_error(self, config):
+        """load_scenario's exception text, or None when the file loads."""
+        f = self._fn("scenario_check")
+        f.argtypes = [C.c_char_p]
+        return None if f(str(config).encode()) == 0 else self._err().decode()
+
+    def trace_map(self, path, workers, seed):
+        f = self._fn("trace_map")
+        f.argtypes = [C.c_char_p, C.c_int, C.c_uint64, _ip, _ip]
+        out = np.zeros(workers, np.int32)
+        nt = C.c_int()
+        self._check(f(str(path).encode(), workers, seed, out.ctypes.data_as(_ip), C.byref(nt)))
+        return out.tolist()
+
+    def trace_at(self, path, i, t):
+        f = self._fn("trace_at")
+        f.argtypes = [C.c_char_p, C.c_int, C.c_double, _dp, _dp]
+        c, m = C.c_double(), C.c_double()
+        self._check(f(str(path).encode(), i, t, C.byref(c), C.byref(m)))
+        return c.value, m.value
+
+    def series_rmse(self, kind, base, cpu, mem, mult, base_speed, seed, measure_from):
+        f = self._fn("series_rmse")
+        c, cp = _d(cpu); m, mp = _d(mem); x, xp = _d(mult)
+        out = C.c_double()
+        self._check(f(C.c_int(kind), C.byref(base), cp, mp, xp, C.c_int(len(c)),
+                      C.c_double(base_speed), C.c_uint64(seed), C.c_int(measure_from),
+                      C.byref(out)))
+        return out.value
+
+
 class RestatementChecker(CpuChecker):
     def __init__(self):
         super().__init__(RESTATEMENT_SO, "orc_")

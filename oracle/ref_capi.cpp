@@ -7,6 +7,8 @@
 // reference API; nothing here re-implements reference arithmetic.
 #include <cstdio>
 #include <cstring>
+#include <filesystem>
+#include <optional>
 #include <exception>
 #include <stdexcept>
 #include <string>
@@ -17,7 +19,9 @@
 #include "lbbsp/coordination.hpp"
 #include "lbbsp/predictor.hpp"
 #include "lbbsp/rng.hpp"
+#include "lbbsp/scenario.hpp"
 #include "lbbsp/sgd.hpp"
+#include "lbbsp/trace.hpp"
 #include "lbbsp_c.h"
 
 using namespace lbbsp;
@@ -137,6 +141,14 @@ SimConfig to_sim(const lbbsp_sim_cfg& c) {
         cfg.dynamics.stragglers.push_back(
             StragglerSpec{s.on_probability, s.cpu_consumed, s.mem_consumed, s.period});
       }
+    if (c.dynamics == LBBSP_DYN_TRACE)
+      for (int i = 0; i < n; ++i) {
+        ResourceTrace t;
+        t.machine_id = std::to_string(i);
+        for (int q = c.trace_offsets[i]; q < c.trace_offsets[i + 1]; ++q)
+          t.points.push_back(TracePoint{c.trace_t[q], c.trace_cpu[q], c.trace_mem[q]});
+        cfg.dynamics.traces.push_back(t);
+      }
     if (c.dynamics == LBBSP_DYN_BENCHMARK) {
       auto& b = cfg.dynamics.benchmark;
       b.iterations = c.bench_iterations;
@@ -150,6 +162,7 @@ SimConfig to_sim(const lbbsp_sim_cfg& c) {
     }
   }
   cfg.predictor = to_pred(c.predictor);
+  if (c.narx_weights_path) cfg.predictor.initial_weights = c.narx_weights_path;
   cfg.learning_rate = c.learning_rate;
   cfg.dataset_seed = c.dataset_seed;
   cfg.dataset_size = c.dataset_size;
@@ -442,6 +455,66 @@ int ref_replay_cpu(const lbbsp_predictor_cfg* pcfg, const uint64_t* seeds, int n
         cursor = (cursor + b) % n;
       }
     }
+  })
+}
+
+
+// ---- scenario / exporters / traces (scenario.cpp, trace.cpp) --------------
+int ref_cmd_run(const char* config, const char* out_dir, int has_seed, uint64_t seed) {
+  std::optional<std::uint64_t> s;
+  if (has_seed) s = seed;
+  return cmd_run(config, out_dir, s);
+}
+
+int ref_cmd_compare(const char* const* configs, int n, const char* out_dir, int has_seed,
+                    uint64_t seed) {
+  std::optional<std::uint64_t> s;
+  if (has_seed) s = seed;
+  std::vector<std::filesystem::path> paths(configs, configs + n);
+  return cmd_compare(paths, out_dir, s);
+}
+
+int ref_cmd_predict_bench(const char* config, const char* out_dir, int has_seed, uint64_t seed) {
+  std::optional<std::uint64_t> s;
+  if (has_seed) s = seed;
+  return cmd_predict_bench(config, out_dir, s);
+}
+
+// load_scenario's error text (ConfigError is a runtime_error -> LBBSP_RUNTIME here)
+int ref_scenario_check(const char* path) { REF_GUARD({ (void)load_scenario(path); }) }
+
+int ref_trace_map(const char* path, int workers, uint64_t seed, int* out, int* n_traces) {
+  REF_GUARD({
+    const auto traces = parse_trace(path);
+    const auto a = map_traces(traces, workers, seed);
+    for (int i = 0; i < workers; ++i) out[i] = static_cast<int>(a[static_cast<std::size_t>(i)]);
+    *n_traces = static_cast<int>(traces.size());
+  })
+}
+
+int ref_trace_at(const char* path, int i, double time_s, double* c, double* m) {
+  REF_GUARD({
+    const auto traces = parse_trace(path);
+    const auto v = trace_at(traces.at(static_cast<std::size_t>(i)), time_s);
+    *c = v.first;
+    *m = v.second;
+  })
+}
+
+int ref_series_rmse(int kind, const lbbsp_predictor_cfg* base, const double* cpu,
+                    const double* mem, const double* mult, int len, double base_speed,
+                    uint64_t seed, int measure_from, double* out) {
+  REF_GUARD({
+    SyntheticSeries series;
+    for (int k = 0; k < len; ++k) {
+      ResourceState rs;
+      rs.cpu_avail = cpu[k];
+      rs.mem_avail = mem[k];
+      rs.speed_mult = mult[k];
+      series.states.push_back(rs);
+    }
+    *out = predictor_series_rmse(static_cast<PredictorKind>(kind), to_pred(*base), series,
+                                 base_speed, seed, measure_from);
   })
 }
 

@@ -57,6 +57,33 @@ SIGNATURES = {
                           _dp, _dp],
     "lbbsp_sim_status": [_vp, _ip, _ip],
     "lbbsp_sim_launches_per_iteration": [_vp, _ip],
+    "lbbsp_sim_metrics": [_vp, C.c_int, C.POINTER(abi.Metrics)],
+    "lbbsp_compute_metrics": [C.POINTER(abi.RecordsView), C.c_int, C.c_int, C.c_int,
+                              C.POINTER(abi.Metrics)],
+    "lbbsp_write_records_csv": [C.POINTER(abi.RecordsView), C.c_char_p],
+    "lbbsp_write_metrics_json": [C.POINTER(abi.Metrics), C.c_double, C.c_int, C.c_int,
+                                 C.c_char_p],
+    "lbbsp_trace_parse": [C.c_char_p, C.POINTER(_vp)],
+    "lbbsp_trace_create": [C.c_int, C.POINTER(C.c_char_p), _ip, _dp, _dp, _dp, C.POINTER(_vp)],
+    "lbbsp_trace_destroy": [_vp],
+    "lbbsp_trace_count": [_vp, _ip],
+    "lbbsp_trace_info": [_vp, C.c_int, C.POINTER(C.c_char_p), _ip, _dp],
+    "lbbsp_trace_points": [_vp, C.c_int, _dp, _dp, _dp],
+    "lbbsp_trace_write": [_vp, C.c_char_p],
+    "lbbsp_trace_map": [_vp, C.c_int, C.c_uint64, _ip],
+    "lbbsp_trace_at": [_vp, C.c_int, C.c_double, _dp, _dp],
+    "lbbsp_narx_load_csv": [C.c_char_p, C.POINTER(abi.NarxModel)],
+    "lbbsp_narx_save_csv": [C.POINTER(abi.NarxModel), C.c_char_p],
+    "lbbsp_scenario_load": [C.c_char_p, C.POINTER(_vp)],
+    "lbbsp_scenario_destroy": [_vp],
+    "lbbsp_scenario_set_seed": [_vp, C.c_uint64],
+    "lbbsp_scenario_get_info": [_vp, C.POINTER(abi.ScenarioInfo)],
+    "lbbsp_scenario_sim_cfg": [_vp, C.POINTER(C.POINTER(abi.SimConfig))],
+    "lbbsp_predictor_series_rmse": [C.c_int, C.POINTER(abi.PredictorConfig), _dp, _dp, _dp,
+                                    C.c_int, C.c_double, C.c_uint64, C.c_int, _dp],
+    "lbbsp_cmd_run": [C.c_char_p, C.c_char_p, C.c_int, C.c_uint64],
+    "lbbsp_cmd_compare": [C.POINTER(C.c_char_p), C.c_int, C.c_char_p, C.c_int, C.c_uint64],
+    "lbbsp_cmd_predict_bench": [C.c_char_p, C.c_char_p, C.c_int, C.c_uint64],
 }
 
 _lib = None

@@ -13,10 +13,11 @@ RUNTIME = -3
 LOGIC = -4
 CUDA = -5
 NCCL = -6
+CONFIG = -7
 
 PRED_MEMORYLESS, PRED_EMA, PRED_NARX, PRED_PERFECT = 0, 1, 2, 3
 SCHEME_BSP, SCHEME_ASP, SCHEME_SSP, SCHEME_LBBSP = 0, 1, 2, 3
-DYN_STATIC, DYN_STRAGGLER, DYN_BENCHMARK = 0, 1, 2
+DYN_STATIC, DYN_STRAGGLER, DYN_BENCHMARK, DYN_TRACE = 0, 1, 2, 3
 PRESET_NONE, PRESET_HOMO, PRESET_HETERO_L2, PRESET_HETERO_L3 = -1, 0, 1, 2
 PRESET_HETERO_L2_STATIC, PRESET_HETERO_L3_STATIC = 3, 4
 
@@ -109,6 +110,9 @@ class SimConfig(C.Structure):
         ("dataset_dim", C.c_int), ("dataset_noise", C.c_double),
         ("convergence_loss", C.c_double), ("convergence_consecutive", C.c_int),
         ("max_updates", C.c_int64), ("seed", C.c_uint64),
+        ("trace_offsets", C.POINTER(C.c_int)), ("trace_t", C.POINTER(C.c_double)),
+        ("trace_cpu", C.POINTER(C.c_double)), ("trace_mem", C.POINTER(C.c_double)),
+        ("narx_weights_path", C.c_char_p),
     ]
 
 
@@ -117,16 +121,46 @@ class IterScalars(C.Structure):
                 ("wall_s", C.c_double)]
 
 
+class RecordsView(C.Structure):
+    """lbbsp_records_view: a host record stream ([rows] scalars, [rows*n] rows)."""
+    _fields_ = [("rows", C.c_int), ("n", C.c_int), ("scalars", C.POINTER(IterScalars)),
+                ("batch", C.POINTER(C.c_int)), ("tp", C.POINTER(C.c_double)),
+                ("tm", C.POINTER(C.c_double)), ("wait", C.POINTER(C.c_double)),
+                ("v_pred", C.POINTER(C.c_double)), ("v_actual", C.POINTER(C.c_double))]
+
+
+class Metrics(C.Structure):
+    """Metrics, cluster_sim.hpp:157-163"""
+    _fields_ = [("updates_to_convergence", C.c_int64), ("mean_per_update_time", C.c_double),
+                ("wastage", C.c_double), ("predictor_rmse", C.c_double), ("converged", C.c_int)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class ScenarioInfo(C.Structure):
+    """lbbsp_scenario_info: ScenarioConfig scalars (scenario.hpp:33-64)"""
+    _fields_ = [("name", C.c_char * 256), ("scheme", C.c_int), ("staleness_threshold", C.c_int),
+                ("workers", C.c_int), ("total_budget", C.c_int), ("predictor", C.c_int),
+                ("alpha", C.c_double), ("warmup_iterations", C.c_int),
+                ("speed_floor", C.c_double), ("base_speed", C.c_double),
+                ("base_comm_s", C.c_double), ("learning_rate", C.c_double),
+                ("convergence_loss", C.c_double), ("convergence_consecutive", C.c_int),
+                ("max_iterations", C.c_int64), ("seed", C.c_uint64), ("paired_sim", C.c_int)]
+
+
 def make_sim_config(scheme="lb-bsp", workers=4, total_budget=512, preset="hetero-l3",
                     base_speed=10.0, dynamics=DYN_STATIC, static_cpu=None, static_mem=None,
                     stragglers=None, predictor="ema", alpha=0.2, warmup_iterations=500,
                     speed_floor=1e-3, train=None, gpu_profiles=None, base_comm_s=0.0,
                     bandwidth_drop=None, learning_rate=0.5, dataset_seed=7, dataset_size=1000,
                     dataset_dim=10, dataset_noise=0.1, convergence_loss=0.40,
-                    convergence_consecutive=10, max_updates=500, seed=1, benchmark=None):
+                    convergence_consecutive=10, max_updates=500, seed=1, benchmark=None,
+                    traces=None, narx_weights_path=None):
     """Defaults follow SimConfig (cluster_sim.hpp:165-180) and PredictorConfig
     (predictor.hpp:107-114). Returns (cfg, keepalive) -- keep the second value
-    alive while cfg is in use (it owns the pointed-to arrays)."""
+    alive while cfg is in use (it owns the pointed-to arrays).
+    traces: per-worker list of (t, cpu, mem) point lists (DYN_TRACE)."""
     keep = []
     c = SimConfig()
     c.scheme = SCHEMES[scheme] if isinstance(scheme, str) else scheme
@@ -165,4 +199,18 @@ def make_sim_config(scheme="lb-bsp", workers=4, total_budget=512, preset="hetero
     c.dataset_noise = dataset_noise
     c.convergence_loss, c.convergence_consecutive = convergence_loss, convergence_consecutive
     c.max_updates, c.seed = max_updates, seed
+    if traces is not None:
+        off, t, cp, mm = [0], [], [], []
+        for pts in traces:
+            for (a, b, d) in pts:
+                t.append(a); cp.append(b); mm.append(d)
+            off.append(len(t))
+        arrs = [(C.c_int * len(off))(*off)] + [(C.c_double * max(len(x), 1))(*x)
+                                                for x in (t, cp, mm)]
+        keep.extend(arrs)
+        c.trace_offsets, c.trace_t, c.trace_cpu, c.trace_mem = arrs
+    if narx_weights_path:
+        b = str(narx_weights_path).encode()
+        keep.append(b)
+        c.narx_weights_path = b
     return c, keep

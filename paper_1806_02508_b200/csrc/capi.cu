@@ -692,6 +692,18 @@ extern "C" int lbbsp_sim_create(const lbbsp_sim_cfg* cfg, lbbsp_sim** out) {
     LBBSP_CUDA_CHECK(S->upload(&d.bmem, bm));
     LBBSP_CUDA_CHECK(S->upload(&d.bmult, bx));
   }
+  if (dyn == LBBSP_DYN_TRACE) {  // Dynamics::at Trace (cluster_sim.cpp:110-115)
+    if (!c.trace_offsets || !c.trace_t || !c.trace_cpu || !c.trace_mem)
+      return set_error(LBBSP_INVALID_ARGUMENT, "simulation: trace dynamics need trace arrays");
+    std::vector<int> off(c.trace_offsets, c.trace_offsets + n + 1);
+    for (int i = 0; i < n; ++i)
+      if (off[i + 1] <= off[i]) return set_error(LBBSP_INVALID_ARGUMENT, "trace_at: empty trace");
+    const size_t P = static_cast<size_t>(off[n]);
+    LBBSP_CUDA_CHECK(S->upload(&d.trace_off, off));
+    LBBSP_CUDA_CHECK(S->upload(&d.trace_t, std::vector<double>(c.trace_t, c.trace_t + P)));
+    LBBSP_CUDA_CHECK(S->upload(&d.trace_c, std::vector<double>(c.trace_cpu, c.trace_cpu + P)));
+    LBBSP_CUDA_CHECK(S->upload(&d.trace_m, std::vector<double>(c.trace_mem, c.trace_mem + P)));
+  }
   if (gpu_mode) {
     std::vector<lbbsp_gpu_profile> prof(c.gpu_profiles, c.gpu_profiles + n);
     LBBSP_CUDA_CHECK(S->upload(&d.prof, prof));
@@ -731,6 +743,7 @@ extern "C" int lbbsp_sim_create(const lbbsp_sim_cfg* cfg, lbbsp_sim** out) {
   LBBSP_CUDA_CHECK(S->alloc(&d.sizes, n));
   LBBSP_CUDA_CHECK(S->alloc(&d.offsets, n));
   LBBSP_CUDA_CHECK(S->alloc(&d.wall, 1));
+  LBBSP_CUDA_CHECK(S->alloc(&d.now, 1));
   LBBSP_CUDA_CHECK(S->alloc(&d.rec_sc, R));
   LBBSP_CUDA_CHECK(S->alloc(&d.rec_batch, R * n));
   LBBSP_CUDA_CHECK(S->alloc(&d.rec_tp, R * n));
@@ -746,7 +759,14 @@ extern "C" int lbbsp_sim_create(const lbbsp_sim_cfg* cfg, lbbsp_sim** out) {
   for (int i = 0; i < n; ++i) seeds[i] = mix_seed(c.seed, 0x9ced1c70ull, static_cast<uint64_t>(i));
   lbbsp_predictor_cfg pc = c.predictor;
   pc.train.min_history = pc.warmup_iterations;
-  int rc = make_pred(&S->pred, &pc, n, static_cast<int>(R), seeds.data(), nullptr);
+  std::vector<lbbsp_narx_model> initial;  // PredictorConfig::initial_weights (predictor.cpp:265)
+  if (c.narx_weights_path && c.narx_weights_path[0]) {
+    lbbsp_narx_model m{};
+    if (int rc = lbbsp_narx_load_csv(c.narx_weights_path, &m)) return rc;
+    initial.assign(n, m);
+  }
+  int rc = make_pred(&S->pred, &pc, n, static_cast<int>(R), seeds.data(),
+                     initial.empty() ? nullptr : initial.data());
   if (rc) return rc;
   d.pred = S->pred.dev;
 
@@ -819,5 +839,44 @@ extern "C" int lbbsp_sim_records(lbbsp_sim* sim, int max_rows, int* rows, lbbsp_
 
 extern "C" int lbbsp_sim_launches_per_iteration(lbbsp_sim* sim, int* launches) {
   *launches = sim->launches ? sim->launches : (sim->dev.pred.kind == LBBSP_PRED_NARX ? 4 : 3);
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_sim_metrics(lbbsp_sim* sim, int rmse_from_iteration, lbbsp_metrics* out) {
+  double* scratch = nullptr;
+  lbbsp_metrics* d_out = nullptr;
+  const size_t cap = static_cast<size_t>(sim->dev.max_updates) * sim->dev.n;
+  LBBSP_CUDA_CHECK(sim->alloc(&scratch, 2 * cap));
+  LBBSP_CUDA_CHECK(sim->alloc(&d_out, 1));
+  LBBSP_CUDA_CHECK(launch_sim_metrics(sim->dev, rmse_from_iteration, scratch, d_out, nullptr));
+  LBBSP_CUDA_CHECK(cudaMemcpy(out, d_out, sizeof *out, cudaMemcpyDeviceToHost));
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_predictor_series_rmse(int kind, const lbbsp_predictor_cfg* base,
+                                           const double* h_cpu, const double* h_mem,
+                                           const double* h_mult, int len, double base_speed,
+                                           uint64_t seed, int measure_from, double* rmse) {
+  LBBSP_REQUIRE_DEVICE();
+  if (len < 1) return set_error(LBBSP_INVALID_ARGUMENT, "predictor_series_rmse: nothing to measure");
+  lbbsp_predictor_cfg pc = *base;
+  pc.kind = kind;
+  pc.train.min_history = pc.warmup_iterations;  // SpeedPredictor ctor (predictor.cpp:264)
+  lbbsp_predictor P;
+  if (int rc = make_pred(&P, &pc, 1, len, &seed, nullptr)) return rc;
+  double* series = nullptr;
+  double* out2 = nullptr;
+  LBBSP_CUDA_CHECK(P.alloc(&series, 3 * static_cast<size_t>(len)));
+  LBBSP_CUDA_CHECK(P.alloc(&out2, 2));
+  LBBSP_CUDA_CHECK(cudaMemcpy(series, h_cpu, sizeof(double) * len, cudaMemcpyHostToDevice));
+  LBBSP_CUDA_CHECK(cudaMemcpy(series + len, h_mem, sizeof(double) * len, cudaMemcpyHostToDevice));
+  LBBSP_CUDA_CHECK(cudaMemcpy(series + 2 * len, h_mult, sizeof(double) * len, cudaMemcpyHostToDevice));
+  LBBSP_CUDA_CHECK(launch_series_rmse(P.dev, series, series + len, series + 2 * len, len,
+                                      base_speed, measure_from, out2, nullptr));
+  double h[2];
+  LBBSP_CUDA_CHECK(cudaMemcpy(h, out2, sizeof h, cudaMemcpyDeviceToHost));
+  if (h[1] == 0.0)
+    return set_error(LBBSP_INVALID_ARGUMENT, "predictor_series_rmse: nothing to measure");
+  *rmse = std::sqrt(h[0] / h[1]);
   return LBBSP_OK;
 }

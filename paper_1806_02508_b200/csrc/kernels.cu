@@ -455,7 +455,8 @@ cudaError_t launch_lr_loss(const double* feat, const double* lab, int N, int d,
 //   sim_update  P8-P10  aggregate+apply, norm, loss, check_stop, observe
 //   pred_train  P10     NARX train_rotation, one CTA per model
 // ---------------------------------------------------------------------------
-__device__ void dyn_at_d(const SimDev& S, int w, long long k, double* c, double* m, double* mult) {
+__device__ void dyn_at_d(const SimDev& S, int w, long long k, double now, double* c, double* m,
+                         double* mult) {
   *c = 1.0;
   *m = 1.0;
   *mult = 1.0;
@@ -486,6 +487,21 @@ __device__ void dyn_at_d(const SimDev& S, int w, long long k, double* c, double*
       *mult = S.bmult[o];
       return;
     }
+    case LBBSP_DYN_TRACE: {  // trace_at (trace.cpp:137-143): last point at or before now
+      int lo = S.trace_off[w], hi = S.trace_off[w + 1];  // upper_bound over [lo, hi)
+      const int first = lo;
+      while (lo < hi) {
+        const int mid = lo + (hi - lo) / 2;
+        if (now < S.trace_t[mid])
+          hi = mid;
+        else
+          lo = mid + 1;
+      }
+      const int p = lo > first ? lo - 1 : first;
+      *c = S.trace_c[p];
+      *m = S.trace_m[p];
+      return;
+    }
   }
 }
 
@@ -502,10 +518,11 @@ __global__ void __launch_bounds__(kSolverThreads) sim_plan_kernel(SimDev S) {
   const int n = S.n, tid = threadIdx.x;
   const long long k = *S.k;
   const int len = *S.pred.len;
+  const double now = *S.now;
   // P1-P3 (cluster_sim.cpp:355-367)
   for (int i = tid; i < n; i += blockDim.x) {
     double c, m, mult;
-    dyn_at_d(S, i, k, &c, &m, &mult);
+    dyn_at_d(S, i, k, now, &c, &m, &mult);
     S.c_now[i] = c;
     S.m_now[i] = m;
     double va = 0.0, vp = 0.0;
@@ -657,6 +674,7 @@ __global__ void __launch_bounds__(512) sim_update_kernel(SimDev S) {
     *S.pred.cursor = (*S.pred.cursor + (S.n + 1) / 2) % S.n;
     *S.rows = row + 1;
     *S.k += 1;
+    *S.now = dadd(*S.now, *S.wall);  // now_ += wall (cluster_sim.cpp:466)
     // check_stop (cluster_sim.cpp:326-334)
     const int below = loss < S.conv_loss ? *S.below + 1 : 0;
     *S.below = below;
@@ -686,6 +704,126 @@ cudaError_t launch_sim_iteration(const SimDev& S, cudaStream_t s, int* launches)
     ++nl;
   }
   if (launches) *launches = nl;
+  return cudaGetLastError();
+}
+
+// compute_metrics (cluster_sim.cpp:217-245) on the device-resident records:
+// per-row terms in parallel, then the reference's three sequential folds by
+// three threads of warp 0 (time_total, wait fractions, squared errors).
+__global__ void __launch_bounds__(256) sim_metrics_kernel(SimDev S, int rmse_from, double* wf,
+                                                          double* se, lbbsp_metrics* out) {
+  const int rows = *S.rows, n = S.n;
+  const size_t total = static_cast<size_t>(rows) * n;
+  for (size_t o = threadIdx.x; o < total; o += blockDim.x) {
+    const size_t r = o / n;
+    const double wall = S.rec_sc[r].wall_s;
+    wf[o] = wall > 0.0 ? ddiv(S.rec_wait[o], wall) : 0.0;
+    const double vp = S.rec_vpred[o];
+    se[o] = -1.0;  // marks "not counted"
+    if (vp > 0.0 && S.rec_sc[r].k >= rmse_from) {
+      const double e = dsub(vp, S.rec_vact[o]);
+      se[o] = dmul(e, e);
+    }
+  }
+  __syncthreads();
+  __shared__ double time_total, wsum, sse;
+  __shared__ long long sse_count;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int r = 0; r < rows; ++r) t = dadd(t, S.rec_sc[r].wall_s);
+    time_total = t;
+  } else if (threadIdx.x == 1) {
+    double a = 0.0;
+    for (size_t o = 0; o < total; ++o) a = dadd(a, wf[o]);
+    wsum = a;
+  } else if (threadIdx.x == 2) {
+    double a = 0.0;
+    long long c = 0;
+    for (size_t o = 0; o < total; ++o)
+      if (se[o] >= 0.0) {
+        a = dadd(a, se[o]);
+        ++c;
+      }
+    sse = a;
+    sse_count = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    lbbsp_metrics m{};
+    m.converged = *S.converged;
+    m.updates_to_convergence = rows;
+    if (rows > 0) {
+      m.mean_per_update_time = ddiv(time_total, static_cast<double>(rows));
+      m.wastage = total > 0 ? ddiv(wsum, static_cast<double>(total)) : 0.0;
+      m.predictor_rmse = sse_count > 0 ? __dsqrt_rn(ddiv(sse, static_cast<double>(sse_count))) : 0.0;
+    }
+    *out = m;
+  }
+}
+
+cudaError_t launch_sim_metrics(const SimDev& S, int rmse_from, double* scratch,
+                               lbbsp_metrics* out, cudaStream_t s) {
+  const size_t cap = static_cast<size_t>(S.max_updates) * S.n;
+  sim_metrics_kernel<<<1, 256, 0, s>>>(S, rmse_from, scratch, scratch + cap, out);
+  return cudaGetLastError();
+}
+
+// predictor_series_rmse (cluster_sim.cpp:645-672): one CTA replays the whole
+// series -- predict (k >= 1 and k >= measure_from), push, train -- with the
+// history, EMA state and NARX model resident; no launch per step.
+__global__ void __launch_bounds__(kTrainThreads) series_rmse_kernel(PredDev P, const double* cpu,
+                                                                    const double* mem,
+                                                                    const double* mult, int len,
+                                                                    double base_speed,
+                                                                    int measure_from, double* out2,
+                                                                    size_t smem_bytes) {
+  extern __shared__ double sm_d[];
+  __shared__ NarxTrainSmem s;
+  __shared__ double sse;
+  __shared__ long long count;
+  if (threadIdx.x == 0) {
+    sse = 0.0;
+    count = 0;
+  }
+  lbbsp_narx_train_cfg cfg = P.train;
+  cfg.min_history = P.warmup;
+  for (int k = 0; k < len; ++k) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double c = cpu[k], m = mem[k];
+      const double pen = m >= 0.5 ? 1.0 : dadd(0.25, dmul(0.75, ddiv(m, 0.5)));  // :22-29
+      const double va = dmul(dmul(dmul(base_speed, c), pen), mult[k]);
+      if (k >= 1 && k >= measure_from) {
+        const double vp = predictor_predict_d(P, 0, k, c, m);
+        const double e = dsub(vp, va);
+        sse = dadd(sse, dmul(e, e));
+        ++count;
+      }
+      observe_d(P, 0, k, va, c, m, 0.0);
+    }
+    __syncthreads();
+    if (P.kind == LBBSP_PRED_NARX) {
+      const int L = k + 1;
+      double* buf = narx_train_scratch_bytes(L) <= smem_bytes ? sm_d : P.scratch;
+      narx_train_block(&P.models[0], P.hv, P.hc, P.hm, L, cfg, &P.reports[0], nullptr, 0, buf, &s);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out2[0] = sse;
+    out2[1] = static_cast<double>(count);
+    *P.len = len;
+  }
+}
+
+cudaError_t launch_series_rmse(const PredDev& P, const double* cpu, const double* mem,
+                               const double* mult, int len, double base_speed, int measure_from,
+                               double* out2, cudaStream_t s) {
+  const size_t smem = train_smem_bytes(P.max_hist);
+  cudaFuncSetAttribute(series_rmse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(kTrainSmemCap));
+  series_rmse_kernel<<<1, kTrainThreads, smem, s>>>(P, cpu, mem, mult, len, base_speed,
+                                                    measure_from, out2, smem);
   return cudaGetLastError();
 }
 

@@ -24,6 +24,10 @@ struct SimDev {
   const double* bcpu;        // [n][bench_len]
   const double* bmem;
   const double* bmult;
+  const int* trace_off;      // [n+1] (Trace dynamics)
+  const double* trace_t;
+  const double* trace_c;
+  const double* trace_m;
   // comm model
   double base_comm;
   int bw_worker;
@@ -49,6 +53,7 @@ struct SimDev {
   int* sizes;
   int* offsets;
   double* wall;
+  double* now;  // simulated clock (Simulation::now_, cluster_sim.cpp:466)
   // workload (reference logistic regression, fp64)
   const double* feat;  // [N][d]
   const double* lab;   // [N]
@@ -95,6 +100,15 @@ cudaError_t launch_aggregate_apply(const double* grads, const int* sizes, int n,
 cudaError_t launch_lr_loss(const double* feat, const double* lab, int N, int d,
                            const double* params, double* out, cudaStream_t s);
 cudaError_t launch_sim_iteration(const SimDev& S, cudaStream_t s, int* launches);
+// compute_metrics (cluster_sim.cpp:217-245) over the device-resident records;
+// out = {time_total.., see kernels.cu}; scratch: 2*rows*n doubles.
+cudaError_t launch_sim_metrics(const SimDev& S, int rmse_from, double* scratch,
+                               lbbsp_metrics* out, cudaStream_t s);
+// predictor_series_rmse (cluster_sim.cpp:645-672): P has n == 1 and history
+// capacity >= len; writes {sse, count} to out2.
+cudaError_t launch_series_rmse(const PredDev& P, const double* cpu, const double* mem,
+                               const double* mult, int len, double base_speed, int measure_from,
+                               double* out2, cudaStream_t s);
 
 size_t train_smem_bytes(int max_hist);
 

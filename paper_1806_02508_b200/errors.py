@@ -31,6 +31,11 @@ class LogicError(LbbspError):
     code = abi.LOGIC
 
 
+class ConfigError(RuntimeFailure):
+    """lbbsp::ConfigError (scenario.hpp:13-15), a std::runtime_error"""
+    code = abi.CONFIG
+
+
 class CudaError(LbbspError, RuntimeError):
     code = abi.CUDA
 
@@ -41,7 +46,7 @@ class NcclError(LbbspError, RuntimeError):
 
 _BY_CODE = {abi.INVALID_ARGUMENT: InvalidArgument, abi.OUT_OF_RANGE: OutOfRange,
             abi.RUNTIME: RuntimeFailure, abi.LOGIC: LogicError, abi.CUDA: CudaError,
-            abi.NCCL: NcclError}
+            abi.NCCL: NcclError, abi.CONFIG: ConfigError}
 
 
 def raise_for(code, message):

@@ -448,3 +448,236 @@ class Simulation:
         """Simulation::run (cluster_sim.cpp:633-643): all rounds on device."""
         self.run_rounds(int(self.cfg.max_updates))
         return self.records()
+
+    def metrics(self) -> abi.Metrics:
+        """SimResult::metrics = compute_metrics(records, converged, warmup)
+        (cluster_sim.cpp:638), computed on device from the resident records."""
+        m = abi.Metrics()
+        check(lib().lbbsp_sim_metrics(self._h, int(self.cfg.predictor.warmup_iterations),
+                                      C.byref(m)))
+        return m
+
+    @classmethod
+    def from_scenario(cls, scenario: "Scenario") -> "Simulation":
+        """Simulation(build_sim_config(cfg)) (scenario.cpp:219-304)."""
+        sim = cls(scenario.sim_config())
+        sim._scenario = scenario  # the config's arrays live in the scenario
+        return sim
+
+
+# --------------------------------------------------------------------------
+# Records, metrics and exporters (cluster_sim.cpp:217-245, scenario.cpp:60-358)
+# --------------------------------------------------------------------------
+def _records_view(r: SimResult):
+    rows, n = r.batch.shape
+    sc = (abi.IterScalars * max(rows, 1))(*[abi.IterScalars(int(r.k[i]), float(r.grad_norm[i]),
+                                                            float(r.loss[i]), float(r.wall[i]))
+                                            for i in range(rows)])
+    keep = [sc]
+    arrs = []
+    for name in ("tp", "tm", "wait", "v_pred", "v_actual"):
+        a = np.ascontiguousarray(getattr(r, name), dtype=np.float64).reshape(-1)
+        keep.append(a)
+        arrs.append(a.ctypes.data_as(_dp))
+    b = np.ascontiguousarray(r.batch, dtype=np.int32).reshape(-1)
+    keep.append(b)
+    v = abi.RecordsView(rows, n, sc, b.ctypes.data_as(_ip), *arrs)
+    return v, keep
+
+
+def compute_metrics(records: SimResult, converged: bool, rmse_from_iteration: int,
+                    rounded: bool = False) -> abi.Metrics:
+    """compute_metrics (cluster_sim.cpp:217-245); rounded=True applies the
+    exporter's 9-significant-digit rounding first (scenario.cpp:66-88)."""
+    v, keep = _records_view(records)
+    m = abi.Metrics()
+    check(lib().lbbsp_compute_metrics(C.byref(v), int(bool(converged)), int(rmse_from_iteration),
+                                      int(bool(rounded)), C.byref(m)))
+    return m
+
+
+def write_records_csv(records: SimResult, path) -> None:
+    """write_records_csv (scenario.cpp:306-342)."""
+    v, keep = _records_view(records)
+    check(lib().lbbsp_write_records_csv(C.byref(v), str(path).encode()))
+
+
+def write_metrics_json(metrics: abi.Metrics, convergence_loss: float, convergence_consecutive: int,
+                       warmup_iterations: int, path) -> None:
+    """write_metrics_json (scenario.cpp:344-358)."""
+    check(lib().lbbsp_write_metrics_json(C.byref(metrics), float(convergence_loss),
+                                         int(convergence_consecutive), int(warmup_iterations),
+                                         str(path).encode()))
+
+
+# --------------------------------------------------------------------------
+# trace.hpp: recorded resource traces
+# --------------------------------------------------------------------------
+@dataclass
+class ResourceTrace:
+    """ResourceTrace (trace.hpp:18-24): points as (t_offset_s, cpu, mem)."""
+    machine_id: str
+    points: list
+
+    def mean_cpu(self) -> float:
+        s = 0.0
+        for p in self.points:
+            s += p[1]
+        return s / len(self.points) if self.points else 0.0
+
+
+class _Traces:
+    def __init__(self, h):
+        self._h = h
+
+    def __del__(self):
+        try:
+            lib().lbbsp_trace_destroy(self._h)
+        except Exception:
+            pass
+
+    @classmethod
+    def parse(cls, path):
+        h = C.c_void_p()
+        check(lib().lbbsp_trace_parse(str(path).encode(), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_list(cls, traces: Sequence[ResourceTrace]):
+        ids = (C.c_char_p * max(len(traces), 1))(*[t.machine_id.encode() for t in traces])
+        off = [0]
+        for t in traces:
+            off.append(off[-1] + len(t.points))
+        pts = [p for t in traces for p in t.points]
+        cols = [np.array([p[j] for p in pts] or [0.0]) for j in range(3)]
+        o = np.array(off, np.int32)
+        h = C.c_void_p()
+        check(lib().lbbsp_trace_create(len(traces), ids, o.ctypes.data_as(_ip),
+                                       *[c.ctypes.data_as(_dp) for c in cols], C.byref(h)))
+        return cls(h)
+
+    def to_list(self):
+        n = C.c_int()
+        check(lib().lbbsp_trace_count(self._h, C.byref(n)))
+        out = []
+        for i in range(n.value):
+            mid, cnt, mean = C.c_char_p(), C.c_int(), C.c_double()
+            check(lib().lbbsp_trace_info(self._h, i, C.byref(mid), C.byref(cnt), C.byref(mean)))
+            cols = [np.zeros(max(cnt.value, 1)) for _ in range(3)]
+            check(lib().lbbsp_trace_points(self._h, i, *[c.ctypes.data_as(_dp) for c in cols]))
+            out.append(ResourceTrace(mid.value.decode(),
+                                     [(float(cols[0][q]), float(cols[1][q]), float(cols[2][q]))
+                                      for q in range(cnt.value)]))
+        return out
+
+
+def parse_trace(path) -> List[ResourceTrace]:
+    """parse_trace (trace.cpp:54-97)."""
+    return _Traces.parse(path).to_list()
+
+
+def write_trace(traces: Sequence[ResourceTrace], path) -> None:
+    """write_trace (trace.cpp:99-107)."""
+    t = _Traces.from_list(traces)
+    check(lib().lbbsp_trace_write(t._h, str(path).encode()))
+
+
+def map_traces(traces: Sequence[ResourceTrace], workers: int, seed: int) -> List[int]:
+    """map_traces (trace.cpp:109-135)."""
+    t = _Traces.from_list(traces)
+    out = np.zeros(max(workers, 1), np.int32)
+    check(lib().lbbsp_trace_map(t._h, int(workers), C.c_uint64(seed), out.ctypes.data_as(_ip)))
+    return [int(x) for x in out[:workers]]
+
+
+def trace_at(trace: ResourceTrace, time_s: float):
+    """trace_at (trace.cpp:137-143) -> (cpu, mem)."""
+    t = _Traces.from_list([trace])
+    c, m = C.c_double(), C.c_double()
+    check(lib().lbbsp_trace_at(t._h, 0, float(time_s), C.byref(c), C.byref(m)))
+    return c.value, m.value
+
+
+def load_narx_csv(path) -> Narx:
+    """load_narx_csv (predictor.cpp:215-243)."""
+    m = Narx()
+    check(lib().lbbsp_narx_load_csv(str(path).encode(), C.byref(m)))
+    return m
+
+
+def save_narx_csv(model: NarxModel, path) -> None:
+    """save_narx_csv (predictor.cpp:198-213)."""
+    check(lib().lbbsp_narx_save_csv(C.byref(model), str(path).encode()))
+
+
+# --------------------------------------------------------------------------
+# scenario.hpp: JSON scenarios and the CLI entry points
+# --------------------------------------------------------------------------
+class Scenario:
+    """ScenarioConfig loaded by load_scenario (scenario.cpp:92-181)."""
+
+    def __init__(self, path):
+        h = C.c_void_p()
+        check(lib().lbbsp_scenario_load(str(path).encode(), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        try:
+            lib().lbbsp_scenario_destroy(self._h)
+        except Exception:
+            pass
+
+    @property
+    def info(self) -> abi.ScenarioInfo:
+        i = abi.ScenarioInfo()
+        check(lib().lbbsp_scenario_get_info(self._h, C.byref(i)))
+        return i
+
+    def set_seed(self, seed: int) -> None:
+        check(lib().lbbsp_scenario_set_seed(self._h, C.c_uint64(seed)))
+
+    def sim_config(self) -> abi.SimConfig:
+        """build_sim_config (scenario.cpp:219-294); owned by this object."""
+        p = C.POINTER(abi.SimConfig)()
+        check(lib().lbbsp_scenario_sim_cfg(self._h, C.byref(p)))
+        return p.contents
+
+
+def load_scenario(path) -> Scenario:
+    return Scenario(path)
+
+
+def predictor_series_rmse(kind, base: PredictorConfig, cpu, mem, mult, base_speed: float,
+                          seed: int, measure_from: int) -> float:
+    """predictor_series_rmse (cluster_sim.cpp:645-672), one device CTA."""
+    c, cp = _d(cpu); m, mp = _d(mem); x, xp = _d(mult)
+    kind = abi.PREDICTORS[kind] if isinstance(kind, str) else int(kind)
+    out = C.c_double()
+    check(lib().lbbsp_predictor_series_rmse(kind, C.byref(base), cp, mp, xp, len(c),
+                                            float(base_speed), C.c_uint64(seed),
+                                            int(measure_from), C.byref(out)))
+    return out.value
+
+
+def _seed_args(seed_override):
+    return (0, 0) if seed_override is None else (1, int(seed_override))
+
+
+def cmd_run(config, out_dir, seed_override: Optional[int] = None) -> int:
+    """cmd_run (scenario.cpp:369-386); returns the CLI exit status."""
+    h, s = _seed_args(seed_override)
+    return lib().lbbsp_cmd_run(str(config).encode(), str(out_dir).encode(), h, C.c_uint64(s))
+
+
+def cmd_compare(configs, out_dir, seed_override: Optional[int] = None) -> int:
+    """cmd_compare (scenario.cpp:388-423)."""
+    h, s = _seed_args(seed_override)
+    arr = (C.c_char_p * max(len(configs), 1))(*[str(c).encode() for c in configs])
+    return lib().lbbsp_cmd_compare(arr, len(configs), str(out_dir).encode(), h, C.c_uint64(s))
+
+
+def cmd_predict_bench(config, out_dir, seed_override: Optional[int] = None) -> int:
+    """cmd_predict_bench (scenario.cpp:425-481)."""
+    h, s = _seed_args(seed_override)
+    return lib().lbbsp_cmd_predict_bench(str(config).encode(), str(out_dir).encode(), h,
+                                         C.c_uint64(s))

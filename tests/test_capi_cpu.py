@@ -41,6 +41,18 @@ def test_compute_entry_points_fail_loudly_without_device():
         lbbsp.Simulation(workers=2, total_budget=8, max_updates=2)
 
 
+def test_cli_fails_loudly_without_device(tmp_path, capfd):
+    """cmd_run parses the scenario on the host, then needs the device driver."""
+    from paper_1806_02508_b200._lib import lib
+    from paper_1806_02508_b200 import lbbsp
+    if lib().lbbsp_device_count() > 0:
+        pytest.skip("a device is present")
+    cfg = tmp_path / "homo.json"
+    cfg.write_text('{"scheme": "bsp", "workers": 2, "total_budget": 8, "max_iterations": 3}')
+    assert lbbsp.cmd_run(cfg, tmp_path / "out") == 1
+    assert "no CPU fallback" in capfd.readouterr().err
+
+
 def test_reference_signature_shim_is_built():
     exe = os.path.join(REPO, "tests", "cpp", "test_shim")
     assert os.path.exists(exe), "build() compiles tests/cpp/test_shim against include/lbbsp_b200.hpp"

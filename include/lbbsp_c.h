@@ -589,6 +589,8 @@ int lbbsp_mlp_read_result_async(lbbsp_mlp* m, int* h_sizes, double* h_loss);
 /* Mean per-phase device time of the rounds run so far: phase p of the last
  * round as {min start, max end} over workers (globaltimer ns); n_phases out. */
 int lbbsp_mlp_phase_times(lbbsp_mlp* m, double* h_phase_ns, int* n_phases);
+/* Per-worker device time of each phase of the last round: h_ns[p*n_local+i]. */
+int lbbsp_mlp_worker_phase_times(lbbsp_mlp* m, double* h_ns, int* n_phases);
 /* algorithmic work of one round on this rank: GEMM flops, reduction bytes */
 int lbbsp_mlp_work(lbbsp_mlp* m, double* gemm_flops, double* reduce_bytes);
 

@@ -112,21 +112,25 @@ def lbbsp_round_bf16(params, data_x, data_y, stream, sizes, lr, weighted=True, s
     for l in range(L - 1):
         h = bf16(np.maximum(h @ Wq[l].T + P[l][1], 0.0))
         acts.append(h)
-    if small_head:
-        logits = h @ P[-1][0].T + P[-1][1]
-    else:
-        logits = bf16(h @ Wq[-1].T + P[-1][1])
+    # the small head runs on warp MMAs: bf16 W and bf16 dlogits operands,
+    # fp32 accumulation; its bias gradient sums the unrounded dlogits
+    logits = h @ Wq[-1].T + P[-1][1]
+    if not small_head:
+        logits = bf16(logits)
     p, _ = softmax_ce(logits, y)
     d = p.copy()
     d[np.arange(B), y] -= 1.0
     d *= scale[:, None]
-    if not small_head:
-        d = bf16(d)
     grads = [None] * L
     for l in range(L - 1, -1, -1):
+        if small_head and l == L - 1:
+            grads[l] = (bf16(d).T @ acts[l], d.sum(axis=0))
+            d = bf16((bf16(d) @ Wq[l]) * (acts[l] > 0))
+            continue
+        if l == L - 1:
+            d = bf16(d)
         grads[l] = (d.T @ acts[l], d.sum(axis=0))
         if l > 0:
-            Wl = P[l][0] if (small_head and l == L - 1) else Wq[l]
-            d = bf16((d @ Wl) * (acts[l] > 0))
+            d = bf16((d @ Wq[l]) * (acts[l] > 0))
     new = [(W - lr * gW, b - lr * gb) for (W, b), (gW, gb) in zip(P, grads)]
     return new, grads

@@ -9,7 +9,7 @@ import os
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblbbsp_b200.so")
+LIB_PATH = os.environ.get("LBBSP_LIB_OVERRIDE") or os.path.join(HERE, "liblbbsp_b200.so")
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)
@@ -57,6 +57,7 @@ SIGNATURES = {
                           _dp, _dp],
     "lbbsp_sim_status": [_vp, _ip, _ip],
     "lbbsp_sim_launches_per_iteration": [_vp, _ip],
+    "lbbsp_benchmark_series": [C.c_uint64, C.c_int, C.c_int] + [C.c_double] * 6 + [_dp] * 3,
     "lbbsp_sim_metrics": [_vp, C.c_int, C.POINTER(abi.Metrics)],
     "lbbsp_compute_metrics": [C.POINTER(abi.RecordsView), C.c_int, C.c_int, C.c_int,
                               C.POINTER(abi.Metrics)],

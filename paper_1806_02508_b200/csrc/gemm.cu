@@ -63,7 +63,7 @@ int num_sms() {
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int ctas,
                     cudaStream_t s) {
-  constexpr int STAGES = BN == 256 ? 4 : 6;
+  constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   constexpr size_t smem = tc::gemm_smem_bytes<BN, STAGES>();
   auto kern = tc::gemm_bf16_tc_kernel<BN, A_MN, B_MN, EPI, STAGES>;
   static bool attr = false;
@@ -119,20 +119,27 @@ int gemm_launch(const GemmPlan& p, cudaStream_t s) {
   // forward / hidden layers
   LBBSP_GEMM_CASE(256, false, false, tc::kEpiBiasReluBf16)
   LBBSP_GEMM_CASE(128, false, false, tc::kEpiBiasReluBf16)
+  LBBSP_GEMM_CASE(64, false, false, tc::kEpiBiasReluBf16)
   LBBSP_GEMM_CASE(256, false, false, tc::kEpiBiasBf16)
   LBBSP_GEMM_CASE(128, false, false, tc::kEpiBiasBf16)
+  LBBSP_GEMM_CASE(64, false, false, tc::kEpiBiasBf16)
   LBBSP_GEMM_CASE(256, false, false, tc::kEpiF32)
   LBBSP_GEMM_CASE(128, false, false, tc::kEpiF32)
+  LBBSP_GEMM_CASE(64, false, false, tc::kEpiF32)
   // dX through ReLU
   LBBSP_GEMM_CASE(256, false, true, tc::kEpiDReluBf16)
   LBBSP_GEMM_CASE(128, false, true, tc::kEpiDReluBf16)
+  LBBSP_GEMM_CASE(64, false, true, tc::kEpiDReluBf16)
   LBBSP_GEMM_CASE(256, false, true, tc::kEpiF32)
   LBBSP_GEMM_CASE(128, false, true, tc::kEpiF32)
+  LBBSP_GEMM_CASE(64, false, true, tc::kEpiF32)
   // dW = dY^T X (per-worker K split)
   LBBSP_GEMM_CASE(256, true, true, tc::kEpiF32)
   LBBSP_GEMM_CASE(128, true, true, tc::kEpiF32)
+  LBBSP_GEMM_CASE(64, true, true, tc::kEpiF32)
   LBBSP_GEMM_CASE(256, true, false, tc::kEpiF32)
   LBBSP_GEMM_CASE(128, true, false, tc::kEpiF32)
+  LBBSP_GEMM_CASE(64, true, false, tc::kEpiF32)
   return set_error(LBBSP_INVALID_ARGUMENT, "gemm: unsupported variant bn=%d a_mn=%d b_mn=%d epi=%d",
                    bn, (int)a_mn, (int)b_mn, epi);
 }
@@ -181,7 +188,7 @@ extern "C" int lbbsp_gemm_bf16(const void* d_a, const void* d_b, void* d_c, int 
   // bn < 0 selects the CTA-pair kernel (256 x |bn| tiles, ungrouped problems)
   const bool pair = bn < 0 && n_groups == 0;
   if (bn < 0) bn = -bn;
-  if (bn != 128 && bn != 256) bn = N > 128 ? 256 : 128;
+  if (bn != 64 && bn != 128 && bn != 256) bn = N > 128 ? 256 : 128;
   int rc = gemm_plan(&p, d_a, d_b, M, N, K, a_mn != 0, b_mn != 0, bn, epilogue, pair);
   if (rc) return rc;
   tc::GemmArgs& a = p.args;

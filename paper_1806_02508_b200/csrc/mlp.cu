@@ -29,6 +29,7 @@
 #include "gemm.cuh"
 #include "host.cuh"
 #include "kernels.cuh"
+#include "head_mma.cuh"
 #include "mlp_kernels.cuh"
 #include "predictor.cuh"
 #include "solver.cuh"
@@ -135,6 +136,7 @@ __global__ void init_params_kernel(float* p, bf16* pb, long long off_w, long lon
 // ---------------------------------------------------------------------------
 struct PlanDev {
   int n_total, n_local, rank, B_total, scheme, static_sizes, sm_budget, trace_len;
+  int dbg_legacy_gather;
   const int* static_sizes_d;
   const double* trace_c;
   const double* trace_m;
@@ -260,12 +262,35 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
   const int rows = *D.local_rows, off = *D.stream_off;
   const int* idx = streams + static_cast<size_t>(k) * B_total + off;
   const int vec = d0 / 8;  // 16-byte chunks per row
-  const long long total = static_cast<long long>(rows) * vec;
-  for (long long t = blockIdx.x * 256ll + threadIdx.x; t < total; t += 256ll * gridDim.x) {
-    const int r = static_cast<int>(t / vec), v = static_cast<int>(t % vec);
-    const int src = idx[r];
-    reinterpret_cast<uint4*>(X)[static_cast<long long>(r) * vec + v] =
-        reinterpret_cast<const uint4*>(data_x)[static_cast<long long>(src) * vec + v];
+  const int total = rows * vec;
+  const int step = 256 * gridDim.x;
+  const uint4* src4 = reinterpret_cast<const uint4*>(data_x);
+  uint4* dst4 = reinterpret_cast<uint4*>(X);
+  if (D.dbg_legacy_gather) {
+    for (long long t = blockIdx.x * 256ll + threadIdx.x; t < total; t += 256ll * gridDim.x) {
+      const int r = static_cast<int>(t / vec), v = static_cast<int>(t % vec);
+      const int src = idx[r];
+      reinterpret_cast<uint4*>(X)[static_cast<long long>(r) * vec + v] =
+          reinterpret_cast<const uint4*>(data_x)[static_cast<long long>(src) * vec + v];
+    }
+  } else
+  // four independent row reads in flight per thread
+  for (int t0 = blockIdx.x * 256 + threadIdx.x; t0 < total; t0 += 4 * step) {
+    uint4 v[4];
+    int dsti[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * step;
+      dsti[u] = -1;
+      if (t < total) {
+        const int r = t / vec, c = t - r * vec;
+        v[u] = __ldg(&src4[static_cast<size_t>(__ldg(&idx[r])) * vec + c]);
+        dsti[u] = t;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (dsti[u] >= 0) dst4[dsti[u]] = v[u];
   }
   for (int r = blockIdx.x * 256 + threadIdx.x; r < rows; r += 256 * gridDim.x) {
     y[r] = data_y[idx[r]];
@@ -287,119 +312,6 @@ __device__ __forceinline__ void phase_begin(unsigned long long* timing, int g) {
 }
 __device__ __forceinline__ void phase_end(unsigned long long* timing, int g) {
   if (timing && threadIdx.x == 0) atomicMax(&timing[2 * g + 1], static_cast<unsigned long long>(gtimer()));
-}
-
-// Last layer with a small output (d_out <= 16) on CUDA cores, one warp per
-// row: logits, softmax-CE (warp shuffles), dlogits * row scale, per-worker dW
-// and db partials of this layer, dH = dlogits W through ReLU(H), and the
-// previous layer's bias gradient (column sums of dH) -- fused, so the 256-wide
-// hidden layer needs no separate bias-reduction pass.
-template <int DOUT, int NK>
-__global__ void __launch_bounds__(256) head_small_kernel(
-    Groups G, int rows_total, const bf16* __restrict__ H, const float* __restrict__ W,
-    const float* __restrict__ bias, const int* __restrict__ y, const float* __restrict__ row_scale,
-    bf16* dH, float* slab, long long slab_stride, long long off_w, long long off_b,
-    long long off_b_prev, double* loss_acc, unsigned long long* timing) {
-  constexpr int DH = 32 * NK;
-  __shared__ float sW[DOUT][DH];
-  __shared__ float sG[DOUT * DH + DOUT + DH];
-  int g, cta_in, cta_cnt;
-  if (!my_group(G, &g, &cta_in, &cta_cnt)) return;
-  phase_begin(timing, g);
-  for (int i = threadIdx.x; i < DOUT * DH; i += blockDim.x) sW[i / DH][i % DH] = W[i];
-  __syncthreads();
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-  const int r0 = G.n ? G.r0[g] : 0, r1 = G.n ? G.r1[g] : rows_total;
-  float acc[DOUT][NK];
-  float accb[DOUT];
-  float accd[NK];
-#pragma unroll
-  for (int t = 0; t < NK; ++t) accd[t] = 0.f;
-#pragma unroll
-  for (int c = 0; c < DOUT; ++c) {
-    accb[c] = 0.f;
-#pragma unroll
-    for (int t = 0; t < NK; ++t) acc[c][t] = 0.f;
-  }
-  double lsum = 0.0;
-  for (int r = r0 + cta_in * nw + warp; r < r1; r += cta_cnt * nw) {
-    float h[NK];
-#pragma unroll
-    for (int t = 0; t < NK; ++t) h[t] = __bfloat162float(H[static_cast<long long>(r) * DH + lane + 32 * t]);
-    float logit[DOUT];
-#pragma unroll
-    for (int c = 0; c < DOUT; ++c) {
-      float sacc = 0.f;
-#pragma unroll
-      for (int t = 0; t < NK; ++t) sacc += h[t] * sW[c][lane + 32 * t];
-      logit[c] = warp_sum(sacc) + bias[c];
-    }
-    float mx = logit[0];
-#pragma unroll
-    for (int c = 1; c < DOUT; ++c) mx = fmaxf(mx, logit[c]);
-    float se = 0.f, p[DOUT];
-#pragma unroll
-    for (int c = 0; c < DOUT; ++c) {
-      p[c] = __expf(logit[c] - mx);
-      se += p[c];
-    }
-    const int yr = y[r];
-    float ly = 0.f;
-#pragma unroll
-    for (int c = 0; c < DOUT; ++c) ly = c == yr ? logit[c] : ly;
-    if (lane == 0) lsum += static_cast<double>(logf(se) + mx - ly);
-    if (dH) {
-      const float inv = 1.f / se, sc = row_scale[r];
-      float dl[DOUT];
-#pragma unroll
-      for (int c = 0; c < DOUT; ++c) {
-        dl[c] = (p[c] * inv - (c == yr ? 1.f : 0.f)) * sc;
-        accb[c] += dl[c];
-#pragma unroll
-        for (int t = 0; t < NK; ++t) acc[c][t] += dl[c] * h[t];
-      }
-#pragma unroll
-      for (int t = 0; t < NK; ++t) {
-        float d = 0.f;
-#pragma unroll
-        for (int c = 0; c < DOUT; ++c) d += dl[c] * sW[c][lane + 32 * t];
-        const bf16 q = __float2bfloat16_rn(h[t] > 0.f ? d : 0.f);
-        dH[static_cast<long long>(r) * DH + lane + 32 * t] = q;
-        accd[t] += __bfloat162float(q);
-      }
-    }
-  }
-  if (loss_acc && lane == 0 && lsum != 0.0) atomicAdd(loss_acc, lsum);
-  if (dH) {
-    // deterministic cross-warp reduction (one warp at a time), then one
-    // global atomic per value per CTA into the worker's partial slab
-    for (int w = 0; w < nw; ++w) {
-      if (warp == w) {
-#pragma unroll
-        for (int c = 0; c < DOUT; ++c) {
-#pragma unroll
-          for (int t = 0; t < NK; ++t) {
-            float* q = &sG[c * DH + lane + 32 * t];
-            *q = (w == 0 ? 0.f : *q) + acc[c][t];
-          }
-          if (lane == 0) sG[DOUT * DH + c] = (w == 0 ? 0.f : sG[DOUT * DH + c]) + accb[c];
-        }
-#pragma unroll
-        for (int t = 0; t < NK; ++t) {
-          float* q = &sG[DOUT * DH + DOUT + lane + 32 * t];
-          *q = (w == 0 ? 0.f : *q) + accd[t];
-        }
-      }
-      __syncthreads();
-    }
-    float* gs = slab + static_cast<long long>(g) * slab_stride;
-    for (int i = threadIdx.x; i < DOUT * DH; i += blockDim.x) atomicAdd(&gs[off_w + i], sG[i]);
-    if (threadIdx.x < DOUT) atomicAdd(&gs[off_b + threadIdx.x], sG[DOUT * DH + threadIdx.x]);
-    for (int i = threadIdx.x; i < DH; i += blockDim.x)
-      atomicAdd(&gs[off_b_prev + i], sG[DOUT * DH + DOUT + i]);
-  }
-  __syncthreads();
-  phase_end(timing, g);
 }
 
 // Large softmax-CE head: one warp per row over bf16 logits [rows][n_out]
@@ -635,6 +547,10 @@ struct lbbsp_mlp {
   std::vector<bf16*> Hd;               // full-dataset forward buffers
   bf16* logits_d = nullptr;
   long long* reg_off = nullptr;
+  float* head_part = nullptr;      // [sms][head_vals] small-head CTA partials
+  double* head_loss = nullptr;     // [sms]
+  unsigned* head_cnt = nullptr;    // [n_local] worker head counters (self-resetting)
+  unsigned* head_cnt_d = nullptr;  // [1] dataset-loss head counter
   long long* reg_len = nullptr;
   int n_reg = 0;
   PlanDev D{};
@@ -721,7 +637,9 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   const int sms = D.sm_budget;
   plan_kernel<<<1, 256, 0, s>>>(D);
   ++nl;
-  gather_kernel<<<sms, 256, 0, s>>>(D, streams, B_total, data_x, data_y, dims[0], X, y, row_scale,
+  const int gather_ctas = getenv("LBBSP_DBG_GATHER_SMS")
+      ? sms : std::max(sms, std::min(sms * 8, (B_cap * (dims[0] / 8) + 1023) / 1024));
+  gather_kernel<<<gather_ctas, 256, 0, s>>>(D, streams, B_total, data_x, data_y, dims[0], X, y, row_scale,
                                      partial, P, reg_off, reg_len, n_reg);
   ++nl;
   if (use_pair) {
@@ -739,9 +657,10 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   const int hl = L - 1;  // last layer index
   if (small_head) {
     const bf16* Hin = L >= 2 ? H[L - 2] : X;
-    head_small_kernel<10, 8><<<sms, 256, 0, s>>>(G, 0, Hin, params + off_w[hl], params + off_b[hl], y,
-                                                  row_scale, dZ[L - 2], partial, P, off_w[hl],
-                                                  off_b[hl], off_b[L - 2], nullptr, phase_slot(ph++));
+    head_mma_kernel<true><<<sms, 256, kHeadMmaSmem, s>>>(
+        G, 0, Hin, params + off_w[hl], params + off_b[hl], y, row_scale, dZ[L - 2], partial, P,
+        off_w[hl], off_b[hl], off_b[L - 2], nullptr, head_part, head_loss, head_cnt,
+        phase_slot(ph++));
   } else {
     softmax_ce_kernel<<<sms, 256, 0, s>>>(G, 0, logits, dims[L], y, row_scale, dZ[L - 1], nullptr,
                                           phase_slot(ph++));
@@ -838,9 +757,9 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     none.n = 0;
     if (small_head) {
       const bf16* Hin = L >= 2 ? Hd[L - 2] : data_x;
-      head_small_kernel<10, 8><<<sms, 256, 0, s>>>(none, N_data, Hin, params + off_w[hl],
-                                                    params + off_b[hl], data_y, nullptr, nullptr,
-                                                    nullptr, 0, 0, 0, 0, D.loss_acc, nullptr);
+      head_mma_kernel<false><<<sms, 256, kHeadMmaSmem, s>>>(
+          none, N_data, Hin, params + off_w[hl], params + off_b[hl], data_y, nullptr, nullptr,
+          nullptr, 0, 0, 0, 0, D.loss_acc, head_part, head_loss, head_cnt_d, nullptr);
     } else {
       softmax_ce_kernel<<<sms, 256, 0, s>>>(none, N_data, logits_d, dims[L], data_y, nullptr, nullptr,
                                             D.loss_acc, nullptr);
@@ -925,6 +844,17 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     LBBSP_CUDA_CHECK(m.alloc(&m.partial, static_cast<size_t>(P) * m.n_local));
   else
     m.partial = m.grad;  // one worker: the dW GEMM writes the gradient directly
+  if (small_head) {
+    const int nsm = num_sms();
+    LBBSP_CUDA_CHECK(m.alloc(&m.head_part, static_cast<size_t>(nsm) * kHeadVals));
+    LBBSP_CUDA_CHECK(m.alloc(&m.head_loss, static_cast<size_t>(nsm)));
+    LBBSP_CUDA_CHECK(m.alloc(&m.head_cnt, static_cast<size_t>(m.n_local)));
+    LBBSP_CUDA_CHECK(m.alloc(&m.head_cnt_d, 1));
+    LBBSP_CUDA_CHECK(cudaFuncSetAttribute(head_mma_kernel<true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadMmaSmem));
+    LBBSP_CUDA_CHECK(cudaFuncSetAttribute(head_mma_kernel<false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadMmaSmem));
+  }
   LBBSP_CUDA_CHECK(m.alloc(&m.data_x, static_cast<size_t>(m.N_data) * d0));
   LBBSP_CUDA_CHECK(m.alloc(&m.data_y, m.N_data));
   LBBSP_CUDA_CHECK(m.alloc(&m.X, static_cast<size_t>(m.B_cap) * d0));
@@ -984,6 +914,7 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   D.static_sizes = c.static_sizes;
   int sms = num_sms();
   D.sm_budget = c.sm_budget > 0 && c.sm_budget < sms ? c.sm_budget : sms;
+  D.dbg_legacy_gather = getenv("LBBSP_DBG_GATHER_OLD") ? 1 : 0;
   D.trace_len = c.trace_len;
   const size_t TL = static_cast<size_t>(n) * c.trace_len;
   double *tc_ = nullptr, *tm_ = nullptr, *tx_ = nullptr, *sh = nullptr;
@@ -1080,10 +1011,14 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     // its CTA partition idle (the emulated-worker C2 shapes)
     const double rows_per_worker = static_cast<double>(m.B_total) / c.world / m.n_local;
     const int ctas_per_worker = std::max(1, D.sm_budget / m.n_local);
+    // widest N tile that still gives a worker about one tile per CTA
     auto pick_bn = [&](double mrows, int ncols) {
-      if (ncols < 256) return 128;
-      const double tiles256 = std::ceil(mrows / 128.0) * std::ceil(ncols / 256.0);
-      return tiles256 * 2 < ctas_per_worker ? 128 : 256;
+      for (int bn : {256, 128}) {
+        if (ncols < bn) continue;
+        const double tiles = std::ceil(mrows / 128.0) * std::ceil(ncols / static_cast<double>(bn));
+        if (tiles >= 0.75 * ctas_per_worker) return bn;
+      }
+      return 64;
     };
     const int bn = pick_bn(rows_per_worker, dout);
     const int epi = last ? tc::kEpiBiasBf16 : tc::kEpiBiasReluBf16;
@@ -1287,8 +1222,23 @@ extern "C" int lbbsp_mlp_phase_times(lbbsp_mlp* m, double* h_phase_ns, int* n_ph
   return LBBSP_OK;
 }
 
+extern "C" int lbbsp_mlp_worker_phase_times(lbbsp_mlp* m, double* h_ns, int* n_phases) {
+  LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->stream));
+  std::vector<unsigned long long> t(2ull * kMaxPhases * m->n_local);
+  LBBSP_CUDA_CHECK(cudaMemcpy(t.data(), m->D.timing, sizeof(unsigned long long) * t.size(),
+                              cudaMemcpyDeviceToHost));
+  *n_phases = m->n_phases;
+  for (int p = 0; p < m->n_phases; ++p)
+    for (int i = 0; i < m->n_local; ++i) {
+      const unsigned long long s = t[2 * (p * m->n_local + i)], e = t[2 * (p * m->n_local + i) + 1];
+      h_ns[p * m->n_local + i] = (s != ~0ull && e > s) ? static_cast<double>(e - s) : 0.0;
+    }
+  return LBBSP_OK;
+}
+
 extern "C" int lbbsp_mlp_work(lbbsp_mlp* m, double* gemm_flops, double* reduce_bytes) {
   if (gemm_flops) *gemm_flops = m->gemm_flops;
   if (reduce_bytes) *reduce_bytes = m->reduce_bytes;
   return LBBSP_OK;
 }
+

@@ -647,6 +647,16 @@ def load_scenario(path) -> Scenario:
     return Scenario(path)
 
 
+def make_benchmark_series(seed: int, iterations=1200, regime_length=50, high_band=(0.75, 1.0),
+                          low_band=(0.30, 0.55), spike_mult=3.0, spike_prob=0.02):
+    """make_benchmark_series (cluster_sim.cpp:41-64) -> (cpu, mem, mult) arrays."""
+    c, m, x = np.zeros(iterations), np.zeros(iterations), np.zeros(iterations)
+    check(lib().lbbsp_benchmark_series(C.c_uint64(seed), iterations, regime_length, *high_band,
+                                       *low_band, spike_mult, spike_prob, c.ctypes.data_as(_dp),
+                                       m.ctypes.data_as(_dp), x.ctypes.data_as(_dp)))
+    return c, m, x
+
+
 def predictor_series_rmse(kind, base: PredictorConfig, cpu, mem, mult, base_speed: float,
                           seed: int, measure_from: int) -> float:
     """predictor_series_rmse (cluster_sim.cpp:645-672), one device CTA."""

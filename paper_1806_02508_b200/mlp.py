@@ -203,6 +203,15 @@ class MlpEngine:
         check(_L().lbbsp_mlp_phase_times(self._h, buf.ctypes.data_as(_dp), C.byref(n)))
         return buf[: n.value] * 1e-9
 
+    def worker_phase_times(self):
+        """[n_phases, n_local] device seconds of each worker in each phase (last round)"""
+        buf = np.zeros(64 * self.cfg.n_workers_local)
+        n = C.c_int()
+        f = _L().lbbsp_mlp_worker_phase_times
+        f.argtypes = [C.c_void_p, _dp, C.POINTER(C.c_int)]
+        check(f(self._h, buf.ctypes.data_as(_dp), C.byref(n)))
+        return buf[: n.value * self.cfg.n_workers_local].reshape(n.value, -1) * 1e-9
+
     def records(self):
         cap = self.cfg.max_iterations
         n = self.n_total

@@ -9,7 +9,7 @@ for r in rows[hi + 1:]:
     if len(r) <= vi:
         continue
     v = float(r[vi].replace(",", ""))
-    v *= {"msecond": 1e3, "usecond": 1.0, "nsecond": 1e-3}.get(r[ui], 1.0)
+    v *= {"msecond": 1e3, "ms": 1e3, "usecond": 1.0, "us": 1.0, "nsecond": 1e-3, "ns": 1e-3}.get(r[ui], 1.0)
     name = r[ki]
     name = name[:100]
     agg.setdefault(name, []).append(v)

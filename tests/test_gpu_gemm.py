@@ -64,7 +64,7 @@ def test_gemm_f32_all_majors(M, N, K, a_mn, b_mn):
     Af = (A.float().t() if a_mn else A.float())
     Bf = (B.float() if b_mn else B.float().t())
     ref = Af @ Bf
-    for bn in (128, 256):
+    for bn in (64, 128, 256):
         out = run_gemm(A, B, M, N, K, a_mn, b_mn, 0, bn=bn)
         err = (out - ref).abs().max().item()
         assert err <= 1e-3 * max(1.0, ref.abs().max().item()), (bn, err)

@@ -81,13 +81,7 @@ def test_device_metrics_equal_host_compute_metrics(sg, tmp_path, name):
 def test_series_rmse_matches_reference(ref):
     """predictor_series_rmse (cluster_sim.cpp:645-672) on device vs the reference."""
     lb = L
-    c, m, x = np.zeros(600), np.zeros(600), np.zeros(600)
-    import ctypes as C
-    from paper_1806_02508_b200._lib import check, lib
-    _dp = C.POINTER(C.c_double)
-    check(lib().lbbsp_benchmark_series(C.c_uint64(21), 600, 40, 0.75, 1.0, 0.3, 0.55, 3.0, 0.02,
-                                       c.ctypes.data_as(_dp), m.ctypes.data_as(_dp),
-                                       x.ctypes.data_as(_dp)))
+    c, m, x = L.make_benchmark_series(21, iterations=600, regime_length=40)
     for kind in (abi.PRED_MEMORYLESS, abi.PRED_EMA, abi.PRED_NARX, abi.PRED_PERFECT):
         base = abi.PredictorConfig.default(kind, warmup_iterations=60)
         got = lb.predictor_series_rmse(kind, base, c, m, x, 10.0, 1234, 60)

@@ -136,7 +136,6 @@ __global__ void init_params_kernel(float* p, bf16* pb, long long off_w, long lon
 // ---------------------------------------------------------------------------
 struct PlanDev {
   int n_total, n_local, rank, B_total, scheme, static_sizes, sm_budget, trace_len;
-  int dbg_legacy_gather;
   const int* static_sizes_d;
   const double* trace_c;
   const double* trace_m;
@@ -266,14 +265,6 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
   const int step = 256 * gridDim.x;
   const uint4* src4 = reinterpret_cast<const uint4*>(data_x);
   uint4* dst4 = reinterpret_cast<uint4*>(X);
-  if (D.dbg_legacy_gather) {
-    for (long long t = blockIdx.x * 256ll + threadIdx.x; t < total; t += 256ll * gridDim.x) {
-      const int r = static_cast<int>(t / vec), v = static_cast<int>(t % vec);
-      const int src = idx[r];
-      reinterpret_cast<uint4*>(X)[static_cast<long long>(r) * vec + v] =
-          reinterpret_cast<const uint4*>(data_x)[static_cast<long long>(src) * vec + v];
-    }
-  } else
   // four independent row reads in flight per thread
   for (int t0 = blockIdx.x * 256 + threadIdx.x; t0 < total; t0 += 4 * step) {
     uint4 v[4];
@@ -637,8 +628,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   const int sms = D.sm_budget;
   plan_kernel<<<1, 256, 0, s>>>(D);
   ++nl;
-  const int gather_ctas = getenv("LBBSP_DBG_GATHER_SMS")
-      ? sms : std::max(sms, std::min(sms * 8, (B_cap * (dims[0] / 8) + 1023) / 1024));
+  const int gather_ctas = std::max(sms, std::min(sms * 8, (B_cap * (dims[0] / 8) + 1023) / 1024));
   gather_kernel<<<gather_ctas, 256, 0, s>>>(D, streams, B_total, data_x, data_y, dims[0], X, y, row_scale,
                                      partial, P, reg_off, reg_len, n_reg);
   ++nl;
@@ -914,7 +904,6 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   D.static_sizes = c.static_sizes;
   int sms = num_sms();
   D.sm_budget = c.sm_budget > 0 && c.sm_budget < sms ? c.sm_budget : sms;
-  D.dbg_legacy_gather = getenv("LBBSP_DBG_GATHER_OLD") ? 1 : 0;
   D.trace_len = c.trace_len;
   const size_t TL = static_cast<size_t>(n) * c.trace_len;
   double *tc_ = nullptr, *tm_ = nullptr, *tx_ = nullptr, *sh = nullptr;

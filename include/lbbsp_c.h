@@ -236,7 +236,8 @@ int lbbsp_aggregate(const double* h_grads, const int* h_sizes, int n, int dim, i
                     double* h_out);
 
 /* ======================================================================== */
-/* Fused iteration driver (A1 step_sync, cluster_sim.cpp:349-469)           */
+/* Fused iteration driver (A1 step_sync, cluster_sim.cpp:349-469; ASP/SSP  */
+/* step_async :486-631 as one persistent event-loop CTA)                    */
 /* ======================================================================== */
 
 enum { LBBSP_SCHEME_BSP = 0, LBBSP_SCHEME_ASP = 1, LBBSP_SCHEME_SSP = 2, LBBSP_SCHEME_LBBSP = 3 };
@@ -311,6 +312,8 @@ typedef struct {
   /* PredictorConfig::initial_weights (predictor.cpp:264-269): NULL or "" =>
    * narx_init(mix_seed(seed, 0x9ced1c70, i)); else load_narx_csv(path) */
   const char* narx_weights_path;
+  /* SchemeConfig::staleness_threshold (coordination.hpp:15-19), SSP only */
+  int staleness_threshold;
 } lbbsp_sim_cfg;
 
 /* IterationRecord (cluster_sim.hpp:149-155) + WorkerIterationStats (:139-147),
@@ -344,6 +347,11 @@ int lbbsp_sim_records(lbbsp_sim* sim, int max_rows, int* rows, lbbsp_iter_scalar
                       int* batch, double* tp, double* tm, double* wait, double* v_pred,
                       double* v_actual, double* params);
 int lbbsp_sim_status(lbbsp_sim* sim, int* done, int* converged);
+/* Worker ids of the record slots ([rows*n]) and the number of worker stats
+ * per record ([rows]): n for BSP/LB-BSP/SSP rounds, 1 for ASP updates. */
+int lbbsp_sim_record_workers(lbbsp_sim* sim, int max_rows, int* worker_id, int* row_workers);
+/* SimResult::total_time_s and max_ssp_skew (cluster_sim.cpp:633-643). */
+int lbbsp_sim_summary(lbbsp_sim* sim, double* total_time_s, int64_t* max_ssp_skew);
 /* Number of CUDA kernels one iteration launches (captured graph nodes). */
 int lbbsp_sim_launches_per_iteration(lbbsp_sim* sim, int* launches);
 
@@ -362,6 +370,8 @@ typedef struct {
   const double* wait;
   const double* v_pred;
   const double* v_actual;
+  const int* worker_id;    /* [rows*n] or NULL (slot i = worker i)          */
+  const int* row_workers;  /* [rows] stats per row or NULL (n; 1 for ASP)   */
 } lbbsp_records_view;
 
 /* Metrics (cluster_sim.hpp:157-163) */

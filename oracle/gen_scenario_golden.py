@@ -54,6 +54,25 @@ EXTRA = {
                         "benchmark_high_band": [0.7, 0.95], "benchmark_low_band": [0.2, 0.5],
                         "max_iterations": 200, "convergence_loss": 1e-4, "seed": 11,
                         "paired_sim": True},
+    # ASP / SSP (Simulation::step_async, cluster_sim.cpp:486-631)
+    "asp_hetero_narx": {"scheme": "asp", "workers": 4, "total_budget": 512, "preset": "hetero-l3",
+                        "predictor": "narx", "warmup_iterations": 20, "max_iterations": 300,
+                        "convergence_loss": 1e-4, "seed": 4},
+    "ssp_hetero": {"scheme": "ssp", "staleness_threshold": 2, "workers": 6, "total_budget": 600,
+                   "preset": "hetero-l3", "predictor": "ema", "warmup_iterations": 30,
+                   "max_iterations": 150, "convergence_loss": 1e-4, "seed": 6},
+    "ssp_gpu_cluster": {"scheme": "ssp", "staleness_threshold": 1, "workers": 4,
+                        "total_budget": 400, "gpu_profiles": [
+                            {"sec_per_sample": 0.002, "base_time_s": 0.05, "saturation_point": 20,
+                             "oom_point": 300, "count": 2},
+                            {"sec_per_sample": 0.0007, "base_time_s": 0.05,
+                             "saturation_point": 30, "oom_point": 400, "count": 2}],
+                        "base_comm_s": 0.1,
+                        "bandwidth_drop": {"worker": 1, "at_iteration": 40, "comm_factor": 4.0},
+                        "max_iterations": 120, "convergence_loss": 1e-4, "seed": 2},
+    "asp_trace": {"scheme": "asp", "workers": 4, "total_budget": 256, "trace_path": "@trace",
+                  "predictor": "memoryless", "max_iterations": 250, "convergence_loss": 1e-4,
+                  "seed": 8, "base_comm_s": 1.0},
 }
 
 # Malformed configs: (name, json text or dict); the expected text is the reference's.
@@ -184,7 +203,8 @@ def main():
                              "records_sha": sha(os.path.join(od, "records.csv")),
                              "metrics_json": open(os.path.join(od, "metrics.json")).read()}
         # compare
-        cmp_names = ["homo_smoke", "hetero_l3_bsp", "hetero_l3_lbbsp", "gpu_cluster", "trace_bsp"]
+        cmp_names = ["homo_smoke", "hetero_l3_bsp", "hetero_l3_lbbsp", "gpu_cluster", "trace_bsp",
+                     "asp_hetero_narx", "ssp_hetero"]
         od = os.path.join(d, "out_cmp")
         assert ref.cmd_compare([paths[n] for n in cmp_names], od) == 0
         out["compare"] = {"configs": cmp_names,

@@ -868,18 +868,215 @@ static void predictor_train(const lbbsp_predictor_cfg* pc, worker_rt* rt) {
   orc_narx_train(&rt->model, rt->v, rt->c, rt->m, rt->len, &tc, &rep, NULL, 0);
 }
 
+/* ---- ASP / SSP: Simulation::step_async (cluster_sim.cpp:486-631) ---------- */
+typedef struct {
+  const lbbsp_sim_cfg* c;
+  int n, B, d, N;
+  const double *feat, *lab;
+  double* params;
+  const int* equal;
+  const dynamics* D;
+  worker_rt* W;
+  int gpu_mode;
+} async_ctx;
+
+typedef struct {
+  int64_t completed;
+  int running, blocked;
+  double block_start, pending_wait, finish;
+  double* grad;          /* inflight gradient [d] */
+  double st[6];          /* x, tp, tm, wait, v_pred, v_act */
+  double c, m;           /* inflight resource state */
+} async_rt;
+
+/* start_worker, cluster_sim.cpp:504-536 */
+static int async_start(const async_ctx* A, async_rt* R, int w, double now, int* stream) {
+  const lbbsp_sim_cfg* c = A->c;
+  async_rt* rt = &R[w];
+  const int64_t j = rt->completed;
+  double cc, mm, mult;
+  dyn_at(A->D, w, j, now, &cc, &mm, &mult);
+  const int x = A->equal[w];
+  double tp, va, vp = 0.0;
+  if (A->gpu_mode) {
+    const lbbsp_gpu_profile* g = &c->gpu_profiles[w];
+    if (x > g->oom_point) return err(LBBSP_RUNTIME, "gpu out of memory: batch %d exceeds oom point %d", x, g->oom_point);
+    tp = g->sec_per_sample * (double)(x > g->saturation_point ? x : g->saturation_point) + g->base_time_s;
+    va = (double)x / tp;
+  } else {
+    va = effective_speed(c->base_speed, cc, mm) * mult;
+    tp = (double)x / va;
+    if (A->W[w].len >= 1)
+      vp = c->predictor.kind == LBBSP_PRED_PERFECT ? va : predictor_predict(&c->predictor, &A->W[w], cc, mm);
+  }
+  const double f = (c->bw_worker == w && c->bw_at_iteration <= j) ? c->bw_factor : 1.0;
+  const double tm = c->base_comm_s * f;
+  orc_sample_stream(c->seed, j, A->B, A->N, stream);
+  int off = 0;
+  for (int i = 0; i < w; ++i) off += A->equal[i];
+  int st = orc_batch_gradient(A->feat, A->lab, A->N, A->d, A->params, stream + off, x, rt->grad);
+  if (st) return st;
+  rt->st[0] = x;
+  rt->st[1] = tp;
+  rt->st[2] = tm;
+  rt->st[3] = rt->pending_wait;
+  rt->st[4] = vp;
+  rt->st[5] = va;
+  rt->c = cc;
+  rt->m = mm;
+  rt->pending_wait = 0.0;
+  rt->running = 1;
+  rt->finish = now + tp + tm;
+  return 0;
+}
+
+static int64_t min_completed(const async_rt* R, int n) {
+  int64_t lo = INT64_MAX;
+  for (int i = 0; i < n; ++i) lo = R[i].completed < lo ? R[i].completed : lo;
+  return lo;
+}
+
+static int async_run(const async_ctx* A, int max_rows, int* count_o, lbbsp_iter_scalars* sc,
+                     int* batch_o, double* tp_o, double* tm_o, double* wait_o, double* vpred_o,
+                     double* vact_o, double* params_o, int* converged_o, int* worker_o, int* nw_o) {
+  const lbbsp_sim_cfg* c = A->c;
+  const int n = A->n, d = A->d, ssp = c->scheme == LBBSP_SCHEME_SSP;
+  const int64_t stale = c->staleness_threshold;
+  const int ring = c->staleness_threshold + 3;
+  async_rt* R = (async_rt*)calloc((size_t)n, sizeof(async_rt));
+  for (int i = 0; i < n; ++i) R[i].grad = (double*)calloc((size_t)d, sizeof(double));
+  double* rg = (double*)calloc((size_t)ring * n * d, sizeof(double));
+  double* rs = (double*)calloc((size_t)ring * n * 6, sizeof(double));
+  int* rcount = (int*)calloc((size_t)ring, sizeof(int));
+  int* stream = (int*)malloc(sizeof(int) * (size_t)A->B);
+  double* agg = (double*)malloc(sizeof(double) * (size_t)d);
+  int* one = (int*)malloc(sizeof(int));
+  double now = 0.0, last_update = 0.0;
+  int64_t clock = 0;
+  int st = 0, count = 0, below = 0, converged = 0;
+  for (int i = 0; i < n && !st; ++i) st = async_start(A, R, i, 0.0, stream); /* ctor (:293-294) */
+  while (!st) {
+    int next = -1; /* earliest finish, ties to the lowest id */
+    for (int i = 0; i < n; ++i) {
+      if (!R[i].running) continue;
+      if (next < 0 || R[i].finish < R[next].finish) next = i;
+    }
+    if (next < 0) break;
+    async_rt* rt = &R[next];
+    worker_rt* W = &A->W[next];
+    now = rt->finish;
+    rt->running = 0;
+    rt->completed += 1;
+    W->v[W->len] = rt->st[5]; /* observe (:309-313) */
+    W->c[W->len] = rt->c;
+    W->m[W->len] = rt->m;
+    W->comm[W->len] = rt->st[2];
+    W->len += 1;
+    predictor_train(&c->predictor, W);
+    int rec = 0, slot = 0, nw = 0;
+    double lossv = 0.0;
+    const double* g_src = NULL;
+    if (!ssp) {
+      *one = (int)rt->st[0];
+      orc_aggregate(rt->grad, one, 1, d, 0, agg);
+      g_src = agg;
+      nw = 1;
+      rec = 1;
+    } else {
+      slot = (int)((rt->completed - 1) % ring);
+      memcpy(rg + ((size_t)slot * n + next) * d, rt->grad, sizeof(double) * d);
+      memcpy(rs + ((size_t)slot * n + next) * 6, rt->st, sizeof rt->st);
+      if (++rcount[slot] == n) {
+        orc_aggregate(rg + (size_t)slot * n * d, A->equal, n, d, 0, agg);
+        g_src = agg;
+        nw = n;
+        rec = 1;
+      }
+    }
+    if (rec) {
+      for (int j = 0; j < d; ++j) A->params[j] -= c->learning_rate * g_src[j]; /* apply_update */
+      clock += 1;
+      double nrm = 0.0;
+      for (int j = 0; j < d; ++j) nrm += g_src[j] * g_src[j];
+      nrm = sqrt(nrm);
+      orc_loss(A->feat, A->lab, A->N, d, A->params, &lossv);
+      if (count < max_rows) {
+        if (sc) {
+          sc[count].k = clock - 1;
+          sc[count].grad_norm = nrm;
+          sc[count].loss = lossv;
+          sc[count].wall_s = now - last_update;
+        }
+        if (nw_o) nw_o[count] = nw;
+        for (int i = 0; i < nw; ++i) {
+          const size_t o = (size_t)count * n + i;
+          const int wid = ssp ? i : next;
+          const double* sv = ssp ? rs + ((size_t)slot * n + i) * 6 : rt->st;
+          if (worker_o) worker_o[o] = wid;
+          if (batch_o) batch_o[o] = (int)sv[0];
+          if (tp_o) tp_o[o] = sv[1];
+          if (tm_o) tm_o[o] = sv[2];
+          if (wait_o) wait_o[o] = sv[3];
+          if (vpred_o) vpred_o[o] = sv[4];
+          if (vact_o) vact_o[o] = sv[5];
+        }
+        if (params_o) memcpy(params_o + (size_t)count * d, A->params, sizeof(double) * d);
+      }
+      last_update = now;
+      if (ssp) rcount[slot] = 0;
+    }
+    /* restart or park the finisher, then re-check the blocked workers */
+    if (!ssp) {
+      st = async_start(A, R, next, now, stream);
+    } else {
+      if (rt->completed - min_completed(R, n) <= stale) {
+        st = async_start(A, R, next, now, stream);
+      } else {
+        rt->blocked = 1;
+        rt->block_start = now;
+      }
+      for (int i = 0; i < n && !st; ++i) {
+        if (!R[i].blocked) continue;
+        if (R[i].completed - min_completed(R, n) <= stale) {
+          R[i].blocked = 0;
+          R[i].pending_wait = now - R[i].block_start;
+          st = async_start(A, R, i, now, stream);
+        }
+      }
+    }
+    if (rec) { /* check_stop (:326-334) */
+      ++count;
+      below = lossv < c->convergence_loss ? below + 1 : 0;
+      if (below >= c->convergence_consecutive) {
+        converged = 1;
+        break;
+      }
+      if (count >= c->max_updates) break;
+    }
+  }
+  *count_o = count;
+  *converged_o = converged;
+  for (int i = 0; i < n; ++i) free(R[i].grad);
+  free(R); free(rg); free(rs); free(rcount); free(stream); free(agg); free(one);
+  return st;
+}
+
 /* Simulation ctor (cluster_sim.cpp:247-296) + run (:633-643) + step_sync
  * (:349-469) for the BSP / LB-BSP schemes. */
 int orc_sim_run(const lbbsp_sim_cfg* c, int max_rows, int* rows, lbbsp_iter_scalars* sc,
                 int* batch_o, double* tp_o, double* tm_o, double* wait_o, double* vpred_o,
-                double* vact_o, double* params_o, int* converged_o) {
+                double* vact_o, double* params_o, int* converged_o, int* worker_o,
+                int* nw_o) {
   const int n = c->n_workers;
   const int B = c->total_budget;
   const int gpu_mode = c->gpu_profiles != NULL;
   if (n < 1) return err(LBBSP_INVALID_ARGUMENT, "simulation: need at least one worker");
   if (B < n) return err(LBBSP_INVALID_ARGUMENT, "simulation: total_budget below worker count");
-  if (c->scheme != LBBSP_SCHEME_BSP && c->scheme != LBBSP_SCHEME_LBBSP)
-    return err(LBBSP_INVALID_ARGUMENT, "oracle: only bsp / lb-bsp (sync) schemes are on the hot path");
+  if (c->scheme < LBBSP_SCHEME_BSP || c->scheme > LBBSP_SCHEME_LBBSP)
+    return err(LBBSP_INVALID_ARGUMENT, "simulation: unknown scheme %d", c->scheme);
+  if (c->staleness_threshold < 0)
+    return err(LBBSP_INVALID_ARGUMENT, "simulation: staleness_threshold must be >= 0");
+  const int async = c->scheme == LBBSP_SCHEME_ASP || c->scheme == LBBSP_SCHEME_SSP;
   if (c->scheme != LBBSP_SCHEME_LBBSP && B % n != 0)
     return err(LBBSP_INVALID_ARGUMENT,
                "simulation: bsp/asp/ssp need total_budget divisible by workers");
@@ -986,7 +1183,7 @@ int orc_sim_run(const lbbsp_sim_cfg* c, int max_rows, int* rows, lbbsp_iter_scal
                        D.bmem + (size_t)i * bc.iterations, D.bmult + (size_t)i * bc.iterations);
   }
 
-  const int64_t cap = c->max_updates > 0 ? c->max_updates : 1;
+  const int64_t cap = (c->max_updates > 0 ? c->max_updates : 1) + (async ? c->staleness_threshold + 2 : 0);
   lbbsp_narx_model initial; /* PredictorConfig::initial_weights (predictor.cpp:265-266) */
   const int have_initial = c->narx_weights_path && c->narx_weights_path[0];
   if (have_initial) {
@@ -1018,7 +1215,12 @@ int orc_sim_run(const lbbsp_sim_cfg* c, int max_rows, int* rows, lbbsp_iter_scal
   int below = 0, converged = 0, count = 0, cursor = 0;
   double now = 0.0; /* Simulation::now_ */
 
-  for (int64_t k = 0;; ++k) {
+  if (async) {
+    async_ctx A = {c, n, B, d, N, feat, lab, params, equal, &D, W, gpu_mode};
+    st = async_run(&A, max_rows, &count, sc, batch_o, tp_o, tm_o, wait_o, vpred_o, vact_o,
+                   params_o, &converged, worker_o, nw_o);
+  }
+  for (int64_t k = 0; !async; ++k) {
     /* P1-P3 (:355-367) */
     for (int i = 0; i < n; ++i) {
       dyn_at(&D, i, k, now, &rc[i], &rm[i], &rmult[i]);
@@ -1117,6 +1319,9 @@ int orc_sim_run(const lbbsp_sim_cfg* c, int max_rows, int* rows, lbbsp_iter_scal
         if (vact_o) vact_o[o] = vact[i];
       }
       if (params_o) memcpy(params_o + (size_t)count * d, params, sizeof(double) * d);
+      if (nw_o) nw_o[count] = n;
+      if (worker_o)
+        for (int i = 0; i < n; ++i) worker_o[(size_t)count * n + i] = i;
     }
     ++count;
     /* P10 observe + train_rotation (:458-464, :309-324) */

@@ -170,15 +170,20 @@ class CpuChecker:
         keys = ("tp", "tm", "wait", "v_pred", "v_actual")
         arr = {k: np.zeros(rows_cap * n) for k in keys}
         batch = np.zeros(rows_cap * n, np.int32)
+        wid = np.zeros(rows_cap * n, np.int32)
+        nw = np.zeros(rows_cap, np.int32)
         params = np.zeros(rows_cap * d)
         rows = C.c_int(); conv = C.c_int()
         self._check(self._fn("sim_run")(
             C.byref(cfg), C.c_int(rows_cap), C.byref(rows), sc, batch.ctypes.data_as(_ip),
             *[arr[k].ctypes.data_as(_dp) for k in keys],
-            params.ctypes.data_as(_dp), C.byref(conv)))
+            params.ctypes.data_as(_dp), C.byref(conv), wid.ctypes.data_as(_ip),
+            nw.ctypes.data_as(_ip)))
         r = rows.value
         out = {k: v[: r * n].reshape(r, n) for k, v in arr.items()}
         out["batch"] = batch[: r * n].reshape(r, n)
+        out["worker_id"] = wid[: r * n].reshape(r, n)
+        out["row_workers"] = nw[:r].copy()
         out["params"] = params[: r * d].reshape(r, d)
         out["k"] = np.array([sc[i].k for i in range(r)])
         out["grad_norm"] = np.array([sc[i].grad_norm for i in range(r)])

@@ -99,6 +99,7 @@ SimConfig to_sim(const lbbsp_sim_cfg& c) {
   SimConfig cfg;
   cfg.scheme.kind = static_cast<SchemeKind>(c.scheme);
   cfg.scheme.total_budget = c.total_budget;
+  cfg.scheme.staleness_threshold = c.staleness_threshold;
   const int n = c.n_workers;
   if (c.gpu_profiles) {
     for (int i = 0; i < n; ++i) {
@@ -374,7 +375,8 @@ int ref_benchmark_series(uint64_t seed, int iterations, double* cpu, double* mem
 // Full reference Simulation run (cluster_sim.cpp:247-296, 633-643) flattened.
 int ref_sim_run(const lbbsp_sim_cfg* c, int max_rows, int* rows, lbbsp_iter_scalars* sc,
                 int* batch, double* tp, double* tm, double* wait, double* v_pred,
-                double* v_actual, double* params, int* converged) {
+                double* v_actual, double* params, int* converged, int* worker_id,
+                int* row_workers) {
   REF_GUARD({
     Simulation sim(to_sim(*c));
     const SimResult r = sim.run();
@@ -384,9 +386,11 @@ int ref_sim_run(const lbbsp_sim_cfg* c, int max_rows, int* rows, lbbsp_iter_scal
     for (const auto& rec : r.records) {
       if (count >= max_rows) break;
       if (sc) sc[count] = lbbsp_iter_scalars{rec.k, rec.grad_norm, rec.loss, rec.wall_s};
-      for (int i = 0; i < n; ++i) {
-        const auto& w = rec.workers[static_cast<std::size_t>(i)];
+      if (row_workers) row_workers[count] = static_cast<int>(rec.workers.size());
+      for (std::size_t i = 0; i < rec.workers.size(); ++i) {
+        const auto& w = rec.workers[i];
         const std::size_t o = static_cast<std::size_t>(count) * n + i;
+        if (worker_id) worker_id[o] = w.worker_id;
         if (batch) batch[o] = w.batch;
         if (tp) tp[o] = w.tp_s;
         if (tm) tm[o] = w.tm_s;

@@ -59,6 +59,8 @@ SIGNATURES = {
     "lbbsp_sim_launches_per_iteration": [_vp, _ip],
     "lbbsp_benchmark_series": [C.c_uint64, C.c_int, C.c_int] + [C.c_double] * 6 + [_dp] * 3,
     "lbbsp_sim_metrics": [_vp, C.c_int, C.POINTER(abi.Metrics)],
+    "lbbsp_sim_record_workers": [_vp, C.c_int, _ip, _ip],
+    "lbbsp_sim_summary": [_vp, _dp, C.POINTER(C.c_int64)],
     "lbbsp_compute_metrics": [C.POINTER(abi.RecordsView), C.c_int, C.c_int, C.c_int,
                               C.POINTER(abi.Metrics)],
     "lbbsp_write_records_csv": [C.POINTER(abi.RecordsView), C.c_char_p],

@@ -112,7 +112,7 @@ class SimConfig(C.Structure):
         ("max_updates", C.c_int64), ("seed", C.c_uint64),
         ("trace_offsets", C.POINTER(C.c_int)), ("trace_t", C.POINTER(C.c_double)),
         ("trace_cpu", C.POINTER(C.c_double)), ("trace_mem", C.POINTER(C.c_double)),
-        ("narx_weights_path", C.c_char_p),
+        ("narx_weights_path", C.c_char_p), ("staleness_threshold", C.c_int),
     ]
 
 
@@ -126,7 +126,8 @@ class RecordsView(C.Structure):
     _fields_ = [("rows", C.c_int), ("n", C.c_int), ("scalars", C.POINTER(IterScalars)),
                 ("batch", C.POINTER(C.c_int)), ("tp", C.POINTER(C.c_double)),
                 ("tm", C.POINTER(C.c_double)), ("wait", C.POINTER(C.c_double)),
-                ("v_pred", C.POINTER(C.c_double)), ("v_actual", C.POINTER(C.c_double))]
+                ("v_pred", C.POINTER(C.c_double)), ("v_actual", C.POINTER(C.c_double)),
+                ("worker_id", C.POINTER(C.c_int)), ("row_workers", C.POINTER(C.c_int))]
 
 
 class Metrics(C.Structure):
@@ -156,7 +157,7 @@ def make_sim_config(scheme="lb-bsp", workers=4, total_budget=512, preset="hetero
                     bandwidth_drop=None, learning_rate=0.5, dataset_seed=7, dataset_size=1000,
                     dataset_dim=10, dataset_noise=0.1, convergence_loss=0.40,
                     convergence_consecutive=10, max_updates=500, seed=1, benchmark=None,
-                    traces=None, narx_weights_path=None):
+                    traces=None, narx_weights_path=None, staleness_threshold=0):
     """Defaults follow SimConfig (cluster_sim.hpp:165-180) and PredictorConfig
     (predictor.hpp:107-114). Returns (cfg, keepalive) -- keep the second value
     alive while cfg is in use (it owns the pointed-to arrays).
@@ -199,6 +200,7 @@ def make_sim_config(scheme="lb-bsp", workers=4, total_budget=512, preset="hetero
     c.dataset_noise = dataset_noise
     c.convergence_loss, c.convergence_consecutive = convergence_loss, convergence_consecutive
     c.max_updates, c.seed = max_updates, seed
+    c.staleness_threshold = staleness_threshold
     if traces is not None:
         off, t, cp, mm = [0], [], [], []
         for pts in traces:

@@ -514,6 +514,8 @@ extern "C" int lbbsp_aggregate(const double* h_grads, const int* h_sizes, int n,
 struct lbbsp_sim {
   lbbsp_sim_cfg cfg{};
   SimDev dev{};
+  AsyncDev adev{};
+  bool async = false;
   lbbsp_predictor pred;
   std::vector<void*> allocs;
   cudaGraph_t graph = nullptr;
@@ -591,9 +593,11 @@ extern "C" int lbbsp_sim_create(const lbbsp_sim_cfg* cfg, lbbsp_sim** out) {
   // Simulation ctor validation (cluster_sim.cpp:249-283)
   if (n < 1) return set_error(LBBSP_INVALID_ARGUMENT, "simulation: need at least one worker");
   if (B < n) return set_error(LBBSP_INVALID_ARGUMENT, "simulation: total_budget below worker count");
-  if (c.scheme != LBBSP_SCHEME_BSP && c.scheme != LBBSP_SCHEME_LBBSP)
-    return set_error(LBBSP_INVALID_ARGUMENT,
-                     "simulation: only the synchronous bsp / lb-bsp schemes are on the hot path");
+  if (c.scheme < LBBSP_SCHEME_BSP || c.scheme > LBBSP_SCHEME_LBBSP)
+    return set_error(LBBSP_INVALID_ARGUMENT, "simulation: unknown scheme %d", c.scheme);
+  if (c.staleness_threshold < 0)
+    return set_error(LBBSP_INVALID_ARGUMENT, "simulation: staleness_threshold must be >= 0");
+  const bool async = c.scheme == LBBSP_SCHEME_ASP || c.scheme == LBBSP_SCHEME_SSP;
   if (c.scheme != LBBSP_SCHEME_LBBSP && B % n != 0)
     return set_error(LBBSP_INVALID_ARGUMENT,
                      "simulation: bsp/asp/ssp need total_budget divisible by workers");
@@ -724,8 +728,11 @@ extern "C" int lbbsp_sim_create(const lbbsp_sim_cfg* cfg, lbbsp_sim** out) {
   LBBSP_CUDA_CHECK(S->alloc(&d.agg, d.d));
 
   const size_t R = static_cast<size_t>(c.max_updates);
+  // sync: one stream per round; async: one per local iteration j (a worker's
+  // j never exceeds the update count, plus the SSP staleness window)
+  const size_t J = async ? R + (c.scheme == LBBSP_SCHEME_SSP ? c.staleness_threshold + 2 : 1) : R;
   int* streams = nullptr;
-  LBBSP_CUDA_CHECK(S->alloc(&streams, R * B));
+  LBBSP_CUDA_CHECK(S->alloc(&streams, J * B));
   d.streams = streams;
   LBBSP_CUDA_CHECK(S->alloc(&d.k, 1));
   LBBSP_CUDA_CHECK(S->alloc(&d.done, 1));
@@ -765,14 +772,42 @@ extern "C" int lbbsp_sim_create(const lbbsp_sim_cfg* cfg, lbbsp_sim** out) {
     if (int rc = lbbsp_narx_load_csv(c.narx_weights_path, &m)) return rc;
     initial.assign(n, m);
   }
-  int rc = make_pred(&S->pred, &pc, n, static_cast<int>(R), seeds.data(),
+  int rc = make_pred(&S->pred, &pc, n, static_cast<int>(J), seeds.data(),
                      initial.empty() ? nullptr : initial.data());
   if (rc) return rc;
   d.pred = S->pred.dev;
 
   // the whole run's sample streams, generated ahead of the iterations
-  LBBSP_CUDA_CHECK(launch_sample_streams(c.seed, 0, static_cast<int>(R), B, c.dataset_size,
+  LBBSP_CUDA_CHECK(launch_sample_streams(c.seed, 0, static_cast<int>(J), B, c.dataset_size,
                                          streams, nullptr));
+  if (async) {
+    AsyncDev& A = S->adev;
+    S->async = true;
+    A.ssp = c.scheme == LBBSP_SCHEME_SSP;
+    A.stale = c.staleness_threshold;
+    A.ring = c.staleness_threshold + 3;
+    A.n_streams = static_cast<int>(J);
+    LBBSP_CUDA_CHECK(S->alloc(&A.started, 1));
+    LBBSP_CUDA_CHECK(S->alloc(&A.completed, n));
+    LBBSP_CUDA_CHECK(S->alloc(&A.running, n));
+    LBBSP_CUDA_CHECK(S->alloc(&A.blocked, n));
+    LBBSP_CUDA_CHECK(S->alloc(&A.hist_len, n));
+    LBBSP_CUDA_CHECK(S->alloc(&A.block_start, n));
+    LBBSP_CUDA_CHECK(S->alloc(&A.pending_wait, n));
+    LBBSP_CUDA_CHECK(S->alloc(&A.finish, n));
+    LBBSP_CUDA_CHECK(S->alloc(&A.inflight_grad, static_cast<size_t>(n) * d.d));
+    LBBSP_CUDA_CHECK(S->alloc(&A.inflight, static_cast<size_t>(n) * 8));
+    if (A.ssp) {
+      LBBSP_CUDA_CHECK(S->alloc(&A.ring_grads, static_cast<size_t>(A.ring) * n * d.d));
+      LBBSP_CUDA_CHECK(S->alloc(&A.ring_stats, static_cast<size_t>(A.ring) * n * 6));
+      LBBSP_CUDA_CHECK(S->alloc(&A.ring_count, A.ring));
+    }
+    LBBSP_CUDA_CHECK(S->alloc(&A.last_update, 1));
+    LBBSP_CUDA_CHECK(S->alloc(&A.clock, 1));
+    LBBSP_CUDA_CHECK(S->alloc(&A.max_skew, 1));
+    LBBSP_CUDA_CHECK(S->alloc(&A.rec_worker, R * n));
+    LBBSP_CUDA_CHECK(S->alloc(&A.rec_nw, R));
+  }
   LBBSP_CUDA_CHECK(cudaDeviceSynchronize());
   *out = S.release();
   return LBBSP_OK;
@@ -785,6 +820,10 @@ extern "C" int lbbsp_sim_destroy(lbbsp_sim* sim) {
 
 extern "C" int lbbsp_sim_run(lbbsp_sim* sim, int iterations, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (sim->async) {  // ASP/SSP: the whole event loop in one persistent CTA
+    if (iterations > 0) LBBSP_CUDA_CHECK(launch_async_sim(sim->dev, sim->adev, iterations, s));
+    return LBBSP_OK;
+  }
   if (!sim->exec) {
     // warm the function attributes outside capture, then capture one round
     LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&sim->cap_stream, cudaStreamNonBlocking));
@@ -838,7 +877,48 @@ extern "C" int lbbsp_sim_records(lbbsp_sim* sim, int max_rows, int* rows, lbbsp_
 }
 
 extern "C" int lbbsp_sim_launches_per_iteration(lbbsp_sim* sim, int* launches) {
-  *launches = sim->launches ? sim->launches : (sim->dev.pred.kind == LBBSP_PRED_NARX ? 4 : 3);
+  if (sim->async)
+    *launches = 1;  // one persistent kernel for all updates of a run_rounds call
+  else
+    *launches = sim->launches ? sim->launches : (sim->dev.pred.kind == LBBSP_PRED_NARX ? 4 : 3);
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_sim_record_workers(lbbsp_sim* sim, int max_rows, int* worker_id,
+                                        int* row_workers) {
+  LBBSP_CUDA_CHECK(cudaDeviceSynchronize());
+  int r = 0;
+  LBBSP_CUDA_CHECK(cudaMemcpy(&r, sim->dev.rows, sizeof(int), cudaMemcpyDeviceToHost));
+  r = std::min(r, max_rows);
+  const int n = sim->dev.n;
+  if (sim->async) {
+    if (worker_id)
+      LBBSP_CUDA_CHECK(cudaMemcpy(worker_id, sim->adev.rec_worker, sizeof(int) * r * n,
+                                  cudaMemcpyDeviceToHost));
+    if (row_workers)
+      LBBSP_CUDA_CHECK(cudaMemcpy(row_workers, sim->adev.rec_nw, sizeof(int) * r,
+                                  cudaMemcpyDeviceToHost));
+  } else {
+    for (int i = 0; i < r; ++i) {
+      if (row_workers) row_workers[i] = n;
+      for (int w = 0; w < n && worker_id; ++w) worker_id[static_cast<size_t>(i) * n + w] = w;
+    }
+  }
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_sim_summary(lbbsp_sim* sim, double* total_time_s, int64_t* max_ssp_skew) {
+  LBBSP_CUDA_CHECK(cudaDeviceSynchronize());
+  double now = 0.0, last = 0.0;
+  long long skew = 0;
+  LBBSP_CUDA_CHECK(cudaMemcpy(&now, sim->dev.now, sizeof now, cudaMemcpyDeviceToHost));
+  if (sim->async) {
+    LBBSP_CUDA_CHECK(cudaMemcpy(&last, sim->adev.last_update, sizeof last, cudaMemcpyDeviceToHost));
+    LBBSP_CUDA_CHECK(cudaMemcpy(&skew, sim->adev.max_skew, sizeof skew, cudaMemcpyDeviceToHost));
+  }
+  // result.total_time_s = last_update_time_ > 0 ? last_update_time_ : now_
+  if (total_time_s) *total_time_s = last > 0.0 ? last : now;
+  if (max_ssp_skew) *max_ssp_skew = skew;
   return LBBSP_OK;
 }
 
@@ -848,7 +928,8 @@ extern "C" int lbbsp_sim_metrics(lbbsp_sim* sim, int rmse_from_iteration, lbbsp_
   const size_t cap = static_cast<size_t>(sim->dev.max_updates) * sim->dev.n;
   LBBSP_CUDA_CHECK(sim->alloc(&scratch, 2 * cap));
   LBBSP_CUDA_CHECK(sim->alloc(&d_out, 1));
-  LBBSP_CUDA_CHECK(launch_sim_metrics(sim->dev, rmse_from_iteration, scratch, d_out, nullptr));
+  LBBSP_CUDA_CHECK(launch_sim_metrics(sim->dev, sim->async ? sim->adev.rec_nw : nullptr,
+                                      rmse_from_iteration, scratch, d_out, nullptr));
   LBBSP_CUDA_CHECK(cudaMemcpy(out, d_out, sizeof *out, cudaMemcpyDeviceToHost));
   return LBBSP_OK;
 }

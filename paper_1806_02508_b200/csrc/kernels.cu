@@ -710,13 +710,18 @@ cudaError_t launch_sim_iteration(const SimDev& S, cudaStream_t s, int* launches)
 // compute_metrics (cluster_sim.cpp:217-245) on the device-resident records:
 // per-row terms in parallel, then the reference's three sequential folds by
 // three threads of warp 0 (time_total, wait fractions, squared errors).
-__global__ void __launch_bounds__(256) sim_metrics_kernel(SimDev S, int rmse_from, double* wf,
-                                                          double* se, lbbsp_metrics* out) {
+__global__ void __launch_bounds__(256) sim_metrics_kernel(SimDev S, const int* rec_nw, int rmse_from,
+                                                          double* wf, double* se, lbbsp_metrics* out) {
   const int rows = *S.rows, n = S.n;
   const size_t total = static_cast<size_t>(rows) * n;
   for (size_t o = threadIdx.x; o < total; o += blockDim.x) {
     const size_t r = o / n;
     const double wall = S.rec_sc[r].wall_s;
+    if (rec_nw && static_cast<int>(o % n) >= rec_nw[r]) {  // ASP rows carry one worker
+      wf[o] = 0.0;
+      se[o] = -2.0;
+      continue;
+    }
     wf[o] = wall > 0.0 ? ddiv(S.rec_wait[o], wall) : 0.0;
     const double vp = S.rec_vpred[o];
     se[o] = -1.0;  // marks "not counted"
@@ -727,15 +732,21 @@ __global__ void __launch_bounds__(256) sim_metrics_kernel(SimDev S, int rmse_fro
   }
   __syncthreads();
   __shared__ double time_total, wsum, sse;
-  __shared__ long long sse_count;
+  __shared__ long long sse_count, row_count;
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int r = 0; r < rows; ++r) t = dadd(t, S.rec_sc[r].wall_s);
     time_total = t;
   } else if (threadIdx.x == 1) {
     double a = 0.0;
-    for (size_t o = 0; o < total; ++o) a = dadd(a, wf[o]);
+    long long c = 0;
+    for (size_t o = 0; o < total; ++o)
+      if (se[o] != -2.0) {
+        a = dadd(a, wf[o]);
+        ++c;
+      }
     wsum = a;
+    row_count = c;
   } else if (threadIdx.x == 2) {
     double a = 0.0;
     long long c = 0;
@@ -754,17 +765,17 @@ __global__ void __launch_bounds__(256) sim_metrics_kernel(SimDev S, int rmse_fro
     m.updates_to_convergence = rows;
     if (rows > 0) {
       m.mean_per_update_time = ddiv(time_total, static_cast<double>(rows));
-      m.wastage = total > 0 ? ddiv(wsum, static_cast<double>(total)) : 0.0;
+      m.wastage = row_count > 0 ? ddiv(wsum, static_cast<double>(row_count)) : 0.0;
       m.predictor_rmse = sse_count > 0 ? __dsqrt_rn(ddiv(sse, static_cast<double>(sse_count))) : 0.0;
     }
     *out = m;
   }
 }
 
-cudaError_t launch_sim_metrics(const SimDev& S, int rmse_from, double* scratch,
+cudaError_t launch_sim_metrics(const SimDev& S, const int* rec_nw, int rmse_from, double* scratch,
                                lbbsp_metrics* out, cudaStream_t s) {
   const size_t cap = static_cast<size_t>(S.max_updates) * S.n;
-  sim_metrics_kernel<<<1, 256, 0, s>>>(S, rmse_from, scratch, scratch + cap, out);
+  sim_metrics_kernel<<<1, 256, 0, s>>>(S, rec_nw, rmse_from, scratch, scratch + cap, out);
   return cudaGetLastError();
 }
 
@@ -824,6 +835,268 @@ cudaError_t launch_series_rmse(const PredDev& P, const double* cpu, const double
                        static_cast<int>(kTrainSmemCap));
   series_rmse_kernel<<<1, kTrainThreads, smem, s>>>(P, cpu, mem, mult, len, base_speed,
                                                     measure_from, out2, smem);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// ASP / SSP (Simulation::step_async, cluster_sim.cpp:486-631). The event loop
+// is inherently sequential -- one worker finishes at a time -- so one
+// persistent CTA runs it end to end: earliest-finish selection, observe + NARX
+// train of the finisher, the parameter-server update (ASP) or round assembly
+// (SSP), the full-dataset loss, the record, and start_worker's gradient for
+// the restarted workers. Every value is computed with the reference's
+// operations in the reference's order (bit-exact records).
+// ---------------------------------------------------------------------------
+constexpr int kAsyncThreads = 512;
+constexpr size_t kAsyncTrainSmemCap = 180 * 1024;
+
+size_t async_smem_bytes(int max_hist) {
+  return std::min(narx_train_scratch_bytes(max_hist), kAsyncTrainSmemCap);
+}
+
+// start_worker (cluster_sim.cpp:504-536) for worker w at time now; CTA-wide.
+__device__ void async_start_worker(const SimDev& S, const AsyncDev& A, int w, double now,
+                                   double* coeff) {
+  __shared__ int x_s, off_s;
+  __shared__ long long j_s;
+  if (threadIdx.x == 0) {
+    const long long j = A.completed[w];
+    double c, m, mult;
+    dyn_at_d(S, w, j, now, &c, &m, &mult);
+    const int x = S.equal[w];
+    double tp, va, vp = 0.0;
+    if (S.gpu_mode) {
+      const lbbsp_gpu_profile p = S.prof[w];
+      if (x < 1 || x > p.oom_point) set_status(S.status, LBBSP_RUNTIME, LBBSP_E_GPU_OOM, x, p.oom_point);
+      tp = dadd(dmul(p.sec_per_sample, static_cast<double>(x > p.saturation_point ? x : p.saturation_point)),
+                p.base_time_s);
+      va = ddiv(static_cast<double>(x), tp);
+    } else {
+      const double pen = m >= 0.5 ? 1.0 : dadd(0.25, dmul(0.75, ddiv(m, 0.5)));
+      va = dmul(dmul(dmul(S.base_speed, c), pen), mult);
+      tp = ddiv(static_cast<double>(x), va);
+      if (A.hist_len[w] >= 1)
+        vp = S.pred.kind == LBBSP_PRED_PERFECT ? va : predictor_predict_d(S.pred, w, A.hist_len[w], c, m);
+    }
+    const double f = (S.bw_worker == w && S.bw_at <= j) ? S.bw_factor : 1.0;  // tm_at (:13-20)
+    const double tm = dmul(S.base_comm, f);
+    double* inf = A.inflight + static_cast<size_t>(w) * 8;
+    inf[0] = x;
+    inf[1] = tp;
+    inf[2] = tm;
+    inf[3] = A.pending_wait[w];
+    inf[4] = vp;
+    inf[5] = va;
+    inf[6] = c;
+    inf[7] = m;
+    A.pending_wait[w] = 0.0;
+    A.running[w] = 1;
+    A.finish[w] = dadd(dadd(now, tp), tm);
+    int off = 0;
+    for (int i = 0; i < w; ++i) off += S.equal[i];
+    x_s = x;
+    off_s = off;
+    j_s = j < A.n_streams - 1 ? j : A.n_streams - 1;
+  }
+  __syncthreads();
+  // gradient against the parameters pulled now, over stream(j)[off, off + x)
+  const int* idx = S.streams + static_cast<size_t>(j_s) * S.B + off_s;
+  lr_segment_grad(S.feat, S.lab, S.N, S.d, S.params, idx, x_s,
+                  A.inflight_grad + static_cast<size_t>(w) * S.d, S.status, coeff);
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool ssp_gate_d(long long clock, long long min_clock, long long s) {
+  return clock - min_clock <= s;  // coordination.cpp:70-73
+}
+
+__global__ void __launch_bounds__(kAsyncThreads) async_sim_kernel(SimDev S, AsyncDev A, int updates,
+                                                                  size_t smem_bytes) {
+  extern __shared__ double sm_d[];
+  __shared__ double coeff[kGradChunk];
+  __shared__ double terms[kLossChunk];
+  __shared__ NarxTrainSmem ts;
+  __shared__ int next_s, rec_s, stop_s, restart_s;
+  __shared__ double nrm;
+  const int n = S.n, d = S.d, tid = threadIdx.x;
+  if (*S.done) return;
+  if (!*A.started) {  // the constructor starts every worker at t = 0 (:293-294)
+    for (int w = 0; w < n; ++w) async_start_worker(S, A, w, 0.0, coeff);
+    if (tid == 0) *A.started = 1;
+    __syncthreads();
+  }
+  lbbsp_narx_train_cfg tcfg = S.pred.train;
+  tcfg.min_history = S.pred.warmup;
+  int produced = 0;
+  while (produced < updates) {
+    if (tid == 0) {
+      stop_s = 0;
+      rec_s = 0;
+      int next = -1;  // earliest finish, ties to the lowest id (:541-548)
+      for (int i = 0; i < n; ++i) {
+        if (!A.running[i]) continue;
+        if (next < 0 || A.finish[i] < A.finish[next]) next = i;
+      }
+      if (next < 0 || S.status->code) {
+        *S.done = 1;
+        stop_s = 1;
+      } else {
+        *S.now = A.finish[next];
+        A.running[next] = 0;
+        A.completed[next] += 1;
+        const double* inf = A.inflight + static_cast<size_t>(next) * 8;
+        observe_d(S.pred, next, A.hist_len[next], inf[5], inf[6], inf[7], inf[2]);  // (:309-313)
+        A.hist_len[next] += 1;
+      }
+      next_s = next;
+    }
+    __syncthreads();
+    if (stop_s) break;
+    const int w = next_s;
+    const double now = *S.now;
+    // rt.predictor.train(rt.history) (:558)
+    if (S.pred.kind == LBBSP_PRED_NARX) {
+      const int L = A.hist_len[w] < S.pred.max_hist ? A.hist_len[w] : S.pred.max_hist;
+      const size_t o = static_cast<size_t>(w) * S.pred.max_hist;
+      double* buf = narx_train_scratch_bytes(L) <= smem_bytes ? sm_d : S.pred.scratch;
+      narx_train_block(&S.pred.models[w], S.pred.hv + o, S.pred.hc + o, S.pred.hm + o, L, tcfg,
+                       &S.pred.reports[w], nullptr, 0, buf, &ts);
+    }
+    __syncthreads();
+    const double* inf = A.inflight + static_cast<size_t>(w) * 8;
+    if (!A.ssp) {  // ASP: one update, one record (:563-575)
+      __shared__ int one;
+      if (tid == 0) one = static_cast<int>(inf[0]);
+      __syncthreads();
+      block_aggregate_apply(A.inflight_grad + static_cast<size_t>(w) * d, &one, 1, d, 0, S.lr,
+                            S.params, S.agg, &nrm, S.status);
+      const double loss = block_lr_loss(S.feat, S.lab, S.N, d, S.params, terms);
+      if (tid == 0) {
+        *A.clock += 1;
+        const int row = *S.rows;
+        S.rec_sc[row].k = *A.clock - 1;
+        S.rec_sc[row].grad_norm = nrm;
+        S.rec_sc[row].loss = loss;
+        S.rec_sc[row].wall_s = dsub(now, *A.last_update);
+        *A.last_update = now;
+        const size_t o = static_cast<size_t>(row) * n;
+        A.rec_worker[o] = w;
+        A.rec_nw[row] = 1;
+        S.rec_batch[o] = static_cast<int>(inf[0]);
+        S.rec_tp[o] = inf[1];
+        S.rec_tm[o] = inf[2];
+        S.rec_wait[o] = inf[3];
+        S.rec_vpred[o] = inf[4];
+        S.rec_vact[o] = inf[5];
+        rec_s = 1;
+      }
+    } else {  // SSP: buffer until the round has every worker's update (:577-606)
+      __shared__ int slot, full;
+      if (tid == 0) {
+        const long long round = A.completed[w] - 1;
+        slot = static_cast<int>(round % A.ring);
+        double* st = A.ring_stats + (static_cast<size_t>(slot) * n + w) * 6;
+        for (int q = 0; q < 6; ++q) st[q] = inf[q];
+        full = ++A.ring_count[slot] == n;
+      }
+      __syncthreads();
+      double* rg = A.ring_grads + static_cast<size_t>(slot) * n * d;
+      for (int j = tid; j < d; j += blockDim.x)
+        rg[static_cast<size_t>(w) * d + j] = A.inflight_grad[static_cast<size_t>(w) * d + j];
+      __syncthreads();
+      if (full) {
+        block_aggregate_apply(rg, S.equal, n, d, 0, S.lr, S.params, S.agg, &nrm, S.status);
+        const double loss = block_lr_loss(S.feat, S.lab, S.N, d, S.params, terms);
+        if (tid == 0) {
+          *A.clock += 1;
+          const int row = *S.rows;
+          S.rec_sc[row].k = *A.clock - 1;
+          S.rec_sc[row].grad_norm = nrm;
+          S.rec_sc[row].loss = loss;
+          S.rec_sc[row].wall_s = dsub(now, *A.last_update);
+          *A.last_update = now;
+          A.rec_nw[row] = n;
+          for (int i = 0; i < n; ++i) {
+            const size_t o = static_cast<size_t>(row) * n + i;
+            const double* st = A.ring_stats + (static_cast<size_t>(slot) * n + i) * 6;
+            A.rec_worker[o] = i;
+            S.rec_batch[o] = static_cast<int>(st[0]);
+            S.rec_tp[o] = st[1];
+            S.rec_tm[o] = st[2];
+            S.rec_wait[o] = st[3];
+            S.rec_vpred[o] = st[4];
+            S.rec_vact[o] = st[5];
+          }
+          A.ring_count[slot] = 0;
+          rec_s = 1;
+        }
+      }
+    }
+    __syncthreads();
+    // restart or park the finisher, then re-check the blocked workers (:609-626)
+    if (!A.ssp) {
+      async_start_worker(S, A, w, now, coeff);
+    } else {
+      for (int i = -1; i < n; ++i) {  // i = -1: the finisher
+        if (tid == 0) {
+          long long lo = LLONG_MAX;
+          for (int q = 0; q < n; ++q) lo = A.completed[q] < lo ? A.completed[q] : lo;
+          restart_s = 0;
+          if (i < 0) {
+            if (ssp_gate_d(A.completed[w], lo, A.stale)) {
+              restart_s = 1;
+            } else {
+              A.blocked[w] = 1;
+              A.block_start[w] = now;
+            }
+          } else if (A.blocked[i] && ssp_gate_d(A.completed[i], lo, A.stale)) {
+            A.blocked[i] = 0;
+            A.pending_wait[i] = dsub(now, A.block_start[i]);
+            restart_s = 1;
+          }
+        }
+        __syncthreads();
+        if (restart_s) async_start_worker(S, A, i < 0 ? w : i, now, coeff);
+        __syncthreads();
+      }
+      if (tid == 0) {  // track_skew (:492-502)
+        long long hi = LLONG_MIN, lo = LLONG_MAX;
+        for (int q = 0; q < n; ++q) {
+          const long long c = A.running[q] ? A.completed[q] + 1 : A.completed[q];
+          hi = c > hi ? c : hi;
+          lo = c < lo ? c : lo;
+        }
+        *A.max_skew = hi - lo > *A.max_skew ? hi - lo : *A.max_skew;
+      }
+    }
+    __syncthreads();
+    if (rec_s) {
+      if (tid == 0) {  // records_.push_back + check_stop (:336-347, :326-334)
+        const int row = *S.rows;
+        for (int j = 0; j < d; ++j) S.rec_params[static_cast<size_t>(row) * d + j] = S.params[j];
+        *S.rows = row + 1;
+        const double loss = S.rec_sc[row].loss;
+        const int below = loss < S.conv_loss ? *S.below + 1 : 0;
+        *S.below = below;
+        if (below >= S.conv_consec) {
+          *S.converged = 1;
+          *S.done = 1;
+        }
+        if (row + 1 >= S.max_updates) *S.done = 1;
+        stop_s = *S.done;
+      }
+      __syncthreads();
+      ++produced;
+      if (stop_s) break;
+    }
+  }
+}
+
+cudaError_t launch_async_sim(const SimDev& S, const AsyncDev& A, int updates, cudaStream_t s) {
+  const size_t smem = async_smem_bytes(S.pred.max_hist);
+  cudaFuncSetAttribute(async_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(kAsyncTrainSmemCap));
+  async_sim_kernel<<<1, kAsyncThreads, smem, s>>>(S, A, updates, smem);
   return cudaGetLastError();
 }
 

@@ -69,6 +69,34 @@ struct SimDev {
   PredDev pred;
 };
 
+// Event-driven ASP/SSP state (Simulation::step_async, cluster_sim.cpp:486-631):
+// per-worker runtime (WorkerRuntime async fields, cluster_sim.hpp:209-224),
+// the SSP round buffers and the per-row worker lists of the records.
+struct AsyncDev {
+  int ssp;           // 0: ASP, 1: SSP
+  long long stale;   // staleness_threshold
+  int ring;          // SSP round-buffer slots
+  int n_streams;     // pre-generated local-iteration streams
+  int* started;      // device flag: workers launched at t = 0
+  long long* completed;
+  int* running;
+  int* blocked;
+  int* hist_len;     // per-worker SpeedHistory length
+  double* block_start;
+  double* pending_wait;
+  double* finish;
+  double* inflight_grad;  // [n][d]
+  double* inflight;       // [n][8]: x, tp, tm, wait, v_pred, v_act, c, m
+  double* ring_grads;     // [ring][n][d]
+  double* ring_stats;     // [ring][n][6]
+  int* ring_count;        // [ring]
+  double* last_update;
+  long long* clock;       // ModelState::clock
+  long long* max_skew;
+  int* rec_worker;        // [rows][n] worker id of each record slot
+  int* rec_nw;            // [rows] stats per record (1 for ASP, n for SSP)
+};
+
 // ---- launchers (return cudaError_t) -----------------------------------------
 cudaError_t launch_solve_prop(const double* d_speeds, int n, int budget, double speed_floor,
                               int* d_sizes, lbbsp_dev_status* d_status, cudaStream_t s);
@@ -100,9 +128,12 @@ cudaError_t launch_aggregate_apply(const double* grads, const int* sizes, int n,
 cudaError_t launch_lr_loss(const double* feat, const double* lab, int N, int d,
                            const double* params, double* out, cudaStream_t s);
 cudaError_t launch_sim_iteration(const SimDev& S, cudaStream_t s, int* launches);
+// ASP/SSP: up to `updates` records in one persistent CTA (no host round trip).
+cudaError_t launch_async_sim(const SimDev& S, const AsyncDev& A, int updates, cudaStream_t s);
+size_t async_smem_bytes(int max_hist);
 // compute_metrics (cluster_sim.cpp:217-245) over the device-resident records;
 // out = {time_total.., see kernels.cu}; scratch: 2*rows*n doubles.
-cudaError_t launch_sim_metrics(const SimDev& S, int rmse_from, double* scratch,
+cudaError_t launch_sim_metrics(const SimDev& S, const int* rec_nw, int rmse_from, double* scratch,
                                lbbsp_metrics* out, cudaStream_t s);
 // predictor_series_rmse (cluster_sim.cpp:645-672): P has n == 1 and history
 // capacity >= len; writes {sse, count} to out2.

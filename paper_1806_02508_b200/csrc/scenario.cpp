@@ -501,13 +501,10 @@ lbbsp_narx_train_cfg default_train_cfg(int min_history) {  // NarxTrainConfig (p
 
 // build_sim_config (scenario.cpp:219-294)
 void build_sim_config(const Scenario& c, BuiltSim& b) {
-  if (c.scheme != LBBSP_SCHEME_BSP && c.scheme != LBBSP_SCHEME_LBBSP)
-    fail(LBBSP_INVALID_ARGUMENT, std::string("scheme ") + scheme_name(c.scheme) +
-                                     " is not implemented by the device driver (ASP/SSP are out "
-                                     "of scope)");
   lbbsp_sim_cfg& s = b.cfg;
   s = lbbsp_sim_cfg{};
   s.scheme = c.scheme;
+  s.staleness_threshold = c.staleness_threshold;
   s.n_workers = c.workers;
   s.total_budget = c.total_budget;
   s.preset = LBBSP_PRESET_NONE;
@@ -589,13 +586,17 @@ void build_sim_config(const Scenario& c, BuiltSim& b) {
 struct Records {  // a host copy of a device record stream
   int rows = 0, n = 0;
   std::vector<lbbsp_iter_scalars> sc;
-  std::vector<int> batch;
+  std::vector<int> batch, worker_id, row_workers;
   std::vector<double> tp, tm, wait, v_pred, v_actual;
   lbbsp_records_view view() const {
-    return lbbsp_records_view{rows,      n,         sc.data(),     batch.data(),     tp.data(),
-                              tm.data(), wait.data(), v_pred.data(), v_actual.data()};
+    return lbbsp_records_view{rows,          n,           sc.data(),        batch.data(),
+                              tp.data(),     tm.data(),   wait.data(),      v_pred.data(),
+                              v_actual.data(), worker_id.data(), row_workers.data()};
   }
 };
+
+int row_stats(const lbbsp_records_view& r, int i) { return r.row_workers ? r.row_workers[i] : r.n; }
+int slot_worker(const lbbsp_records_view& r, size_t o, int w) { return r.worker_id ? r.worker_id[o] : w; }
 
 // compute_metrics (cluster_sim.cpp:217-245) -- sequential folds in record order.
 lbbsp_metrics compute_metrics(const lbbsp_records_view& r, bool converged, int rmse_from,
@@ -610,7 +611,7 @@ lbbsp_metrics compute_metrics(const lbbsp_records_view& r, bool converged, int r
   for (int i = 0; i < r.rows; ++i) {
     const double wall = rd(r.scalars[i].wall_s);
     time_total += wall;
-    for (int w = 0; w < r.n; ++w) {
+    for (int w = 0; w < row_stats(r, i); ++w) {
       const size_t o = static_cast<size_t>(i) * r.n + w;
       wait_fraction_sum += wall > 0.0 ? rd(r.wait[o]) / wall : 0.0;
       ++row_count;
@@ -637,11 +638,11 @@ void write_records_csv(const lbbsp_records_view& r, const std::string& path) {
   buf.reserve(1 << 16);
   buf += "k,worker_id,x,tp_s,tm_s,wait_s,v_pred,v_actual,loss,iter_wall_s\n";
   for (int i = 0; i < r.rows; ++i) {
-    for (int w = 0; w < r.n; ++w) {
+    for (int w = 0; w < row_stats(r, i); ++w) {
       const size_t o = static_cast<size_t>(i) * r.n + w;
       buf += std::to_string(r.scalars[i].k);
       buf += ',';
-      buf += std::to_string(w);
+      buf += std::to_string(slot_worker(r, o, w));
       buf += ',';
       buf += std::to_string(r.batch[o]);
       for (const double v : {r.tp[o], r.tm[o], r.wait[o], r.v_pred[o], r.v_actual[o],
@@ -702,11 +703,14 @@ SimRun run_sim(const lbbsp_sim_cfg& cfg) {
   r.sc.resize(cap);
   r.batch.resize(cap * n);
   for (auto* v : {&r.tp, &r.tm, &r.wait, &r.v_pred, &r.v_actual}) v->resize(cap * n);
+  r.worker_id.resize(cap * n);
+  r.row_workers.resize(cap);
   int done = 0, conv = 0;
   check(lbbsp_sim_status(h.p, &done, &conv));
   check(lbbsp_sim_records(h.p, static_cast<int>(cap), &r.rows, r.sc.data(), r.batch.data(),
                           r.tp.data(), r.tm.data(), r.wait.data(), r.v_pred.data(),
                           r.v_actual.data(), nullptr));
+  check(lbbsp_sim_record_workers(h.p, static_cast<int>(cap), r.worker_id.data(), r.row_workers.data()));
   out.converged = conv != 0;
   check(lbbsp_sim_metrics(h.p, cfg.predictor.warmup_iterations, &out.metrics));
   return out;

@@ -385,6 +385,8 @@ class SimResult:
     params: np.ndarray
     converged: bool = False
     extra: dict = field(default_factory=dict)
+    worker_id: Optional[np.ndarray] = None    # [rows, n] worker of each slot (ASP: slot 0)
+    row_workers: Optional[np.ndarray] = None  # [rows] stats per record (ASP: 1)
 
 
 class Simulation:
@@ -435,8 +437,13 @@ class Simulation:
                                         ("tp", "tm", "wait", "v_pred", "v_actual")],
                                       params.ctypes.data_as(_dp)))
         r = rows.value
+        wid = np.zeros(cap * n, np.int32)
+        nw = np.zeros(cap, np.int32)
+        check(lib().lbbsp_sim_record_workers(self._h, cap, wid.ctypes.data_as(_ip),
+                                             nw.ctypes.data_as(_ip)))
         done, conv = self.status()
-        return SimResult(k=np.array([sc[i].k for i in range(r)]),
+        return SimResult(worker_id=wid[: r * n].reshape(r, n), row_workers=nw[:r].copy(),
+                         k=np.array([sc[i].k for i in range(r)]),
                          loss=np.array([sc[i].loss for i in range(r)]),
                          grad_norm=np.array([sc[i].grad_norm for i in range(r)]),
                          wall=np.array([sc[i].wall_s for i in range(r)]),
@@ -448,6 +455,12 @@ class Simulation:
         """Simulation::run (cluster_sim.cpp:633-643): all rounds on device."""
         self.run_rounds(int(self.cfg.max_updates))
         return self.records()
+
+    def summary(self):
+        """(SimResult::total_time_s, max_ssp_skew) (cluster_sim.cpp:633-643)"""
+        t, k = C.c_double(), C.c_int64()
+        check(lib().lbbsp_sim_summary(self._h, C.byref(t), C.byref(k)))
+        return t.value, k.value
 
     def metrics(self) -> abi.Metrics:
         """SimResult::metrics = compute_metrics(records, converged, warmup)
@@ -481,7 +494,13 @@ def _records_view(r: SimResult):
         arrs.append(a.ctypes.data_as(_dp))
     b = np.ascontiguousarray(r.batch, dtype=np.int32).reshape(-1)
     keep.append(b)
-    v = abi.RecordsView(rows, n, sc, b.ctypes.data_as(_ip), *arrs)
+    ids = [None, None]
+    for q, a in enumerate((r.worker_id, r.row_workers)):
+        if a is not None:
+            a = np.ascontiguousarray(a, dtype=np.int32).reshape(-1)
+            keep.append(a)
+            ids[q] = a.ctypes.data_as(_ip)
+    v = abi.RecordsView(rows, n, sc, b.ctypes.data_as(_ip), *arrs, *ids)
     return v, keep
 
 

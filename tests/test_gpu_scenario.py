@@ -28,7 +28,9 @@ def sg():
 
 @pytest.mark.parametrize("name", ["homo_smoke", "hetero_l3_bsp", "hetero_l3_lbbsp",
                                   "gpu_cluster", "bench_predictors", "trace_lbbsp_narx",
-                                  "trace_bsp", "narx_warm_start", "benchmark_small"])
+                                  "trace_bsp", "narx_warm_start", "benchmark_small",
+                                  "asp_hetero_narx", "ssp_hetero", "ssp_gpu_cluster",
+                                  "asp_trace"])
 def test_cmd_run_byte_identical(sg, tmp_path, name):
     cfg = write_config(str(tmp_path), name, sg["configs"][name])
     out = tmp_path / "out"
@@ -68,7 +70,8 @@ def test_cmd_predict_bench_byte_identical(sg, tmp_path, name):
     assert (tmp_path / "o" / "predict_bench.csv").read_text() == sg["predict_bench"][name]
 
 
-@pytest.mark.parametrize("name", ["hetero_l3_lbbsp", "trace_lbbsp_narx", "gpu_cluster"])
+@pytest.mark.parametrize("name", ["hetero_l3_lbbsp", "trace_lbbsp_narx", "gpu_cluster",
+                                  "asp_hetero_narx", "ssp_hetero"])
 def test_device_metrics_equal_host_compute_metrics(sg, tmp_path, name):
     s = L.load_scenario(write_config(str(tmp_path), name, sg["configs"][name]))
     sim = L.Simulation.from_scenario(s)

@@ -54,7 +54,8 @@ def result_from_oracle(r):
     return L.SimResult(k=r["k"], loss=r["loss"], grad_norm=r["grad_norm"], wall=r["wall"],
                        batch=r["batch"], tp=r["tp"], tm=r["tm"], wait=r["wait"],
                        v_pred=r["v_pred"], v_actual=r["v_actual"], params=r["params"],
-                       converged=r["converged"])
+                       converged=r["converged"], worker_id=r.get("worker_id"),
+                       row_workers=r.get("row_workers"))
 
 
 def test_config_errors_match_reference(sg, tmp_path):
@@ -86,10 +87,11 @@ def test_config_fields_and_defaults(sg, tmp_path):
                                                           "preset": "weird"}))
     with pytest.raises(ConfigError, match="config: field 'preset': unknown preset: weird"):
         s.sim_config()
-    # ASP/SSP load (they are valid reference configs) but the device driver rejects them
-    s = L.load_scenario(write_config(str(tmp_path), "a", {"scheme": "asp", "workers": 4}))
-    with pytest.raises(Exception, match="out of scope"):
-        s.sim_config()
+    # ASP / SSP carry the staleness threshold into the simulation config
+    s = L.load_scenario(write_config(str(tmp_path), "a", {"scheme": "ssp", "workers": 4,
+                                                          "staleness_threshold": 3}))
+    c = s.sim_config()
+    assert (c.scheme, c.staleness_threshold) == (abi.SCHEME_SSP, 3)
 
 
 def test_trace_errors_match_reference(sg, tmp_path):
@@ -133,7 +135,9 @@ def test_narx_csv_roundtrip(tmp_path, orc):
 
 @pytest.mark.parametrize("name", ["homo_smoke", "hetero_l3_bsp", "hetero_l3_lbbsp",
                                   "gpu_cluster", "bench_predictors", "trace_lbbsp_narx",
-                                  "trace_bsp", "narx_warm_start", "benchmark_small"])
+                                  "trace_bsp", "narx_warm_start", "benchmark_small",
+                                  "asp_hetero_narx", "ssp_hetero", "ssp_gpu_cluster",
+                                  "asp_trace"])
 def test_exported_files_byte_identical(sg, orc, tmp_path, name):
     """cmd_run's outputs (records.csv, metrics.json) rebuilt from the product's
     loader + build_sim_config + exporters over the restatement's record stream

@@ -8,6 +8,7 @@
 #pragma once
 #include <array>
 #include <cstdint>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -24,11 +25,17 @@ struct BatchAssignment {
   int total_budget = 0;
 };
 
+// lbbsp::ConfigError (scenario.hpp:13-15)
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 // status -> reference exception type
 inline void throw_if(int rc) {
   if (rc == LBBSP_OK) return;
   const std::string msg = lbbsp_last_error();
   switch (rc) {
+    case LBBSP_CONFIG: throw ConfigError(msg);
     case LBBSP_INVALID_ARGUMENT: throw std::invalid_argument(msg);
     case LBBSP_OUT_OF_RANGE: throw std::out_of_range(msg);
     case LBBSP_LOGIC: throw std::logic_error(msg);
@@ -114,6 +121,26 @@ inline std::vector<double> aggregate(std::span<const double> grads, std::span<co
   throw_if(lbbsp_aggregate(grads.data(), sizes.data(), static_cast<int>(sizes.size()), dim,
                            weighted ? 1 : 0, out.data()));
   return out;
+}
+
+// scenario.hpp:82-90 -- CLI entry points over the device driver (exit status)
+inline int cmd_run(const std::string& config, const std::string& out_dir,
+                   std::optional<std::uint64_t> seed_override = std::nullopt) {
+  return lbbsp_cmd_run(config.c_str(), out_dir.c_str(), seed_override ? 1 : 0,
+                       seed_override.value_or(0));
+}
+
+inline int cmd_predict_bench(const std::string& config, const std::string& out_dir,
+                             std::optional<std::uint64_t> seed_override = std::nullopt) {
+  return lbbsp_cmd_predict_bench(config.c_str(), out_dir.c_str(), seed_override ? 1 : 0,
+                                 seed_override.value_or(0));
+}
+
+// predictor.cpp:215-243
+inline lbbsp_narx_model load_narx_csv(const std::string& path) {
+  lbbsp_narx_model m{};
+  throw_if(lbbsp_narx_load_csv(path.c_str(), &m));
+  return m;
 }
 
 }  // namespace lbbsp::b200

@@ -102,6 +102,23 @@ def benchmark_trace(n_workers, iterations, seed=3, **bench):
     return c, m, x
 
 
+def recorded_trace(path, n_workers, iterations, seed=1, seconds_per_iteration=60.0):
+    """A recorded resource-trace CSV (parse_trace + map_traces, trace.cpp:54-135)
+    as the engine's iteration-indexed straggler trace: worker i follows the
+    machine map_traces assigns it, sampled with trace_at (trace.cpp:137-143)
+    at t = k * seconds_per_iteration. cpu_avail
+    drives the SM cap, mem_avail is recorded beside it, no transient spikes."""
+    from . import lbbsp as LB
+    traces = LB.parse_trace(path)
+    assign = LB.map_traces(traces, n_workers, seed)
+    c = np.zeros((n_workers, iterations)); m = np.zeros_like(c)
+    for i, t in enumerate(assign):
+        tr = traces[t]
+        for k in range(iterations):
+            c[i, k], m[i, k] = LB.trace_at(tr, k * seconds_per_iteration)
+    return c, m, np.ones_like(c)
+
+
 def constant_trace(n_workers, iterations, availability=None):
     a = np.ones(n_workers) if availability is None else np.asarray(availability, dtype=np.float64)
     c = np.repeat(a[:, None], iterations, axis=1)

@@ -192,3 +192,16 @@ def test_metrics_recomputable_from_records(sg, orc, tmp_path):
     assert abs(m.mean_per_update_time - sum(walls.values()) / len(walls)) < 1e-9
     assert abs(m.wastage - wf / len(rows)) < 1e-9
     assert abs(m.predictor_rmse - (sse / cnt) ** 0.5) < 1e-9
+
+
+def test_recorded_trace_drives_the_mlp_engine_schedule(sg):
+    """The MLP engine's straggler input from a trace CSV (map_traces + trace_at
+    at iteration-indexed times) matches the reference's mapping and lookup."""
+    from paper_1806_02508_b200.mlp import recorded_trace
+    c, m, x = recorded_trace(TRACE_CSV, 4, 30, seed=5, seconds_per_iteration=120.0)
+    traces = L.parse_trace(TRACE_CSV)
+    assign = sg["trace_map"]["4_5"]
+    for i in range(4):
+        for k in (0, 7, 29):
+            assert (c[i, k], m[i, k]) == L.trace_at(traces[assign[i]], 120.0 * k)
+    assert (x == 1.0).all() and c.shape == (4, 30)

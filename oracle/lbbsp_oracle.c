@@ -485,7 +485,9 @@ static double fwd_w(const narx_w* w, const double* z, double* hidden) {
 }
 
 /* mse, predictor.cpp:102-109 */
+long long orc_debug_evals = 0; /* test instrumentation: objective evaluations */
 static double mse(const narx_w* w, const double* Z, const double* T, int cnt) {
+  orc_debug_evals += 1;
   double total = 0.0;
   for (int i = 0; i < cnt; ++i) {
     const double e = fwd_w(w, Z + 8 * i, NULL) - T[i];

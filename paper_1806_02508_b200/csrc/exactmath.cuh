@@ -122,13 +122,12 @@ __device__ __forceinline__ double glibc_tanh(double x) {
     if ((ix | lo_word(x)) == 0) return x;
     if (ix < 0x3c800000u) return dmul(x, dadd(1.0, x));
     const double ax = fabs(x);
-    if (ix >= 0x3ff00000u) {
-      const double t = glibc_expm1(dadd(ax, ax));
-      z = dsub(1.0, ddiv(2.0, dadd(t, 2.0)));
-    } else {
-      const double t = glibc_expm1(dmul(-2.0, ax));
-      z = ddiv(-t, dadd(t, 2.0));
-    }
+    // one expm1 call site for both ranges keeps a warp's lanes converged
+    // (the arguments and the final combination are exactly glibc's)
+    const bool big = ix >= 0x3ff00000u;
+    const double t = glibc_expm1(big ? dadd(ax, ax) : dmul(-2.0, ax));
+    const double den = dadd(t, 2.0);
+    z = big ? dsub(1.0, ddiv(2.0, den)) : ddiv(-t, den);
   } else {
     z = 1.0;  // one - tiny
   }

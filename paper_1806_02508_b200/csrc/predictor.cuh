@@ -140,30 +140,21 @@ __device__ inline double block_eval(const double* wt, const double* Z, const dou
     s->val = ddiv(total, static_cast<double>(cnt));
   } else if (tid >= 32 && tid < 43) {
     const int k = tid - 32;
-    // term_i = a_i * b_i (or a_i alone), folded left to right
-    const double* a = k < 8 ? DZ : (k == 8 ? DZ : DY);
+    // term_i = a_i * b_i, or a_i alone for the bias terms (k = 8, 10), which is
+    // the same value as a_i * 1.0 -- so all 11 lanes run one loop, no divergence
+    const double* a = k <= 8 ? DZ : DY;
     const double* b = k < 8 ? Z + static_cast<size_t>(k) * cnt : (k == 9 ? H : nullptr);
+    const bool hb = b != nullptr;
     double acc = 0.0;
     int i = 0;
-    if (b) {
-      for (; i + 8 <= cnt; i += 8) {
-        double t[8];
+    for (; i + 8 <= cnt; i += 8) {
+      double t[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) t[q] = dmul(a[i + q], b[i + q]);
+      for (int q = 0; q < 8; ++q) t[q] = dmul(a[i + q], hb ? b[i + q] : 1.0);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc = dadd(acc, t[q]);
-      }
-      for (; i < cnt; ++i) acc = dadd(acc, dmul(a[i], b[i]));
-    } else {
-      for (; i + 8 <= cnt; i += 8) {
-        double t[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) t[q] = a[i + q];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc = dadd(acc, t[q]);
-      }
-      for (; i < cnt; ++i) acc = dadd(acc, a[i]);
+      for (int q = 0; q < 8; ++q) acc = dadd(acc, t[q]);
     }
+    for (; i < cnt; ++i) acc = dadd(acc, dmul(a[i], hb ? b[i] : 1.0));
     gout[k] = acc;
   }
   __syncthreads();

@@ -169,14 +169,26 @@ struct PlanDev {
   double* rec_t;
   double* rec_loss;
   lbbsp_dev_status* status;
+  unsigned long long* stamps;  // [16] globaltimer at kernel boundaries (last round)
 };
 
-// P1-P4: trace -> caps, predictor -> v_pred, solver -> sizes, local slice
-__global__ void __launch_bounds__(256) plan_kernel(PlanDev D) {
+__device__ __forceinline__ void stamp(const PlanDev& D, int i) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) D.stamps[i] = gtimer();
+}
+
+// P1-P4: trace -> caps, predictor -> v_pred, solver -> sizes, local slice,
+// plus the Eq. 6/7 row scales of this rank's rows. Everything thread 0 walks
+// sequentially lives in shared memory (no dependent global round trips).
+__global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) {
   __shared__ SolverSmem sm;
   __shared__ double rem[LBBSP_MAX_WORKERS];
   __shared__ double avail[LBBSP_MAX_WORKERS];
+  __shared__ double vp_s[LBBSP_MAX_WORKERS];
+  __shared__ double share_s[LBBSP_MAX_WORKERS];
+  __shared__ int sz[LBBSP_MAX_WORKERS];
+  __shared__ int r0_s[LBBSP_MAX_WORKERS + 1];
   const int tid = threadIdx.x, n = D.n_total;
+  stamp(D, 0);
   const long long k = *D.k;
   const int len = min(*D.pred.len, D.pred.max_hist);
   if (k >= D.max_rows && tid == 0)
@@ -185,36 +197,40 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D) {
   for (int i = tid; i < n; i += blockDim.x) {
     const size_t o = static_cast<size_t>(i) * D.trace_len + ti;
     const double c = D.trace_c[o], m = D.trace_m[o], mult = D.trace_mult[o];
+    share_s[i] = D.share[i];
     D.c_now[i] = c;
     D.m_now[i] = m;
     const double a = dmul(c, mult);
     avail[i] = a < 1.0 ? a : 1.0;
-    D.v_pred[i] = len >= 1 ? predictor_predict_d(D.pred, i, len, c, m) : 0.0;
+    const double vp = len >= 1 ? predictor_predict_d(D.pred, i, len, c, m) : 0.0;
+    vp_s[i] = vp;
+    D.v_pred[i] = vp;
   }
   __syncthreads();
   int code = 0;
   if (D.static_sizes) {
-    for (int i = tid; i < n; i += blockDim.x) D.sizes_all[i] = D.static_sizes_d[i];
+    for (int i = tid; i < n; i += blockDim.x) sz[i] = D.static_sizes_d[i];
   } else if (D.scheme == LBBSP_SCHEME_LBBSP && k > 0) {
-    code = block_cpu_allocate(D.v_pred, n, D.B_total, D.pred.floor, D.sizes_all, rem, &sm, D.status);
+    code = block_cpu_allocate(vp_s, n, D.B_total, D.pred.floor, sz, rem, &sm, D.status);
   } else {
     for (int i = tid; i < n; i += blockDim.x)
-      D.sizes_all[i] = D.B_total / n + (i < D.B_total % n ? 1 : 0);  // equal_split
+      sz[i] = D.B_total / n + (i < D.B_total % n ? 1 : 0);  // equal_split
   }
   __syncthreads();
   if (code) return;
+  const int first = D.rank * D.n_local;
   if (tid == 0) {
-    const int first = D.rank * D.n_local;
     int off = 0;
-    for (int i = 0; i < first; ++i) off += D.sizes_all[i];
+    for (int i = 0; i < first; ++i) off += sz[i];
     *D.stream_off = off;
     int r = 0, c0 = 0;
     for (int i = 0; i < D.n_local; ++i) {
       const int w = first + i;
+      r0_s[i] = r;
       D.r0[i] = r;
-      r += D.sizes_all[w];
+      r += sz[w];
       D.r1[i] = r;
-      const double share = D.share[w];
+      const double share = share_s[w];
       int cap = static_cast<int>(floor(static_cast<double>(D.sm_budget) * share * avail[w]));
       cap = cap < 1 ? 1 : cap;
       if (c0 + cap > D.sm_budget) cap = D.sm_budget - c0 > 0 ? D.sm_budget - c0 : 1;
@@ -222,6 +238,7 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D) {
       D.ctan[i] = cap;
       c0 += cap;
     }
+    r0_s[D.n_local] = r;
     *D.local_rows = r;
     // the previous round's full-dataset loss (computed beside its observe branch)
     const int prev = *D.rows - 1;
@@ -233,23 +250,43 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D) {
     D.timing[2 * i] = ~0ull;
     D.timing[2 * i + 1] = 0ull;
   }
+  if (tid == 0) {
+    D.stamps[6] = ~0ull;  // loss-branch head {first start, last end}
+    D.stamps[7] = 0ull;
+  }
+  for (int i = tid; i < n; i += blockDim.x) D.sizes_all[i] = sz[i];
   __syncthreads();
+  // row scales: Eq. 7 folds 1/B into every row; Eq. 6 (BSP) 1/(n b_i) per worker
+  const int rows = r0_s[D.n_local];
+  if (D.scheme == LBBSP_SCHEME_LBBSP) {
+    const float s = 1.0f / static_cast<float>(D.B_total);
+    for (int r = tid; r < rows; r += blockDim.x) row_scale[r] = s;
+  } else {
+    for (int g = 0; g < D.n_local; ++g) {
+      const float s = 1.0f / (static_cast<float>(D.n_total) * static_cast<float>(sz[first + g]));
+      for (int r = r0_s[g] + tid; r < r0_s[g + 1]; r += blockDim.x) row_scale[r] = s;
+    }
+  }
   const int row = *D.rows;
   if (row < D.max_rows) {
     for (int i = tid; i < n; i += blockDim.x) {
-      D.rec_sizes[static_cast<size_t>(row) * n + i] = D.sizes_all[i];
-      D.rec_vpred[static_cast<size_t>(row) * n + i] = D.v_pred[i];
+      D.rec_sizes[static_cast<size_t>(row) * n + i] = sz[i];
+      D.rec_vpred[static_cast<size_t>(row) * n + i] = vp_s[i];
     }
     for (int i = tid; i < D.n_local; i += blockDim.x)
       D.rec_caps[static_cast<size_t>(row) * n + D.rank * D.n_local + i] = D.ctan[i];
   }
+  stamp(D, 1);
 }
 
 // P6: X[r] = data[stream[off + r]], labels, row scale (Eq. 7: 1/B; Eq. 6: 1/(n b_i))
+// fixed_rows > 0: a single rank gathers the whole batch [0, B) of stream k,
+// which does not depend on the plan, so it runs beside plan_kernel.
 __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const bf16* data_x,
-                              const int* data_y, int d0, bf16* X, int* y, float* row_scale,
+                              const int* data_y, int d0, bf16* X, int* y, int fixed_rows,
                               float* slab, long long slab_stride, const long long* reg_off,
                               const long long* reg_len, int n_reg) {
+  stamp(D, 2);
   // zero the partial regions accumulated with atomics (biases, small head)
   for (int sl = 0; sl < D.n_local; ++sl)
     for (int rg = 0; rg < n_reg; ++rg) {
@@ -258,7 +295,8 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
         p[i] = 0.f;
     }
   const long long k = min(*D.k, static_cast<long long>(D.max_rows - 1));  // capacity-guarded
-  const int rows = *D.local_rows, off = *D.stream_off;
+  const int rows = fixed_rows > 0 ? fixed_rows : *D.local_rows;
+  const int off = fixed_rows > 0 ? 0 : *D.stream_off;
   const int* idx = streams + static_cast<size_t>(k) * B_total + off;
   const int vec = d0 / 8;  // 16-byte chunks per row
   const int total = rows * vec;
@@ -283,19 +321,7 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
     for (int u = 0; u < 4; ++u)
       if (dsti[u] >= 0) dst4[dsti[u]] = v[u];
   }
-  for (int r = blockIdx.x * 256 + threadIdx.x; r < rows; r += 256 * gridDim.x) {
-    y[r] = data_y[idx[r]];
-    float s;
-    if (D.scheme == LBBSP_SCHEME_LBBSP) {
-      s = 1.0f / static_cast<float>(B_total);
-    } else {
-      int g = 0;
-      while (g + 1 < D.n_local && r >= D.r1[g]) ++g;
-      s = 1.0f / (static_cast<float>(D.n_total) *
-                  static_cast<float>(D.sizes_all[D.rank * D.n_local + g]));
-    }
-    row_scale[r] = s;
-  }
+  for (int r = blockIdx.x * 256 + threadIdx.x; r < rows; r += 256 * gridDim.x) y[r] = data_y[idx[r]];
 }
 
 __device__ __forceinline__ void phase_begin(unsigned long long* timing, int g) {
@@ -405,7 +431,9 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
 // reduces into grad (the allreduce then runs on grad).
 __global__ void __launch_bounds__(256) reduce_apply_kernel(const float* __restrict__ partial, int n,
                                                            long long P, float* grad, float* params,
-                                                           bf16* pb, float lr, int apply) {
+                                                           bf16* pb, float lr, int apply,
+                                                           unsigned long long* stamps) {
+  if (stamps && threadIdx.x == 0 && blockIdx.x == 0) stamps[5] = gtimer();
   const long long nv = P / 4;
   for (long long v = blockIdx.x * 256ll + threadIdx.x; v < nv; v += 256ll * gridDim.x) {
     float4 s = reinterpret_cast<const float4*>(partial)[v];
@@ -471,6 +499,7 @@ __global__ void speed_kernel(PlanDev D, int n_phases) {
 
 // P10: push every worker's (v, c, m) (cluster_sim.cpp:309-313), advance round
 __global__ void observe_kernel(PlanDev D, int fused_speed_phases) {
+  stamp(D, 3);
   if (fused_speed_phases > 0) {  // single rank: measured speeds computed here
     const int i = threadIdx.x;
     if (i < D.n_local) {
@@ -501,6 +530,7 @@ __global__ void observe_kernel(PlanDev D, int fused_speed_phases) {
     *D.rows = row + 1;
     *D.k += 1;
   }
+  stamp(D, 4);
 }
 
 }  // namespace mlp
@@ -524,6 +554,7 @@ struct lbbsp_mlp {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_speed = nullptr, ev_comm = nullptr;
+  cudaEvent_t ev_gather0 = nullptr, ev_gather1 = nullptr;
   cudaEvent_t ev_layer[LBBSP_MLP_MAX_LAYERS] = {};
   cudaStream_t comm_stream = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -562,6 +593,8 @@ struct lbbsp_mlp {
     if (stream) cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_gather0) cudaEventDestroy(ev_gather0);
+    if (ev_gather1) cudaEventDestroy(ev_gather1);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_speed) cudaEventDestroy(ev_speed);
     if (ev_comm) cudaEventDestroy(ev_comm);
@@ -626,12 +659,21 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   const Groups G = groups();
   int nl = 0, ph = 0;
   const int sms = D.sm_budget;
-  plan_kernel<<<1, 256, 0, s>>>(D);
-  ++nl;
   const int gather_ctas = std::max(sms, std::min(sms * 8, (B_cap * (dims[0] / 8) + 1023) / 1024));
-  gather_kernel<<<gather_ctas, 256, 0, s>>>(D, streams, B_total, data_x, data_y, dims[0], X, y, row_scale,
-                                     partial, P, reg_off, reg_len, n_reg);
-  ++nl;
+  if (cfg.world == 1) {  // one rank gathers all B rows: independent of the plan
+    LBBSP_CUDA_CHECK(cudaEventRecord(ev_gather0, s));
+    LBBSP_CUDA_CHECK(cudaStreamWaitEvent(side, ev_gather0, 0));
+    gather_kernel<<<gather_ctas, 256, 0, side>>>(D, streams, B_total, data_x, data_y, dims[0], X, y,
+                                                 B_total, partial, P, reg_off, reg_len, n_reg);
+    LBBSP_CUDA_CHECK(cudaEventRecord(ev_gather1, side));
+    plan_kernel<<<1, 256, 0, s>>>(D, row_scale);
+    LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_gather1, 0));
+  } else {
+    plan_kernel<<<1, 256, 0, s>>>(D, row_scale);
+    gather_kernel<<<gather_ctas, 256, 0, s>>>(D, streams, B_total, data_x, data_y, dims[0], X, y, 0,
+                                              partial, P, reg_off, reg_len, n_reg);
+  }
+  nl += 2;
   if (use_pair) {
     zero_dz_tail_kernel<<<8, 256, 0, s>>>(D, dz_ptrs, dz_widths, L, dz_end, B_cap);
     ++nl;
@@ -700,7 +742,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
       LBBSP_CUDA_CHECK(cudaEventRecord(ev_comm, comm_stream));
       LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_comm, 0));
     } else {
-      reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 0);
+      reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 0, D.stamps);
       ++nl;
       if (nccl_api()->AllReduce(grad, grad, static_cast<size_t>(P), ncclFloat, ncclSum, comm, s) !=
           ncclSuccess)
@@ -730,9 +772,9 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   }
   // ---- aggregate + apply ----
   if (cfg.world > 1 && !bucketed) {
-    reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(grad, 1, P, grad, params, pb, lr, 1);
+    reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(grad, 1, P, grad, params, pb, lr, 1, D.stamps);
   } else {
-    reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 1);
+    reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 1, D.stamps);
   }
   ++nl;
   // ---- full-dataset loss (step_sync P9, cluster_sim.cpp:445) ----
@@ -749,7 +791,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
       const bf16* Hin = L >= 2 ? Hd[L - 2] : data_x;
       head_mma_kernel<false><<<sms, 256, kHeadMmaSmem, s>>>(
           none, N_data, Hin, params + off_w[hl], params + off_b[hl], data_y, nullptr, nullptr,
-          nullptr, 0, 0, 0, 0, D.loss_acc, head_part, head_loss, head_cnt_d, nullptr);
+          nullptr, 0, 0, 0, 0, D.loss_acc, head_part, head_loss, head_cnt_d, D.stamps + 6);
     } else {
       softmax_ce_kernel<<<sms, 256, 0, s>>>(none, N_data, logits_d, dims[L], data_y, nullptr, nullptr,
                                             D.loss_acc, nullptr);
@@ -810,6 +852,8 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking));
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.side, cudaStreamNonBlocking));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_fork, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_gather0, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_gather1, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_join, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_speed, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_comm, cudaEventDisableTiming));
@@ -942,6 +986,7 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   else
     D.v_obs_all = D.v_obs_local;
   LBBSP_CUDA_CHECK(m.alloc(&D.loss_acc, 1));
+  LBBSP_CUDA_CHECK(m.alloc(&D.stamps, 16));
   D.N_data = m.N_data;
   D.loss_on = c.loss_every > 0 ? 1 : 0;
   LBBSP_CUDA_CHECK(m.alloc(&D.train_first, 1));
@@ -1231,3 +1276,14 @@ extern "C" int lbbsp_mlp_work(lbbsp_mlp* m, double* gemm_flops, double* reduce_b
   return LBBSP_OK;
 }
 
+
+// Debug timeline of the last round: stamps[16] then timing[kMaxPhases][n_local][2]
+// (globaltimer ns). Not part of the stable C-ABI.
+extern "C" int lbbsp_mlp_debug_timeline(lbbsp_mlp* m, unsigned long long* out, int* n_phases) {
+  LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->stream));
+  LBBSP_CUDA_CHECK(cudaMemcpy(out, m->D.stamps, sizeof(unsigned long long) * 16, cudaMemcpyDeviceToHost));
+  LBBSP_CUDA_CHECK(cudaMemcpy(out + 16, m->D.timing, sizeof(unsigned long long) * 2 * kMaxPhases * m->n_local,
+                              cudaMemcpyDeviceToHost));
+  *n_phases = m->n_phases;
+  return LBBSP_OK;
+}

@@ -428,8 +428,11 @@ def main():
         dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
     n_total = WORKERS_PER_GPU * world
     B = BATCH_PER_GPU * world
-    e2e_steps = min(args.steps, 50)
-    iters = args.warmup + args.steps + e2e_steps + 8
+    e2e_steps = args.steps
+    # the timed rounds are steady-state LB-BSP + NARX rounds: at least the
+    # predictor warm-up (50 rounds, EMA before it) plus 10 rounds precede them
+    warm = max(args.warmup, WARMUP_NARX + 10)
+    iters = warm + args.steps + 8
     trace = benchmark_trace(n_total, iters, seed=TRACE_SEED)
 
     def make(scheme, tr):
@@ -478,18 +481,24 @@ def main():
     # ---- main arm: LB-BSP under the recorded trace ----
     eng = make("lb-bsp", trace)
     with Clocks(local) as clk:
-        ms_lb, phases = timed(eng, args.steps, args.warmup, phases=True)
+        ms_lb, phases = timed(eng, args.steps, warm, phases=True)
     rec = eng.records()
     launches = eng.launches_per_iteration()
     gemm_flops, _ = eng.work()
 
+    del eng
+
     # ---- e2e through the C-ABI with host buffers (pinned), per-step H2D/D2H ----
+    # a fresh engine over the same rounds as the timed arm (same warm-up), so
+    # both numbers see the same predictor / straggler history
+    eng = make("lb-bsp", trace)
     x_host, y_host = eng.dataset()
     xb = torch.from_numpy(x_host).to(torch.bfloat16).pin_memory()
     yb = torch.from_numpy(y_host.astype(np.int32)).pin_memory()
     out_sizes = torch.zeros(n_total, dtype=torch.int32).pin_memory()
     out_loss = torch.zeros(1, dtype=torch.float64).pin_memory()
     st = torch.cuda.ExternalStream(eng.stream)
+    eng.run(warm)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -513,10 +522,10 @@ def main():
 
     # ---- BSP and no-straggler ideal on the same trace / config ----
     eng_b = make("bsp", trace)
-    ms_bsp, _ = timed(eng_b, args.steps, args.warmup)
+    ms_bsp, _ = timed(eng_b, args.steps, warm)
     del eng_b
     eng_i = make("lb-bsp", constant_trace(n_total, iters))
-    ms_ideal, _ = timed(eng_i, args.steps, args.warmup)
+    ms_ideal, _ = timed(eng_i, args.steps, warm)
     del eng_i
 
     # ---- C3-shape straggler demonstration (compute-bound) ----
@@ -555,7 +564,8 @@ def main():
                        "global_batch": B, "workers": n_total,
                        "parallelism": f"dp{n_total} (emulated {WORKERS_PER_GPU}/GPU)",
                        "trace": "make_benchmark_series seed 3, iteration-indexed",
-                       "l2": "256 MB buffer zeroed between timed steps, outside the events"},
+                       "l2": "256 MB buffer zeroed between timed steps, outside the events",
+                       "rounds_before_timing": warm},
             "bsp": {"value": B / (ms_bsp * 1e-3), "ms_per_step": ms_bsp},
             "ideal_no_straggler": {"value": B / (ms_ideal * 1e-3), "ms_per_step": ms_ideal},
             "lbbsp_over_bsp": ms_bsp / ms_lb,

@@ -79,7 +79,7 @@ static int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static int launch_t2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int ctas,
                      cudaStream_t s) {
-  constexpr int STAGES = BN == 256 ? 6 : 8;
+  constexpr int STAGES = BN == 256 ? 7 : 8;
   constexpr size_t smem = tc::gemm2_smem_bytes<BN, STAGES>();
   auto kern = tc::gemm_bf16_tc2_kernel<BN, A_MN, B_MN, EPI, STAGES>;
   static bool attr = false;

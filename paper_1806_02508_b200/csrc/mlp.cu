@@ -555,6 +555,10 @@ struct lbbsp_mlp {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_speed = nullptr, ev_comm = nullptr;
   cudaEvent_t ev_gather0 = nullptr, ev_gather1 = nullptr;
+  cudaStream_t copy_stream = nullptr;  // e2e input staging (lbbsp_mlp_load_data_async)
+  cudaEvent_t ev_staged = nullptr, ev_refreshed = nullptr;
+  bf16* stage_x = nullptr;
+  int* stage_y = nullptr;
   cudaEvent_t ev_layer[LBBSP_MLP_MAX_LAYERS] = {};
   cudaStream_t comm_stream = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -594,6 +598,9 @@ struct lbbsp_mlp {
     if (side) cudaStreamDestroy(side);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_gather0) cudaEventDestroy(ev_gather0);
+    if (ev_staged) cudaEventDestroy(ev_staged);
+    if (ev_refreshed) cudaEventDestroy(ev_refreshed);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ev_gather1) cudaEventDestroy(ev_gather1);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_speed) cudaEventDestroy(ev_speed);
@@ -1208,11 +1215,29 @@ extern "C" int lbbsp_mlp_launches_per_iteration(lbbsp_mlp* m, int* launches) {
   return LBBSP_OK;
 }
 
+// The host->device copy runs on a copy stream into a staging buffer, so it
+// overlaps the round still executing; the next round then starts with a
+// device-to-device refresh of the resident dataset (stream-ordered after the
+// previous round, which read it).
 extern "C" int lbbsp_mlp_load_data_async(lbbsp_mlp* m, const void* h_x_bf16, const int* h_labels) {
-  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_x, h_x_bf16, sizeof(bf16) * m->N_data * m->dims[0],
-                                   cudaMemcpyHostToDevice, m->stream));
-  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_y, h_labels, sizeof(int) * m->N_data,
-                                   cudaMemcpyHostToDevice, m->stream));
+  const size_t bx = sizeof(bf16) * m->N_data * m->dims[0], by = sizeof(int) * m->N_data;
+  if (!m->copy_stream) {
+    LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
+    LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m->ev_staged, cudaEventDisableTiming));
+    LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m->ev_refreshed, cudaEventDisableTiming));
+    LBBSP_CUDA_CHECK(m->alloc(&m->stage_x, bx / sizeof(bf16)));
+    LBBSP_CUDA_CHECK(m->alloc(&m->stage_y, by / sizeof(int)));
+    LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_refreshed, m->stream));
+  }
+  // staging is free once the previous refresh consumed it
+  LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->copy_stream, m->ev_refreshed, 0));
+  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_x, h_x_bf16, bx, cudaMemcpyHostToDevice, m->copy_stream));
+  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_y, h_labels, by, cudaMemcpyHostToDevice, m->copy_stream));
+  LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_staged, m->copy_stream));
+  LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->stream, m->ev_staged, 0));
+  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_x, m->stage_x, bx, cudaMemcpyDeviceToDevice, m->stream));
+  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_y, m->stage_y, by, cudaMemcpyDeviceToDevice, m->stream));
+  LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_refreshed, m->stream));
   return LBBSP_OK;
 }
 

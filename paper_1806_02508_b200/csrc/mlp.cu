@@ -497,6 +497,91 @@ __global__ void speed_kernel(PlanDev D, int n_phases) {
   if (row < D.max_rows) D.rec_t[static_cast<size_t>(row) * D.n_total + w] = t;
 }
 
+// Measured speed v_i = b_i / t_i of local worker i from its phase times.
+__device__ inline double local_speed(const PlanDev& D, int i, int n_phases, double* t_out) {
+  double t = 0.0;
+  for (int p = 0; p < n_phases; ++p) {
+    const unsigned long long s0 = D.timing[2 * (p * D.n_local + i)], e0 = D.timing[2 * (p * D.n_local + i) + 1];
+    if (s0 != ~0ull && e0 > s0) t += static_cast<double>(e0 - s0) * 1e-9;
+  }
+  const double b = static_cast<double>(D.sizes_all[D.rank * D.n_local + i]);
+  if (t_out) *t_out = t;
+  return t > 0.0 ? b / t : b;
+}
+
+// P10 fused: observe (cluster_sim.cpp:309-313) + train_rotation (:315-324)
+// in one launch. CTA j < nb trains model (cursor + j) % n on the history
+// extended by this round's observation (it writes that one sample itself --
+// the same bits the observe CTA writes); the last CTA computes every speed,
+// pushes every history and EMA state, and advances the round counters once
+// all training CTAs have read them (a device-side arrival count; all CTAs
+// are co-resident, nb < SM count).
+__global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D, int fused_speed_phases,
+                                                                     unsigned* arrive,
+                                                                     size_t smem_bytes) {
+  extern __shared__ double sm_d[];
+  __shared__ NarxTrainSmem ts;
+  const int nb = gridDim.x - 1;
+  const int n = D.n_total, tid = threadIdx.x;
+  if (static_cast<int>(blockIdx.x) < nb) {
+    __shared__ int len_s, w_s;
+    if (tid == 0) {
+      len_s = *D.pred.len;
+      w_s = (*D.pred.cursor + static_cast<int>(blockIdx.x)) % n;
+      __threadfence();
+      atomicAdd(arrive, 1u);
+    }
+    __syncthreads();
+    const int len = len_s, w = w_s;
+    const size_t o = static_cast<size_t>(w) * D.pred.max_hist;
+    if (tid == 0 && len < D.pred.max_hist) {
+      const double v = fused_speed_phases > 0 ? local_speed(D, w - D.rank * D.n_local, fused_speed_phases, nullptr)
+                                              : D.v_obs_all[w];
+      D.pred.hv[o + len] = v;
+      D.pred.hc[o + len] = D.c_now[w];
+      D.pred.hm[o + len] = D.m_now[w];
+    }
+    __syncthreads();
+    const int L = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
+    double* buf = narx_train_scratch_bytes(L) <= smem_bytes
+                      ? sm_d
+                      : D.pred.scratch + static_cast<size_t>(blockIdx.x) * 13 * D.pred.max_hist;
+    lbbsp_narx_train_cfg cfg = D.pred.train;
+    cfg.min_history = D.pred.warmup;
+    narx_train_block(&D.pred.models[w], D.pred.hv + o, D.pred.hc + o, D.pred.hm + o, L, cfg,
+                     &D.pred.reports[w], nullptr, 0, buf, &ts);
+    return;
+  }
+  if (tid == 0) D.stamps[3] = gtimer();
+  if (fused_speed_phases > 0) {  // single rank: measured speeds computed here
+    for (int i = tid; i < D.n_local; i += blockDim.x) {
+      double t;
+      D.v_obs_local[i] = local_speed(D, i, fused_speed_phases, &t);
+      const int rw = *D.rows;
+      if (rw < D.max_rows) D.rec_t[static_cast<size_t>(rw) * D.n_total + D.rank * D.n_local + i] = t;
+    }
+    __syncthreads();
+  }
+  const int len = *D.pred.len;
+  const int row = *D.rows;
+  for (int i = tid; i < n; i += blockDim.x) {
+    observe_d(D.pred, i, len, D.v_obs_all[i], D.c_now[i], D.m_now[i], 0.0);
+    if (row < D.max_rows) D.rec_vobs[static_cast<size_t>(row) * n + i] = D.v_obs_all[i];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    while (atomicAdd(arrive, 0u) < static_cast<unsigned>(nb)) {
+    }
+    *arrive = 0u;
+    *D.pred.len = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
+    *D.train_first = *D.pred.cursor;
+    *D.pred.cursor = (*D.pred.cursor + (n + 1) / 2) % n;
+    *D.rows = row + 1;
+    *D.k += 1;
+    D.stamps[4] = gtimer();
+  }
+}
+
 // P10: push every worker's (v, c, m) (cluster_sim.cpp:309-313), advance round
 __global__ void observe_kernel(PlanDev D, int fused_speed_phases) {
   stamp(D, 3);
@@ -577,6 +662,7 @@ struct lbbsp_mlp {
   double* head_loss = nullptr;     // [sms]
   unsigned* head_cnt = nullptr;    // [n_local] worker head counters (self-resetting)
   unsigned* head_cnt_d = nullptr;  // [1] dataset-loss head counter
+  unsigned* arrive = nullptr;      // observe_train_kernel arrival count (self-resetting)
   long long* reg_len = nullptr;
   int n_reg = 0;
   PlanDev D{};
@@ -771,11 +857,19 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     so = side;
   }
   // ---- observe branch ----
-  observe_kernel<<<1, 256, 0, so>>>(D, cfg.world > 1 ? 0 : n_phases);
-  ++nl;
-  if (pred.dev.kind == LBBSP_PRED_NARX) {
-    LBBSP_CUDA_CHECK(launch_pred_train_from(pred.dev, D.train_first, so));
+  const int nb = (n_total + 1) / 2;
+  if (pred.dev.kind == LBBSP_PRED_NARX && nb + 1 <= num_sms()) {
+    const size_t tsm = train_smem_bytes(pred.dev.max_hist);
+    observe_train_kernel<<<nb + 1, kTrainThreads, tsm, so>>>(D, cfg.world > 1 ? 0 : n_phases,
+                                                             arrive, tsm);
     ++nl;
+  } else {
+    observe_kernel<<<1, 256, 0, so>>>(D, cfg.world > 1 ? 0 : n_phases);
+    ++nl;
+    if (pred.dev.kind == LBBSP_PRED_NARX) {
+      LBBSP_CUDA_CHECK(launch_pred_train_from(pred.dev, D.train_first, so));
+      ++nl;
+    }
   }
   // ---- aggregate + apply ----
   if (cfg.world > 1 && !bucketed) {
@@ -994,6 +1088,9 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     D.v_obs_all = D.v_obs_local;
   LBBSP_CUDA_CHECK(m.alloc(&D.loss_acc, 1));
   LBBSP_CUDA_CHECK(m.alloc(&D.stamps, 16));
+  LBBSP_CUDA_CHECK(m.alloc(&m.arrive, 1));
+  LBBSP_CUDA_CHECK(cudaFuncSetAttribute(observe_train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024));
   D.N_data = m.N_data;
   D.loss_on = c.loss_every > 0 ? 1 : 0;
   LBBSP_CUDA_CHECK(m.alloc(&D.train_first, 1));
@@ -1052,16 +1149,24 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     // its CTA partition idle (the emulated-worker C2 shapes)
     const double rows_per_worker = static_cast<double>(m.B_total) / c.world / m.n_local;
     const int ctas_per_worker = std::max(1, D.sm_budget / m.n_local);
-    // widest N tile that still gives a worker about one tile per CTA
-    auto pick_bn = [&](double mrows, int ncols) {
+    // widest N tile that still gives a worker's CTAs enough tiles; the row
+    // (forward) GEMMs run on trace-capped partitions, typically about half
+    // the nominal share, so they need fewer tiles per nominal CTA (measured
+    // on C2, scripts/c2_bn_sweep.py)
+    auto pick_bn = [&](double mrows, int ncols, double fill = 0.75) {
       for (int bn : {256, 128}) {
         if (ncols < bn) continue;
         const double tiles = std::ceil(mrows / 128.0) * std::ceil(ncols / static_cast<double>(bn));
-        if (tiles >= 0.75 * ctas_per_worker) return bn;
+        if (tiles >= fill * ctas_per_worker) return bn;
       }
       return 64;
     };
-    const int bn = pick_bn(rows_per_worker, dout);
+    auto env_bn = [](const char* name, int dflt) {  // tuning override (experiments)
+      const char* v = getenv(name);
+      const int b = v ? atoi(v) : 0;
+      return (b == 64 || b == 128 || b == 256) ? b : dflt;
+    };
+    const int bn = env_bn("LBBSP_BN_FWD", pick_bn(rows_per_worker, dout, 0.4));
     const int epi = last ? tc::kEpiBiasBf16 : tc::kEpiBiasReluBf16;
     const bool pr = m.use_pair;
     int rc = gemm_plan(&m.fwd[l], Ain, m.pb + m.off_w[l], m.B_cap, dout, din, false, false,
@@ -1077,8 +1182,8 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     m.fwd_d[l].args.ldc = dout;
     m.fwd_d[l].args.bias = m.params + m.off_b[l];
     // dW_l = dZ_l^T A_l : M=dout, N=din, K=rows ; A = dZ_l [rows][dout] MN-major, B = A_l [rows][din] MN-major
-    const int bn_w = pick_bn(static_cast<double>(dout), din);
-    const int bn_x = pick_bn(rows_per_worker, din);
+    const int bn_w = env_bn("LBBSP_BN_DW", pick_bn(static_cast<double>(dout), din));
+    const int bn_x = env_bn("LBBSP_BN_DX", pick_bn(rows_per_worker, din));
     rc = gemm_plan(&m.dw[l], m.dZ[l], Ain, dout, din, m.B_cap, true, true, pr ? 256 : bn_w,
                    tc::kEpiF32, pr);
     if (rc) return rc;

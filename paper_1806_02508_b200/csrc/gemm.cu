@@ -62,7 +62,7 @@ int num_sms() {
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int ctas,
-                    cudaStream_t s) {
+                    cudaStream_t s, bool pdl) {
   constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   constexpr size_t smem = tc::gemm_smem_bytes<BN, STAGES>();
   auto kern = tc::gemm_bf16_tc_kernel<BN, A_MN, B_MN, EPI, STAGES>;
@@ -71,14 +71,13 @@ static int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
-  kern<<<ctas, tc::kGemmThreads, smem, s>>>(ta, tb, a);
-  LBBSP_CUDA_CHECK(cudaGetLastError());
+  LBBSP_CUDA_CHECK(launch_maybe_pdl(kern, ctas, tc::kGemmThreads, smem, s, pdl, ta, tb, a));
   return LBBSP_OK;
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static int launch_t2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int ctas,
-                     cudaStream_t s) {
+                     cudaStream_t s, bool pdl) {
   constexpr int STAGES = BN == 256 ? 7 : 8;
   constexpr size_t smem = tc::gemm2_smem_bytes<BN, STAGES>();
   auto kern = tc::gemm_bf16_tc2_kernel<BN, A_MN, B_MN, EPI, STAGES>;
@@ -87,18 +86,17 @@ static int launch_t2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArg
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
-  kern<<<ctas, tc::kGemmThreads, smem, s>>>(ta, tb, a);
-  LBBSP_CUDA_CHECK(cudaGetLastError());
+  LBBSP_CUDA_CHECK(launch_maybe_pdl(kern, ctas, tc::kGemmThreads, smem, s, pdl, ta, tb, a));
   return LBBSP_OK;
 }
 
 #define LBBSP_GEMM2_CASE(BN_, AMN, BMN, EPI_)                                          \
   if (bn == BN_ && a_mn == AMN && b_mn == BMN && epi == EPI_)                          \
-    return launch_t2<BN_, AMN, BMN, EPI_>(p.ta, p.tb, p.args, ctas, s);
+    return launch_t2<BN_, AMN, BMN, EPI_>(p.ta, p.tb, p.args, ctas, s, p.pdl);
 
 #define LBBSP_GEMM_CASE(BN_, AMN, BMN, EPI_)                                           \
   if (bn == BN_ && a_mn == AMN && b_mn == BMN && epi == EPI_)                          \
-    return launch_t<BN_, AMN, BMN, EPI_>(p.ta, p.tb, p.args, ctas, s);
+    return launch_t<BN_, AMN, BMN, EPI_>(p.ta, p.tb, p.args, ctas, s, p.pdl);
 
 int gemm_launch(const GemmPlan& p, cudaStream_t s) {
   const int bn = p.bn, epi = p.args_epi;

@@ -1,5 +1,6 @@
 // gemm.cuh -- host-side plan for the tcgen05 GEMM (gemm_tc.cuh).
 #pragma once
+#include <utility>
 #include <cuda.h>
 
 #include "gemm_tc.cuh"
@@ -15,7 +16,26 @@ struct GemmPlan {
   int args_epi = 0;
   int ctas = 148;
   bool pair = false;  // CTA-pair (cta_group::2) kernel: 256 x bn tiles, ungrouped only
+  bool pdl = false;   // programmatic dependent launch (prologue overlaps the previous kernel)
 };
+
+// Launches `kern` with the programmatic-stream-serialization attribute when
+// pdl is set (the kernel must call pdl_wait() before reading its inputs).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_maybe_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem,
+                             cudaStream_t s, bool pdl, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 int make_tmap_bf16(CUtensorMap* tm, const void* ptr, long long inner, long long outer, long long ld,
                    int box_outer);

@@ -95,6 +95,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_base_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // the prologue above overlaps the previous kernel (programmatic launch);
+  // everything below may read its outputs (A operand, groups from the plan)
+  pdl_wait();
+  pdl_launch_dependents();
   // ---- which worker (group) does this CTA serve? --------------------------------
   if (threadIdx.x == 0) {
     int g = -1, cta_in = 0, cta_cnt = gridDim.x;
@@ -116,23 +137,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     grp_slot[1] = cta_in;
     grp_slot[2] = cta_cnt;
   }
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
-    }
-    fence_barrier_init();
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
-  }
-  if (warp == 1) tmem_alloc<kTmemCols>(tmem_base_slot);
-  tc_fence_before();
   __syncthreads();
-  tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
   const int g = grp_slot[0], cta_in = grp_slot[1], cta_cnt = grp_slot[2];
 

@@ -108,23 +108,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
-  // One worker per GPU (n_groups <= 1): its rows (kRows) or K range (kKSplit)
-  // and its SM cap come from device memory, set by the round's plan kernel.
-  // A k-split worker's K range is rounded up to the 64-row block; the rows
-  // past its end are kept zero in the A operand by the producer of dZ.
-  int cta_lo = 0, cta_n = gridDim.x, r0 = 0, r1 = args.mode == kRows ? args.M : args.K;
-  if (args.n_groups == 1) {
-    cta_lo = args.g_cta0[0];
-    cta_n = args.g_ctan[0];
-    r0 = args.g_r0[0];
-    r1 = args.g_r1[0];
-  }
-  cta_lo &= ~1;
-  cta_n &= ~1;
-  if (cta_n < 2) cta_n = 2;
-  const bool idle = static_cast<int>(blockIdx.x) < cta_lo || static_cast<int>(blockIdx.x) >= cta_lo + cta_n;
-  const int pair = (static_cast<int>(blockIdx.x) - cta_lo) / 2, n_pairs = cta_n / 2;
-
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -143,6 +126,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  pdl_wait();  // prologue above overlaps the previous kernel (programmatic launch)
+  pdl_launch_dependents();
+  // One worker per GPU (n_groups <= 1): its rows (kRows) or K range (kKSplit)
+  // and its SM cap come from device memory, set by the round's plan kernel.
+  // A k-split worker's K range is rounded up to the 64-row block; the rows
+  // past its end are kept zero in the A operand by the producer of dZ.
+  int cta_lo = 0, cta_n = gridDim.x, r0 = 0, r1 = args.mode == kRows ? args.M : args.K;
+  if (args.n_groups == 1) {
+    cta_lo = args.g_cta0[0];
+    cta_n = args.g_ctan[0];
+    r0 = args.g_r0[0];
+    r1 = args.g_r1[0];
+  }
+  cta_lo &= ~1;
+  cta_n &= ~1;
+  if (cta_n < 2) cta_n = 2;
+  const bool idle = static_cast<int>(blockIdx.x) < cta_lo || static_cast<int>(blockIdx.x) >= cta_lo + cta_n;
+  const int pair = (static_cast<int>(blockIdx.x) - cta_lo) / 2, n_pairs = cta_n / 2;
+
 
   int m_begin, m_len, k_begin, k_len;
   if (args.mode == kRows) {

@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 
 #include "mlp_kernels.cuh"
+#include "tc_ptx.cuh"
 
 namespace lbbsp {
 namespace mlp {
@@ -104,22 +105,20 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
   // latency-bound, and fewer CTA partials keep the final combine short
   cta_cnt = min(cta_cnt, max(1, (n_tiles + 7) / 8));
   if (cta_in >= cta_cnt) return;
-  if (timing && threadIdx.x == 0) atomicMin(&timing[2 * g], static_cast<unsigned long long>(gtimer()));
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int gq = lane >> 2, tq = lane & 3;
   const int wstride = cta_cnt * 8;
   int tile = cta_in * 8 + warp;
   const uint32_t hbuf0 = smem_addr(sm + kHmH + warp * 2 * 8192);
-  // first tile's loads overlap the weight-fragment setup
-  if (tile < n_tiles) stage_tile(hbuf0, H, r0 + tile * 16, r1, lane);
 
   // W (fp32 master): one cp.async round into smem, then bf16 B fragments
-  // (zero for classes >= 10)
+  // (zero for classes >= 10). W and the worker groups were final before the
+  // previous kernel started, so this overlaps it (programmatic launch).
   const float* wraw = reinterpret_cast<const float*>(sm + kHmWraw);
   for (int i = threadIdx.x; i < kHeadNC * kHeadDH / 4; i += blockDim.x)
     cp_async16(smem_addr(sm + kHmWraw + 16 * i), W + 4 * i, 16);
   cp_async_commit();
-  cp_async_wait<0>();  // also lands this warp's first H tile
+  cp_async_wait<0>();
   __syncthreads();
   uint2* wl = reinterpret_cast<uint2*>(sm + kHmWl);
   uint2* wd = reinterpret_cast<uint2*>(sm + kHmWd);
@@ -135,6 +134,10 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
     wd[i] = make_uint2(pack_bf16(wv(c, n), wv(c + 1, n)), pack_bf16(wv(c + 8, n), wv(c + 9, n)));
   }
   __syncthreads();
+  tc::pdl_wait();  // H, labels and row scales come from the kernels before
+  tc::pdl_launch_dependents();
+  if (timing && threadIdx.x == 0) atomicMin(&timing[2 * g], static_cast<unsigned long long>(gtimer()));
+  if (tile < n_tiles) stage_tile(hbuf0, H, r0 + tile * 16, r1, lane);
 
   const float b_lo0 = bias[2 * tq], b_lo1 = bias[2 * tq + 1];
   const float b_hi0 = tq == 0 ? bias[8] : 0.f, b_hi1 = tq == 0 ? bias[9] : 0.f;

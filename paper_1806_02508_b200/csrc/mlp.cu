@@ -180,6 +180,7 @@ __device__ __forceinline__ void stamp(const PlanDev& D, int i) {
 // plus the Eq. 6/7 row scales of this rank's rows. Everything thread 0 walks
 // sequentially lives in shared memory (no dependent global round trips).
 __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) {
+  tc::pdl_launch_dependents();  // the forward GEMM's prologue may start now
   __shared__ SolverSmem sm;
   __shared__ double rem[LBBSP_MAX_WORKERS];
   __shared__ double avail[LBBSP_MAX_WORKERS];
@@ -433,6 +434,8 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(const float* __restri
                                                            long long P, float* grad, float* params,
                                                            bf16* pb, float lr, int apply,
                                                            unsigned long long* stamps) {
+  tc::pdl_wait();  // the worker partials come from the backward GEMMs
+  tc::pdl_launch_dependents();
   if (stamps && threadIdx.x == 0 && blockIdx.x == 0) stamps[5] = gtimer();
   const long long nv = P / 4;
   for (long long v = blockIdx.x * 256ll + threadIdx.x; v < nv; v += 256ll * gridDim.x) {
@@ -663,6 +666,7 @@ struct lbbsp_mlp {
   unsigned* head_cnt = nullptr;    // [n_local] worker head counters (self-resetting)
   unsigned* head_cnt_d = nullptr;  // [1] dataset-loss head counter
   unsigned* arrive = nullptr;      // observe_train_kernel arrival count (self-resetting)
+  bool use_pdl = true;             // programmatic dependent launch on the worker-phase chain
   long long* reg_len = nullptr;
   int n_reg = 0;
   PlanDev D{};
@@ -743,6 +747,7 @@ int launch_grouped(lbbsp_mlp* m, GemmPlan& p, int mode, unsigned long long* timi
   p.args.g_ctan = m->D.ctan;
   p.args.timing = timing;
   p.ctas = m->D.sm_budget;
+  p.pdl = m->use_pdl;
   return gemm_launch(p, s);
 }
 
@@ -782,10 +787,12 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   const int hl = L - 1;  // last layer index
   if (small_head) {
     const bf16* Hin = L >= 2 ? H[L - 2] : X;
-    head_mma_kernel<true><<<sms, 256, kHeadMmaSmem, s>>>(
-        G, 0, Hin, params + off_w[hl], params + off_b[hl], y, row_scale, dZ[L - 2], partial, P,
-        off_w[hl], off_b[hl], off_b[L - 2], nullptr, head_part, head_loss, head_cnt,
-        phase_slot(ph++));
+    LBBSP_CUDA_CHECK(launch_maybe_pdl(
+        head_mma_kernel<true>, sms, 256, kHeadMmaSmem, s, use_pdl, G, 0, Hin,
+        static_cast<const float*>(params + off_w[hl]), static_cast<const float*>(params + off_b[hl]),
+        static_cast<const int*>(y), static_cast<const float*>(row_scale), dZ[L - 2], partial, P,
+        off_w[hl], off_b[hl], off_b[L - 2], static_cast<double*>(nullptr), head_part, head_loss,
+        head_cnt, phase_slot(ph++)));
   } else {
     softmax_ce_kernel<<<sms, 256, 0, s>>>(G, 0, logits, dims[L], y, row_scale, dZ[L - 1], nullptr,
                                           phase_slot(ph++));
@@ -875,13 +882,16 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   if (cfg.world > 1 && !bucketed) {
     reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(grad, 1, P, grad, params, pb, lr, 1, D.stamps);
   } else {
-    reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 1, D.stamps);
+    LBBSP_CUDA_CHECK(launch_maybe_pdl(reduce_apply_kernel, sms * 4, 256, 0, s, use_pdl,
+                                      static_cast<const float*>(partial), n_local, P, grad, params, pb,
+                                      lr, 1, D.stamps));
   }
   ++nl;
   // ---- full-dataset loss (step_sync P9, cluster_sim.cpp:445) ----
   if (D.loss_on) {
     for (int l = 0; l < Lg; ++l) {
       fwd_d[l].ctas = std::min(fwd_d[l].ctas, sms) & ~1;
+      fwd_d[l].pdl = use_pdl;
       int rc = gemm_launch(fwd_d[l], s);
       if (rc) return rc;
       ++nl;
@@ -890,9 +900,12 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     none.n = 0;
     if (small_head) {
       const bf16* Hin = L >= 2 ? Hd[L - 2] : data_x;
-      head_mma_kernel<false><<<sms, 256, kHeadMmaSmem, s>>>(
-          none, N_data, Hin, params + off_w[hl], params + off_b[hl], data_y, nullptr, nullptr,
-          nullptr, 0, 0, 0, 0, D.loss_acc, head_part, head_loss, head_cnt_d, D.stamps + 6);
+      LBBSP_CUDA_CHECK(launch_maybe_pdl(
+          head_mma_kernel<false>, sms, 256, kHeadMmaSmem, s, use_pdl, none, N_data, Hin,
+          static_cast<const float*>(params + off_w[hl]), static_cast<const float*>(params + off_b[hl]),
+          static_cast<const int*>(data_y), static_cast<const float*>(nullptr),
+          static_cast<bf16*>(nullptr), static_cast<float*>(nullptr), 0ll, 0ll, 0ll, 0ll, D.loss_acc,
+          head_part, head_loss, head_cnt_d, D.stamps + 6));
     } else {
       softmax_ce_kernel<<<sms, 256, 0, s>>>(none, N_data, logits_d, dims[L], data_y, nullptr, nullptr,
                                             D.loss_acc, nullptr);
@@ -949,6 +962,7 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   m.B_cap = c.global_batch;  // a rank can be handed (almost) the whole batch
   m.N_data = c.dataset_size;
   m.small_head = small_head;
+  m.use_pdl = !getenv("LBBSP_NO_PDL");
   m.max_rows = c.max_iterations > 0 ? c.max_iterations : 1;
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking));
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.side, cudaStreamNonBlocking));
@@ -1175,8 +1189,12 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     m.fwd[l].args.c_bf16 = last ? m.logits : m.H[l];
     m.fwd[l].args.ldc = dout;
     m.fwd[l].args.bias = m.params + m.off_b[l];
+    // the dataset forward (loss branch) uses the whole GPU: narrow tiles
+    // when its row count alone would leave most SMs idle
+    const int bn_d = env_bn("LBBSP_BN_LOSS",
+                            std::ceil(m.N_data / 128.0) * std::ceil(dout / 128.0) < sms / 2 ? 64 : bn);
     rc = gemm_plan(&m.fwd_d[l], Ain_d, m.pb + m.off_w[l], m.N_data, dout, din, false, false,
-                   pr ? 256 : bn, epi, pr);
+                   pr ? 256 : bn_d, epi, pr);
     if (rc) return rc;
     m.fwd_d[l].args.c_bf16 = last ? m.logits_d : m.Hd[l];
     m.fwd_d[l].args.ldc = dout;

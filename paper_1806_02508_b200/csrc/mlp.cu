@@ -332,7 +332,7 @@ __device__ __forceinline__ void phase_end(unsigned long long* timing, int g) {
   if (timing && threadIdx.x == 0) atomicMax(&timing[2 * g + 1], static_cast<unsigned long long>(gtimer()));
 }
 
-// Large softmax-CE head: one warp per row over bf16 logits [rows][n_out]
+// Large softmax-CE head: one warp per row -- the fallback for other widths over bf16 logits [rows][n_out]
 // (n_out % 256 == 0): loss and dZ = (softmax - onehot) * row_scale.
 __global__ void __launch_bounds__(256) softmax_ce_kernel(
     Groups G, int rows_total, const bf16* __restrict__ logits, int n_out,
@@ -397,20 +397,158 @@ __global__ void __launch_bounds__(256) softmax_ce_kernel(
   phase_end(timing, g);
 }
 
-// db partial of worker g = column sums of dZ over its rows (N % 8 == 0)
-__global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __restrict__ dZ, int N,
-                                                        float* slab, long long slab_stride,
-                                                        long long off_b, unsigned long long* timing) {
+// Softmax-CE head for n_out = 256 * NV (NV <= 16): one warp per row, the row
+// read once into registers (max, sum and dlogits from the same values), and
+// the next row's loads issued before this row's math.
+template <int NV>
+__global__ void __launch_bounds__(256) softmax_ce_reg_kernel(
+    Groups G, int rows_total, const bf16* __restrict__ logits, const int* __restrict__ y,
+    const float* __restrict__ row_scale, bf16* dZ, double* loss_acc, unsigned long long* timing) {
+  constexpr int n_out = 256 * NV;
   int g, cta_in, cta_cnt;
   if (!my_group(G, &g, &cta_in, &cta_cnt)) return;
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+  phase_begin(timing, g);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  const int r0 = G.n ? G.r0[g] : 0, r1 = G.n ? G.r1[g] : rows_total;
+  double lsum = 0.0;
+  const int stride = cta_cnt * nw;
+  int r = r0 + cta_in * nw + warp;
+  uint4 nq[NV];
+  if (r < r1) {
+    const uint4* row = reinterpret_cast<const uint4*>(logits + static_cast<long long>(r) * n_out);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) nq[v] = __ldg(&row[lane + 32 * v]);
+  }
+  for (; r < r1; r += stride) {
+    uint4 q[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) q[v] = nq[v];
+    if (r + stride < r1) {
+      const uint4* nrow = reinterpret_cast<const uint4*>(logits + static_cast<long long>(r + stride) * n_out);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) nq[v] = __ldg(&nrow[lane + 32 * v]);
+    }
+    float mx = -1e30f;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q[v]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(b2[j]);
+        mx = fmaxf(mx, fmaxf(f.x, f.y));
+      }
+    }
+    mx = warp_max(mx);
+    float se = 0.f;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q[v]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(b2[j]);
+        se += __expf(f.x - mx) + __expf(f.y - mx);
+      }
+    }
+    se = warp_sum(se);
+    const int yr = y[r];
+    const float ly = __bfloat162float(logits[static_cast<long long>(r) * n_out + yr]);
+    if (lane == 0) lsum += static_cast<double>(logf(se) + mx - ly);
+    if (dZ) {
+      const float inv = 1.f / se, sc = row_scale[r];
+      uint4* out = reinterpret_cast<uint4*>(dZ + static_cast<long long>(r) * n_out);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q[v]);
+        uint4 o;
+        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(b2[j]);
+          const int c = (lane + 32 * v) * 8 + 2 * j;
+          const float a = (__expf(f.x - mx) * inv - (c == yr ? 1.f : 0.f)) * sc;
+          const float b = (__expf(f.y - mx) * inv - (c + 1 == yr ? 1.f : 0.f)) * sc;
+          o2[j] = __floats2bfloat162_rn(a, b);
+        }
+        out[lane + 32 * v] = o;
+      }
+    }
+  }
+  if (loss_acc && lane == 0 && lsum != 0.0) atomicAdd(loss_acc, lsum);
+  __syncthreads();
+  phase_end(timing, g);
+}
+
+static cudaError_t launch_softmax_ce(int sms, cudaStream_t s, bool pdl, Groups G, int rows_total,
+                                     const bf16* logits, int n_out, const int* y,
+                                     const float* row_scale, bf16* dZ, double* loss_acc,
+                                     unsigned long long* timing) {
+  switch (n_out) {
+#define LBBSP_SMX(NV_)                                                                          \
+  case 256 * NV_:                                                                               \
+    return launch_maybe_pdl(softmax_ce_reg_kernel<NV_>, sms, 256, 0, s, pdl, G, rows_total, logits, \
+                            y, row_scale, dZ, loss_acc, timing);
+    LBBSP_SMX(1)
+    LBBSP_SMX(2)
+    LBBSP_SMX(4)
+    LBBSP_SMX(8)
+    LBBSP_SMX(16)
+#undef LBBSP_SMX
+    default:
+      softmax_ce_kernel<<<sms, 256, 0, s>>>(G, rows_total, logits, n_out, y, row_scale, dZ,
+                                            loss_acc, timing);
+      return cudaGetLastError();
+  }
+}
+
+
+// db partial of worker g = column sums of dZ over its rows (N % 8 == 0)
+// Bias gradient db = column sums of dZ over the worker's rows, written into
+// the worker's slab. Two deterministic stages: CTA (rb, cb) sums a block of
+// rows for 2048 columns (8 per thread, 16-B loads) into its own scratch row;
+// the worker's last CTA adds the row blocks in order.
+constexpr int kBiasCols = 2048;
+constexpr int kBiasMaxRowBlocks = 32;
+__global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __restrict__ dZ, int N,
+                                                        float* slab, long long slab_stride,
+                                                        long long off_b, float* scratch,
+                                                        unsigned* counters,
+                                                        unsigned long long* timing) {
+  int g, cta_in, cta_cnt;
+  if (!my_group(G, &g, &cta_in, &cta_cnt)) return;
+  const int ncb = (N + kBiasCols - 1) / kBiasCols;
+  const int rbs = max(1, min(kBiasMaxRowBlocks, cta_cnt / ncb));
+  const int used = rbs * ncb;
+  if (cta_in >= used) return;
   phase_begin(timing, g);
   const int r0 = G.r0[g], r1 = G.r1[g];
-  const int nv = N / 8;
-  float* gs = slab + static_cast<long long>(g) * slab_stride + off_b;
-  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int r = r0 + cta_in; r < r1; r += cta_cnt) {
-      const uint4 q = reinterpret_cast<const uint4*>(dZ + static_cast<long long>(r) * N)[v];
+  const int cb = cta_in % ncb, rb = cta_in / ncb;
+  const int rows = r1 - r0, per = (rows + rbs - 1) / rbs;
+  const int ra = r0 + rb * per, rz = min(r1, ra + per);
+  const int c0 = blockIdx.x - cta_in;  // the worker's first CTA
+  const int col = cb * kBiasCols + threadIdx.x * 8;
+  float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (col < N) {
+    int r = ra;
+#pragma unroll 1
+    for (; r + 8 <= rz; r += 8) {  // eight rows in flight
+      uint4 q[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) q[u] = *reinterpret_cast<const uint4*>(dZ + static_cast<long long>(r + u) * N + col);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q[u]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(b2[j]);
+          a[2 * j] += f.x;
+          a[2 * j + 1] += f.y;
+        }
+      }
+    }
+    for (; r < rz; ++r) {
+      const uint4 q = *reinterpret_cast<const uint4*>(dZ + static_cast<long long>(r) * N + col);
       const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -419,11 +557,41 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
         a[2 * j + 1] += f.y;
       }
     }
-    if (r0 + cta_in < r1)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) atomicAdd(&gs[v * 8 + j], a[j]);
+    float* dst = scratch + static_cast<long long>(blockIdx.x) * kBiasCols + threadIdx.x * 8;
+    *reinterpret_cast<float4*>(dst) = make_float4(a[0], a[1], a[2], a[3]);
+    *reinterpret_cast<float4*>(dst + 4) = make_float4(a[4], a[5], a[6], a[7]);
   }
+  __threadfence();
   __syncthreads();
+  __shared__ int last;
+  if (threadIdx.x == 0) last = atomicAdd(&counters[g], 1u) == static_cast<unsigned>(used - 1);
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    float* gs = slab + static_cast<long long>(g) * slab_stride + off_b;
+    // float4 columns; all row-block partials of a column in flight at once,
+    // added in row-block order
+    for (int c4 = threadIdx.x; c4 < N / 4; c4 += blockDim.x) {
+      const int c = 4 * c4, b = c / kBiasCols, o = c % kBiasCols;
+      float4 t[kBiasMaxRowBlocks];
+#pragma unroll
+      for (int q = 0; q < kBiasMaxRowBlocks; ++q)
+        if (q < rbs)
+          t[q] = __ldcg(reinterpret_cast<const float4*>(
+              &scratch[static_cast<long long>(c0 + q * ncb + b) * kBiasCols + o]));
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < kBiasMaxRowBlocks; ++q)
+        if (q < rbs) {
+          v.x += t[q].x;
+          v.y += t[q].y;
+          v.z += t[q].z;
+          v.w += t[q].w;
+        }
+      *reinterpret_cast<float4*>(&gs[c]) = v;
+    }
+    if (threadIdx.x == 0) counters[g] = 0u;
+  }
   phase_end(timing, g);
 }
 
@@ -666,6 +834,8 @@ struct lbbsp_mlp {
   unsigned* head_cnt = nullptr;    // [n_local] worker head counters (self-resetting)
   unsigned* head_cnt_d = nullptr;  // [1] dataset-loss head counter
   unsigned* arrive = nullptr;      // observe_train_kernel arrival count (self-resetting)
+  float* bias_part = nullptr;      // [sms][kBiasCols] bias-gradient row-block partials
+  unsigned* bias_cnt = nullptr;    // [n_local] bias_grad_kernel counters (self-resetting)
   bool use_pdl = true;             // programmatic dependent launch on the worker-phase chain
   long long* reg_len = nullptr;
   int n_reg = 0;
@@ -794,8 +964,8 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
         off_w[hl], off_b[hl], off_b[L - 2], static_cast<double*>(nullptr), head_part, head_loss,
         head_cnt, phase_slot(ph++)));
   } else {
-    softmax_ce_kernel<<<sms, 256, 0, s>>>(G, 0, logits, dims[L], y, row_scale, dZ[L - 1], nullptr,
-                                          phase_slot(ph++));
+    LBBSP_CUDA_CHECK(launch_softmax_ce(sms, s, use_pdl, G, 0, logits, dims[L], y, row_scale,
+                                       dZ[L - 1], nullptr, phase_slot(ph++)));
   }
   ++nl;
   // ---- backward ----
@@ -807,7 +977,8 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   const bool bucketed = cfg.world > 1 && n_local == 1 && !small_head;
   for (int l = Lg - 1; l >= 0; --l) {
     if (!(small_head && l == L - 2)) {  // the small head already summed this bias gradient
-      bias_grad_kernel<<<sms, 256, 0, s>>>(G, dZ[l], dims[l + 1], partial, P, off_b[l], phase_slot(ph++));
+      bias_grad_kernel<<<sms, 256, 0, s>>>(G, dZ[l], dims[l + 1], partial, P, off_b[l], bias_part,
+                                           bias_cnt, phase_slot(ph++));
       ++nl;
     }
     int rc = launch_grouped(this, dw[l], tc::kKSplit, phase_slot(ph++), s);
@@ -820,6 +991,12 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
       if (nccl_api()->AllReduce(partial + seg0, partial + seg0, static_cast<size_t>(seg1 - seg0),
                                 ncclFloat, ncclSum, comm, comm_stream) != ncclSuccess)
         return set_error(LBBSP_NCCL, "ncclAllReduce (bucket %d) failed", l);
+      // apply this layer's update as soon as its bucket is reduced, beside
+      // the rest of the backward pass
+      reduce_apply_kernel<<<sms * 2, 256, 0, comm_stream>>>(
+          partial + seg0, 1, seg1 - seg0, grad + seg0, params + seg0, pb + seg0,
+          static_cast<float>(cfg.learning_rate), 1, nullptr);
+      ++nl;
     }
     if (l > 0) {
       rc = launch_grouped(this, dx[l], tc::kRows, phase_slot(ph++), s);
@@ -842,11 +1019,9 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
       LBBSP_CUDA_CHECK(cudaEventRecord(ev_comm, comm_stream));
       LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_comm, 0));
     } else {
-      reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 0, D.stamps);
-      ++nl;
-      if (nccl_api()->AllReduce(grad, grad, static_cast<size_t>(P), ncclFloat, ncclSum, comm, s) !=
-          ncclSuccess)
-        return set_error(LBBSP_NCCL, "ncclAllReduce failed");
+      // speeds first: the observe / NARX branch (the usual critical tail)
+      // forks right after this small all-gather; the gradient all-reduce
+      // follows on the loss branch
       if (nccl_api()->AllGather(D.v_obs_local, D.v_obs_all, static_cast<size_t>(n_local), ncclDouble,
                                 comm, s) != ncclSuccess)
         return set_error(LBBSP_NCCL, "ncclAllGather failed");
@@ -878,15 +1053,21 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
       ++nl;
     }
   }
-  // ---- aggregate + apply ----
-  if (cfg.world > 1 && !bucketed) {
+  // ---- aggregate + apply (the bucketed path applied per layer above) ----
+  if (bucketed) {
+  } else if (cfg.world > 1) {
+    reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 0, D.stamps);
+    ++nl;
+    if (nccl_api()->AllReduce(grad, grad, static_cast<size_t>(P), ncclFloat, ncclSum, comm, s) !=
+        ncclSuccess)
+      return set_error(LBBSP_NCCL, "ncclAllReduce failed");
     reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(grad, 1, P, grad, params, pb, lr, 1, D.stamps);
   } else {
-    LBBSP_CUDA_CHECK(launch_maybe_pdl(reduce_apply_kernel, sms * 4, 256, 0, s, use_pdl,
-                                      static_cast<const float*>(partial), n_local, P, grad, params, pb,
-                                      lr, 1, D.stamps));
+    // not a programmatic launch: early-resident apply CTAs would hold the SMs
+    // the (higher-priority) NARX branch needs when the backward ends
+    reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 1, D.stamps);
   }
-  ++nl;
+  if (!bucketed) ++nl;
   // ---- full-dataset loss (step_sync P9, cluster_sim.cpp:445) ----
   if (D.loss_on) {
     for (int l = 0; l < Lg; ++l) {
@@ -907,8 +1088,8 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
           static_cast<bf16*>(nullptr), static_cast<float*>(nullptr), 0ll, 0ll, 0ll, 0ll, D.loss_acc,
           head_part, head_loss, head_cnt_d, D.stamps + 6));
     } else {
-      softmax_ce_kernel<<<sms, 256, 0, s>>>(none, N_data, logits_d, dims[L], data_y, nullptr, nullptr,
-                                            D.loss_acc, nullptr);
+      LBBSP_CUDA_CHECK(launch_softmax_ce(sms, s, use_pdl, none, N_data, logits_d, dims[L], data_y,
+                                         nullptr, nullptr, D.loss_acc, nullptr));
     }
     ++nl;
   }
@@ -965,7 +1146,11 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   m.use_pdl = !getenv("LBBSP_NO_PDL");
   m.max_rows = c.max_iterations > 0 ? c.max_iterations : 1;
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking));
-  LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.side, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;  // the observe / NARX branch is the round's usual critical tail
+    LBBSP_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    LBBSP_CUDA_CHECK(cudaStreamCreateWithPriority(&m.side, cudaStreamNonBlocking, hi));
+  }
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_fork, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_gather0, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_gather1, cudaEventDisableTiming));
@@ -1103,6 +1288,8 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(m.alloc(&D.loss_acc, 1));
   LBBSP_CUDA_CHECK(m.alloc(&D.stamps, 16));
   LBBSP_CUDA_CHECK(m.alloc(&m.arrive, 1));
+  LBBSP_CUDA_CHECK(m.alloc(&m.bias_part, static_cast<size_t>(num_sms()) * kBiasCols));
+  LBBSP_CUDA_CHECK(m.alloc(&m.bias_cnt, static_cast<size_t>(m.n_local)));
   LBBSP_CUDA_CHECK(cudaFuncSetAttribute(observe_train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         200 * 1024));
   D.N_data = m.N_data;
@@ -1264,7 +1451,8 @@ extern "C" int lbbsp_mlp_run(lbbsp_mlp* m, int iterations) {
     cudaError_t e2 = cudaStreamEndCapture(m->stream, &m->graph);
     if (rc) return rc;
     LBBSP_CUDA_CHECK(e2);
-    LBBSP_CUDA_CHECK(cudaGraphInstantiate(&m->exec, m->graph, 0));
+    // honour the side (observe / NARX) stream's higher priority inside the graph
+    LBBSP_CUDA_CHECK(cudaGraphInstantiate(&m->exec, m->graph, cudaGraphInstantiateFlagUseNodePriority));
   }
   for (int i = 0; i < iterations; ++i) LBBSP_CUDA_CHECK(cudaGraphLaunch(m->exec, m->stream));
   return LBBSP_OK;

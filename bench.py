@@ -470,6 +470,10 @@ def main():
             dist.broadcast_object_list(uid, src=0)
             with stdout_to_stderr():
                 eng.init_comm(uid[0])
+            if not os.environ.get("LBBSP_NO_PEERS"):  # NVLink peer exchange (speeds, gradients)
+                hs = [None] * world
+                dist.all_gather_object(hs, eng.peer_handle())
+                eng.init_peers(hs)
         return eng
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2 (126 MB)

@@ -143,6 +143,7 @@ struct PlanDev {
   const double* share;  // [n_total]
   PredDev pred;
   long long* k;
+  long long* round_k;  // k snapshot taken by the plan (stable for the whole round)
   int* rows;
   int max_rows;
   int* sizes_all;      // [n_total]
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
   stamp(D, 0);
   const long long k = *D.k;
   const int len = min(*D.pred.len, D.pred.max_hist);
+  if (tid == 0) *D.round_k = k;
   if (k >= D.max_rows && tid == 0)
     set_status(D.status, LBBSP_RUNTIME, LBBSP_E_MLP_CAPACITY, k, D.max_rows);
   const long long ti = k < D.trace_len - 1 ? k : D.trace_len - 1;
@@ -789,6 +791,129 @@ __global__ void observe_kernel(PlanDev D, int fused_speed_phases) {
   stamp(D, 4);
 }
 
+// ---------------------------------------------------------------------------
+// NVLink peer-memory exchange for several workers per GPU on several GPUs
+// (C2 at N > 1): the speed all-gather and the gradient all-reduce as our own
+// kernels over CUDA-IPC-mapped peer buffers instead of NCCL calls.
+//   push:  every rank stores its payload into slot[rank] of every peer's
+//          buffer (NVLink stores), fences at system scope, then bumps the
+//          per-writer counter in each peer's buffer (system-scope atomics);
+//   pull:  a rank waits until every writer's counter reached this round's
+//          target, then reads the slots from its own memory -- summing the
+//          gradient slots in rank order, so the all-reduce is deterministic.
+// Counters only grow (target = (round + 1) * writer CTAs), so nothing resets.
+// ---------------------------------------------------------------------------
+constexpr int kMaxPeers = 8;
+struct PeerDev {
+  int world, rank;
+  unsigned long long* cnt_local;              // [2][kMaxPeers]: speeds, gradients
+  unsigned long long* cnt_peer[kMaxPeers];
+  double* spd_local;                          // [world * n_local]
+  double* spd_peer[kMaxPeers];
+  float* grd_local;                           // [world][P]
+  float* grd_peer[kMaxPeers];
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// spin until every writer's counter reached `want`; returns false on timeout
+__device__ bool wait_counters(const PeerDev& X, int which, unsigned long long want,
+                              lbbsp_dev_status* st) {
+  const unsigned long long t0 = gtimer();
+  for (int r = 0; r < X.world; ++r) {
+    while (ld_acquire_sys(&X.cnt_local[which * kMaxPeers + r]) < want) {
+      if (gtimer() - t0 > 2000000000ull) {  // 2 s: a peer is gone -- fail, do not hang
+        set_status(st, LBBSP_NCCL, 0, r, static_cast<long long>(want));
+        return false;
+      }
+    }
+  }
+  return true;
+}
+
+// measured speeds of the local workers -> every rank's v_obs_all
+__global__ void peer_speed_kernel(PlanDev D, PeerDev X, int n_phases) {
+  const int tid = threadIdx.x;
+  for (int i = tid; i < D.n_local; i += blockDim.x) {
+    double t;
+    const double v = local_speed(D, i, n_phases, &t);
+    D.v_obs_local[i] = v;
+    const int row = *D.rows;
+    if (row < D.max_rows) D.rec_t[static_cast<size_t>(row) * D.n_total + D.rank * D.n_local + i] = t;
+    for (int r = 0; r < X.world; ++r) X.spd_peer[r][X.rank * D.n_local + i] = v;
+  }
+  __threadfence_system();
+  __syncthreads();
+  __shared__ int ok;
+  if (tid == 0) {
+    for (int r = 0; r < X.world; ++r) atomicAdd_system(&X.cnt_peer[r][0 * kMaxPeers + X.rank], 1ull);
+    ok = wait_counters(X, 0, static_cast<unsigned long long>(*D.round_k) + 1, D.status);
+  }
+  __syncthreads();
+  if (!ok) return;
+  for (int i = tid; i < D.n_total; i += blockDim.x) D.v_obs_all[i] = __ldcg(&X.spd_local[i]);
+}
+
+// sum of the local worker slabs -> slot[rank] of every rank's gradient buffer
+__global__ void __launch_bounds__(256) peer_grad_push_kernel(const float* __restrict__ partial, int n,
+                                                             long long P, PeerDev X) {
+  const long long nv = P / 4;
+  for (long long v = blockIdx.x * 256ll + threadIdx.x; v < nv; v += 256ll * gridDim.x) {
+    float4 a = reinterpret_cast<const float4*>(partial)[v];
+    for (int g = 1; g < n; ++g) {
+      const float4 b = reinterpret_cast<const float4*>(partial + static_cast<long long>(g) * P)[v];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    for (int r = 0; r < X.world; ++r)
+      reinterpret_cast<float4*>(X.grd_peer[r] + static_cast<long long>(X.rank) * P)[v] = a;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int r = 0; r < X.world; ++r) atomicAdd_system(&X.cnt_peer[r][1 * kMaxPeers + X.rank], 1ull);
+}
+
+// wait for every rank's slot, sum in rank order, SGD apply + bf16 copy
+__global__ void __launch_bounds__(256) peer_grad_apply_kernel(long long P, float* grad, float* params,
+                                                              bf16* pb, float lr, PeerDev X,
+                                                              const long long* round_k,
+                                                              int push_ctas,
+                                                              lbbsp_dev_status* st) {
+  __shared__ int ok;
+  if (threadIdx.x == 0)
+    ok = wait_counters(X, 1, (static_cast<unsigned long long>(*round_k) + 1) * push_ctas, st);
+  __syncthreads();
+  if (!ok) return;
+  const long long nv = P / 4;
+  for (long long v = blockIdx.x * 256ll + threadIdx.x; v < nv; v += 256ll * gridDim.x) {
+    float4 a = __ldcg(reinterpret_cast<const float4*>(X.grd_local) + v);
+    for (int r = 1; r < X.world; ++r) {
+      const float4 b = __ldcg(reinterpret_cast<const float4*>(X.grd_local + static_cast<long long>(r) * P) + v);
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    reinterpret_cast<float4*>(grad)[v] = a;
+    float4 w = reinterpret_cast<float4*>(params)[v];
+    w.x -= lr * a.x;
+    w.y -= lr * a.y;
+    w.z -= lr * a.z;
+    w.w -= lr * a.w;
+    reinterpret_cast<float4*>(params)[v] = w;
+    __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(pb) + 2 * v;
+    o[0] = __floats2bfloat162_rn(w.x, w.y);
+    o[1] = __floats2bfloat162_rn(w.z, w.w);
+  }
+}
+
 }  // namespace mlp
 }  // namespace lbbsp
 
@@ -820,6 +945,13 @@ struct lbbsp_mlp {
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   ncclComm_t comm = nullptr;
+  // NVLink peer exchange (lbbsp_mlp_init_peers): replaces the NCCL calls of
+  // the several-workers-per-GPU path when set
+  bool peers = false;
+  PeerDev px{};
+  void* peer_buf = nullptr;               // local IPC-exported buffer
+  void* peer_map[kMaxPeers] = {};          // opened peer buffers
+  size_t peer_off_spd = 0, peer_off_grd = 0;
   int launches = 0;
   // device buffers
   bf16 *data_x = nullptr, *X = nullptr, *pb = nullptr, *logits = nullptr, *dlogits = nullptr;
@@ -851,6 +983,9 @@ struct lbbsp_mlp {
   int* dz_widths = nullptr;
 
   ~lbbsp_mlp() {
+    for (void* p : peer_map)
+      if (p && p != peer_buf) cudaIpcCloseMemHandle(p);
+    if (peer_buf) cudaFree(peer_buf);
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     if (comm && nccl_api()) nccl_api()->CommDestroy(comm);
@@ -1007,7 +1142,10 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   n_phases = ph;
   // measured speeds; on several GPUs all-gathered (after the gradient buckets)
   const float lr = static_cast<float>(cfg.learning_rate);
-  if (cfg.world > 1) {
+  if (cfg.world > 1 && peers && !bucketed) {
+    peer_speed_kernel<<<1, 256, 0, s>>>(D, px, n_phases);  // speeds, all-gathered over NVLink
+    ++nl;
+  } else if (cfg.world > 1) {
     speed_kernel<<<1, 32 * ((n_local + 31) / 32), 0, s>>>(D, n_phases);
     ++nl;
     if (bucketed) {
@@ -1055,6 +1193,11 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   }
   // ---- aggregate + apply (the bucketed path applied per layer above) ----
   if (bucketed) {
+  } else if (cfg.world > 1 && peers) {
+    // one-shot all-reduce over NVLink peer memory, summed in rank order
+    peer_grad_push_kernel<<<sms, 256, 0, s>>>(partial, n_local, P, px);
+    peer_grad_apply_kernel<<<sms, 256, 0, s>>>(P, grad, params, pb, lr, px, D.round_k, sms, D.status);
+    nl += 2;
   } else if (cfg.world > 1) {
     reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 0, D.stamps);
     ++nl;
@@ -1287,6 +1430,7 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     D.v_obs_all = D.v_obs_local;
   LBBSP_CUDA_CHECK(m.alloc(&D.loss_acc, 1));
   LBBSP_CUDA_CHECK(m.alloc(&D.stamps, 16));
+  LBBSP_CUDA_CHECK(m.alloc(&D.round_k, 1));
   LBBSP_CUDA_CHECK(m.alloc(&m.arrive, 1));
   LBBSP_CUDA_CHECK(m.alloc(&m.bias_part, static_cast<size_t>(num_sms()) * kBiasCols));
   LBBSP_CUDA_CHECK(m.alloc(&m.bias_cnt, static_cast<size_t>(m.n_local)));
@@ -1437,6 +1581,54 @@ extern "C" int lbbsp_mlp_init_comm(lbbsp_mlp* m, const unsigned char h_id[128]) 
   std::memcpy(id.internal, h_id, 128);
   ncclResult_t r = api->CommInitRank(&m->comm, m->cfg.world, id, m->cfg.rank);
   if (r != ncclSuccess) return set_error(LBBSP_NCCL, "ncclCommInitRank: %s", api->GetErrorString(r));
+  return LBBSP_OK;
+}
+
+// NVLink peer exchange setup: every rank exports one device buffer (CUDA IPC
+// handle, 64 bytes); after the handles are all-gathered on the host, every
+// rank maps its peers' buffers. Must precede the first lbbsp_mlp_run.
+extern "C" int lbbsp_mlp_peer_handle(lbbsp_mlp* m, unsigned char h_handle[64]) {
+  if (m->cfg.world > kMaxPeers)
+    return set_error(LBBSP_INVALID_ARGUMENT, "mlp: peer exchange supports at most %d GPUs", kMaxPeers);
+  if (!m->peer_buf) {
+    const int W = m->cfg.world;
+    m->peer_off_spd = 256;
+    m->peer_off_grd = (m->peer_off_spd + sizeof(double) * W * m->n_local + 255) / 256 * 256;
+    const size_t bytes = m->peer_off_grd + sizeof(float) * W * static_cast<size_t>(m->P);
+    LBBSP_CUDA_CHECK(cudaMalloc(&m->peer_buf, bytes));
+    LBBSP_CUDA_CHECK(cudaMemset(m->peer_buf, 0, bytes));
+  }
+  cudaIpcMemHandle_t h;
+  LBBSP_CUDA_CHECK(cudaIpcGetMemHandle(&h, m->peer_buf));
+  std::memcpy(h_handle, &h, 64);
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_mlp_init_peers(lbbsp_mlp* m, const unsigned char* h_handles) {
+  const int W = m->cfg.world, R = m->cfg.rank;
+  if (!m->peer_buf) return set_error(LBBSP_LOGIC, "mlp: lbbsp_mlp_peer_handle first");
+  if (m->exec) return set_error(LBBSP_LOGIC, "mlp: peers must be set up before the first round");
+  PeerDev& X = m->px;
+  X.world = W;
+  X.rank = R;
+  for (int r = 0; r < W; ++r) {
+    if (r == R) {
+      m->peer_map[r] = m->peer_buf;
+    } else {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, h_handles + 64 * r, 64);
+      LBBSP_CUDA_CHECK(cudaIpcOpenMemHandle(&m->peer_map[r], h, cudaIpcMemLazyEnablePeerAccess));
+    }
+    char* b = static_cast<char*>(m->peer_map[r]);
+    X.cnt_peer[r] = reinterpret_cast<unsigned long long*>(b);
+    X.spd_peer[r] = reinterpret_cast<double*>(b + m->peer_off_spd);
+    X.grd_peer[r] = reinterpret_cast<float*>(b + m->peer_off_grd);
+  }
+  char* lb = static_cast<char*>(m->peer_buf);
+  X.cnt_local = reinterpret_cast<unsigned long long*>(lb);
+  X.spd_local = reinterpret_cast<double*>(lb + m->peer_off_spd);
+  X.grd_local = reinterpret_cast<float*>(lb + m->peer_off_grd);
+  m->peers = true;
   return LBBSP_OK;
 }
 

@@ -189,6 +189,16 @@ class MlpEngine:
     def init_comm(self, uid: bytes):
         check(_L().lbbsp_mlp_init_comm(self._h, C.c_char_p(uid)))
 
+    def peer_handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        check(_L().lbbsp_mlp_peer_handle(self._h, buf))
+        return buf.raw
+
+    def init_peers(self, handles):
+        """handles: the per-rank 64-byte IPC handles in rank order."""
+        blob = b"".join(handles)
+        check(_L().lbbsp_mlp_init_peers(self._h, C.c_char_p(blob)))
+
     # -- run --------------------------------------------------------------------
     def run(self, iterations):
         check(_L().lbbsp_mlp_run(self._h, int(iterations)))

@@ -17,6 +17,10 @@ for pred in ("narx", "ema"):
     uid = [MlpEngine.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     eng.init_comm(uid[0])
+    if not os.environ.get("LBBSP_NO_PEERS"):
+        hs = [None] * world
+        dist.all_gather_object(hs, eng.peer_handle())
+        eng.init_peers(hs)
     st = torch.cuda.ExternalStream(eng.stream)
     eng.run(100)
     for rep in range(3):

@@ -1431,6 +1431,13 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(m.alloc(&D.loss_acc, 1));
   LBBSP_CUDA_CHECK(m.alloc(&D.stamps, 16));
   LBBSP_CUDA_CHECK(m.alloc(&D.round_k, 1));
+  // end-to-end plumbing (lbbsp_mlp_load_data_async / read_result_async)
+  LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.copy_stream, cudaStreamNonBlocking));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_staged, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_refreshed, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(m.alloc(&m.stage_x, static_cast<size_t>(m.N_data) * c.dims[0]));
+  LBBSP_CUDA_CHECK(m.alloc(&m.stage_y, static_cast<size_t>(m.N_data)));
+  LBBSP_CUDA_CHECK(m.alloc(&m.result, static_cast<size_t>(m.n_total) + 2));
   LBBSP_CUDA_CHECK(m.alloc(&m.arrive, 1));
   LBBSP_CUDA_CHECK(m.alloc(&m.bias_part, static_cast<size_t>(num_sms()) * kBiasCols));
   LBBSP_CUDA_CHECK(m.alloc(&m.bias_cnt, static_cast<size_t>(m.n_local)));
@@ -1724,14 +1731,8 @@ extern "C" int lbbsp_mlp_launches_per_iteration(lbbsp_mlp* m, int* launches) {
 // previous round, which read it).
 extern "C" int lbbsp_mlp_load_data_async(lbbsp_mlp* m, const void* h_x_bf16, const int* h_labels) {
   const size_t bx = sizeof(bf16) * m->N_data * m->dims[0], by = sizeof(int) * m->N_data;
-  if (!m->copy_stream) {
-    LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
-    LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m->ev_staged, cudaEventDisableTiming));
-    LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m->ev_refreshed, cudaEventDisableTiming));
-    LBBSP_CUDA_CHECK(m->alloc(&m->stage_x, bx / sizeof(bf16)));
-    LBBSP_CUDA_CHECK(m->alloc(&m->stage_y, by / sizeof(int)));
-    LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_refreshed, m->stream));
-  }
+  // staging buffers, copy stream and events are created with the engine (an
+  // allocation here would synchronise the device inside the caller's loop)
   // staging is free once the previous refresh consumed it
   LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->copy_stream, m->ev_refreshed, 0));
   LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_x, h_x_bf16, bx, cudaMemcpyHostToDevice, m->copy_stream));
@@ -1755,9 +1756,6 @@ __global__ void last_row_kernel(const int* rows, const int* rec_sizes, const dou
 }  // namespace
 
 extern "C" int lbbsp_mlp_read_result_async(lbbsp_mlp* m, int* h_sizes, double* h_loss) {
-  if (!m->result) {
-    LBBSP_CUDA_CHECK(m->alloc(&m->result, m->n_total + 2));
-  }
   int* rs = reinterpret_cast<int*>(m->result);
   double* rl = m->result + (m->n_total + 1) / 2 + 1;
   last_row_kernel<<<1, 256, 0, m->stream>>>(m->D.rows, m->D.rec_sizes, m->D.loss_acc, m->N_data,

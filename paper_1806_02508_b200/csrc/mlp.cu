@@ -1725,6 +1725,15 @@ extern "C" int lbbsp_mlp_launches_per_iteration(lbbsp_mlp* m, int* launches) {
   return LBBSP_OK;
 }
 
+namespace {
+__global__ void refresh_kernel(const uint4* __restrict__ sx, uint4* __restrict__ dx, size_t nx,
+                               const int* __restrict__ sy, int* __restrict__ dy, int ny) {
+  for (size_t i = blockIdx.x * 256ull + threadIdx.x; i < nx; i += 256ull * gridDim.x) dx[i] = sx[i];
+  for (int i = blockIdx.x * 256 + threadIdx.x; i < ny; i += 256 * gridDim.x) dy[i] = sy[i];
+}
+
+}  // namespace
+
 // The host->device copy runs on a copy stream into a staging buffer, so it
 // overlaps the round still executing; the next round then starts with a
 // device-to-device refresh of the resident dataset (stream-ordered after the
@@ -1739,8 +1748,10 @@ extern "C" int lbbsp_mlp_load_data_async(lbbsp_mlp* m, const void* h_x_bf16, con
   LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_y, h_labels, by, cudaMemcpyHostToDevice, m->copy_stream));
   LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_staged, m->copy_stream));
   LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->stream, m->ev_staged, 0));
-  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_x, m->stage_x, bx, cudaMemcpyDeviceToDevice, m->stream));
-  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_y, m->stage_y, by, cudaMemcpyDeviceToDevice, m->stream));
+  refresh_kernel<<<num_sms(), 256, 0, m->stream>>>(reinterpret_cast<const uint4*>(m->stage_x),
+                                                  reinterpret_cast<uint4*>(m->data_x), bx / 16,
+                                                  m->stage_y, m->data_y, m->N_data);
+  LBBSP_CUDA_CHECK(cudaGetLastError());
   LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_refreshed, m->stream));
   return LBBSP_OK;
 }
@@ -1755,7 +1766,22 @@ __global__ void last_row_kernel(const int* rows, const int* rec_sizes, const dou
 }
 }  // namespace
 
+// Page-locked host buffers are written by the kernel itself (zero-copy over
+// the unified address space); other host memory goes through a D2H copy.
 extern "C" int lbbsp_mlp_read_result_async(lbbsp_mlp* m, int* h_sizes, double* h_loss) {
+  cudaPointerAttributes a{}, b{};
+  const bool mapped = cudaPointerGetAttributes(&a, h_sizes) == cudaSuccess &&
+                      cudaPointerGetAttributes(&b, h_loss) == cudaSuccess &&
+                      a.type == cudaMemoryTypeHost && b.type == cudaMemoryTypeHost &&
+                      a.devicePointer && b.devicePointer;
+  cudaGetLastError();
+  if (mapped) {
+    last_row_kernel<<<1, 256, 0, m->stream>>>(m->D.rows, m->D.rec_sizes, m->D.loss_acc, m->N_data,
+                                              m->n_total, static_cast<int*>(a.devicePointer),
+                                              static_cast<double*>(b.devicePointer));
+    LBBSP_CUDA_CHECK(cudaGetLastError());
+    return LBBSP_OK;
+  }
   int* rs = reinterpret_cast<int*>(m->result);
   double* rl = m->result + (m->n_total + 1) / 2 + 1;
   last_row_kernel<<<1, 256, 0, m->stream>>>(m->D.rows, m->D.rec_sizes, m->D.loss_acc, m->N_data,

@@ -95,3 +95,35 @@ def test_lbbsp_balances_stragglers_and_loss_falls():
     last = rec["sizes"][-1]
     assert last[0] > last[6]            # the fast worker gets more samples
     assert rec["loss"][-1] < rec["loss"][0]
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_end_to_end_plumbing(pinned):
+    """load_data_async (staged H2D + on-device refresh) and read_result_async
+    (zero-copy into page-locked buffers, a D2H copy otherwise) deliver the
+    newest round's sizes and loss; a replaced dataset is what the round uses."""
+    import torch
+    from paper_1806_02508_b200.mlp import constant_trace
+    n, B, iters = 8, 4096, 12
+    eng = _engine(dims=[784, 256, 10], global_batch=B, n_workers_local=n, predictor="ema",
+                  max_iterations=iters, trace=constant_trace(n, iters), learning_rate=0.05)
+    x, y = eng.dataset()
+    x2 = np.ascontiguousarray(x[::-1])            # a different dataset: rows reversed
+    y2 = np.ascontiguousarray(y[::-1].astype(np.int32))
+    xb = torch.from_numpy(x2).to(torch.bfloat16)
+    yb = torch.from_numpy(y2)
+    sz = torch.zeros(n, dtype=torch.int32)
+    ls = torch.zeros(1, dtype=torch.float64)
+    if pinned:
+        xb, yb, sz, ls = xb.pin_memory(), yb.pin_memory(), sz.pin_memory(), ls.pin_memory()
+    eng.run(3)
+    for _ in range(4):
+        eng.load_data_async(xb.data_ptr(), yb.data_ptr())
+        eng.run(1)
+        eng.read_result_async(sz.data_ptr(), ls.data_ptr())
+    torch.cuda.synchronize()
+    rec = eng.records()
+    assert sz.tolist() == rec["sizes"][rec["rows"] - 1].tolist()
+    xd, yd = eng.dataset()
+    assert np.array_equal(yd, y2)
+    assert ls.item() > 0 and np.isfinite(ls.item())

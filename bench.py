@@ -61,6 +61,16 @@ class stdout_to_stderr:
         os.close(self.saved)
 
 
+def comm_sm_budget(world):
+    """SMs the worker GEMMs may use when one worker per GPU all-reduces its
+    gradient buckets during the backward pass: the collectives need SMs of
+    their own to overlap the 1-CTA-per-SM GEMMs (0 = all SMs)."""
+    if world <= 1:
+        return 0
+    k = int(os.environ.get("LBBSP_COMM_SMS", "0"))
+    return 148 - k if k > 0 else 0
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -270,7 +280,8 @@ def main_c3(args):
     def make(scheme, av):
         eng = MlpEngine(dims=dims, global_batch=B, n_workers_local=1, world=world, rank=rank,
                         scheme=scheme, predictor="ema", learning_rate=0.01, seed=1,
-                        max_iterations=iters, trace=constant_trace(world, iters, av))
+                        max_iterations=iters, trace=constant_trace(world, iters, av),
+                        sm_budget=comm_sm_budget(world))
         if world > 1:
             uid = [MlpEngine.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
@@ -367,7 +378,14 @@ def main_c5(args):
     rounds = args.steps
     setup = 2  # untimed rounds per engine: graph instantiation + NCCL connection setup
     iters = setup + rounds + 8
-    trace = benchmark_trace(world, iters, seed=TRACE_SEED)
+    # per-GPU make_benchmark_series (fast/slow regimes of 50 rounds), GPU i's
+    # series shifted by i * 100 / N rounds so the GPUs' slow regimes are
+    # staggered in time (the reference's benchmark dynamics switch every
+    # worker at the same rounds, which leaves no relative straggler to adapt to)
+    period = 100
+    raw = benchmark_trace(world, iters + period, seed=TRACE_SEED)
+    trace = tuple(np.stack([a[i, (i * period) // world:(i * period) // world + iters] for i in range(world)])
+                  for a in raw)
     mean_avail = np.minimum(1.0, trace[0] * trace[2]).mean(axis=1)
     static = lbbsp.cpu_allocate(mean_avail.tolist(), B).sizes
 
@@ -375,7 +393,7 @@ def main_c5(args):
         eng = MlpEngine(dims=dims, global_batch=B, n_workers_local=1, world=world, rank=rank,
                         scheme=scheme, predictor=predictor, warmup_iterations=WARMUP_NARX,
                         learning_rate=0.01, seed=1, max_iterations=iters, trace=trace,
-                        static_sizes=static_sizes)
+                        static_sizes=static_sizes, sm_budget=comm_sm_budget(world))
         if world > 1:
             uid = [MlpEngine.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
@@ -417,7 +435,8 @@ def main_c5(args):
                 "data": "synthetic",
                 "config": {"workload": "C5: MLP 4x(4096x4096) bf16, one worker per GPU, 2048 "
                                        "samples per GPU, per-GPU time-varying SM availability "
-                                       "(make_benchmark_series seed 3), all rounds after 2 "
+                                       "(make_benchmark_series seed 3, GPU i shifted by "
+                                       "100*i/N rounds), all rounds after 2 "
                                        "setup rounds timed, including the NARX warm-up",
                            "global_batch": B,
                            "parallelism": f"dp{world}", "static_sizes": static},

@@ -111,6 +111,7 @@ int gemm_launch(const GemmPlan& p, cudaStream_t s) {
     LBBSP_GEMM2_CASE(256, false, true, tc::kEpiDReluBf16)
     LBBSP_GEMM2_CASE(256, false, true, tc::kEpiF32)
     LBBSP_GEMM2_CASE(256, true, true, tc::kEpiF32)
+    LBBSP_GEMM2_CASE(256, true, true, tc::kEpiBf16)
     return set_error(LBBSP_INVALID_ARGUMENT, "gemm: unsupported pair variant bn=%d a_mn=%d b_mn=%d epi=%d",
                      bn, (int)a_mn, (int)b_mn, epi);
   }
@@ -133,6 +134,8 @@ int gemm_launch(const GemmPlan& p, cudaStream_t s) {
   LBBSP_GEMM_CASE(64, false, true, tc::kEpiF32)
   // dW = dY^T X (per-worker K split)
   LBBSP_GEMM_CASE(256, true, true, tc::kEpiF32)
+  LBBSP_GEMM_CASE(256, true, true, tc::kEpiBf16)
+  LBBSP_GEMM_CASE(128, true, true, tc::kEpiBf16)
   LBBSP_GEMM_CASE(128, true, true, tc::kEpiF32)
   LBBSP_GEMM_CASE(64, true, true, tc::kEpiF32)
   LBBSP_GEMM_CASE(256, true, false, tc::kEpiF32)

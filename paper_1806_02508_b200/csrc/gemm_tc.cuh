@@ -35,7 +35,8 @@ enum Epilogue {
   kEpiBiasReluBf16 = 1, // C_bf16 = relu(acc + bias)
   kEpiBiasBf16 = 2,     // C_bf16 = acc + bias
   kEpiDReluBf16 = 3,    // C_bf16 = acc * (aux > 0)   (dX through ReLU)
-  kEpiBiasReluBoth = 4  // C_bf16 = relu(acc + bias) and C_f32 = same (testing)
+  kEpiBiasReluBoth = 4, // C_bf16 = relu(acc + bias) and C_f32 = same (testing)
+  kEpiBf16 = 5          // C_bf16 = acc (bf16 gradient buckets for the all-reduce)
 };
 
 struct GemmArgs {

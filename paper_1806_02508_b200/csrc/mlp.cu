@@ -515,7 +515,7 @@ constexpr int kBiasMaxRowBlocks = 32;
 __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __restrict__ dZ, int N,
                                                         float* slab, long long slab_stride,
                                                         long long off_b, float* scratch,
-                                                        unsigned* counters,
+                                                        unsigned* counters, bf16* out_b16,
                                                         unsigned long long* timing) {
   int g, cta_in, cta_cnt;
   if (!my_group(G, &g, &cta_in, &cta_cnt)) return;
@@ -590,7 +590,13 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
           v.z += t[q].z;
           v.w += t[q].w;
         }
-      *reinterpret_cast<float4*>(&gs[c]) = v;
+      if (out_b16) {
+        __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(out_b16 + c);
+        o[0] = __floats2bfloat162_rn(v.x, v.y);
+        o[1] = __floats2bfloat162_rn(v.z, v.w);
+      } else {
+        *reinterpret_cast<float4*>(&gs[c]) = v;
+      }
     }
     if (threadIdx.x == 0) counters[g] = 0u;
   }
@@ -624,6 +630,31 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(const float* __restri
     __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(pb) + 2 * v;
     o[0] = __floats2bfloat162_rn(w.x, w.y);
     o[1] = __floats2bfloat162_rn(w.z, w.w);
+  }
+}
+
+// SGD apply from an all-reduced bf16 gradient bucket (+ the bf16 weight copy)
+__global__ void __launch_bounds__(256) apply_bf16_kernel(const bf16* __restrict__ g, long long n,
+                                                         float* params, bf16* pb, float lr) {
+  const long long nv = n / 8;
+  for (long long v = blockIdx.x * 256ll + threadIdx.x; v < nv; v += 256ll * gridDim.x) {
+    const uint4 q = reinterpret_cast<const uint4*>(g)[v];
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+    float4* p4 = reinterpret_cast<float4*>(params) + 2 * v;
+    float4 w0 = p4[0], w1 = p4[1];
+    const float2 a = __bfloat1622float2(g2[0]), b = __bfloat1622float2(g2[1]);
+    const float2 c = __bfloat1622float2(g2[2]), d = __bfloat1622float2(g2[3]);
+    w0.x -= lr * a.x; w0.y -= lr * a.y; w0.z -= lr * b.x; w0.w -= lr * b.y;
+    w1.x -= lr * c.x; w1.y -= lr * c.y; w1.z -= lr * d.x; w1.w -= lr * d.y;
+    p4[0] = w0;
+    p4[1] = w1;
+    uint4 o;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+    o2[0] = __floats2bfloat162_rn(w0.x, w0.y);
+    o2[1] = __floats2bfloat162_rn(w0.z, w0.w);
+    o2[2] = __floats2bfloat162_rn(w1.x, w1.y);
+    o2[3] = __floats2bfloat162_rn(w1.z, w1.w);
+    reinterpret_cast<uint4*>(pb)[v] = o;
   }
 }
 
@@ -967,6 +998,7 @@ struct lbbsp_mlp {
   unsigned* head_cnt_d = nullptr;  // [1] dataset-loss head counter
   unsigned* arrive = nullptr;      // observe_train_kernel arrival count (self-resetting)
   float* bias_part = nullptr;      // [sms][kBiasCols] bias-gradient row-block partials
+  bf16* gradb = nullptr;           // [P] bf16 gradient buckets (bucketed all-reduce path)
   unsigned* bias_cnt = nullptr;    // [n_local] bias_grad_kernel counters (self-resetting)
   bool use_pdl = true;             // programmatic dependent launch on the worker-phase chain
   long long* reg_len = nullptr;
@@ -1113,7 +1145,8 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   for (int l = Lg - 1; l >= 0; --l) {
     if (!(small_head && l == L - 2)) {  // the small head already summed this bias gradient
       bias_grad_kernel<<<sms, 256, 0, s>>>(G, dZ[l], dims[l + 1], partial, P, off_b[l], bias_part,
-                                           bias_cnt, phase_slot(ph++));
+                                           bias_cnt, gradb ? gradb + off_b[l] : nullptr,
+                                           phase_slot(ph++));
       ++nl;
     }
     int rc = launch_grouped(this, dw[l], tc::kKSplit, phase_slot(ph++), s);
@@ -1123,14 +1156,23 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
       const long long seg0 = off_w[l], seg1 = l + 1 < L ? off_w[l + 1] : P;
       LBBSP_CUDA_CHECK(cudaEventRecord(ev_layer[l], s));
       LBBSP_CUDA_CHECK(cudaStreamWaitEvent(comm_stream, ev_layer[l], 0));
-      if (nccl_api()->AllReduce(partial + seg0, partial + seg0, static_cast<size_t>(seg1 - seg0),
-                                ncclFloat, ncclSum, comm, comm_stream) != ncclSuccess)
-        return set_error(LBBSP_NCCL, "ncclAllReduce (bucket %d) failed", l);
       // apply this layer's update as soon as its bucket is reduced, beside
       // the rest of the backward pass
-      reduce_apply_kernel<<<sms * 2, 256, 0, comm_stream>>>(
-          partial + seg0, 1, seg1 - seg0, grad + seg0, params + seg0, pb + seg0,
-          static_cast<float>(cfg.learning_rate), 1, nullptr);
+      if (gradb) {
+        if (nccl_api()->AllReduce(gradb + seg0, gradb + seg0, static_cast<size_t>(seg1 - seg0),
+                                  ncclBfloat16, ncclSum, comm, comm_stream) != ncclSuccess)
+          return set_error(LBBSP_NCCL, "ncclAllReduce (bucket %d) failed", l);
+        apply_bf16_kernel<<<sms * 2, 256, 0, comm_stream>>>(gradb + seg0, seg1 - seg0, params + seg0,
+                                                            pb + seg0,
+                                                            static_cast<float>(cfg.learning_rate));
+      } else {
+        if (nccl_api()->AllReduce(partial + seg0, partial + seg0, static_cast<size_t>(seg1 - seg0),
+                                  ncclFloat, ncclSum, comm, comm_stream) != ncclSuccess)
+          return set_error(LBBSP_NCCL, "ncclAllReduce (bucket %d) failed", l);
+        reduce_apply_kernel<<<sms * 2, 256, 0, comm_stream>>>(
+            partial + seg0, 1, seg1 - seg0, grad + seg0, params + seg0, pb + seg0,
+            static_cast<float>(cfg.learning_rate), 1, nullptr);
+      }
       ++nl;
     }
     if (l > 0) {
@@ -1321,6 +1363,10 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     LBBSP_CUDA_CHECK(m.alloc(&m.partial, static_cast<size_t>(P) * m.n_local));
   else
     m.partial = m.grad;  // one worker: the dW GEMM writes the gradient directly
+  // one worker per GPU on several GPUs: the gradient buckets travel in bf16
+  // (half the all-reduce bytes; SURVEY 8(d) sizes the C3 all-reduce in bf16)
+  if (c.world > 1 && m.n_local == 1 && !small_head && !getenv("LBBSP_FP32_BUCKETS"))
+    LBBSP_CUDA_CHECK(m.alloc(&m.gradb, static_cast<size_t>(P)));
   if (small_head) {
     const int nsm = num_sms();
     LBBSP_CUDA_CHECK(m.alloc(&m.head_part, static_cast<size_t>(nsm) * kHeadVals));
@@ -1541,9 +1587,10 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     const int bn_w = env_bn("LBBSP_BN_DW", pick_bn(static_cast<double>(dout), din));
     const int bn_x = env_bn("LBBSP_BN_DX", pick_bn(rows_per_worker, din));
     rc = gemm_plan(&m.dw[l], m.dZ[l], Ain, dout, din, m.B_cap, true, true, pr ? 256 : bn_w,
-                   tc::kEpiF32, pr);
+                   m.gradb ? tc::kEpiBf16 : tc::kEpiF32, pr);
     if (rc) return rc;
     m.dw[l].args.c_f32 = m.partial + m.off_w[l];
+    if (m.gradb) m.dw[l].args.c_bf16 = m.gradb + m.off_w[l];
     m.dw[l].args.ldc = din;
     m.dw[l].args.group_stride = P;
     if (l > 0) {

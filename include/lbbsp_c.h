@@ -148,6 +148,11 @@ int lbbsp_narx_predict(const lbbsp_narx_model* h_model, const double h_speeds[2]
                        const double h_cpu[3], const double h_mem[3], double floor,
                        double* h_out);
 
+/* Verification hook: the device restatement of glibc tanh that every NARX
+ * forward uses (exactmath.cuh; std::tanh at predictor.cpp:60,109,117),
+ * evaluated elementwise over n host inputs. */
+int lbbsp_glibc_tanh(const double* h_x, double* h_y, long long n);
+
 /* narx_train_online (predictor.cpp:155-196) over one host history.
  * h_loss_log (optional, may be NULL) receives one entry per accepted epoch
  * (NarxModel::training_loss), capacity max_epochs. Bit-exact fp64 kernel. */

@@ -27,6 +27,7 @@ SIGNATURES = {
     "lbbsp_narx_init": [C.c_uint64, C.POINTER(abi.NarxModel)],
     "lbbsp_ema": [_dp, C.c_int, C.c_double, _dp],
     "lbbsp_narx_predict": [C.POINTER(abi.NarxModel), _dp, _dp, _dp, C.c_double, _dp],
+    "lbbsp_glibc_tanh": [_dp, _dp, C.c_longlong],
     "lbbsp_narx_train_online": [C.POINTER(abi.NarxModel), _dp, _dp, _dp, C.c_int,
                                 C.POINTER(abi.NarxTrainConfig), C.POINTER(abi.NarxReport), _dp],
     "lbbsp_predictor_create": [C.POINTER(abi.PredictorConfig), C.c_int, C.c_int,

@@ -239,6 +239,26 @@ extern "C" int lbbsp_narx_predict(const lbbsp_narx_model* h_model, const double 
   return LBBSP_OK;
 }
 
+namespace {
+__global__ void glibc_tanh_kernel(const double* x, double* y, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    y[i] = glibc_tanh(x[i]);
+}
+}  // namespace
+
+extern "C" int lbbsp_glibc_tanh(const double* h_x, double* h_y, long long n) {
+  LBBSP_REQUIRE_DEVICE();
+  if (n < 0) return set_error(LBBSP_INVALID_ARGUMENT, "glibc_tanh: negative length");
+  if (n == 0) return LBBSP_OK;
+  DBuf<double> x(n), y(n);
+  LBBSP_CUDA_CHECK(cudaMemcpy(x.p, h_x, sizeof(double) * n, cudaMemcpyHostToDevice));
+  glibc_tanh_kernel<<<148 * 4, 256>>>(x.p, y.p, n);
+  LBBSP_CUDA_CHECK(cudaGetLastError());
+  LBBSP_CUDA_CHECK(cudaMemcpy(h_y, y.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return LBBSP_OK;
+}
+
 extern "C" int lbbsp_narx_train_online(lbbsp_narx_model* h_model, const double* h_speed,
                                        const double* h_cpu, const double* h_mem, int len,
                                        const lbbsp_narx_train_cfg* cfg,
@@ -296,7 +316,7 @@ static int make_pred(lbbsp_predictor* P, const lbbsp_predictor_cfg* cfg, int n, 
   LBBSP_CUDA_CHECK(P->alloc(&d.models, n));
   LBBSP_CUDA_CHECK(P->alloc(&d.reports, n));
   const bool need_scratch = narx_train_scratch_bytes(max_hist) > train_smem_bytes(max_hist);
-  LBBSP_CUDA_CHECK(P->alloc(&d.scratch, need_scratch ? static_cast<size_t>(n) * 13 * max_hist : 1));
+  LBBSP_CUDA_CHECK(P->alloc(&d.scratch, need_scratch ? static_cast<size_t>(n) * (narx_train_scratch_bytes(max_hist) / sizeof(double)) : 1));
   LBBSP_CUDA_CHECK(P->alloc(&d.len, 1));
   LBBSP_CUDA_CHECK(P->alloc(&d.cursor, 1));
   std::vector<lbbsp_narx_model> models(n);

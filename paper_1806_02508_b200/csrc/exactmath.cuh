@@ -31,6 +31,13 @@ __device__ __forceinline__ double with_hi(double x, uint32_t hi) {
 
 // glibc 2.39 __expm1_fma (fdlibm s_expm1.c compiled with -mfma); constants
 // read from libm's .rodata (see oracle/lbbsp_oracle.c orc_expm1_glibc_fma).
+//
+// Written without data-dependent branches so that a warp whose lanes fall in
+// different argument ranges does not serialise them: the argument reduction is
+// one formula for every k (for k = 0 it gives hi = x, lo = 0, c = 0 and for
+// k = +-1 it gives glibc's x -+ ln2_hi / +-ln2_lo, each bit-identical to the
+// branchy source), and every final combination is formed and the one glibc
+// returns is selected. Only the non-finite / overflow inputs branch.
 __device__ __forceinline__ double glibc_expm1(double x) {
   const double o_threshold = 0x1.62e42fefa39efp+9, ln2_hi = 0x1.62e42fee00000p-1,
                ln2_lo = 0x1.a39ef35793c76p-33, invln2 = 0x1.71547652b82fep+0;
@@ -40,98 +47,79 @@ __device__ __forceinline__ double glibc_expm1(double x) {
   uint32_t hx = hi_word(x);
   const uint32_t xsb = hx & 0x80000000u;
   hx &= 0x7fffffffu;
-  double hi, lo, c = 0.0, t;
-  int k;
-  if (hx >= 0x4043687Au) {
-    if (hx >= 0x40862E42u) {
-      if (hx >= 0x7ff00000u) {
-        if (((hx & 0xfffffu) | lo_word(x)) != 0) return dadd(x, x);
-        return xsb == 0 ? x : -1.0;
-      }
-      if (x > o_threshold) return __int_as_float(0x7f800000);  // +inf
+  if (hx >= 0x40862E42u) {  // |x| >= 709.78: inf, nan, overflow, -1
+    if (hx >= 0x7ff00000u) {
+      if (((hx & 0xfffffu) | lo_word(x)) != 0) return dadd(x, x);
+      return xsb == 0 ? x : -1.0;
     }
-    if (xsb != 0) return -1.0;  // tiny - one rounds to -1
+    if (x > o_threshold) return __int_as_float(0x7f800000);  // +inf
   }
-  if (hx > 0x3fd62e42u) {
-    if (hx < 0x3FF0A2B2u) {
-      if (xsb == 0) {
-        hi = dsub(x, ln2_hi);
-        lo = ln2_lo;
-        k = 1;
-      } else {
-        hi = dadd(x, ln2_hi);
-        lo = -ln2_lo;
-        k = -1;
-      }
-    } else {
-      k = static_cast<int>(dadd(dmul(invln2, x), xsb == 0 ? 0.5 : -0.5));
-      t = static_cast<double>(k);
-      hi = dfma(-t, ln2_hi, x);
-      lo = dmul(t, ln2_lo);
-    }
-    x = dsub(hi, lo);
-    c = dsub(dsub(hi, x), lo);
-  } else if (hx < 0x3c900000u) {
-    return x;  // |x| < 2^-54 (inexact flag only)
-  } else {
-    k = 0;
-  }
-  const double hfx = dmul(x, 0.5);
-  const double hxs = dmul(x, hfx);
+  const bool neg_one = hx >= 0x4043687Au && xsb != 0;  // tiny - one rounds to -1
+  const bool tiny = hx < 0x3c900000u;                  // |x| < 2^-54 (inexact only)
+  int k = 0;
+  if (hx > 0x3fd62e42u)
+    k = hx < 0x3FF0A2B2u ? (xsb == 0 ? 1 : -1)
+                         : static_cast<int>(dadd(dmul(invln2, x), xsb == 0 ? 0.5 : -0.5));
+  const double tk = static_cast<double>(k);
+  const double hi = dfma(-tk, ln2_hi, x);
+  const double lo = dmul(tk, ln2_lo);
+  const double xr = dsub(hi, lo);
+  const double c = dsub(dsub(hi, xr), lo);
+  const double hfx = dmul(xr, 0.5);
+  const double hxs = dmul(xr, hfx);
   const double R1 = dfma(hxs, Q1, 1.0);
   const double R2 = dfma(hxs, Q3, Q2);
   const double R3 = dfma(hxs, Q5, Q4);
   const double h2 = dmul(hxs, hxs);
   const double h4 = dmul(h2, h2);
   const double r1 = dfma(h4, R3, dfma(h2, R2, R1));
-  t = dfma(-r1, hfx, 3.0);
-  double e = dmul(ddiv(dsub(r1, t), dfma(-x, t, 6.0)), hxs);
-  if (k == 0) return dsub(x, dfma(e, x, -hxs));
-  e = dfma(dsub(e, c), x, -c);
-  e = dsub(e, hxs);
-  if (k == -1) return dfma(0.5, dsub(x, e), -0.5);
-  if (k == 1) {
-    if (x < -0.25) return dmul(dsub(e, dadd(x, 0.5)), -2.0);
-    return dfma(dsub(x, e), 2.0, 1.0);
-  }
-  double y;
-  if (k <= -2 || k > 56) {
-    y = dsub(1.0, dsub(e, x));
-    y = with_hi(y, hi_word(y) + (static_cast<uint32_t>(k) << 20));
-    return dsub(y, 1.0);
-  }
-  if (k < 20) {
-    t = __hiloint2double(static_cast<int>(0x3ff00000u - (0x200000u >> k)), 0);
-    y = dsub(t, dsub(e, x));
-  } else {
-    t = __hiloint2double(static_cast<int>(static_cast<uint32_t>(0x3ff - k) << 20), 0);
-    y = dadd(dsub(x, dadd(e, t)), 1.0);
-  }
-  return with_hi(y, hi_word(y) + (static_cast<uint32_t>(k) << 20));
+  const double t = dfma(-r1, hfx, 3.0);
+  const double e = dmul(ddiv(dsub(r1, t), dfma(-xr, t, 6.0)), hxs);
+  // k == 0
+  const double res0 = dsub(xr, dfma(e, xr, -hxs));
+  // k != 0
+  const double e2 = dsub(dfma(dsub(e, c), xr, -c), hxs);
+  const double res_m1 = dfma(0.5, dsub(xr, e2), -0.5);
+  const double res_p1 = xr < -0.25 ? dmul(dsub(e2, dadd(xr, 0.5)), -2.0)
+                                   : dfma(dsub(xr, e2), 2.0, 1.0);
+  const uint32_t kshift = static_cast<uint32_t>(k) << 20;
+  const double ya = dsub(1.0, dsub(e2, xr));                      // k <= -2 || k > 56
+  const double res_a = dsub(with_hi(ya, hi_word(ya) + kshift), 1.0);
+  const int kb = k > 0 && k < 20 ? k : 1;                         // k < 20
+  const double tb = __hiloint2double(static_cast<int>(0x3ff00000u - (0x200000u >> kb)), 0);
+  const double yb = dsub(tb, dsub(e2, xr));
+  const double res_b = with_hi(yb, hi_word(yb) + kshift);
+  const int kc = k >= 20 && k <= 56 ? k : 20;                     // 20 <= k <= 56
+  const double tc = __hiloint2double(static_cast<int>(static_cast<uint32_t>(0x3ff - kc) << 20), 0);
+  const double yc = dadd(dsub(xr, dadd(e2, tc)), 1.0);
+  const double res_c = with_hi(yc, hi_word(yc) + kshift);
+  double r = (k <= -2 || k > 56) ? res_a : (k < 20 ? res_b : res_c);
+  r = k == 1 ? res_p1 : r;
+  r = k == -1 ? res_m1 : r;
+  r = k == 0 ? res0 : r;
+  r = tiny ? x : r;
+  return neg_one ? -1.0 : r;
 }
 
-// glibc 2.39 tanh (sysdeps/ieee754/dbl-64/s_tanh.c; no FMA in tanh itself).
+// glibc 2.39 tanh (sysdeps/ieee754/dbl-64/s_tanh.c; no FMA in tanh itself):
+// the two |x| ranges share one expm1 and one division (numerator selected),
+// and the zero / tiny / saturated results are selected, so lanes stay converged.
 __device__ __forceinline__ double glibc_tanh(double x) {
   const uint32_t jx = hi_word(x), ix = jx & 0x7fffffffu;
   if (ix >= 0x7ff00000u) {
     if (jx & 0x80000000u) return dsub(ddiv(1.0, x), 1.0);
     return dadd(ddiv(1.0, x), 1.0);
   }
-  double z;
-  if (ix < 0x40360000u) {
-    if ((ix | lo_word(x)) == 0) return x;
-    if (ix < 0x3c800000u) return dmul(x, dadd(1.0, x));
-    const double ax = fabs(x);
-    // one expm1 call site for both ranges keeps a warp's lanes converged
-    // (the arguments and the final combination are exactly glibc's)
-    const bool big = ix >= 0x3ff00000u;
-    const double t = glibc_expm1(big ? dadd(ax, ax) : dmul(-2.0, ax));
-    const double den = dadd(t, 2.0);
-    z = big ? dsub(1.0, ddiv(2.0, den)) : ddiv(-t, den);
-  } else {
-    z = 1.0;  // one - tiny
-  }
-  return (jx & 0x80000000u) ? -z : z;
+  const double ax = fabs(x);
+  const bool big = ix >= 0x3ff00000u;
+  const double t = glibc_expm1(big ? dadd(ax, ax) : dmul(-2.0, ax));
+  const double den = dadd(t, 2.0);
+  const double q = ddiv(big ? 2.0 : -t, den);
+  double z = big ? dsub(1.0, q) : q;
+  z = ix >= 0x40360000u ? 1.0 : z;  // |x| >= 22: one - tiny
+  z = (jx & 0x80000000u) ? -z : z;
+  z = ix < 0x3c800000u ? dmul(x, dadd(1.0, x)) : z;  // |x| < 2^-55
+  return (ix | lo_word(x)) == 0 ? x : z;
 }
 
 // ---- rng.hpp:9-42 ----------------------------------------------------------

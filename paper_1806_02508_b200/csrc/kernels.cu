@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kTrainThreads) pred_train_kernel(PredDev P, in
   const int L = len < P.max_hist ? len : P.max_hist;
   double* buf = narx_train_scratch_bytes(L) <= smem_bytes
                     ? sm_d
-                    : P.scratch + static_cast<size_t>(blockIdx.x) * 13 * P.max_hist;
+                    : P.scratch + blockIdx.x * (narx_train_scratch_bytes(P.max_hist) / sizeof(double));
   lbbsp_narx_train_cfg cfg = P.train;
   cfg.min_history = P.warmup;
   const size_t o = static_cast<size_t>(w) * P.max_hist;

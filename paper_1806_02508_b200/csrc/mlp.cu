@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
     const int L = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
     double* buf = narx_train_scratch_bytes(L) <= smem_bytes
                       ? sm_d
-                      : D.pred.scratch + static_cast<size_t>(blockIdx.x) * 13 * D.pred.max_hist;
+                      : D.pred.scratch + blockIdx.x * (narx_train_scratch_bytes(D.pred.max_hist) / sizeof(double));
     lbbsp_narx_train_cfg cfg = D.pred.train;
     cfg.min_history = D.pred.warmup;
     narx_train_block(&D.pred.models[w], D.pred.hv + o, D.pred.hc + o, D.pred.hm + o, L, cfg,

@@ -87,10 +87,18 @@ __device__ inline void observe_d(const PredDev& P, int w, int len, double v, dou
   P.comm_last[w] = tm;
 }
 
-// Bytes of per-sample scratch a training call needs (13 doubles per sample).
-__host__ __device__ __forceinline__ size_t narx_train_scratch_bytes(int len) {
+// Training scratch: 21 per-sample arrays (Z[8], T, E, G[11]) of stride
+// narx_train_stride(len) doubles -- a multiple of 16 plus one, so the arrays
+// start in distinct shared-memory bank pairs and the 12 fold lanes (E, G[0..10])
+// read conflict-free; the stride also covers the zero padding of the folds to
+// a multiple of 8 terms.
+constexpr int kNarxArrays = 21;
+__host__ __device__ __forceinline__ int narx_train_stride(int len) {
   const int cnt = len > 2 ? len - 2 : 1;
-  return static_cast<size_t>(cnt) * 13 * sizeof(double);
+  return (cnt + 15) / 16 * 16 + 1;
+}
+__host__ __device__ __forceinline__ size_t narx_train_scratch_bytes(int len) {
+  return static_cast<size_t>(narx_train_stride(len)) * kNarxArrays * sizeof(double);
 }
 
 struct NarxTrainSmem {
@@ -101,61 +109,58 @@ struct NarxTrainSmem {
 
 // One evaluation of the training objective at weights wt, fused with the
 // gradient at wt (predictor.cpp:102-134). Per-sample terms are computed in
-// parallel; then, concurrently in two warps, thread 0 folds the squared errors
-// left to right (mse, :104-107) and threads 32..42 fold the 11 gradient
-// accumulators left to right (loss_gradient, :121-132). The gradient is
+// parallel: the squared error E_i (mse, :104-107) and the 11 gradient terms
+// G_k,i (loss_gradient, :121-132: dz*z_k, dz, dy*h, dy -- each the same single
+// product the reference forms). Then lanes 0..11 of warp 1 fold E and G_0..10
+// left to right, one array per lane, 8 terms ahead in registers so only the
+// dependent DADD chain is exposed (the folds are zero padded to a multiple of
+// 8; adding +0.0 to a sum that starts at +0.0 is the identity). The gradient is
 // speculative: it is exactly the next epoch's loss_gradient(model) whenever
 // the trial is accepted (same weights, same per-sample operations, same
 // order), and is discarded otherwise.
 __device__ inline double block_eval(const double* wt, const double* Z, const double* T, double* E,
-                                    double* H, double* DY, double* DZ, int cnt, double scale,
-                                    double* gout, NarxTrainSmem* s) {
+                                    double* G, int S, int cnt, double scale, double* gout,
+                                    NarxTrainSmem* s) {
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    double z[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) z[j] = Z[static_cast<size_t>(j) * S + i];
     double a = wt[8];
-    for (int j = 0; j < 8; ++j) a = dadd(a, dmul(wt[j], Z[static_cast<size_t>(j) * cnt + i]));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a = dadd(a, dmul(wt[j], z[j]));
     const double h = glibc_tanh(a);
     const double y = dadd(dmul(wt[9], h), wt[10]);
     const double e = dsub(y, T[i]);
     E[i] = dmul(e, e);
     const double dy = dmul(scale, e);
-    H[i] = h;
-    DY[i] = dy;
-    DZ[i] = dmul(dmul(dy, wt[9]), dsub(1.0, dmul(h, h)));
+    const double dz = dmul(dmul(dy, wt[9]), dsub(1.0, dmul(h, h)));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) G[static_cast<size_t>(j) * S + i] = dmul(dz, z[j]);
+    G[static_cast<size_t>(8) * S + i] = dz;
+    G[static_cast<size_t>(9) * S + i] = dmul(dy, h);
+    G[static_cast<size_t>(10) * S + i] = dy;
   }
   __syncthreads();
-  const int tid = threadIdx.x;
-  // left-to-right folds; loads are hoisted 8 at a time so only the dependent
-  // DADD chain is on the critical path (the fold order is unchanged)
-  if (tid == 0) {
-    double total = 0.0;
-    int i = 0;
-    for (; i + 8 <= cnt; i += 8) {
-      double e[8];
+  if (threadIdx.x >= 32 && threadIdx.x < 44) {
+    const int k = threadIdx.x - 32;
+    const double* src = k < 11 ? G + static_cast<size_t>(k) * S : E;
+    const int n8 = (cnt + 7) / 8 * 8;
+    double acc = 0.0, cur[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) e[q] = E[i + q];
+    for (int q = 0; q < 8; ++q) cur[q] = src[q];
+    for (int i = 8; i < n8; i += 8) {
+      double nxt[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) total = dadd(total, e[q]);
+      for (int q = 0; q < 8; ++q) nxt[q] = src[i + q];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc = dadd(acc, cur[q]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
     }
-    for (; i < cnt; ++i) total = dadd(total, E[i]);
-    s->val = ddiv(total, static_cast<double>(cnt));
-  } else if (tid >= 32 && tid < 43) {
-    const int k = tid - 32;
-    // term_i = a_i * b_i, or a_i alone for the bias terms (k = 8, 10), which is
-    // the same value as a_i * 1.0 -- so all 11 lanes run one loop, no divergence
-    const double* a = k <= 8 ? DZ : DY;
-    const double* b = k < 8 ? Z + static_cast<size_t>(k) * cnt : (k == 9 ? H : nullptr);
-    const bool hb = b != nullptr;
-    double acc = 0.0;
-    int i = 0;
-    for (; i + 8 <= cnt; i += 8) {
-      double t[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) t[q] = dmul(a[i + q], hb ? b[i + q] : 1.0);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc = dadd(acc, t[q]);
-    }
-    for (; i < cnt; ++i) acc = dadd(acc, dmul(a[i], hb ? b[i] : 1.0));
-    gout[k] = acc;
+    for (int q = 0; q < 8; ++q) acc = dadd(acc, cur[q]);
+    if (k < 11) gout[k] = acc;
+    else s->val = ddiv(acc, static_cast<double>(cnt));
   }
   __syncthreads();
   return s->val;
@@ -199,42 +204,46 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
   }
   __syncthreads();
   const int cnt = L - 2;
-  double* Z = buf;                              // [8][cnt]
-  double* T = Z + static_cast<size_t>(8) * cnt;  // [cnt]
-  double* H = T + cnt;
-  double* DY = H + cnt;
-  double* DZ = DY + cnt;
-  double* E = DZ + cnt;
+  const int S = narx_train_stride(L);
+  double* Z = buf;                             // [8][S]
+  double* T = Z + static_cast<size_t>(8) * S;  // [S]
+  double* E = T + S;                           // [S]
+  double* G = E + S;                           // [11][S]
+  // zero padding of the folds (never written by the evaluations)
+  for (int i = cnt + tid; i < (cnt + 7) / 8 * 8; i += blockDim.x) {
+    E[i] = 0.0;
+    for (int k = 0; k < 11; ++k) G[static_cast<size_t>(k) * S + i] = 0.0;
+  }
   const double mv = s->sc[0], sv = s->sc[1], mc = s->sc[2], scd = s->sc[3], mm = s->sc[4],
                sm = s->sc[5];
   // build_training_set (predictor.cpp:89-100)
   for (int i = tid; i < cnt; i += blockDim.x) {
     const int t = i + 2;
-    Z[0 * cnt + i] = ddiv(dsub(v[t - 1], mv), sv);
-    Z[1 * cnt + i] = ddiv(dsub(v[t - 2], mv), sv);
-    Z[2 * cnt + i] = ddiv(dsub(c[t], mc), scd);
-    Z[3 * cnt + i] = ddiv(dsub(c[t - 1], mc), scd);
-    Z[4 * cnt + i] = ddiv(dsub(c[t - 2], mc), scd);
-    Z[5 * cnt + i] = ddiv(dsub(m[t], mm), sm);
-    Z[6 * cnt + i] = ddiv(dsub(m[t - 1], mm), sm);
-    Z[7 * cnt + i] = ddiv(dsub(m[t - 2], mm), sm);
+    Z[0 * S + i] = ddiv(dsub(v[t - 1], mv), sv);
+    Z[1 * S + i] = ddiv(dsub(v[t - 2], mv), sv);
+    Z[2 * S + i] = ddiv(dsub(c[t], mc), scd);
+    Z[3 * S + i] = ddiv(dsub(c[t - 1], mc), scd);
+    Z[4 * S + i] = ddiv(dsub(c[t - 2], mc), scd);
+    Z[5 * S + i] = ddiv(dsub(m[t], mm), sm);
+    Z[6 * S + i] = ddiv(dsub(m[t - 1], mm), sm);
+    Z[7 * S + i] = ddiv(dsub(m[t - 2], mm), sm);
     T[i] = ddiv(dsub(v[t], mv), sv);
   }
   __syncthreads();
   const double scale = ddiv(2.0, static_cast<double>(cnt));
   // current = mse(model) (:165), and loss_gradient(model) of epoch 0
-  double current = block_eval(s->w, Z, T, E, H, DY, DZ, cnt, scale, s->g, s);
+  double current = block_eval(s->w, Z, T, E, G, S, cnt, scale, s->g, s);
   for (int epoch = 0; epoch < cfg.max_epochs; ++epoch) {
     double step = cfg.step;
     if (tid < 11) s->trial[tid] = dsub(s->w[tid], dmul(step, s->g[tid]));  // apply_step :136-143
     __syncthreads();
-    double next = block_eval(s->trial, Z, T, E, H, DY, DZ, cnt, scale, s->gs, s);
+    double next = block_eval(s->trial, Z, T, E, G, S, cnt, scale, s->gs, s);
     int halvings = 0;
     while (next > current && halvings < 20) {
       step = dmul(step, 0.5);
       if (tid < 11) s->trial[tid] = dsub(s->w[tid], dmul(step, s->g[tid]));
       __syncthreads();
-      next = block_eval(s->trial, Z, T, E, H, DY, DZ, cnt, scale, s->gs, s);
+      next = block_eval(s->trial, Z, T, E, G, S, cnt, scale, s->gs, s);
       ++halvings;
     }
     if (next > current) break;  // no descent direction left (:182)

@@ -157,6 +157,15 @@ def narx_predict(model: NarxModel, recent_speeds, cpu_window, mem_window,
     return out.value
 
 
+def glibc_tanh(xs) -> np.ndarray:
+    """The device restatement of glibc tanh (exactmath.cuh) over an array."""
+    x = np.ascontiguousarray(xs, dtype=np.float64)
+    y = np.empty_like(x)
+    check(lib().lbbsp_glibc_tanh(x.ctypes.data_as(C.POINTER(C.c_double)),
+                                 y.ctypes.data_as(C.POINTER(C.c_double)), x.size))
+    return y
+
+
 @dataclass
 class NarxTrainReport:
     ran: bool = False

@@ -137,6 +137,28 @@ def test_device_tanh_bit_exact_vs_glibc(lb, golden):
     assert bad == 0
 
 
+def test_device_tanh_batch_bit_exact_vs_host_libm(lb, golden):
+    """glibc_tanh over ~1.2M inputs covering every expm1 reduction branch
+    (k = 0, +-1, 2..19, 20..56, > 56), the range boundaries and the golden
+    vectors, against the host libm (the reference's std::tanh)."""
+    import math
+    rng = np.random.default_rng(7)
+    ln2 = math.log(2)  # expm1(+-2|x|) switches branch at |x| = (k + 0.5) ln2 / 2
+    bounds = [0.0, 2.0 ** -55, 2.0 ** -28, 0.25 * ln2, 0.75 * ln2, 1.0, 1.25 * ln2,
+              9.75 * ln2, 19.4, 28.25 * ln2, 22.0, 28.0]
+    near = np.concatenate([np.nextafter(b, np.inf) + np.arange(-40, 40) * np.spacing(max(b, 1e-300))
+                           for b in bounds])
+    xs = np.concatenate([rng.uniform(-25, 25, 400000), rng.uniform(-1.2, 1.2, 400000),
+                         rng.normal(0, 1e-3, 100000), rng.uniform(0.3, 0.4, 100000),
+                         rng.uniform(0.5, 0.55, 100000), near, -near,
+                         np.array([1e-310, -1e-310, 1e300, -1e300, np.inf, -np.inf]),
+                         fromhex(golden("predictor")["tanh"]["x"])])
+    got = lb.glibc_tanh(xs)
+    want = np.array([math.tanh(x) for x in xs])
+    bad = np.flatnonzero(got.view(np.uint64) != want.view(np.uint64))
+    assert bad.size == 0, f"{bad.size} mismatches, e.g. {[(xs[i], got[i], want[i]) for i in bad[:3]]}"
+
+
 def test_narx_train_golden(lb, golden):
     for case in golden("predictor")["narx_train"]:
         m = _model(fromhex(case["model_in"]))

@@ -598,6 +598,13 @@ def main():
     ph_fwd = float(phases[0]) if phases is not None and len(phases) else 0.0
     ph_dw = float(phases[3]) if phases is not None and len(phases) > 3 else 0.0
     achieved = fwd_flops / ph_fwd / 1e12 if ph_fwd > 0 else 0.0
+    # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
+    traffic = None
+    try:
+        cap = json.load(open(os.path.join(REPO, "profiles", "r01_c2_fwd_gemm_ncu.json")))
+        traffic = int(cap["dram_bytes_read"]) + int(cap["dram_bytes_write"])
+    except Exception:
+        pass
 
     if rank == 0:
         clocks = clk.summary()
@@ -624,7 +631,9 @@ def main():
                                                       "partitions)",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf if peak_tf else None,
-                         "peak_source": peak_src, "traffic": None,
+                         "peak_source": peak_src, "traffic": traffic,
+                         "traffic_source": "profiles/r01_c2_fwd_gemm_ncu.json (dram__bytes_read.sum "
+                                           "+ dram__bytes_write.sum, one launch)",
                          "note": "C2 GEMMs are latency-bound (SURVEY 8(d)); see profiles/ for "
                                  "the C3 tensor-bound numbers"},
             "gpu_launches": launches * args.steps,

@@ -10,7 +10,7 @@ for C in $CFGS; do
     echo "$C n$N rc=$?" >> $O/status_multi
   done
 done
-for N in 2 4; do
+[ -n "$NO_REF" ] || for N in 2 4; do
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
     --master-port $((29600 + N)) bench.py --gpus $N --impl reference > $O/ref_n$N.json 2> $O/ref_n$N.err
   echo "ref n$N rc=$?" >> $O/status_multi

@@ -39,6 +39,27 @@ constexpr int kHmLoss = kHmBp + 8 * 256 * 4;           // [8] f64
 constexpr int kHmWraw = kHmLoss + 8 * 8 + 64;          // W fp32 staging [10][256]
 constexpr int kHeadMmaSmem = kHmWraw + kHeadNC * kHeadDH * 4;
 constexpr int kHeadFrag = 32 * 4 * 32;                 // dW accumulator entries per warp
+// CTA partials are kept in the warps' fragment order (coalesced writes):
+// [kHeadFrag dW | 4x32 db | 8x32 prev db]; padded classes are carried and dropped
+// when the worker's last CTA maps the sums to natural order
+constexpr int kHeadPartVals = kHeadFrag + 4 * 32 + 8 * 32;
+
+// fragment-order partial index -> natural index (dW [class][col] | db [class] |
+// prev db [col]), -1 for the padded classes
+__device__ __forceinline__ int head_frag_to_natural(int k) {
+  if (k < kHeadFrag) {
+    const int j = k >> 7, e = (k >> 5) & 3, l = k & 31;
+    const int cls = (l >> 2) + (e >= 2 ? 8 : 0), col = 8 * j + 2 * (l & 3) + (e & 1);
+    return cls < kHeadNC ? cls * kHeadDH + col : -1;
+  }
+  if (k < kHeadFrag + 128) {
+    const int u = (k - kHeadFrag) >> 5, l = k & 31;
+    const int cls = (u < 2 ? 2 * l + u : 8 + 2 * l + (u - 2));
+    return ((l >> 2) == 0 && (u < 2 || l == 0)) ? kHeadNC * kHeadDH + cls : -1;
+  }
+  const int u = (k - kHeadFrag - 128) >> 5, l = k & 31;
+  return kHeadNC * kHeadDH + kHeadNC + 8 * l + u;
+}
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -299,7 +320,7 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
   if (lane == 0) wl_loss[warp] = lsum;
   // per-warp partials in fragment order (lane-contiguous, conflict-free):
   // [kHeadFrag dW | 4x32 db | 8x32 prev db]
-  constexpr int kWarpVals = kHeadFrag + 4 * 32 + 8 * 32;
+  constexpr int kWarpVals = kHeadPartVals;
   static_assert(8 * kWarpVals * 4 <= kHmLoss - kHmH, "partials overlap the loss slots");
   float* red = reinterpret_cast<float*>(sm + kHmH);  // [8][kWarpVals] over H, dl, bp
   if (TRAIN) {
@@ -330,20 +351,7 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
       float v = red[k];
 #pragma unroll
       for (int w = 1; w < 8; ++w) v += red[w * kWarpVals + k];
-      int o = -1;  // natural index: dW [class][col] | db [class] | prev db [col]
-      if (k < kHeadFrag) {
-        const int j = k >> 7, e = (k >> 5) & 3, l = k & 31;
-        const int cls = (l >> 2) + (e >= 2 ? 8 : 0), col = 8 * j + 2 * (l & 3) + (e & 1);
-        if (cls < kHeadNC) o = cls * kHeadDH + col;
-      } else if (k < kHeadFrag + 128) {
-        const int u = (k - kHeadFrag) >> 5, l = k & 31;
-        const int cls = (u < 2 ? 2 * l + u : 8 + 2 * l + (u - 2));
-        if ((l >> 2) == 0 && (u < 2 || l == 0)) o = kHeadNC * kHeadDH + cls;
-      } else {
-        const int u = (k - kHeadFrag - 128) >> 5, l = k & 31;
-        o = kHeadNC * kHeadDH + kHeadNC + 8 * l + u;
-      }
-      if (o >= 0) cta_part[static_cast<long long>(blockIdx.x) * kHeadVals + o] = v;
+      cta_part[static_cast<long long>(blockIdx.x) * kHeadPartVals + k] = v;
     }
   if (threadIdx.x == 0) {
     double l = 0.0;
@@ -360,22 +368,34 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
     const int c0 = blockIdx.x - cta_in;
     if (TRAIN) {
       float* gs = slab + static_cast<long long>(g) * slab_stride;
-      constexpr int kPer = (kHeadVals + 255) / 256;
+      constexpr int kPer = (kHeadPartVals + 255) / 256;
       float v[kPer];
 #pragma unroll
       for (int u = 0; u < kPer; ++u) v[u] = 0.f;
-      for (int c = 0; c < cta_cnt; ++c) {  // CTA order; kPer loads in flight
-        const float* src = cta_part + static_cast<long long>(c0 + c) * kHeadVals;
+      // CTA order; the loads of 4 CTAs are issued before their adds, so a
+      // worker with <= 4 CTAs pays one L2 round trip
+      for (int c4 = 0; c4 < cta_cnt; c4 += 4) {
+        float x[4][kPer];
 #pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-          const int i = threadIdx.x + 256 * u;
-          if (i < kHeadVals) v[u] += __ldcg(&src[i]);
-        }
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int u = 0; u < kPer; ++u) {
+            const int i = threadIdx.x + 256 * u;
+            x[q][u] = c4 + q < cta_cnt && i < kHeadPartVals
+                          ? __ldcg(&cta_part[static_cast<long long>(c0 + c4 + q) * kHeadPartVals + i])
+                          : 0.f;
+          }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int u = 0; u < kPer; ++u)
+            if (c4 + q < cta_cnt) v[u] += x[q][u];
       }
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
-        const int i = threadIdx.x + 256 * u;
-        if (i >= kHeadVals) continue;
+        const int k = threadIdx.x + 256 * u;
+        const int i = k < kHeadPartVals ? head_frag_to_natural(k) : -1;
+        if (i < 0) continue;
         const long long o = i < kHeadNC * kHeadDH ? off_w + i
                             : i < kHeadNC * kHeadDH + kHeadNC ? off_b + (i - kHeadNC * kHeadDH)
                                                               : off_b_prev + (i - kHeadNC * kHeadDH - kHeadNC);

@@ -1369,7 +1369,7 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     LBBSP_CUDA_CHECK(m.alloc(&m.gradb, static_cast<size_t>(P)));
   if (small_head) {
     const int nsm = num_sms();
-    LBBSP_CUDA_CHECK(m.alloc(&m.head_part, static_cast<size_t>(nsm) * kHeadVals));
+    LBBSP_CUDA_CHECK(m.alloc(&m.head_part, static_cast<size_t>(nsm) * kHeadPartVals));
     LBBSP_CUDA_CHECK(m.alloc(&m.head_loss, static_cast<size_t>(nsm)));
     LBBSP_CUDA_CHECK(m.alloc(&m.head_cnt, static_cast<size_t>(m.n_local)));
     LBBSP_CUDA_CHECK(m.alloc(&m.head_cnt_d, 1));

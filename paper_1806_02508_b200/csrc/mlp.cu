@@ -203,7 +203,12 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
     share_s[i] = D.share[i];
     D.c_now[i] = c;
     D.m_now[i] = m;
-    const double a = dmul(c, mult);
+    // SM availability = the worker's relative speed in the reference model,
+    // effective_speed * speed_mult = c * MemPenalty(m) * mult (cluster_sim.cpp:22-29),
+    // capped at 1: memory pressure lowers the worker's SM share the way it lowers
+    // v0 there (HBM is chip-wide, so it cannot slow one co-resident partition alone)
+    const double pen = m >= 0.5 ? 1.0 : dadd(0.25, dmul(0.75, ddiv(m, 0.5)));
+    const double a = dmul(dmul(c, pen), mult);
     avail[i] = a < 1.0 ? a : 1.0;
     const double vp = len >= 1 ? predictor_predict_d(D.pred, i, len, c, m) : 0.0;
     vp_s[i] = vp;

@@ -106,8 +106,9 @@ def recorded_trace(path, n_workers, iterations, seed=1, seconds_per_iteration=60
     """A recorded resource-trace CSV (parse_trace + map_traces, trace.cpp:54-135)
     as the engine's iteration-indexed straggler trace: worker i follows the
     machine map_traces assigns it, sampled with trace_at (trace.cpp:137-143)
-    at t = k * seconds_per_iteration. cpu_avail
-    drives the SM cap, mem_avail is recorded beside it, no transient spikes."""
+    at t = k * seconds_per_iteration. The SM cap
+    follows cpu_avail * MemPenalty(mem_avail) (cluster_sim.cpp:22-29); no
+    transient spikes."""
     from . import lbbsp as LB
     traces = LB.parse_trace(path)
     assign = LB.map_traces(traces, n_workers, seed)

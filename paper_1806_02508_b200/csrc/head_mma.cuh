@@ -162,23 +162,30 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
 
   const float b_lo0 = bias[2 * tq], b_lo1 = bias[2 * tq + 1];
   const float b_hi0 = tq == 0 ? bias[8] : 0.f, b_hi1 = tq == 0 ? bias[9] : 0.f;
-  float dw[32][4];
+  // dW is column-sliced: warp w accumulates dW[:, 32w .. 32w+32) over every
+  // tile of the CTA (A = dl^T of tile t, B = H of tile t), so no cross-warp
+  // reduction of dW is needed; the tiles' dl and H are shared through smem
+  float dw[4][4];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) dw[j][0] = dw[j][1] = dw[j][2] = dw[j][3] = 0.f;
+  for (int j = 0; j < 4; ++j) dw[j][0] = dw[j][1] = dw[j][2] = dw[j][3] = 0.f;
   float dbh[4] = {0.f, 0.f, 0.f, 0.f};
   float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // prev db, cols 8*lane..+7
   double lsum = 0.0;
   uint8_t* dls = sm + kHmDl + warp * 512;
   int buf = 0;
-  for (; tile < n_tiles; tile += wstride) {
+  const int first_tile = cta_in * 8;
+  const int n_iter = n_tiles > first_tile ? (n_tiles - first_tile + wstride - 1) / wstride : 0;
+  for (int it = 0; it < n_iter; ++it, tile += wstride) {
+    const bool have = tile < n_tiles;
     const int row0 = r0 + tile * 16;
     const uint32_t hb = hbuf0 + buf * 8192;
     uint8_t* hp = sm + kHmH + warp * 2 * 8192 + buf * 8192;
     const int next = tile + wstride;
     const int ra = row0 + gq, rb = row0 + gq + 8;
     const bool va = ra < r1, vb = rb < r1;
-    const int ya = va ? y[ra] : -1, yb = vb ? y[rb] : -1;
-    const float rsa = TRAIN && va ? row_scale[ra] : 0.f, rsb = TRAIN && vb ? row_scale[rb] : 0.f;
+    const int ya = have && va ? y[ra] : -1, yb = have && vb ? y[rb] : -1;
+    const float rsa = TRAIN && have && va ? row_scale[ra] : 0.f;
+    const float rsb = TRAIN && have && vb ? row_scale[rb] : 0.f;
     if (next < n_tiles) {
       stage_tile(hbuf0 + (buf ^ 1) * 8192, H, r0 + next * 16, r1, lane);
       cp_async_wait<1>();
@@ -186,8 +193,10 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
       cp_async_wait<0>();
     }
     __syncwarp();
-    // ---- logits: 16 k-steps x 2 class tiles, two independent chains each ----
+    uint32_t ad[4] = {0u, 0u, 0u, 0u};  // dl as the m16k16 A operand of dH = dl W
     const int mi = lane >> 3, lr = (lane & 7) + (mi & 1) * 8;
+    if (have) {
+    // ---- logits: 16 k-steps x 2 class tiles, two independent chains each ----
     float lo[4] = {0.f, 0.f, 0.f, 0.f}, hi[4] = {0.f, 0.f, 0.f, 0.f};
     float lo2[4] = {0.f, 0.f, 0.f, 0.f}, hi2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -260,24 +269,37 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
       dbh[3] += dhi[1] + dhi[3];
       // dl as the A operand of dH = dl W (the m16n8 accumulator layout is the
       // m16k16 A layout), and as [row][class] bf16 for dl^T via ldmatrix.trans
-      uint32_t ad[4] = {pack_bf16(dlo[0], dlo[1]), pack_bf16(dlo[2], dlo[3]),
-                        pack_bf16(dhi[0], dhi[1]), pack_bf16(dhi[2], dhi[3])};
+      ad[0] = pack_bf16(dlo[0], dlo[1]);
+      ad[1] = pack_bf16(dlo[2], dlo[3]);
+      ad[2] = pack_bf16(dhi[0], dhi[1]);
+      ad[3] = pack_bf16(dhi[2], dhi[3]);
       *reinterpret_cast<uint32_t*>(dls + gq * 32 + 4 * tq) = ad[0];
       *reinterpret_cast<uint32_t*>(dls + (gq + 8) * 32 + 4 * tq) = ad[1];
       *reinterpret_cast<uint32_t*>(dls + gq * 32 + 16 + 4 * tq) = ad[2];
       *reinterpret_cast<uint32_t*>(dls + (gq + 8) * 32 + 16 + 4 * tq) = ad[3];
-      __syncwarp();
-      uint32_t at[4];
-      ldsm_x4_t(smem_addr(dls) + ((lane & 7) + (mi >> 1) * 8) * 32 + (mi & 1) * 16, at);
-      // ---- dW += dl^T H : 16 n-tile pairs ----
+    }
+    }  // have
+    if (TRAIN) {
+      __syncthreads();  // every tile's dl and H of this iteration are in smem
+      // ---- dW[:, 32 warp .. +32) += dl_t^T H_t over the CTA's tiles t ----
+#pragma unroll 1
+      for (int t = 0; t < 8; ++t) {
+        if (first_tile + t + it * wstride >= n_tiles) break;
+        uint32_t at[4];
+        ldsm_x4_t(smem_addr(sm + kHmDl + t * 512) + ((lane & 7) + (mi >> 1) * 8) * 32 + (mi & 1) * 16,
+                  at);
+        const uint32_t ht = smem_addr(sm + kHmH + t * 2 * 8192) + buf * 8192;
 #pragma unroll
-      for (int p = 0; p < 16; ++p) {
-        uint32_t b[4];
-        ldsm_x4_t(hb + hsw(lr, 2 * p + (mi >> 1)), b);
-        mma16816(dw[2 * p], at, b[0], b[1]);
-        mma16816(dw[2 * p + 1], at, b[2], b[3]);
+        for (int p = 0; p < 2; ++p) {
+          uint32_t b[4];
+          ldsm_x4_t(ht + hsw(lr, 2 * (2 * warp + p) + (mi >> 1)), b);
+          mma16816(dw[2 * p], at, b[0], b[1]);
+          mma16816(dw[2 * p + 1], at, b[2], b[3]);
+        }
       }
-      __syncwarp();
+      __syncthreads();  // H tiles may now be overwritten by dH
+    }
+    if (TRAIN && have) {
       // ---- dH = (dl W) * (H > 0), written in place over the H tile ----
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -320,10 +342,17 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
   if (lane == 0) wl_loss[warp] = lsum;
   // per-warp partials in fragment order (lane-contiguous, conflict-free):
   // [kHeadFrag dW | 4x32 db | 8x32 prev db]
-  constexpr int kWarpVals = kHeadPartVals;
-  static_assert(8 * kWarpVals * 4 <= kHmLoss - kHmH, "partials overlap the loss slots");
-  float* red = reinterpret_cast<float*>(sm + kHmH);  // [8][kWarpVals] over H, dl, bp
+  // dW: each warp's column slice goes straight to the CTA partial, in the
+  // fragment order of head_frag_to_natural (n-tile j = 4 warp + p);
+  // db / prev db: per-warp values summed over the 8 warps in warp order
+  constexpr int kSmallVals = kHeadPartVals - kHeadFrag;  // 4x32 db | 8x32 prev db
+  float* red = reinterpret_cast<float*>(sm + kHmH);     // [8][kSmallVals] over the H tiles
+  float* part = cta_part + static_cast<long long>(blockIdx.x) * kHeadPartVals;
   if (TRAIN) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) part[((4 * warp + p) * 4 + e) * 32 + lane] = dw[p][e];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       float v = dbh[u];
@@ -335,74 +364,36 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
   }
   __syncthreads();  // every warp is done with its H tiles
   if (TRAIN) {
-    float* mine = red + warp * kWarpVals;
+    float* mine = red + warp * kSmallVals;
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
+    for (int u = 0; u < 4; ++u) mine[u * 32 + lane] = dbh[u];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) mine[(j * 4 + e) * 32 + lane] = dw[j][e];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) mine[kHeadFrag + u * 32 + lane] = dbh[u];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) mine[kHeadFrag + 128 + u * 32 + lane] = cs[u];
+    for (int u = 0; u < 8; ++u) mine[128 + u * 32 + lane] = cs[u];
   }
   __syncthreads();
   if (TRAIN)
-    for (int k = threadIdx.x; k < kWarpVals; k += blockDim.x) {
+    for (int k = threadIdx.x; k < kSmallVals; k += blockDim.x) {
       float v = red[k];
 #pragma unroll
-      for (int w = 1; w < 8; ++w) v += red[w * kWarpVals + k];
-      cta_part[static_cast<long long>(blockIdx.x) * kHeadPartVals + k] = v;
+      for (int w = 1; w < 8; ++w) v += red[w * kSmallVals + k];
+      part[kHeadFrag + k] = v;
     }
   if (threadIdx.x == 0) {
     double l = 0.0;
     for (int w = 0; w < 8; ++w) l += wl_loss[w];
     cta_loss[blockIdx.x] = l;
   }
-  // ---- the worker's last CTA combines the CTA partials in CTA order ----
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&counters[g], 1u) == static_cast<unsigned>(cta_cnt - 1);
-  __syncthreads();
-  if (last) {
+  // Training: the CTA partials are combined by head_combine_kernel, launched
+  // beside the next backward GEMM (off the worker-phase chain). Dataset loss:
+  // the last CTA sums the CTA losses in CTA order.
+  if (!TRAIN) {
     __threadfence();
-    const int c0 = blockIdx.x - cta_in;
-    if (TRAIN) {
-      float* gs = slab + static_cast<long long>(g) * slab_stride;
-      constexpr int kPer = (kHeadPartVals + 255) / 256;
-      float v[kPer];
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) v[u] = 0.f;
-      // CTA order; the loads of 4 CTAs are issued before their adds, so a
-      // worker with <= 4 CTAs pays one L2 round trip
-      for (int c4 = 0; c4 < cta_cnt; c4 += 4) {
-        float x[4][kPer];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int u = 0; u < kPer; ++u) {
-            const int i = threadIdx.x + 256 * u;
-            x[q][u] = c4 + q < cta_cnt && i < kHeadPartVals
-                          ? __ldcg(&cta_part[static_cast<long long>(c0 + c4 + q) * kHeadPartVals + i])
-                          : 0.f;
-          }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int u = 0; u < kPer; ++u)
-            if (c4 + q < cta_cnt) v[u] += x[q][u];
-      }
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int k = threadIdx.x + 256 * u;
-        const int i = k < kHeadPartVals ? head_frag_to_natural(k) : -1;
-        if (i < 0) continue;
-        const long long o = i < kHeadNC * kHeadDH ? off_w + i
-                            : i < kHeadNC * kHeadDH + kHeadNC ? off_b + (i - kHeadNC * kHeadDH)
-                                                              : off_b_prev + (i - kHeadNC * kHeadDH - kHeadNC);
-        gs[o] = v[u];
-      }
-    }
-    if (threadIdx.x == 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&counters[g], 1u) == static_cast<unsigned>(cta_cnt - 1);
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      const int c0 = blockIdx.x - cta_in;
       if (loss_acc) {
         double l = 0.0;
         for (int c = 0; c < cta_cnt; ++c) l += __ldcg(&cta_loss[c0 + c]);
@@ -413,6 +404,52 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
   }
   if (timing && threadIdx.x == 0) atomicMax(&timing[2 * g + 1], static_cast<unsigned long long>(gtimer()));
 }
+
+// Sums each worker's head CTA partials in CTA order (the same CTAs and order
+// head_mma_kernel<true> used) and writes dW | db | prev db into the worker's
+// gradient slab. Grid: n_local x kCombineSlices CTAs of 256 threads.
+constexpr int kCombineSlices = 6;
+__global__ void __launch_bounds__(256) head_combine_kernel(Groups G, const float* __restrict__ cta_part,
+                                                           float* slab, long long slab_stride,
+                                                           long long off_w, long long off_b,
+                                                           long long off_b_prev) {
+  const int g = blockIdx.x / kCombineSlices, slice = blockIdx.x % kCombineSlices;
+  if (g >= G.n) return;
+  const int n_tiles = (G.r1[g] - G.r0[g] + 15) / 16;
+  const int c0 = G.cta0[g];
+  const int cnt = min(G.ctan[g], max(1, (n_tiles + 7) / 8));
+  const int k = slice * 256 * 3 + threadIdx.x;  // 3 values per thread, 6 x 768 >= kHeadPartVals
+  float v[3] = {0.f, 0.f, 0.f};
+  for (int c4 = 0; c4 < cnt; c4 += 4) {  // 4 CTAs' loads in flight per round trip
+    float x[4][3];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int i = k + 256 * u;
+        x[q][u] = c4 + q < cnt && i < kHeadPartVals
+                      ? __ldcg(&cta_part[static_cast<long long>(c0 + c4 + q) * kHeadPartVals + i])
+                      : 0.f;
+      }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        if (c4 + q < cnt) v[u] += x[q][u];
+  }
+  float* gs = slab + static_cast<long long>(g) * slab_stride;
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int kk = k + 256 * u;
+    const int i = kk < kHeadPartVals ? head_frag_to_natural(kk) : -1;
+    if (i < 0) continue;
+    const long long o = i < kHeadNC * kHeadDH ? off_w + i
+                        : i < kHeadNC * kHeadDH + kHeadNC ? off_b + (i - kHeadNC * kHeadDH)
+                                                          : off_b_prev + (i - kHeadNC * kHeadDH - kHeadNC);
+    gs[o] = v[u];
+  }
+}
+static_assert(kCombineSlices * 768 >= kHeadPartVals, "combine slices do not cover the partials");
 
 }  // namespace mlp
 }  // namespace lbbsp

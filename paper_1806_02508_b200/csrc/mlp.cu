@@ -972,6 +972,7 @@ struct lbbsp_mlp {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_speed = nullptr, ev_comm = nullptr;
   cudaEvent_t ev_gather0 = nullptr, ev_gather1 = nullptr;
+  cudaEvent_t ev_head0 = nullptr, ev_head1 = nullptr;  // head partial combine beside the backward
   cudaStream_t copy_stream = nullptr;  // e2e input staging (lbbsp_mlp_load_data_async)
   cudaEvent_t ev_staged = nullptr, ev_refreshed = nullptr;
   bf16* stage_x = nullptr;
@@ -1034,6 +1035,8 @@ struct lbbsp_mlp {
     if (ev_refreshed) cudaEventDestroy(ev_refreshed);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ev_gather1) cudaEventDestroy(ev_gather1);
+    if (ev_head0) cudaEventDestroy(ev_head0);
+    if (ev_head1) cudaEventDestroy(ev_head1);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_speed) cudaEventDestroy(ev_speed);
     if (ev_comm) cudaEventDestroy(ev_comm);
@@ -1135,6 +1138,14 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
         static_cast<const int*>(y), static_cast<const float*>(row_scale), dZ[L - 2], partial, P,
         off_w[hl], off_b[hl], off_b[L - 2], static_cast<double*>(nullptr), head_part, head_loss,
         head_cnt, phase_slot(ph++)));
+    ++nl;
+    // the CTA partials are summed beside the backward GEMMs; joined before the
+    // gradient slabs are consumed
+    LBBSP_CUDA_CHECK(cudaEventRecord(ev_head0, s));
+    LBBSP_CUDA_CHECK(cudaStreamWaitEvent(side, ev_head0, 0));
+    head_combine_kernel<<<n_local * kCombineSlices, 256, 0, side>>>(
+        G, head_part, partial, P, off_w[hl], off_b[hl], off_b[L - 2]);
+    LBBSP_CUDA_CHECK(cudaEventRecord(ev_head1, side));
   } else {
     LBBSP_CUDA_CHECK(launch_softmax_ce(sms, s, use_pdl, G, 0, logits, dims[L], y, row_scale,
                                        dZ[L - 1], nullptr, phase_slot(ph++)));
@@ -1187,6 +1198,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     }
   }
   n_phases = ph;
+  if (small_head) LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_head1, 0));
   // measured speeds; on several GPUs all-gathered (after the gradient buckets)
   const float lr = static_cast<float>(cfg.learning_rate);
   if (cfg.world > 1 && peers && !bucketed) {
@@ -1344,6 +1356,8 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_fork, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_gather0, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_gather1, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_head0, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_head1, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_join, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_speed, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_comm, cudaEventDisableTiming));

@@ -315,7 +315,7 @@ static int make_pred(lbbsp_predictor* P, const lbbsp_predictor_cfg* cfg, int n, 
   LBBSP_CUDA_CHECK(P->alloc(&d.comm_ema_lag, n));
   LBBSP_CUDA_CHECK(P->alloc(&d.models, n));
   LBBSP_CUDA_CHECK(P->alloc(&d.reports, n));
-  const bool need_scratch = narx_train_scratch_bytes(max_hist) > train_smem_bytes(max_hist);
+  const bool need_scratch = narx_train_min_bytes(max_hist) > train_smem_bytes(max_hist);
   LBBSP_CUDA_CHECK(P->alloc(&d.scratch, need_scratch ? static_cast<size_t>(n) * (narx_train_scratch_bytes(max_hist) / sizeof(double)) : 1));
   LBBSP_CUDA_CHECK(P->alloc(&d.len, 1));
   LBBSP_CUDA_CHECK(P->alloc(&d.cursor, 1));

@@ -116,8 +116,10 @@ __global__ void __launch_bounds__(kTrainThreads) narx_train_one_kernel(
     double* gscratch, size_t smem_bytes) {
   extern __shared__ double sm_d[];
   __shared__ NarxTrainSmem s;
-  double* buf = narx_train_scratch_bytes(len) <= smem_bytes ? sm_d : gscratch;
-  narx_train_block(m, v, c, mm, len, cfg, rep, loss_log, loss_cap, buf, &s);
+  size_t nd = 0;
+  double* buf = narx_train_buf(len, sm_d, smem_bytes, gscratch,
+                               narx_train_scratch_bytes(len) / sizeof(double), &nd);
+  narx_train_block(m, v, c, mm, len, cfg, rep, loss_log, loss_cap, buf, nd, &s);
 }
 
 cudaError_t launch_narx_train_one(lbbsp_narx_model* d_model, const double* d_v, const double* d_c,
@@ -179,14 +181,14 @@ __global__ void __launch_bounds__(kTrainThreads) pred_train_kernel(PredDev P, in
   const int w = (first + blockIdx.x) % P.n;
   const int len = *P.len;
   const int L = len < P.max_hist ? len : P.max_hist;
-  double* buf = narx_train_scratch_bytes(L) <= smem_bytes
-                    ? sm_d
-                    : P.scratch + blockIdx.x * (narx_train_scratch_bytes(P.max_hist) / sizeof(double));
+  const size_t slot = narx_train_scratch_bytes(P.max_hist) / sizeof(double);
+  size_t nd = 0;
+  double* buf = narx_train_buf(L, sm_d, smem_bytes, P.scratch + blockIdx.x * slot, slot, &nd);
   lbbsp_narx_train_cfg cfg = P.train;
   cfg.min_history = P.warmup;
   const size_t o = static_cast<size_t>(w) * P.max_hist;
   narx_train_block(&P.models[w], P.hv + o, P.hc + o, P.hm + o, L, cfg, &P.reports[w], nullptr, 0,
-                   buf, &s);
+                   buf, nd, &s);
 }
 
 cudaError_t launch_pred_train_from(const PredDev& P, const int* first_slot, cudaStream_t s) {
@@ -815,8 +817,11 @@ __global__ void __launch_bounds__(kTrainThreads) series_rmse_kernel(PredDev P, c
     __syncthreads();
     if (P.kind == LBBSP_PRED_NARX) {
       const int L = k + 1;
-      double* buf = narx_train_scratch_bytes(L) <= smem_bytes ? sm_d : P.scratch;
-      narx_train_block(&P.models[0], P.hv, P.hc, P.hm, L, cfg, &P.reports[0], nullptr, 0, buf, &s);
+      size_t nd = 0;
+      double* buf = narx_train_buf(L, sm_d, smem_bytes, P.scratch,
+                                   narx_train_scratch_bytes(P.max_hist) / sizeof(double), &nd);
+      narx_train_block(&P.models[0], P.hv, P.hc, P.hm, L, cfg, &P.reports[0], nullptr, 0, buf, nd,
+                       &s);
     }
   }
   __syncthreads();
@@ -958,9 +963,11 @@ __global__ void __launch_bounds__(kAsyncThreads) async_sim_kernel(SimDev S, Asyn
     if (S.pred.kind == LBBSP_PRED_NARX) {
       const int L = A.hist_len[w] < S.pred.max_hist ? A.hist_len[w] : S.pred.max_hist;
       const size_t o = static_cast<size_t>(w) * S.pred.max_hist;
-      double* buf = narx_train_scratch_bytes(L) <= smem_bytes ? sm_d : S.pred.scratch;
+      size_t nd = 0;
+      double* buf = narx_train_buf(L, sm_d, smem_bytes, S.pred.scratch,
+                                   narx_train_scratch_bytes(S.pred.max_hist) / sizeof(double), &nd);
       narx_train_block(&S.pred.models[w], S.pred.hv + o, S.pred.hc + o, S.pred.hm + o, L, tcfg,
-                       &S.pred.reports[w], nullptr, 0, buf, &ts);
+                       &S.pred.reports[w], nullptr, 0, buf, nd, &ts);
     }
     __syncthreads();
     const double* inf = A.inflight + static_cast<size_t>(w) * 8;

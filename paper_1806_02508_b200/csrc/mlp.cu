@@ -752,13 +752,13 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
     }
     __syncthreads();
     const int L = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
-    double* buf = narx_train_scratch_bytes(L) <= smem_bytes
-                      ? sm_d
-                      : D.pred.scratch + blockIdx.x * (narx_train_scratch_bytes(D.pred.max_hist) / sizeof(double));
+    const size_t slot = narx_train_scratch_bytes(D.pred.max_hist) / sizeof(double);
+    size_t nd = 0;
+    double* buf = narx_train_buf(L, sm_d, smem_bytes, D.pred.scratch + blockIdx.x * slot, slot, &nd);
     lbbsp_narx_train_cfg cfg = D.pred.train;
     cfg.min_history = D.pred.warmup;
     narx_train_block(&D.pred.models[w], D.pred.hv + o, D.pred.hc + o, D.pred.hm + o, L, cfg,
-                     &D.pred.reports[w], nullptr, 0, buf, &ts);
+                     &D.pred.reports[w], nullptr, 0, buf, nd, &ts);
     return;
   }
   if (tid == 0) D.stamps[3] = gtimer();

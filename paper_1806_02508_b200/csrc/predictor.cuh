@@ -87,18 +87,38 @@ __device__ inline void observe_d(const PredDev& P, int w, int len, double v, dou
   P.comm_last[w] = tm;
 }
 
-// Training scratch: 21 per-sample arrays (Z[8], T, E, G[11]) of stride
-// narx_train_stride(len) doubles -- a multiple of 16 plus one, so the arrays
-// start in distinct shared-memory bank pairs and the 12 fold lanes (E, G[0..10])
-// read conflict-free; the stride also covers the zero padding of the folds to
-// a multiple of 8 terms.
-constexpr int kNarxArrays = 21;
+// Training scratch: per-sample arrays of stride narx_train_stride(len)
+// doubles -- a multiple of 16 plus one, so the arrays start in distinct
+// shared-memory bank pairs and the 12 fold lanes (E, G[0..10]) read
+// conflict-free; the stride also covers the zero padding of the folds to a
+// multiple of 8 terms. Layout: Z[8], T, then one or two evaluation buffers
+// {E, G[11]} (the second one holds the speculative halved-step evaluation).
+constexpr int kNarxArraysMin = 21;   // Z[8], T, E, G[11]
+constexpr int kNarxArrays = 33;      // + a second {E, G[11]}
 __host__ __device__ __forceinline__ int narx_train_stride(int len) {
   const int cnt = len > 2 ? len - 2 : 1;
   return (cnt + 15) / 16 * 16 + 1;
 }
+// bytes for the full (two-buffer) layout; allocations are sized with this
 __host__ __device__ __forceinline__ size_t narx_train_scratch_bytes(int len) {
   return static_cast<size_t>(narx_train_stride(len)) * kNarxArrays * sizeof(double);
+}
+// bytes for the one-buffer layout (no speculative halving)
+__host__ __device__ __forceinline__ size_t narx_train_min_bytes(int len) {
+  return static_cast<size_t>(narx_train_stride(len)) * kNarxArraysMin * sizeof(double);
+}
+
+// Training scratch for one call: shared memory when at least the one-buffer
+// layout fits there, else the caller's global slot (sized for the full layout).
+__device__ __forceinline__ double* narx_train_buf(int L, double* smem, size_t smem_bytes,
+                                                  double* gslot, size_t gslot_doubles,
+                                                  size_t* doubles) {
+  if (narx_train_min_bytes(L) <= smem_bytes) {
+    *doubles = smem_bytes / sizeof(double);
+    return smem;
+  }
+  *doubles = gslot_doubles;
+  return gslot;
 }
 
 struct NarxTrainSmem {
@@ -107,21 +127,14 @@ struct NarxTrainSmem {
   int stall, epochs, stop;
 };
 
-// One evaluation of the training objective at weights wt, fused with the
-// gradient at wt (predictor.cpp:102-134). Per-sample terms are computed in
-// parallel: the squared error E_i (mse, :104-107) and the 11 gradient terms
-// G_k,i (loss_gradient, :121-132: dz*z_k, dz, dy*h, dy -- each the same single
-// product the reference forms). Then lanes 0..11 of warp 1 fold E and G_0..10
-// left to right, one array per lane, 8 terms ahead in registers so only the
-// dependent DADD chain is exposed (the folds are zero padded to a multiple of
-// 8; adding +0.0 to a sum that starts at +0.0 is the identity). The gradient is
-// speculative: it is exactly the next epoch's loss_gradient(model) whenever
-// the trial is accepted (same weights, same per-sample operations, same
-// order), and is discarded otherwise.
-__device__ inline double block_eval(const double* wt, const double* Z, const double* T, double* E,
-                                    double* G, int S, int cnt, double scale, double* gout,
-                                    NarxTrainSmem* s) {
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+// Per-sample pass of one evaluation (predictor.cpp:102-134) over samples
+// first, first + stride, ...: the squared error E_i (mse, :104-107) and the 11
+// gradient terms G_k,i (loss_gradient, :121-132: dz*z_k, dz, dy*h, dy -- each
+// the same single product the reference forms).
+__device__ __forceinline__ void narx_eval_terms(const double* wt, const double* Z, const double* T,
+                                                double* E, double* G, int S, int cnt, double scale,
+                                                int first, int stride) {
+  for (int i = first; i < cnt; i += stride) {
     double z[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) z[j] = Z[static_cast<size_t>(j) * S + i];
@@ -140,7 +153,27 @@ __device__ inline double block_eval(const double* wt, const double* Z, const dou
     G[static_cast<size_t>(9) * S + i] = dmul(dy, h);
     G[static_cast<size_t>(10) * S + i] = dy;
   }
-  __syncthreads();
+}
+
+// One evaluation of the training objective fused with the gradient. If fwd_w
+// is given, all threads first form the per-sample terms of fwd_w in buffer
+// (E, G); otherwise they are already there (a speculative pass). Then lanes
+// 0..11 of warp 1 fold E and G_0..10 left to right, one array per lane, 8 terms
+// ahead in registers so only the dependent DADD chain is exposed (the folds are
+// zero padded to a multiple of 8; adding +0.0 to a sum that starts at +0.0 is
+// the identity). Meanwhile, if spec_step > 0, every other thread forms the
+// terms of the halved trial w - spec_step * g in (Es, Gs): it is exactly the
+// next evaluation whenever this trial is rejected (apply_step :136-143 with
+// the halved step, same operations), and is discarded otherwise. The gradient
+// folded here is likewise the next epoch's loss_gradient(model) whenever the
+// trial is accepted.
+__device__ inline double block_eval(const double* fwd_w, const double* Z, const double* T,
+                                    double* E, double* G, double* Es, double* Gs, int S, int cnt,
+                                    double scale, double spec_step, double* gout, NarxTrainSmem* s) {
+  if (fwd_w) {
+    narx_eval_terms(fwd_w, Z, T, E, G, S, cnt, scale, threadIdx.x, blockDim.x);
+    __syncthreads();
+  }
   if (threadIdx.x >= 32 && threadIdx.x < 44) {
     const int k = threadIdx.x - 32;
     const double* src = k < 11 ? G + static_cast<size_t>(k) * S : E;
@@ -161,19 +194,27 @@ __device__ inline double block_eval(const double* wt, const double* Z, const dou
     for (int q = 0; q < 8; ++q) acc = dadd(acc, cur[q]);
     if (k < 11) gout[k] = acc;
     else s->val = ddiv(acc, static_cast<double>(cnt));
+  } else if (spec_step > 0.0 && (threadIdx.x < 32 || threadIdx.x >= 64)) {
+    double sw[11];
+#pragma unroll
+    for (int t = 0; t < 11; ++t) sw[t] = dsub(s->w[t], dmul(spec_step, s->g[t]));
+    const int idx = threadIdx.x < 32 ? threadIdx.x : threadIdx.x - 32;
+    narx_eval_terms(sw, Z, T, Es, Gs, S, cnt, scale, idx, blockDim.x - 32);
   }
   __syncthreads();
   return s->val;
 }
 
 // narx_train_online (predictor.cpp:155-196) for one model with history
-// (v, c, m)[0..L). buf: 13*(L-2) doubles (shared or global). Bit-exact: every
+// (v, c, m)[0..L). buf: buf_doubles doubles of scratch (shared or global), at
+// least narx_train_min_bytes(L); with narx_train_scratch_bytes(L) the halved
+// trial step is evaluated speculatively beside each fold. Bit-exact: every
 // value the reference computes is computed with the same operations in the
 // same order; only independent work is overlapped.
 __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, const double* c,
                                         const double* m, int L, const lbbsp_narx_train_cfg cfg,
                                         lbbsp_narx_report* rep, double* loss_log, int loss_cap,
-                                        double* buf, NarxTrainSmem* s) {
+                                        double* buf, size_t buf_doubles, NarxTrainSmem* s) {
   const int tid = threadIdx.x;
   const int minh = cfg.min_history > 3 ? cfg.min_history : 3;
   if (L < minh) {
@@ -207,13 +248,13 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
   const int S = narx_train_stride(L);
   double* Z = buf;                             // [8][S]
   double* T = Z + static_cast<size_t>(8) * S;  // [S]
-  double* E = T + S;                           // [S]
-  double* G = E + S;                           // [11][S]
+  double* EG[2] = {T + S, T + 13 * static_cast<size_t>(S)};  // {E [S], G [11][S]} x 2
+  const bool spec = buf_doubles >= static_cast<size_t>(kNarxArrays) * S &&
+                    cnt <= static_cast<int>(blockDim.x) - 32;
   // zero padding of the folds (never written by the evaluations)
-  for (int i = cnt + tid; i < (cnt + 7) / 8 * 8; i += blockDim.x) {
-    E[i] = 0.0;
-    for (int k = 0; k < 11; ++k) G[static_cast<size_t>(k) * S + i] = 0.0;
-  }
+  for (int i = cnt + tid; i < (cnt + 7) / 8 * 8; i += blockDim.x)
+    for (int b = 0; b < (spec ? 2 : 1); ++b)
+      for (int k = 0; k < 12; ++k) EG[b][static_cast<size_t>(k) * S + i] = 0.0;
   const double mv = s->sc[0], sv = s->sc[1], mc = s->sc[2], scd = s->sc[3], mm = s->sc[4],
                sm = s->sc[5];
   // build_training_set (predictor.cpp:89-100)
@@ -231,19 +272,31 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
   }
   __syncthreads();
   const double scale = ddiv(2.0, static_cast<double>(cnt));
+  auto E_ = [&](int b) { return EG[b]; };
+  auto G_ = [&](int b) { return EG[b] + S; };
   // current = mse(model) (:165), and loss_gradient(model) of epoch 0
-  double current = block_eval(s->w, Z, T, E, G, S, cnt, scale, s->g, s);
+  double current = block_eval(s->w, Z, T, E_(0), G_(0), nullptr, nullptr, S, cnt, scale, 0.0,
+                              s->g, s);
   for (int epoch = 0; epoch < cfg.max_epochs; ++epoch) {
     double step = cfg.step;
     if (tid < 11) s->trial[tid] = dsub(s->w[tid], dmul(step, s->g[tid]));  // apply_step :136-143
     __syncthreads();
-    double next = block_eval(s->trial, Z, T, E, G, S, cnt, scale, s->gs, s);
+    int b = 0;
+    double next = block_eval(s->trial, Z, T, E_(b), G_(b), E_(1), G_(1), S, cnt, scale,
+                             spec ? dmul(step, 0.5) : 0.0, s->gs, s);
     int halvings = 0;
     while (next > current && halvings < 20) {
       step = dmul(step, 0.5);
       if (tid < 11) s->trial[tid] = dsub(s->w[tid], dmul(step, s->g[tid]));
       __syncthreads();
-      next = block_eval(s->trial, Z, T, E, G, S, cnt, scale, s->gs, s);
+      if (spec) {  // this trial's terms were formed beside the previous fold
+        b ^= 1;
+        next = block_eval(nullptr, Z, T, E_(b), G_(b), E_(b ^ 1), G_(b ^ 1), S, cnt, scale,
+                          dmul(step, 0.5), s->gs, s);
+      } else {
+        next = block_eval(s->trial, Z, T, E_(0), G_(0), nullptr, nullptr, S, cnt, scale, 0.0,
+                          s->gs, s);
+      }
       ++halvings;
     }
     if (next > current) break;  // no descent direction left (:182)

@@ -516,7 +516,8 @@ static cudaError_t launch_softmax_ce(int sms, cudaStream_t s, bool pdl, Groups G
 // rows for 2048 columns (8 per thread, 16-B loads) into its own scratch row;
 // the worker's last CTA adds the row blocks in order.
 constexpr int kBiasCols = 2048;
-constexpr int kBiasMaxRowBlocks = 32;
+constexpr int kBiasMaxRowBlocks = 64;
+constexpr int kBiasRowsInFlight = 16;  // 16 x 16 B per thread: 64 KB in flight per CTA
 __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __restrict__ dZ, int N,
                                                         float* slab, long long slab_stride,
                                                         long long off_b, float* scratch,
@@ -539,12 +540,13 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
   if (col < N) {
     int r = ra;
 #pragma unroll 1
-    for (; r + 8 <= rz; r += 8) {  // eight rows in flight
-      uint4 q[8];
+    for (; r + kBiasRowsInFlight <= rz; r += kBiasRowsInFlight) {
+      uint4 q[kBiasRowsInFlight];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) q[u] = *reinterpret_cast<const uint4*>(dZ + static_cast<long long>(r + u) * N + col);
+      for (int u = 0; u < kBiasRowsInFlight; ++u)
+        q[u] = *reinterpret_cast<const uint4*>(dZ + static_cast<long long>(r + u) * N + col);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kBiasRowsInFlight; ++u) {
         const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q[u]);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -580,21 +582,23 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
     // added in row-block order
     for (int c4 = threadIdx.x; c4 < N / 4; c4 += blockDim.x) {
       const int c = 4 * c4, b = c / kBiasCols, o = c % kBiasCols;
-      float4 t[kBiasMaxRowBlocks];
-#pragma unroll
-      for (int q = 0; q < kBiasMaxRowBlocks; ++q)
-        if (q < rbs)
-          t[q] = __ldcg(reinterpret_cast<const float4*>(
-              &scratch[static_cast<long long>(c0 + q * ncb + b) * kBiasCols + o]));
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q0 = 0; q0 < rbs; q0 += 16) {  // 16 partials in flight, added in row-block order
+        float4 t[16];
 #pragma unroll
-      for (int q = 0; q < kBiasMaxRowBlocks; ++q)
-        if (q < rbs) {
-          v.x += t[q].x;
-          v.y += t[q].y;
-          v.z += t[q].z;
-          v.w += t[q].w;
-        }
+        for (int q = 0; q < 16; ++q)
+          if (q0 + q < rbs)
+            t[q] = __ldcg(reinterpret_cast<const float4*>(
+                &scratch[static_cast<long long>(c0 + (q0 + q) * ncb + b) * kBiasCols + o]));
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (q0 + q < rbs) {
+            v.x += t[q].x;
+            v.y += t[q].y;
+            v.z += t[q].z;
+            v.w += t[q].w;
+          }
+      }
       if (out_b16) {
         __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(out_b16 + c);
         o[0] = __floats2bfloat162_rn(v.x, v.y);

@@ -171,10 +171,25 @@ struct PlanDev {
   double* rec_loss;
   lbbsp_dev_status* status;
   unsigned long long* stamps;  // [16] globaltimer at kernel boundaries (last round)
+  unsigned* gather_done;       // single rank: CTAs of the beside-the-plan gather that finished
+  int gather_ctas;             // > 0: the plan completes only once they all have
 };
 
 __device__ __forceinline__ void stamp(const PlanDev& D, int i) {
   if (threadIdx.x == 0 && blockIdx.x == 0) D.stamps[i] = gtimer();
+}
+
+// Single rank: the gather of the whole batch runs beside the plan; the plan
+// completes only once every gather CTA has, so the forward GEMM depends on the
+// plan alone and keeps its programmatic (overlapped) launch.
+__device__ __forceinline__ void wait_gather(const PlanDev& D) {
+  if (D.gather_ctas > 0 && threadIdx.x == 0) {
+    unsigned seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(D.gather_done) : "memory");
+    } while (seen < static_cast<unsigned>(D.gather_ctas));
+    *D.gather_done = 0u;
+  }
 }
 
 // P1-P4: trace -> caps, predictor -> v_pred, solver -> sizes, local slice,
@@ -225,7 +240,10 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
       sz[i] = D.B_total / n + (i < D.B_total % n ? 1 : 0);  // equal_split
   }
   __syncthreads();
-  if (code) return;
+  if (code) {
+    wait_gather(D);
+    return;
+  }
   const int first = D.rank * D.n_local;
   if (tid == 0) {
     int off = 0;
@@ -284,6 +302,7 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
     for (int i = tid; i < D.n_local; i += blockDim.x)
       D.rec_caps[static_cast<size_t>(row) * n + D.rank * D.n_local + i] = D.ctan[i];
   }
+  wait_gather(D);
   stamp(D, 1);
 }
 
@@ -330,6 +349,13 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
       if (dsti[u] >= 0) dst4[dsti[u]] = v[u];
   }
   for (int r = blockIdx.x * 256 + threadIdx.x; r < rows; r += 256 * gridDim.x) y[r] = data_y[idx[r]];
+  if (fixed_rows > 0 && D.gather_ctas > 0) {  // tell the plan (see plan_kernel)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(D.gather_done, 1u);
+    }
+  }
 }
 
 __device__ __forceinline__ void phase_begin(unsigned long long* timing, int g) {
@@ -1107,6 +1133,9 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   int nl = 0, ph = 0;
   const int sms = D.sm_budget;
   const int gather_ctas = std::max(sms, std::min(sms * 8, (B_cap * (dims[0] / 8) + 1023) / 1024));
+  // single rank: the plan waits for the gather on the device (no graph join);
+  // set before either kernel is captured, both read it
+  D.gather_ctas = cfg.world == 1 ? gather_ctas : 0;
   if (cfg.world == 1) {  // one rank gathers all B rows: independent of the plan
     LBBSP_CUDA_CHECK(cudaEventRecord(ev_gather0, s));
     LBBSP_CUDA_CHECK(cudaStreamWaitEvent(side, ev_gather0, 0));
@@ -1114,7 +1143,6 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
                                                  B_total, partial, P, reg_off, reg_len, n_reg);
     LBBSP_CUDA_CHECK(cudaEventRecord(ev_gather1, side));
     plan_kernel<<<1, 256, 0, s>>>(D, row_scale);
-    LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_gather1, 0));
   } else {
     plan_kernel<<<1, 256, 0, s>>>(D, row_scale);
     gather_kernel<<<gather_ctas, 256, 0, s>>>(D, streams, B_total, data_x, data_y, dims[0], X, y, 0,
@@ -1508,6 +1536,11 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(m.alloc(&m.stage_y, static_cast<size_t>(m.N_data)));
   LBBSP_CUDA_CHECK(m.alloc(&m.result, static_cast<size_t>(m.n_total) + 2));
   LBBSP_CUDA_CHECK(m.alloc(&m.arrive, 1));
+  {
+    unsigned* gd = nullptr;
+    LBBSP_CUDA_CHECK(m.alloc(&gd, 1));
+    m.D.gather_done = gd;
+  }
   LBBSP_CUDA_CHECK(m.alloc(&m.bias_part, static_cast<size_t>(num_sms()) * kBiasCols));
   LBBSP_CUDA_CHECK(m.alloc(&m.bias_cnt, static_cast<size_t>(m.n_local)));
   LBBSP_CUDA_CHECK(cudaFuncSetAttribute(observe_train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

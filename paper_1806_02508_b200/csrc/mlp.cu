@@ -208,6 +208,9 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
   stamp(D, 0);
   const long long k = *D.k;
   const int len = min(*D.pred.len, D.pred.max_hist);
+  // scalars needed later, loaded now beside k (no dependent round trips later)
+  const int rows_now = *D.rows;
+  const double loss_prev = tid == 0 && D.loss_on ? *D.loss_acc : 0.0;
   if (tid == 0) *D.round_k = k;
   if (k >= D.max_rows && tid == 0)
     set_status(D.status, LBBSP_RUNTIME, LBBSP_E_MLP_CAPACITY, k, D.max_rows);
@@ -267,9 +270,9 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
     r0_s[D.n_local] = r;
     *D.local_rows = r;
     // the previous round's full-dataset loss (computed beside its observe branch)
-    const int prev = *D.rows - 1;
+    const int prev = rows_now - 1;
     if (prev >= 0 && prev < D.max_rows)
-      D.rec_loss[prev] = D.loss_on ? *D.loss_acc / static_cast<double>(D.N_data) : -1.0;
+      D.rec_loss[prev] = D.loss_on ? loss_prev / static_cast<double>(D.N_data) : -1.0;
     *D.loss_acc = 0.0;
   }
   for (int i = tid; i < kMaxPhases * D.n_local; i += blockDim.x) {
@@ -293,7 +296,7 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
       for (int r = r0_s[g] + tid; r < r0_s[g + 1]; r += blockDim.x) row_scale[r] = s;
     }
   }
-  const int row = *D.rows;
+  const int row = rows_now;
   if (row < D.max_rows) {
     for (int i = tid; i < n; i += blockDim.x) {
       D.rec_sizes[static_cast<size_t>(row) * n + i] = sz[i];

@@ -324,6 +324,10 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
       for (long long i = blockIdx.x * 256ll + threadIdx.x; i < reg_len[rg]; i += 256ll * gridDim.x)
         p[i] = 0.f;
     }
+  // several ranks: the slice offset and length come from the plan (programmatic
+  // launch: the zeroing above overlaps the plan)
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
   const long long k = min(*D.k, static_cast<long long>(D.max_rows - 1));  // capacity-guarded
   const int rows = fixed_rows > 0 ? fixed_rows : *D.local_rows;
   const int off = fixed_rows > 0 ? 0 : *D.stream_off;
@@ -906,6 +910,8 @@ __device__ bool wait_counters(const PeerDev& X, int which, unsigned long long wa
 
 // measured speeds of the local workers -> every rank's v_obs_all
 __global__ void peer_speed_kernel(PlanDev D, PeerDev X, int n_phases) {
+  tc::pdl_wait();  // the phase stamps of the backward GEMMs
+  tc::pdl_launch_dependents();
   const int tid = threadIdx.x;
   for (int i = tid; i < D.n_local; i += blockDim.x) {
     double t;
@@ -1148,8 +1154,12 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     plan_kernel<<<1, 256, 0, s>>>(D, row_scale);
   } else {
     plan_kernel<<<1, 256, 0, s>>>(D, row_scale);
-    gather_kernel<<<gather_ctas, 256, 0, s>>>(D, streams, B_total, data_x, data_y, dims[0], X, y, 0,
-                                              partial, P, reg_off, reg_len, n_reg);
+    LBBSP_CUDA_CHECK(launch_maybe_pdl(gather_kernel, gather_ctas, 256, 0, s, use_pdl, D,
+                                      static_cast<const int*>(streams), B_total,
+                                      static_cast<const bf16*>(data_x),
+                                      static_cast<const int*>(data_y), dims[0], X, y, 0, partial, P,
+                                      static_cast<const long long*>(reg_off),
+                                      static_cast<const long long*>(reg_len), n_reg));
   }
   nl += 2;
   if (use_pair) {
@@ -1233,11 +1243,11 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     }
   }
   n_phases = ph;
-  if (small_head) LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_head1, 0));
   // measured speeds; on several GPUs all-gathered (after the gradient buckets)
   const float lr = static_cast<float>(cfg.learning_rate);
   if (cfg.world > 1 && peers && !bucketed) {
-    peer_speed_kernel<<<1, 256, 0, s>>>(D, px, n_phases);  // speeds, all-gathered over NVLink
+    // speeds, all-gathered over NVLink
+    LBBSP_CUDA_CHECK(launch_maybe_pdl(peer_speed_kernel, 1, 256, 0, s, use_pdl, D, px, n_phases));
     ++nl;
   } else if (cfg.world > 1) {
     speed_kernel<<<1, 32 * ((n_local + 31) / 32), 0, s>>>(D, n_phases);
@@ -1286,6 +1296,8 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     }
   }
   // ---- aggregate + apply (the bucketed path applied per layer above) ----
+  // the small head's CTA partials were combined on the side stream
+  if (small_head) LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_head1, 0));
   if (bucketed) {
   } else if (cfg.world > 1 && peers) {
     // one-shot all-reduce over NVLink peer memory, summed in rank order

@@ -184,9 +184,14 @@ __device__ __forceinline__ void stamp(const PlanDev& D, int i) {
 // plan alone and keeps its programmatic (overlapped) launch.
 __device__ __forceinline__ void wait_gather(const PlanDev& D) {
   if (D.gather_ctas > 0 && threadIdx.x == 0) {
+    const unsigned long long t0 = gtimer();
     unsigned seen;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(D.gather_done) : "memory");
+      if (gtimer() - t0 > 2000000000ull) {  // 2 s: the gather never ran -- fail, do not hang
+        set_status(D.status, LBBSP_RUNTIME, 0, seen, D.gather_ctas);
+        break;
+      }
     } while (seen < static_cast<unsigned>(D.gather_ctas));
     *D.gather_done = 0u;
   }

@@ -147,7 +147,7 @@ def reference_arm(args):
                                          max(args.steps, 20), 30.0)
     value = BATCH_PER_GPU / t_round
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
-            "steps": done, "warmup": WARMUP_NARX, "ms_per_step": t_round * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_round * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": "C2: MLP 784-256-10, 8 workers, global batch 4096, "
@@ -473,9 +473,11 @@ def main():
     n_total = WORKERS_PER_GPU * world
     B = BATCH_PER_GPU * world
     e2e_steps = args.steps
-    # the timed rounds are steady-state LB-BSP + NARX rounds: at least the
-    # predictor warm-up (50 rounds, EMA before it) plus 10 rounds precede them
-    warm = max(args.warmup, WARMUP_NARX + 10)
+    # the timed rounds are steady-state LB-BSP + NARX rounds: they begin 50
+    # rounds after the predictor warm-up (50 rounds, EMA before it), when every
+    # model has been trained ~25 times by the rotation -- the predictor's steady
+    # state rather than its cold start (the same window for every arm)
+    warm = max(args.warmup, WARMUP_NARX + 50)
     iters = warm + args.steps + 8
     trace = benchmark_trace(n_total, iters, seed=TRACE_SEED)
 

@@ -544,10 +544,15 @@ def main():
     # both numbers see the same predictor / straggler history
     eng = make("lb-bsp", trace)
     x_host, y_host = eng.dataset()
-    xb = torch.from_numpy(x_host).to(torch.bfloat16).pin_memory()
-    yb = torch.from_numpy(y_host.astype(np.int32)).pin_memory()
-    out_sizes = torch.zeros(n_total, dtype=torch.int32).pin_memory()
-    out_loss = torch.zeros(1, dtype=torch.float64).pin_memory()
+    # page-locked host buffers allocated as such (torch.empty(pin_memory=True));
+    # on this pool they upload ~3x faster than tensor.pin_memory() copies
+    # (1.57 MB: 32 us vs 91 us, scripts/h2d_probe.py)
+    xb = torch.empty(x_host.shape, dtype=torch.bfloat16, pin_memory=True)
+    xb.copy_(torch.from_numpy(x_host).to(torch.bfloat16))
+    yb = torch.empty(y_host.shape, dtype=torch.int32, pin_memory=True)
+    yb.copy_(torch.from_numpy(y_host.astype(np.int32)))
+    out_sizes = torch.zeros(n_total, dtype=torch.int32, pin_memory=True)
+    out_loss = torch.zeros(1, dtype=torch.float64, pin_memory=True)
     st = torch.cuda.ExternalStream(eng.stream)
     eng.run(warm)
     torch.cuda.synchronize()

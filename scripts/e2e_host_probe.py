@@ -11,9 +11,9 @@ for mode in ("run only", "e2e", "run only", "e2e", "load only", "read only"):
                     predictor=os.environ.get("PRED", "narx"), warmup_iterations=50,
                     max_iterations=400, trace=benchmark_trace(n, 400, seed=3), learning_rate=0.05)
     x, y = eng.dataset()
-    xb = torch.from_numpy(x).to(torch.bfloat16).pin_memory()
-    yb = torch.from_numpy(y.astype(np.int32)).pin_memory()
-    osz = torch.zeros(n, dtype=torch.int32).pin_memory(); ol = torch.zeros(1, dtype=torch.float64).pin_memory()
+    xb = torch.empty(x.shape, dtype=torch.bfloat16, pin_memory=True); xb.copy_(torch.from_numpy(x).to(torch.bfloat16))
+    yb = torch.empty(y.shape, dtype=torch.int32, pin_memory=True); yb.copy_(torch.from_numpy(y.astype(np.int32)))
+    osz = torch.zeros(n, dtype=torch.int32, pin_memory=True); ol = torch.zeros(1, dtype=torch.float64, pin_memory=True)
     st = torch.cuda.ExternalStream(eng.stream)
     eng.run(100); torch.cuda.synchronize()
     s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)

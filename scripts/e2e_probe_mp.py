@@ -20,9 +20,9 @@ if not os.environ.get("LBBSP_NO_PEERS"):
     dist.all_gather_object(hs, eng.peer_handle())
     eng.init_peers(hs)
 x, y = eng.dataset()
-xb = torch.from_numpy(x).to(torch.bfloat16).pin_memory()
-yb = torch.from_numpy(y.astype(np.int32)).pin_memory()
-osz = torch.zeros(n, dtype=torch.int32).pin_memory(); ol = torch.zeros(1, dtype=torch.float64).pin_memory()
+xb = torch.empty(x.shape, dtype=torch.bfloat16, pin_memory=True); xb.copy_(torch.from_numpy(x).to(torch.bfloat16))
+yb = torch.empty(y.shape, dtype=torch.int32, pin_memory=True); yb.copy_(torch.from_numpy(y.astype(np.int32)))
+osz = torch.zeros(n, dtype=torch.int32, pin_memory=True); ol = torch.zeros(1, dtype=torch.float64, pin_memory=True)
 st = torch.cuda.ExternalStream(eng.stream)
 eng.run(60)
 torch.cuda.synchronize(); dist.barrier()

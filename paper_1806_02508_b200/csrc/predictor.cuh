@@ -88,16 +88,16 @@ __device__ inline void observe_d(const PredDev& P, int w, int len, double v, dou
 }
 
 // Training scratch: per-sample arrays of stride narx_train_stride(len)
-// doubles -- a multiple of 16 plus one, so the arrays start in distinct
+// doubles -- a multiple of 16 plus 17 (= 1 mod 16), so the arrays start in distinct
 // shared-memory bank pairs and the 12 fold lanes (E, G[0..10]) read
 // conflict-free; the stride also covers the zero padding of the folds to a
-// multiple of 8 terms. Layout: Z[8], T, then one or two evaluation buffers
+// multiple of 16 terms and 16 doubles of prefetch slack. Layout: Z[8], T, then one or two evaluation buffers
 // {E, G[11]} (the second one holds the speculative halved-step evaluation).
 constexpr int kNarxArraysMin = 21;   // Z[8], T, E, G[11]
 constexpr int kNarxArrays = 33;      // + a second {E, G[11]}
 __host__ __device__ __forceinline__ int narx_train_stride(int len) {
   const int cnt = len > 2 ? len - 2 : 1;
-  return (cnt + 15) / 16 * 16 + 1;
+  return (cnt + 15) / 16 * 16 + 17;  // + 16 doubles of prefetch slack
 }
 // bytes for the full (two-buffer) layout; allocations are sized with this
 __host__ __device__ __forceinline__ size_t narx_train_scratch_bytes(int len) {
@@ -160,7 +160,7 @@ __device__ __forceinline__ void narx_eval_terms(const double* wt, const double* 
 // (E, G); otherwise they are already there (a speculative pass). Then lanes
 // 0..11 of warp 1 fold E and G_0..10 left to right, one array per lane, 8 terms
 // ahead in registers so only the dependent DADD chain is exposed (the folds are
-// zero padded to a multiple of 8; adding +0.0 to a sum that starts at +0.0 is
+// zero padded to a multiple of 16; adding +0.0 to a sum that starts at +0.0 is
 // the identity). Meanwhile, if spec_step > 0, every other thread forms the
 // terms of the halved trial w - spec_step * g in (Es, Gs): it is exactly the
 // next evaluation whenever this trial is rejected (apply_step :136-143 with
@@ -177,21 +177,22 @@ __device__ inline double block_eval(const double* fwd_w, const double* Z, const 
   if (threadIdx.x >= 32 && threadIdx.x < 44) {
     const int k = threadIdx.x - 32;
     const double* src = k < 11 ? G + static_cast<size_t>(k) * S : E;
-    const int n8 = (cnt + 7) / 8 * 8;
-    double acc = 0.0, cur[8];
+    // two 8-term register blocks alternate (no register moves); the block
+    // after the last one is read from the stride's slack and never added
+    const int n16 = (cnt + 15) / 16 * 16;
+    double acc = 0.0, a[8], b[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) cur[q] = src[q];
-    for (int i = 8; i < n8; i += 8) {
-      double nxt[8];
+    for (int q = 0; q < 8; ++q) a[q] = src[q];
+    for (int i = 0; i < n16; i += 16) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) nxt[q] = src[i + q];
+      for (int q = 0; q < 8; ++q) b[q] = src[i + 8 + q];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc = dadd(acc, cur[q]);
+      for (int q = 0; q < 8; ++q) acc = dadd(acc, a[q]);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+      for (int q = 0; q < 8; ++q) a[q] = src[i + 16 + q];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc = dadd(acc, b[q]);
     }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc = dadd(acc, cur[q]);
     if (k < 11) gout[k] = acc;
     else s->val = ddiv(acc, static_cast<double>(cnt));
   } else if (spec_step > 0.0 && (threadIdx.x < 32 || threadIdx.x >= 64)) {
@@ -252,7 +253,7 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
   const bool spec = buf_doubles >= static_cast<size_t>(kNarxArrays) * S &&
                     cnt <= static_cast<int>(blockDim.x) - 32;
   // zero padding of the folds (never written by the evaluations)
-  for (int i = cnt + tid; i < (cnt + 7) / 8 * 8; i += blockDim.x)
+  for (int i = cnt + tid; i < (cnt + 15) / 16 * 16; i += blockDim.x)
     for (int b = 0; b < (spec ? 2 : 1); ++b)
       for (int k = 0; k < 12; ++k) EG[b][static_cast<size_t>(k) * S + i] = 0.0;
   const double mv = s->sc[0], sv = s->sc[1], mc = s->sc[2], scd = s->sc[3], mm = s->sc[4],

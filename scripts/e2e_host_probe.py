@@ -6,7 +6,7 @@ import numpy as np
 import torch
 from paper_1806_02508_b200.mlp import MlpEngine, benchmark_trace
 n = 8
-for mode in ("run only", "e2e", "run only", "e2e", "load only", "read only"):
+for mode in ("run only", "e2e", "load only", "read only", "run only", "e2e", "load only", "read only"):
     eng = MlpEngine(dims=[784, 256, 10], global_batch=4096, n_workers_local=8,
                     predictor=os.environ.get("PRED", "narx"), warmup_iterations=50,
                     max_iterations=400, trace=benchmark_trace(n, 400, seed=3), learning_rate=0.05)

@@ -33,7 +33,7 @@ def rel(a, b):
 
 
 @pytest.mark.parametrize("dims,B,n", [([784, 256, 10], 4096, 8), ([512, 512, 512, 256], 1024, 4),
-                                    ([512, 512, 512, 256], 1000, 1)])
+                                    ([512, 512, 512, 256], 1000, 1), ([1024, 4096, 256], 512, 2)])
 def test_one_round_matches_restatement(orc, dims, B, n):
     """One round vs (a) the bf16-aware restatement (same rounding points:
     relative L2 error of each update <= 2e-3) and (b) the pure fp64

@@ -544,9 +544,7 @@ def main():
     # both numbers see the same predictor / straggler history
     eng = make("lb-bsp", trace)
     x_host, y_host = eng.dataset()
-    # page-locked host buffers allocated as such (torch.empty(pin_memory=True));
-    # on this pool they upload ~3x faster than tensor.pin_memory() copies
-    # (1.57 MB: 32 us vs 91 us, scripts/h2d_probe.py)
+    # page-locked host buffers (the upload overlaps the round in flight)
     xb = torch.empty(x_host.shape, dtype=torch.bfloat16, pin_memory=True)
     xb.copy_(torch.from_numpy(x_host).to(torch.bfloat16))
     yb = torch.empty(y_host.shape, dtype=torch.int32, pin_memory=True)

@@ -1018,12 +1018,9 @@ struct lbbsp_mlp {
   cudaEvent_t ev_gather0 = nullptr, ev_gather1 = nullptr;
   cudaEvent_t ev_head0 = nullptr, ev_head1 = nullptr;  // head partial combine beside the backward
   cudaStream_t copy_stream = nullptr;  // e2e input staging (lbbsp_mlp_load_data_async)
-  // two staging slots: an upload waits only for the refresh that consumed
-  // its slot two loads ago, so its latency jitter is absorbed
-  cudaEvent_t ev_staged[2] = {nullptr, nullptr}, ev_refreshed[2] = {nullptr, nullptr};
-  bf16* stage_x[2] = {nullptr, nullptr};
-  int* stage_y[2] = {nullptr, nullptr};
-  int stage_slot = 0;
+  cudaEvent_t ev_staged = nullptr, ev_refreshed = nullptr;
+  bf16* stage_x = nullptr;
+  int* stage_y = nullptr;
   cudaEvent_t ev_layer[LBBSP_MLP_MAX_LAYERS] = {};
   cudaStream_t comm_stream = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -1078,10 +1075,8 @@ struct lbbsp_mlp {
     if (side) cudaStreamDestroy(side);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_gather0) cudaEventDestroy(ev_gather0);
-    for (int i = 0; i < 2; ++i) {
-      if (ev_staged[i]) cudaEventDestroy(ev_staged[i]);
-      if (ev_refreshed[i]) cudaEventDestroy(ev_refreshed[i]);
-    }
+    if (ev_staged) cudaEventDestroy(ev_staged);
+    if (ev_refreshed) cudaEventDestroy(ev_refreshed);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ev_gather1) cudaEventDestroy(ev_gather1);
     if (ev_head0) cudaEventDestroy(ev_head0);
@@ -1555,12 +1550,10 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(m.alloc(&D.round_k, 1));
   // end-to-end plumbing (lbbsp_mlp_load_data_async / read_result_async)
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.copy_stream, cudaStreamNonBlocking));
-  for (int i = 0; i < 2; ++i) {
-    LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_staged[i], cudaEventDisableTiming));
-    LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_refreshed[i], cudaEventDisableTiming));
-    LBBSP_CUDA_CHECK(m.alloc(&m.stage_x[i], static_cast<size_t>(m.N_data) * c.dims[0]));
-    LBBSP_CUDA_CHECK(m.alloc(&m.stage_y[i], static_cast<size_t>(m.N_data)));
-  }
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_staged, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_refreshed, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(m.alloc(&m.stage_x, static_cast<size_t>(m.N_data) * c.dims[0]));
+  LBBSP_CUDA_CHECK(m.alloc(&m.stage_y, static_cast<size_t>(m.N_data)));
   LBBSP_CUDA_CHECK(m.alloc(&m.result, static_cast<size_t>(m.n_total) + 2));
   LBBSP_CUDA_CHECK(m.alloc(&m.arrive, 1));
   {
@@ -1873,18 +1866,16 @@ extern "C" int lbbsp_mlp_load_data_async(lbbsp_mlp* m, const void* h_x_bf16, con
   // staging buffers, copy stream and events are created with the engine (an
   // allocation here would synchronise the device inside the caller's loop)
   // staging is free once the previous refresh consumed it
-  const int sl = m->stage_slot;
-  m->stage_slot ^= 1;
-  LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->copy_stream, m->ev_refreshed[sl], 0));
-  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_x[sl], h_x_bf16, bx, cudaMemcpyHostToDevice, m->copy_stream));
-  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_y[sl], h_labels, by, cudaMemcpyHostToDevice, m->copy_stream));
-  LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_staged[sl], m->copy_stream));
-  LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->stream, m->ev_staged[sl], 0));
-  refresh_kernel<<<num_sms(), 256, 0, m->stream>>>(reinterpret_cast<const uint4*>(m->stage_x[sl]),
+  LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->copy_stream, m->ev_refreshed, 0));
+  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_x, h_x_bf16, bx, cudaMemcpyHostToDevice, m->copy_stream));
+  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_y, h_labels, by, cudaMemcpyHostToDevice, m->copy_stream));
+  LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_staged, m->copy_stream));
+  LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->stream, m->ev_staged, 0));
+  refresh_kernel<<<num_sms(), 256, 0, m->stream>>>(reinterpret_cast<const uint4*>(m->stage_x),
                                                   reinterpret_cast<uint4*>(m->data_x), bx / 16,
-                                                  m->stage_y[sl], m->data_y, m->N_data);
+                                                  m->stage_y, m->data_y, m->N_data);
   LBBSP_CUDA_CHECK(cudaGetLastError());
-  LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_refreshed[sl], m->stream));
+  LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_refreshed, m->stream));
   return LBBSP_OK;
 }
 

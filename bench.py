@@ -71,6 +71,22 @@ def comm_sm_budget(world):
     return 148 - k if k > 0 else 0
 
 
+def connect(eng, world, rank):
+    """NCCL communicator (speed all-gather, fallback all-reduce) plus the NVLink
+    peer-memory exchange (CUDA IPC): several workers per GPU use it for speeds
+    and gradients; one worker per GPU for the copy-engine gradient buckets.
+    LBBSP_NO_PEERS=1 keeps NCCL only."""
+    import torch.distributed as dist
+    uid = [eng.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    with stdout_to_stderr():
+        eng.init_comm(uid[0])
+    if not os.environ.get("LBBSP_NO_PEERS"):
+        hs = [None] * world
+        dist.all_gather_object(hs, eng.peer_handle())
+        eng.init_peers(hs)
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -283,10 +299,7 @@ def main_c3(args):
                         max_iterations=iters, trace=constant_trace(world, iters, av),
                         sm_budget=comm_sm_budget(world))
         if world > 1:
-            uid = [MlpEngine.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(uid, src=0)
-            with stdout_to_stderr():
-                eng.init_comm(uid[0])
+            connect(eng, world, rank)
         return eng
 
     def timed(eng):
@@ -395,10 +408,7 @@ def main_c5(args):
                         learning_rate=0.01, seed=1, max_iterations=iters, trace=trace,
                         static_sizes=static_sizes, sm_budget=comm_sm_budget(world))
         if world > 1:
-            uid = [MlpEngine.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(uid, src=0)
-            with stdout_to_stderr():
-                eng.init_comm(uid[0])
+            connect(eng, world, rank)
         return eng
 
     out = {}
@@ -487,14 +497,7 @@ def main():
                         warmup_iterations=WARMUP_NARX, learning_rate=0.05, seed=1,
                         max_iterations=iters + 4, trace=tr)
         if world > 1:
-            uid = [MlpEngine.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(uid, src=0)
-            with stdout_to_stderr():
-                eng.init_comm(uid[0])
-            if not os.environ.get("LBBSP_NO_PEERS"):  # NVLink peer exchange (speeds, gradients)
-                hs = [None] * world
-                dist.all_gather_object(hs, eng.peer_handle())
-                eng.init_peers(hs)
+            connect(eng, world, rank)
         return eng
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2 (126 MB)

@@ -994,6 +994,74 @@ __global__ void __launch_bounds__(256) peer_grad_apply_kernel(long long P, float
   }
 }
 
+// ---------------------------------------------------------------------------
+// One worker per GPU (C3, C5): copy-engine bucket exchange. Each layer's bf16
+// gradient bucket is pushed into slot[rank] of every peer's buffer by
+// cudaMemcpyAsync (the copy engines move it over NVLink without SMs, so the
+// transfer overlaps the persistent backward GEMMs); a one-warp kernel then
+// bumps the bucket's arrival counter in each peer. The receiver waits on the
+// counters with one CTA and the apply kernel sums the slots in rank order
+// (fp32, identical on every rank) and updates the weights.
+// Counter layout: cnt[(2 + l) * kMaxPeers + writer], target = round + 1.
+// ---------------------------------------------------------------------------
+__global__ void peer_bucket_signal_kernel(PeerDev X, int l) {
+  __threadfence_system();  // the copies before this kernel are complete in stream order
+  const int r = threadIdx.x;
+  if (r < X.world && r != X.rank) atomicAdd_system(&X.cnt_peer[r][(2 + l) * kMaxPeers + X.rank], 1ull);
+}
+
+__global__ void peer_bucket_wait_kernel(PeerDev X, int l, const long long* round_k,
+                                        lbbsp_dev_status* st) {
+  const unsigned long long want = static_cast<unsigned long long>(*round_k) + 1;
+  const unsigned long long t0 = gtimer();
+  const int r = threadIdx.x;
+  if (r < X.world && r != X.rank) {
+    while (ld_acquire_sys(&X.cnt_local[(2 + l) * kMaxPeers + r]) < want) {
+      if (gtimer() - t0 > 2000000000ull) {  // 2 s: a peer is gone -- fail, do not hang
+        set_status(st, LBBSP_NCCL, 2 + l, r, static_cast<long long>(want));
+        break;
+      }
+    }
+  }
+}
+
+// params[seg] -= lr * sum_r slot_r[seg] (own slot = the local bucket), + bf16 copy
+__global__ void __launch_bounds__(256) peer_bucket_apply_kernel(PeerDev X, long long seg0, long long n,
+                                                                long long P, const bf16* __restrict__ own,
+                                                                float* params, bf16* pb, float lr) {
+  const long long nv = n / 8;
+  const bf16* slots = reinterpret_cast<const bf16*>(X.grd_local);
+  for (long long v = blockIdx.x * 256ll + threadIdx.x; v < nv; v += 256ll * gridDim.x) {
+    float a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = 0.f;
+    for (int r = 0; r < X.world; ++r) {
+      const bf16* src = r == X.rank ? own + seg0 : slots + static_cast<long long>(r) * P + seg0;
+      const uint4 q = __ldcg(reinterpret_cast<const uint4*>(src) + v);
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(g2[j]);
+        a[2 * j] += f.x;
+        a[2 * j + 1] += f.y;
+      }
+    }
+    float4* p4 = reinterpret_cast<float4*>(params + seg0) + 2 * v;
+    float4 w0 = p4[0], w1 = p4[1];
+    w0.x -= lr * a[0]; w0.y -= lr * a[1]; w0.z -= lr * a[2]; w0.w -= lr * a[3];
+    w1.x -= lr * a[4]; w1.y -= lr * a[5]; w1.z -= lr * a[6]; w1.w -= lr * a[7];
+    p4[0] = w0;
+    p4[1] = w1;
+    uint4 o;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+    o2[0] = __floats2bfloat162_rn(w0.x, w0.y);
+    o2[1] = __floats2bfloat162_rn(w0.z, w0.w);
+    o2[2] = __floats2bfloat162_rn(w1.x, w1.y);
+    o2[3] = __floats2bfloat162_rn(w1.z, w1.w);
+    reinterpret_cast<uint4*>(pb + seg0)[v] = o;
+  }
+}
+
 }  // namespace mlp
 }  // namespace lbbsp
 
@@ -1023,12 +1091,16 @@ struct lbbsp_mlp {
   int* stage_y = nullptr;
   cudaEvent_t ev_layer[LBBSP_MLP_MAX_LAYERS] = {};
   cudaStream_t comm_stream = nullptr;
+  // copy-engine bucket exchange (one worker per GPU with peers, LBBSP_NCCL_BUCKETS unset)
+  cudaStream_t xfer_stream = nullptr;
+  cudaEvent_t ev_xfer = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   ncclComm_t comm = nullptr;
   // NVLink peer exchange (lbbsp_mlp_init_peers): replaces the NCCL calls of
   // the several-workers-per-GPU path when set
   bool peers = false;
+  bool ce_ok = false;  // copy-engine bucket exchange usable (bf16 buckets, 8-element aligned)
   PeerDev px{};
   void* peer_buf = nullptr;               // local IPC-exported buffer
   void* peer_map[kMaxPeers] = {};          // opened peer buffers
@@ -1084,6 +1156,8 @@ struct lbbsp_mlp {
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_speed) cudaEventDestroy(ev_speed);
     if (ev_comm) cudaEventDestroy(ev_comm);
+    if (ev_xfer) cudaEventDestroy(ev_xfer);
+    if (xfer_stream) cudaStreamDestroy(xfer_stream);
     for (auto& e : ev_layer)
       if (e) cudaEventDestroy(e);
     if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -1208,6 +1282,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   // backward pass (bucketed allreduce); the speed all-gather follows on the
   // same stream, so the communicator sees one fixed order on every rank.
   const bool bucketed = cfg.world > 1 && n_local == 1 && !small_head;
+  const bool ce_buckets = bucketed && peers && gradb && ce_ok;
   for (int l = Lg - 1; l >= 0; --l) {
     if (!(small_head && l == L - 2)) {  // the small head already summed this bias gradient
       bias_grad_kernel<<<sms, 256, 0, s>>>(G, dZ[l], dims[l + 1], partial, P, off_b[l], bias_part,
@@ -1224,7 +1299,23 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
       LBBSP_CUDA_CHECK(cudaStreamWaitEvent(comm_stream, ev_layer[l], 0));
       // apply this layer's update as soon as its bucket is reduced, beside
       // the rest of the backward pass
-      if (gradb) {
+      if (ce_buckets) {
+        // push this bucket into slot[rank] of every peer (copy engines), then
+        // raise the peers' arrival counters; wait for the peers' buckets and
+        // apply the rank-ordered sum on the comm stream
+        LBBSP_CUDA_CHECK(cudaStreamWaitEvent(xfer_stream, ev_layer[l], 0));
+        const size_t bytes = sizeof(bf16) * static_cast<size_t>(seg1 - seg0);
+        for (int r = 0; r < cfg.world; ++r) {
+          if (r == cfg.rank) continue;
+          bf16* dst = reinterpret_cast<bf16*>(px.grd_peer[r]) + static_cast<long long>(cfg.rank) * P + seg0;
+          LBBSP_CUDA_CHECK(cudaMemcpyAsync(dst, gradb + seg0, bytes, cudaMemcpyDeviceToDevice, xfer_stream));
+        }
+        peer_bucket_signal_kernel<<<1, 32, 0, xfer_stream>>>(px, l);
+        peer_bucket_wait_kernel<<<1, 32, 0, comm_stream>>>(px, l, D.round_k, D.status);
+        peer_bucket_apply_kernel<<<sms * 2, 256, 0, comm_stream>>>(
+            px, seg0, seg1 - seg0, P, gradb, params, pb, static_cast<float>(cfg.learning_rate));
+        nl += 2;
+      } else if (gradb) {
         if (nccl_api()->AllReduce(gradb + seg0, gradb + seg0, static_cast<size_t>(seg1 - seg0),
                                   ncclBfloat16, ncclSum, comm, comm_stream) != ncclSuccess)
           return set_error(LBBSP_NCCL, "ncclAllReduce (bucket %d) failed", l);
@@ -1265,6 +1356,10 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
         return set_error(LBBSP_NCCL, "ncclAllGather failed");
       LBBSP_CUDA_CHECK(cudaEventRecord(ev_comm, comm_stream));
       LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_comm, 0));
+      if (ce_buckets) {  // the local buckets must not be overwritten before they left
+        LBBSP_CUDA_CHECK(cudaEventRecord(ev_xfer, xfer_stream));
+        LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_xfer, 0));
+      }
     } else {
       // speeds first: the observe / NARX branch (the usual critical tail)
       // forks right after this small all-gather; the gradient all-reduce
@@ -1415,6 +1510,8 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_comm, cudaEventDisableTiming));
   for (auto& e : m.ev_layer) LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.comm_stream, cudaStreamNonBlocking));
+  LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.xfer_stream, cudaStreamNonBlocking));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_xfer, cudaEventDisableTiming));
 
   // flat parameter layout, 64-element aligned segments
   auto pad = [](long long x) { return (x + 63) / 64 * 64; };
@@ -1722,7 +1819,8 @@ extern "C" int lbbsp_mlp_peer_handle(lbbsp_mlp* m, unsigned char h_handle[64]) {
     return set_error(LBBSP_INVALID_ARGUMENT, "mlp: peer exchange supports at most %d GPUs", kMaxPeers);
   if (!m->peer_buf) {
     const int W = m->cfg.world;
-    m->peer_off_spd = 256;
+    // counters: [2 + LBBSP_MLP_MAX_LAYERS][kMaxPeers] (speeds, gradients, per-bucket arrivals)
+    m->peer_off_spd = (sizeof(unsigned long long) * kMaxPeers * (2 + LBBSP_MLP_MAX_LAYERS) + 255) / 256 * 256;
     m->peer_off_grd = (m->peer_off_spd + sizeof(double) * W * m->n_local + 255) / 256 * 256;
     const size_t bytes = m->peer_off_grd + sizeof(float) * W * static_cast<size_t>(m->P);
     LBBSP_CUDA_CHECK(cudaMalloc(&m->peer_buf, bytes));
@@ -1759,6 +1857,13 @@ extern "C" int lbbsp_mlp_init_peers(lbbsp_mlp* m, const unsigned char* h_handles
   X.spd_local = reinterpret_cast<double*>(lb + m->peer_off_spd);
   X.grd_local = reinterpret_cast<float*>(lb + m->peer_off_grd);
   m->peers = true;
+  // copy-engine bucket exchange: each bucket (W_l | b_l) moves as whole uint4s
+  bool al = m->gradb != nullptr && m->P % 8 == 0 && !getenv("LBBSP_NCCL_BUCKETS");
+  for (int l = 0; al && l < m->L; ++l) {
+    const long long seg0 = m->off_w[l], seg1 = l + 1 < m->L ? m->off_w[l + 1] : m->P;
+    al = seg0 % 8 == 0 && (seg1 - seg0) % 8 == 0;
+  }
+  m->ce_ok = al;
   return LBBSP_OK;
 }
 

@@ -1,0 +1,54 @@
+"""Multi-GPU check (run with torchrun on >= 2 GPUs), one worker per GPU: the
+copy-engine bucket exchange (bf16 layer buckets pushed into the peers' IPC
+slots, rank-ordered fp32 sum + apply) gives the same parameters on every rank
+and matches the NCCL bf16 bucket all-reduce (LBBSP_NCCL_BUCKETS=1) within the
+bf16 rounding of the summed gradient, after several rounds with static sizes
+(the exchange step of the sharded path)."""
+import os, sys
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+import numpy as np
+import torch
+import torch.distributed as dist
+from paper_1806_02508_b200.mlp import MlpEngine, constant_trace
+
+world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
+torch.cuda.set_device(local)
+dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+dims = [1024, 1024, 1024, 1024]
+rounds = 12
+out = {}
+for mode in ("nccl", "ce"):
+    if mode == "nccl":
+        os.environ["LBBSP_NCCL_BUCKETS"] = "1"
+    else:
+        os.environ.pop("LBBSP_NCCL_BUCKETS", None)
+    sizes = [1024 + 256 * (i % 2) - 128 for i in range(world)]  # ragged per-GPU batches
+    eng = MlpEngine(dims=dims, global_batch=sum(sizes), n_workers_local=1, world=world, rank=rank,
+                    scheme="lb-bsp", predictor="ema", learning_rate=0.05, max_iterations=rounds + 4,
+                    trace=constant_trace(world, rounds + 4), static_sizes=sizes)
+    uid = [MlpEngine.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    eng.init_comm(uid[0])
+    hs = [None] * world
+    dist.all_gather_object(hs, eng.peer_handle())
+    eng.init_peers(hs)
+    eng.run(rounds)
+    torch.cuda.synchronize()
+    flat = np.concatenate([np.concatenate([w.ravel(), b]) for w, b in eng.params()])
+    out[mode] = (flat, eng.records()["loss"][:rounds])
+    del eng
+p0, l0 = out["nccl"]
+p1, l1 = out["ce"]
+# every rank holds bitwise the same parameters on the copy-engine path
+allp = [None] * world
+dist.all_gather_object(allp, p1)
+same = all(np.array_equal(allp[0], a) for a in allp)
+diff = float(np.max(np.abs(p0 - p1)))
+moved = float(np.max(np.abs(p0 - allp[0]))) if rank else 0.0
+ldiff = float(np.max(np.abs(l0 - l1) / np.maximum(1e-12, np.abs(l0))))
+print(f"rank {rank}: ranks bitwise equal {same}, max |params nccl - ce| = {diff:.3e} "
+      f"(max |p| {float(np.max(np.abs(p0))):.3e}), max rel loss diff {ldiff:.3e}", flush=True)
+assert same
+assert diff <= 2e-3 * max(1.0, float(np.max(np.abs(p0)))), diff  # bf16 rounding of the bucket sum
+assert ldiff <= 1e-2, ldiff
+dist.destroy_process_group()

@@ -1857,8 +1857,12 @@ extern "C" int lbbsp_mlp_init_peers(lbbsp_mlp* m, const unsigned char* h_handles
   X.spd_local = reinterpret_cast<double*>(lb + m->peer_off_spd);
   X.grd_local = reinterpret_cast<float*>(lb + m->peer_off_grd);
   m->peers = true;
-  // copy-engine bucket exchange: each bucket (W_l | b_l) moves as whole uint4s
-  bool al = m->gradb != nullptr && m->P % 8 == 0 && !getenv("LBBSP_NCCL_BUCKETS");
+  // copy-engine bucket exchange: each bucket (W_l | b_l) moves as whole uint4s.
+  // Default at 2 GPUs only: the one-shot push sends (N-1)*P*2 bytes per GPU,
+  // which at N=4 measured slower than NCCL's ring (2(N-1)/N*P*2 bytes; C3
+  // no-straggler round 1.74 vs 1.42 ms). LBBSP_CE_BUCKETS=1 forces it.
+  bool al = m->gradb != nullptr && m->P % 8 == 0 && !getenv("LBBSP_NCCL_BUCKETS") &&
+            (W == 2 || getenv("LBBSP_CE_BUCKETS"));
   for (int l = 0; al && l < m->L; ++l) {
     const long long seg0 = m->off_w[l], seg1 = l + 1 < m->L ? m->off_w[l + 1] : m->P;
     al = seg0 % 8 == 0 && (seg1 - seg0) % 8 == 0;

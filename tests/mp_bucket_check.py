@@ -17,6 +17,7 @@ dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cu
 dims = [1024, 1024, 1024, 1024]
 rounds = 12
 out = {}
+os.environ["LBBSP_CE_BUCKETS"] = "1"  # also at N > 2, where NCCL is the default
 for mode in ("nccl", "ce"):
     if mode == "nccl":
         os.environ["LBBSP_NCCL_BUCKETS"] = "1"

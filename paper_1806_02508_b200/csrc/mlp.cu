@@ -1062,6 +1062,63 @@ __global__ void __launch_bounds__(256) peer_bucket_apply_kernel(PeerDev X, long 
   }
 }
 
+// Two-shot variant (N > 2): slice j of a bucket goes only to rank j
+// (reduce-scatter by copy engine), rank j sums slice j over the ranks in rank
+// order in fp32 and rounds the sum to bf16 (as the NCCL bf16 all-reduce
+// does), the bf16 slice sums are copied into every rank's all-gather buffer,
+// and every rank applies the whole bucket from it: 2(N-1)/N*P*2 bytes per GPU,
+// the ring all-reduce's volume, instead of the one-shot (N-1)*P*2. The owner
+// applies the same rounded sum, so every rank holds bitwise equal weights.
+// Counters: reduce-scatter arrivals at row 2 + l, all-gather arrivals at row
+// 2 + LBBSP_MLP_MAX_LAYERS + l.
+__global__ void __launch_bounds__(256) peer_slice_reduce_kernel(PeerDev X, long long s0, long long n,
+                                                                long long P, const bf16* __restrict__ own,
+                                                                bf16* __restrict__ ag) {
+  const long long nv = n / 8;
+  const bf16* slots = reinterpret_cast<const bf16*>(X.grd_local);
+  for (long long v = blockIdx.x * 256ll + threadIdx.x; v < nv; v += 256ll * gridDim.x) {
+    float a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = 0.f;
+    for (int r = 0; r < X.world; ++r) {
+      const bf16* src = r == X.rank ? own + s0 : slots + static_cast<long long>(r) * P + s0;
+      const uint4 q = __ldcg(reinterpret_cast<const uint4*>(src) + v);
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(g2[j]);
+        a[2 * j] += f.x;
+        a[2 * j + 1] += f.y;
+      }
+    }
+    uint4 o;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o2[j] = __floats2bfloat162_rn(a[2 * j], a[2 * j + 1]);
+    reinterpret_cast<uint4*>(ag + s0)[v] = o;
+  }
+}
+
+__global__ void peer_signal_row_kernel(PeerDev X, int row) {
+  __threadfence_system();
+  const int r = threadIdx.x;
+  if (r < X.world && r != X.rank) atomicAdd_system(&X.cnt_peer[r][row * kMaxPeers + X.rank], 1ull);
+}
+
+__global__ void peer_wait_row_kernel(PeerDev X, int row, const long long* round_k, lbbsp_dev_status* st) {
+  const unsigned long long want = static_cast<unsigned long long>(*round_k) + 1;
+  const unsigned long long t0 = gtimer();
+  const int r = threadIdx.x;
+  if (r < X.world && r != X.rank) {
+    while (ld_acquire_sys(&X.cnt_local[row * kMaxPeers + r]) < want) {
+      if (gtimer() - t0 > 2000000000ull) {
+        set_status(st, LBBSP_NCCL, row, r, static_cast<long long>(want));
+        break;
+      }
+    }
+  }
+}
+
 }  // namespace mlp
 }  // namespace lbbsp
 
@@ -1094,6 +1151,22 @@ struct lbbsp_mlp {
   // copy-engine bucket exchange (one worker per GPU with peers, LBBSP_NCCL_BUCKETS unset)
   cudaStream_t xfer_stream = nullptr;
   cudaEvent_t ev_xfer = nullptr;
+  // one copy stream per peer (two-shot): the copies to different peers run concurrently
+  cudaStream_t peer_cs[kMaxPeers] = {};
+  cudaEvent_t ev_pc0 = nullptr, ev_pc[kMaxPeers] = {};
+  // copies (dst[r], src[r], bytes[r]) for every peer r != rank, issued after
+  // the work already on `from` and joined back into it
+  cudaError_t fan_copy(cudaStream_t from, void* const* dst, const void* const* src, const size_t* bytes) {
+    cudaError_t e = cudaEventRecord(ev_pc0, from);
+    for (int r = 0; e == cudaSuccess && r < cfg.world; ++r) {
+      if (r == cfg.rank) continue;
+      e = cudaStreamWaitEvent(peer_cs[r], ev_pc0, 0);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(dst[r], src[r], bytes[r], cudaMemcpyDeviceToDevice, peer_cs[r]);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_pc[r], peer_cs[r]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(from, ev_pc[r], 0);
+    }
+    return e;
+  }
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   ncclComm_t comm = nullptr;
@@ -1101,6 +1174,7 @@ struct lbbsp_mlp {
   // the several-workers-per-GPU path when set
   bool peers = false;
   bool ce_ok = false;  // copy-engine bucket exchange usable (bf16 buckets, 8-element aligned)
+  bool ce_two_shot = false;  // reduce-scatter + all-gather variant (N > 2)
   PeerDev px{};
   void* peer_buf = nullptr;               // local IPC-exported buffer
   void* peer_map[kMaxPeers] = {};          // opened peer buffers
@@ -1157,6 +1231,11 @@ struct lbbsp_mlp {
     if (ev_speed) cudaEventDestroy(ev_speed);
     if (ev_comm) cudaEventDestroy(ev_comm);
     if (ev_xfer) cudaEventDestroy(ev_xfer);
+    if (ev_pc0) cudaEventDestroy(ev_pc0);
+    for (int r = 0; r < kMaxPeers; ++r) {
+      if (ev_pc[r]) cudaEventDestroy(ev_pc[r]);
+      if (peer_cs[r]) cudaStreamDestroy(peer_cs[r]);
+    }
     if (xfer_stream) cudaStreamDestroy(xfer_stream);
     for (auto& e : ev_layer)
       if (e) cudaEventDestroy(e);
@@ -1299,7 +1378,39 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
       LBBSP_CUDA_CHECK(cudaStreamWaitEvent(comm_stream, ev_layer[l], 0));
       // apply this layer's update as soon as its bucket is reduced, beside
       // the rest of the backward pass
-      if (ce_buckets) {
+      if (ce_buckets && ce_two_shot) {
+        // reduce-scatter: slice r of this bucket -> slot[rank] of rank r
+        const long long n = seg1 - seg0, W = cfg.world;
+        auto sl0 = [&](long long r) { return seg0 + (n / 8 * r / W) * 8; };
+        LBBSP_CUDA_CHECK(cudaStreamWaitEvent(xfer_stream, ev_layer[l], 0));
+        void* dst[kMaxPeers];
+        const void* src[kMaxPeers];
+        size_t nb[kMaxPeers];
+        for (int r = 0; r < cfg.world; ++r) {
+          dst[r] = reinterpret_cast<bf16*>(px.grd_peer[r]) + static_cast<long long>(cfg.rank) * P + sl0(r);
+          src[r] = gradb + sl0(r);
+          nb[r] = sizeof(bf16) * (sl0(r + 1) - sl0(r));
+        }
+        LBBSP_CUDA_CHECK(fan_copy(xfer_stream, dst, src, nb));
+        peer_signal_row_kernel<<<1, 32, 0, xfer_stream>>>(px, 2 + l);
+        // own slice: rank-ordered fp32 sum -> all-gather buffer of every rank
+        const long long m0 = sl0(cfg.rank), m1 = sl0(cfg.rank + 1);
+        peer_wait_row_kernel<<<1, 32, 0, comm_stream>>>(px, 2 + l, D.round_k, D.status);
+        bf16* ag_local = reinterpret_cast<bf16*>(px.grd_local) + W * P;
+        peer_slice_reduce_kernel<<<sms, 256, 0, comm_stream>>>(px, m0, m1 - m0, P, gradb, ag_local);
+        for (int r = 0; r < cfg.world; ++r) {
+          dst[r] = reinterpret_cast<bf16*>(px.grd_peer[r]) + W * P + m0;
+          src[r] = ag_local + m0;
+          nb[r] = sizeof(bf16) * (m1 - m0);
+        }
+        LBBSP_CUDA_CHECK(fan_copy(comm_stream, dst, src, nb));
+        peer_signal_row_kernel<<<1, 32, 0, comm_stream>>>(px, 2 + LBBSP_MLP_MAX_LAYERS + l);
+        peer_wait_row_kernel<<<1, 32, 0, comm_stream>>>(px, 2 + LBBSP_MLP_MAX_LAYERS + l, D.round_k,
+                                                        D.status);
+        apply_bf16_kernel<<<sms * 2, 256, 0, comm_stream>>>(ag_local + seg0, n, params + seg0, pb + seg0,
+                                                            static_cast<float>(cfg.learning_rate));
+        nl += 5;
+      } else if (ce_buckets) {
         // push this bucket into slot[rank] of every peer (copy engines), then
         // raise the peers' arrival counters; wait for the peers' buckets and
         // apply the rank-ordered sum on the comm stream
@@ -1512,6 +1623,11 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.comm_stream, cudaStreamNonBlocking));
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.xfer_stream, cudaStreamNonBlocking));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_xfer, cudaEventDisableTiming));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_pc0, cudaEventDisableTiming));
+  for (int r = 0; r < kMaxPeers && r < c.world; ++r) {
+    LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.peer_cs[r], cudaStreamNonBlocking));
+    LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_pc[r], cudaEventDisableTiming));
+  }
 
   // flat parameter layout, 64-element aligned segments
   auto pad = [](long long x) { return (x + 63) / 64 * 64; };
@@ -1820,9 +1936,12 @@ extern "C" int lbbsp_mlp_peer_handle(lbbsp_mlp* m, unsigned char h_handle[64]) {
   if (!m->peer_buf) {
     const int W = m->cfg.world;
     // counters: [2 + LBBSP_MLP_MAX_LAYERS][kMaxPeers] (speeds, gradients, per-bucket arrivals)
-    m->peer_off_spd = (sizeof(unsigned long long) * kMaxPeers * (2 + LBBSP_MLP_MAX_LAYERS) + 255) / 256 * 256;
+    m->peer_off_spd = (sizeof(unsigned long long) * kMaxPeers * (2 + 2 * LBBSP_MLP_MAX_LAYERS) + 255) / 256 * 256;
     m->peer_off_grd = (m->peer_off_spd + sizeof(double) * W * m->n_local + 255) / 256 * 256;
-    const size_t bytes = m->peer_off_grd + sizeof(float) * W * static_cast<size_t>(m->P);
+    // gradient region: fp32 slots [W][P] (several workers per GPU), or bf16
+    // slots [W][P] + the bf16 all-gather buffer [P] (copy-engine buckets)
+    const size_t bytes = m->peer_off_grd + std::max(sizeof(float) * W, sizeof(bf16) * (W + 1)) *
+                                               static_cast<size_t>(m->P);
     LBBSP_CUDA_CHECK(cudaMalloc(&m->peer_buf, bytes));
     LBBSP_CUDA_CHECK(cudaMemset(m->peer_buf, 0, bytes));
   }
@@ -1858,11 +1977,14 @@ extern "C" int lbbsp_mlp_init_peers(lbbsp_mlp* m, const unsigned char* h_handles
   X.grd_local = reinterpret_cast<float*>(lb + m->peer_off_grd);
   m->peers = true;
   // copy-engine bucket exchange: each bucket (W_l | b_l) moves as whole uint4s.
-  // Default at 2 GPUs only: the one-shot push sends (N-1)*P*2 bytes per GPU,
-  // which at N=4 measured slower than NCCL's ring (2(N-1)/N*P*2 bytes; C3
-  // no-straggler round 1.74 vs 1.42 ms). LBBSP_CE_BUCKETS=1 forces it.
+  // The one-shot push sends (N-1)*P*2 bytes per GPU; at N=4 it measured
+  // slower than NCCL's ring (2(N-1)/N*P*2 bytes; C3 no-straggler round 1.74
+  // vs 1.42 ms), so N > 2 uses the two-shot variant.
   bool al = m->gradb != nullptr && m->P % 8 == 0 && !getenv("LBBSP_NCCL_BUCKETS") &&
-            (W == 2 || getenv("LBBSP_CE_BUCKETS"));
+            !getenv("LBBSP_NO_CE_BUCKETS");
+  // 2 GPUs: one-shot push (each GPU sends P*2 bytes, one hop to the apply);
+  // more GPUs: reduce-scatter + all-gather (2(N-1)/N*P*2 bytes per GPU)
+  m->ce_two_shot = W > 2 || getenv("LBBSP_CE_TWO_SHOT");
   for (int l = 0; al && l < m->L; ++l) {
     const long long seg0 = m->off_w[l], seg1 = l + 1 < m->L ? m->off_w[l + 1] : m->P;
     al = seg0 % 8 == 0 && (seg1 - seg0) % 8 == 0;

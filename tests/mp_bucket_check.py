@@ -1,6 +1,7 @@
 """Multi-GPU check (run with torchrun on >= 2 GPUs), one worker per GPU: the
 copy-engine bucket exchange (bf16 layer buckets pushed into the peers' IPC
-slots, rank-ordered fp32 sum + apply) gives the same parameters on every rank
+slots, rank-ordered fp32 sum + apply; one-shot, and the reduce-scatter +
+all-gather of bf16-rounded slice sums) gives the same parameters on every rank
 and matches the NCCL bf16 bucket all-reduce (LBBSP_NCCL_BUCKETS=1) within the
 bf16 rounding of the summed gradient, after several rounds with static sizes
 (the exchange step of the sharded path)."""
@@ -17,12 +18,13 @@ dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cu
 dims = [1024, 1024, 1024, 1024]
 rounds = 12
 out = {}
-os.environ["LBBSP_CE_BUCKETS"] = "1"  # also at N > 2, where NCCL is the default
-for mode in ("nccl", "ce"):
+for mode in ("nccl", "ce", "ce_two_shot"):
+    os.environ.pop("LBBSP_NCCL_BUCKETS", None)
+    os.environ.pop("LBBSP_CE_TWO_SHOT", None)
     if mode == "nccl":
         os.environ["LBBSP_NCCL_BUCKETS"] = "1"
-    else:
-        os.environ.pop("LBBSP_NCCL_BUCKETS", None)
+    elif mode == "ce_two_shot":  # the N > 2 default, forced at N = 2 too
+        os.environ["LBBSP_CE_TWO_SHOT"] = "1"
     sizes = [1024 + 256 * (i % 2) - 128 for i in range(world)]  # ragged per-GPU batches
     eng = MlpEngine(dims=dims, global_batch=sum(sizes), n_workers_local=1, world=world, rank=rank,
                     scheme="lb-bsp", predictor="ema", learning_rate=0.05, max_iterations=rounds + 4,
@@ -50,6 +52,17 @@ ldiff = float(np.max(np.abs(l0 - l1) / np.maximum(1e-12, np.abs(l0))))
 print(f"rank {rank}: ranks bitwise equal {same}, max |params nccl - ce| = {diff:.3e} "
       f"(max |p| {float(np.max(np.abs(p0))):.3e}), max rel loss diff {ldiff:.3e}", flush=True)
 assert same
+# two-shot (reduce-scatter + all-gather of the bf16-rounded slice sums):
+# bitwise equal on every rank, within the bf16 rounding of the NCCL path
+p2 = out["ce_two_shot"][0]
+allp2 = [None] * world
+dist.all_gather_object(allp2, p2)
+same2 = all(np.array_equal(allp2[0], a) for a in allp2)
+diff2 = float(np.max(np.abs(p0 - p2)))
+print(f"rank {rank}: two-shot ranks bitwise equal {same2}, max |params nccl - two-shot| = {diff2:.3e}",
+      flush=True)
+assert same2
+assert diff2 <= 2e-3 * max(1.0, float(np.max(np.abs(p0)))), diff2
 assert diff <= 2e-3 * max(1.0, float(np.max(np.abs(p0)))), diff  # bf16 rounding of the bucket sum
 assert ldiff <= 1e-2, ldiff
 dist.destroy_process_group()

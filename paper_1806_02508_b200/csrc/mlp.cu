@@ -1151,22 +1151,6 @@ struct lbbsp_mlp {
   // copy-engine bucket exchange (one worker per GPU with peers, LBBSP_NCCL_BUCKETS unset)
   cudaStream_t xfer_stream = nullptr;
   cudaEvent_t ev_xfer = nullptr;
-  // one copy stream per peer (two-shot): the copies to different peers run concurrently
-  cudaStream_t peer_cs[kMaxPeers] = {};
-  cudaEvent_t ev_pc0 = nullptr, ev_pc[kMaxPeers] = {};
-  // copies (dst[r], src[r], bytes[r]) for every peer r != rank, issued after
-  // the work already on `from` and joined back into it
-  cudaError_t fan_copy(cudaStream_t from, void* const* dst, const void* const* src, const size_t* bytes) {
-    cudaError_t e = cudaEventRecord(ev_pc0, from);
-    for (int r = 0; e == cudaSuccess && r < cfg.world; ++r) {
-      if (r == cfg.rank) continue;
-      e = cudaStreamWaitEvent(peer_cs[r], ev_pc0, 0);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(dst[r], src[r], bytes[r], cudaMemcpyDeviceToDevice, peer_cs[r]);
-      if (e == cudaSuccess) e = cudaEventRecord(ev_pc[r], peer_cs[r]);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(from, ev_pc[r], 0);
-    }
-    return e;
-  }
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   ncclComm_t comm = nullptr;
@@ -1231,11 +1215,6 @@ struct lbbsp_mlp {
     if (ev_speed) cudaEventDestroy(ev_speed);
     if (ev_comm) cudaEventDestroy(ev_comm);
     if (ev_xfer) cudaEventDestroy(ev_xfer);
-    if (ev_pc0) cudaEventDestroy(ev_pc0);
-    for (int r = 0; r < kMaxPeers; ++r) {
-      if (ev_pc[r]) cudaEventDestroy(ev_pc[r]);
-      if (peer_cs[r]) cudaStreamDestroy(peer_cs[r]);
-    }
     if (xfer_stream) cudaStreamDestroy(xfer_stream);
     for (auto& e : ev_layer)
       if (e) cudaEventDestroy(e);
@@ -1383,15 +1362,13 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
         const long long n = seg1 - seg0, W = cfg.world;
         auto sl0 = [&](long long r) { return seg0 + (n / 8 * r / W) * 8; };
         LBBSP_CUDA_CHECK(cudaStreamWaitEvent(xfer_stream, ev_layer[l], 0));
-        void* dst[kMaxPeers];
-        const void* src[kMaxPeers];
-        size_t nb[kMaxPeers];
+        // (one stream for all peers: a copy stream per peer measured slower at N=4)
         for (int r = 0; r < cfg.world; ++r) {
-          dst[r] = reinterpret_cast<bf16*>(px.grd_peer[r]) + static_cast<long long>(cfg.rank) * P + sl0(r);
-          src[r] = gradb + sl0(r);
-          nb[r] = sizeof(bf16) * (sl0(r + 1) - sl0(r));
+          if (r == cfg.rank) continue;
+          bf16* dst = reinterpret_cast<bf16*>(px.grd_peer[r]) + static_cast<long long>(cfg.rank) * P + sl0(r);
+          LBBSP_CUDA_CHECK(cudaMemcpyAsync(dst, gradb + sl0(r), sizeof(bf16) * (sl0(r + 1) - sl0(r)),
+                                           cudaMemcpyDeviceToDevice, xfer_stream));
         }
-        LBBSP_CUDA_CHECK(fan_copy(xfer_stream, dst, src, nb));
         peer_signal_row_kernel<<<1, 32, 0, xfer_stream>>>(px, 2 + l);
         // own slice: rank-ordered fp32 sum -> all-gather buffer of every rank
         const long long m0 = sl0(cfg.rank), m1 = sl0(cfg.rank + 1);
@@ -1399,11 +1376,11 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
         bf16* ag_local = reinterpret_cast<bf16*>(px.grd_local) + W * P;
         peer_slice_reduce_kernel<<<sms, 256, 0, comm_stream>>>(px, m0, m1 - m0, P, gradb, ag_local);
         for (int r = 0; r < cfg.world; ++r) {
-          dst[r] = reinterpret_cast<bf16*>(px.grd_peer[r]) + W * P + m0;
-          src[r] = ag_local + m0;
-          nb[r] = sizeof(bf16) * (m1 - m0);
+          if (r == cfg.rank) continue;
+          bf16* ag_r = reinterpret_cast<bf16*>(px.grd_peer[r]) + W * P;
+          LBBSP_CUDA_CHECK(cudaMemcpyAsync(ag_r + m0, ag_local + m0, sizeof(bf16) * (m1 - m0),
+                                           cudaMemcpyDeviceToDevice, comm_stream));
         }
-        LBBSP_CUDA_CHECK(fan_copy(comm_stream, dst, src, nb));
         peer_signal_row_kernel<<<1, 32, 0, comm_stream>>>(px, 2 + LBBSP_MLP_MAX_LAYERS + l);
         peer_wait_row_kernel<<<1, 32, 0, comm_stream>>>(px, 2 + LBBSP_MLP_MAX_LAYERS + l, D.round_k,
                                                         D.status);
@@ -1623,11 +1600,6 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.comm_stream, cudaStreamNonBlocking));
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.xfer_stream, cudaStreamNonBlocking));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_xfer, cudaEventDisableTiming));
-  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_pc0, cudaEventDisableTiming));
-  for (int r = 0; r < kMaxPeers && r < c.world; ++r) {
-    LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.peer_cs[r], cudaStreamNonBlocking));
-    LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_pc[r], cudaEventDisableTiming));
-  }
 
   // flat parameter layout, 64-element aligned segments
   auto pad = [](long long x) { return (x + 63) / 64 * 64; };
@@ -1977,14 +1949,16 @@ extern "C" int lbbsp_mlp_init_peers(lbbsp_mlp* m, const unsigned char* h_handles
   X.grd_local = reinterpret_cast<float*>(lb + m->peer_off_grd);
   m->peers = true;
   // copy-engine bucket exchange: each bucket (W_l | b_l) moves as whole uint4s.
-  // The one-shot push sends (N-1)*P*2 bytes per GPU; at N=4 it measured
-  // slower than NCCL's ring (2(N-1)/N*P*2 bytes; C3 no-straggler round 1.74
-  // vs 1.42 ms), so N > 2 uses the two-shot variant.
+  // Default at 2 GPUs (one-shot push, C3 no-straggler round 1.31 -> 1.19 ms).
+  // At N=4 the one-shot push ((N-1)*P*2 bytes per GPU) measured 1.74 ms and
+  // the two-shot variant (ring volume) 1.46 ms against NCCL's 1.42 ms, so
+  // N > 2 keeps the NCCL buckets unless LBBSP_CE_BUCKETS=1 (one-shot) or
+  // LBBSP_CE_TWO_SHOT=1.
   bool al = m->gradb != nullptr && m->P % 8 == 0 && !getenv("LBBSP_NCCL_BUCKETS") &&
-            !getenv("LBBSP_NO_CE_BUCKETS");
-  // 2 GPUs: one-shot push (each GPU sends P*2 bytes, one hop to the apply);
-  // more GPUs: reduce-scatter + all-gather (2(N-1)/N*P*2 bytes per GPU)
-  m->ce_two_shot = W > 2 || getenv("LBBSP_CE_TWO_SHOT");
+            (W == 2 || getenv("LBBSP_CE_TWO_SHOT") || getenv("LBBSP_CE_BUCKETS"));
+  // one-shot push (each GPU sends (N-1)*P*2 bytes, one hop to the apply), or
+  // reduce-scatter + all-gather (2(N-1)/N*P*2 bytes per GPU)
+  m->ce_two_shot = getenv("LBBSP_CE_TWO_SHOT") != nullptr;
   for (int l = 0; al && l < m->L; ++l) {
     const long long seg0 = m->off_w[l], seg1 = l + 1 < m->L ? m->off_w[l + 1] : m->P;
     al = seg0 % 8 == 0 && (seg1 - seg0) % 8 == 0;

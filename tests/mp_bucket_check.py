@@ -18,12 +18,13 @@ dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cu
 dims = [1024, 1024, 1024, 1024]
 rounds = 12
 out = {}
+os.environ["LBBSP_CE_BUCKETS"] = "1"  # the copy-engine path also at N > 2 (default: NCCL there)
 for mode in ("nccl", "ce", "ce_two_shot"):
     os.environ.pop("LBBSP_NCCL_BUCKETS", None)
     os.environ.pop("LBBSP_CE_TWO_SHOT", None)
     if mode == "nccl":
         os.environ["LBBSP_NCCL_BUCKETS"] = "1"
-    elif mode == "ce_two_shot":  # the N > 2 default, forced at N = 2 too
+    elif mode == "ce_two_shot":
         os.environ["LBBSP_CE_TWO_SHOT"] = "1"
     sizes = [1024 + 256 * (i % 2) - 128 for i in range(world)]  # ragged per-GPU batches
     eng = MlpEngine(dims=dims, global_batch=sum(sizes), n_workers_local=1, world=world, rank=rank,

@@ -583,11 +583,13 @@ int lbbsp_mlp_destroy(lbbsp_mlp* m);
 /* NCCL plumbing for world > 1: rank 0 gets an id, every rank inits with it. */
 int lbbsp_nccl_unique_id(unsigned char h_id[128]);
 int lbbsp_mlp_init_comm(lbbsp_mlp* m, const unsigned char h_id[128]);
-/* Optional NVLink peer exchange for several workers per GPU on several GPUs:
- * each rank exports a device buffer (64-byte CUDA IPC handle); the caller
- * all-gathers the handles ([world][64], rank order) and passes them back.
- * The speed all-gather and gradient all-reduce then run as peer-memory
- * kernels (rank-ordered, deterministic sum) instead of NCCL calls.
+/* Optional NVLink peer exchange on several GPUs: each rank exports a device
+ * buffer (64-byte CUDA IPC handle); the caller all-gathers the handles
+ * ([world][64], rank order) and passes them back. With several workers per
+ * GPU the speed all-gather and gradient all-reduce then run as peer-memory
+ * kernels (rank-ordered, deterministic sum) instead of NCCL calls; with one
+ * worker per GPU (2 GPUs) the bf16 gradient buckets are pushed by the copy
+ * engines into the peers' buffers and summed in rank order.
  * Call before the first lbbsp_mlp_run. */
 int lbbsp_mlp_peer_handle(lbbsp_mlp* m, unsigned char h_handle[64]);
 int lbbsp_mlp_init_peers(lbbsp_mlp* m, const unsigned char* h_handles);

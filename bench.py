@@ -548,14 +548,25 @@ def main():
     eng = make("lb-bsp", trace)
     x_host, y_host = eng.dataset()
     # page-locked host buffers (the upload overlaps the round in flight)
-    xb = torch.empty(x_host.shape, dtype=torch.bfloat16, pin_memory=True)
+    from paper_1806_02508_b200.hostio import pinned_empty
+    xb = pinned_empty(x_host.shape, torch.bfloat16, local)
     xb.copy_(torch.from_numpy(x_host).to(torch.bfloat16))
-    yb = torch.empty(y_host.shape, dtype=torch.int32, pin_memory=True)
+    yb = pinned_empty(y_host.shape, torch.int32, local)
     yb.copy_(torch.from_numpy(y_host.astype(np.int32)))
-    out_sizes = torch.zeros(n_total, dtype=torch.int32, pin_memory=True)
-    out_loss = torch.zeros(1, dtype=torch.float64, pin_memory=True)
+    out_sizes = pinned_empty((n_total,), torch.int32, local)
+    out_loss = pinned_empty((1,), torch.float64, local)
     st = torch.cuda.ExternalStream(eng.stream)
-    eng.run(warm)
+    # the last e2e_warm warm-up rounds go through the e2e calls themselves: the
+    # first host->device copies out of freshly page-locked buffers run at about
+    # half the link rate (measured 46-103 us vs a steady 35 us for 1.57 MB,
+    # profiles/r01_e2e_warm_probe.txt), so the timed e2e steps start warm, over
+    # the same rounds as the device-resident arm
+    e2e_warm = min(max(args.warmup, 3), warm)
+    eng.run(warm - e2e_warm)
+    for _ in range(e2e_warm):
+        eng.load_data_async(xb.data_ptr(), yb.data_ptr())
+        eng.run(1)
+        eng.read_result_async(out_sizes.data_ptr(), out_loss.data_ptr())
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

@@ -5,15 +5,19 @@ sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 import numpy as np
 import torch
 from paper_1806_02508_b200.mlp import MlpEngine, benchmark_trace
+from paper_1806_02508_b200.hostio import pinned_empty
+MODES = os.environ.get("MODES", "run only,e2e,load only,read only,run only,e2e,load only,read only").split(",")
+LOCAL = os.environ.get("LOCAL", "0") == "1"
 n = 8
-for mode in ("run only", "e2e", "load only", "read only", "run only", "e2e", "load only", "read only"):
+for mode in MODES:
     eng = MlpEngine(dims=[784, 256, 10], global_batch=4096, n_workers_local=8,
                     predictor=os.environ.get("PRED", "narx"), warmup_iterations=50,
                     max_iterations=400, trace=benchmark_trace(n, 400, seed=3), learning_rate=0.05)
     x, y = eng.dataset()
-    xb = torch.empty(x.shape, dtype=torch.bfloat16, pin_memory=True); xb.copy_(torch.from_numpy(x).to(torch.bfloat16))
-    yb = torch.empty(y.shape, dtype=torch.int32, pin_memory=True); yb.copy_(torch.from_numpy(y.astype(np.int32)))
-    osz = torch.zeros(n, dtype=torch.int32, pin_memory=True); ol = torch.zeros(1, dtype=torch.float64, pin_memory=True)
+    pe = pinned_empty if LOCAL else (lambda sh, dt: torch.empty(sh, dtype=dt, pin_memory=True))
+    xb = pe(x.shape, torch.bfloat16); xb.copy_(torch.from_numpy(x).to(torch.bfloat16))
+    yb = pe(y.shape, torch.int32); yb.copy_(torch.from_numpy(y.astype(np.int32)))
+    osz = pe((n,), torch.int32); ol = pe((1,), torch.float64)
     st = torch.cuda.ExternalStream(eng.stream)
     eng.run(100); torch.cuda.synchronize()
     s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)

@@ -182,12 +182,42 @@ def reference_arm(args):
 # GPU arm
 # ---------------------------------------------------------------------------
 class Clocks:
+    """SM clock and clock-event reasons sampled DURING the timed region: an NVML
+    poll every 3 ms on a side thread (the timed regions are 10-30 ms, shorter
+    than nvidia-smi's start-up), nvidia-smi -lms 100 when NVML is missing."""
+
+    NAMES = ((0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"), (0x20, "sw_thermal_slowdown"),
+             (0x4, "sw_power_cap"))
+
     def __init__(self, index):
         self.index = index
         self.p = None
+        self.t = None
+        self.rows = []
         self.path = os.path.join("/tmp", f"lbbsp_clocks_{os.getpid()}.csv")
 
+    def _poll(self, nv, h):
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while True:
+            self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), float(mx),
+                              int(get_r(h))))
+            if self.stop.wait(0.003):
+                break
+
     def __enter__(self):
+        import threading
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.stop = threading.Event()
+            self.t = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.t = None
         try:
             self.f = open(self.path, "w")
             self.p = subprocess.Popen(
@@ -202,6 +232,9 @@ class Clocks:
         return self
 
     def __exit__(self, *a):
+        if self.t:
+            self.stop.set()
+            self.t.join(timeout=5)
         if self.p:
             self.p.terminate()
             try:
@@ -211,6 +244,13 @@ class Clocks:
             self.f.close()
 
     def summary(self):
+        if self.t is not None:
+            if not self.rows:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            sm = sorted(r[0] for r in self.rows)
+            reasons = sorted({n for r in self.rows for bit, n in self.NAMES if r[2] & bit})
+            return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.rows[0][1], "reasons": reasons,
+                    "samples": len(self.rows), "source": "nvml"}
         try:
             rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
         except Exception:

@@ -29,6 +29,7 @@ WORKERS_PER_GPU = 8
 BATCH_PER_GPU = 4096
 WARMUP_NARX = 50
 TRACE_SEED = 3
+WINDOW_ROUNDS = 100  # fixed steady-state window for the BSP / ideal comparisons
 
 
 def parse():
@@ -267,8 +268,8 @@ class Clocks:
 
 def c3_straggler_demo(steps, warmup):
     """BASELINE configs[2] shape on one GPU: wide MLP 4x(4096x4096) bf16, two
-    workers, worker 1 capped to half its SMs (a 2x straggler, the 'one
-    injected 2x straggler'), global batch 4096 (2048 per worker nominal).
+    workers on 74 SMs each, worker 1 at availability 0.5 (a 2x straggler, the
+    'one injected 2x straggler'), global batch 4096 (2048 per worker nominal).
     Measures LB-BSP vs BSP vs the no-straggler ideal on compute-bound work,
     and the tcgen05 GEMM throughput of the worker phases."""
     import torch
@@ -278,6 +279,10 @@ def c3_straggler_demo(steps, warmup):
     dims = [4096] * 5
     n, B = 2, 4096
     iters = warmup + steps + 4
+    try:
+        burst = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["bf16_tflops"]
+    except Exception:
+        burst = 1590.0
     out = {}
     for name, scheme, avail in (("lbbsp", "lb-bsp", [1.0, 0.5]), ("bsp", "bsp", [1.0, 0.5]),
                                 ("ideal", "lb-bsp", [1.0, 1.0])):
@@ -297,18 +302,26 @@ def c3_straggler_demo(steps, warmup):
         rec = eng.records()
         ph = eng.phase_times()
         flops, _ = eng.work()
+        # worker 0 is never interfered: its GEMM throughput on its own
+        # partition (74 of 148 SMs) against the partition's share of the peak
+        r0, t0 = int(rec["sizes"][-1][0]), float(rec["t_worker"][-1][0])
+        tf0 = 2.0 * r0 * 4096 * 4096 * 11 / t0 / 1e12 if t0 > 0 else 0.0
         out[name] = {"ms_per_step": ms, "samples_per_s": B / (ms * 1e-3),
                      "sizes_last": rec["sizes"][-1].tolist(), "caps_last": rec["caps"][-1].tolist(),
                      "worker_ms_last": [round(float(t) * 1e3, 4) for t in rec["t_worker"][-1]],
-                     "gemm_tflops_in_worker_phases": flops / (float(rec["t_worker"][-1].max()) * 1e12)}
+                     "worker_time_ratio_last": float(rec["t_worker"][-1][1] / rec["t_worker"][-1][0]),
+                     "gemm_tflops_worker0": tf0,
+                     "gemm_frac_of_partition_peak_worker0": tf0 / (burst * rec["caps"][-1][0] / 148.0)}
         del eng
     out["lbbsp_over_bsp_speedup"] = out["bsp"]["ms_per_step"] / out["lbbsp"]["ms_per_step"]
     out["lbbsp_over_ideal_time"] = out["lbbsp"]["ms_per_step"] / out["ideal"]["ms_per_step"]
-    # capacity-aware ideal: perfect balance over the SMs left = 1.5x no-straggler
-    cap = (74 + 37) / 148.0
+    # capacity-aware ideal: perfect balance over the capacity
+    # left, (1 + 0.5) / 2 of the no-straggler GPU
+    cap = (1.0 + 0.5) / 2.0
     out["lbbsp_over_capacity_ideal"] = out["lbbsp"]["ms_per_step"] / (out["ideal"]["ms_per_step"] / cap)
-    out["workload"] = ("C3 shape on 1 GPU: MLP 4096x4 (bf16, fp32 accum), 2 workers (worker 1 = 2x "
-                       "straggler: half its SM share), global batch 4096, EMA predictor")
+    out["workload"] = ("C3 shape on 1 GPU: MLP 4096x4 (bf16, fp32 accum), 2 workers of 74 SMs each "
+                       "(worker 1 = 2x straggler: a = 0.5, co-scheduled interference), global "
+                       "batch 4096, EMA predictor")
     return out
 
 
@@ -372,33 +385,45 @@ def main_c3(args):
                      "worker_ms_last": [round(float(t) * 1e3, 4) for t in rec["t_worker"][-1]],
                      "gemm_flops_per_round_this_rank": flops}
         del eng
+    # tensor-core roofline of the worker GEMM phases from the LB-BSP arm
+    # itself: every rank's GEMM flops over its own measured worker time, on
+    # the ranks without injected interference (a straggler's phase time is
+    # stretched to work / a by design); the burst peak (a round is ~1.5 ms)
+    lb = out["lbbsp"]
+    my_rows = lb["sizes_last"][rank]
+    my_t = lb["worker_ms_last"][0] * 1e-3
+    mine = 2.0 * my_rows * 4096 * 4096 * 11 / my_t / 1e12 if my_t > 0 and avail[rank] >= 1.0 else 0.0
+    if world > 1:
+        allv = [None] * world
+        dist.all_gather_object(allv, mine)
+    else:
+        allv = [mine]
+    unloaded = [v for v, a in zip(allv, avail) if a >= 1.0 and v > 0]
     if rank == 0:
         peaks = {}
         try:
             peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
         except Exception:
             pass
-        sust = peaks.get("bf16_tflops_sustained", 1400.0)
-        lb = out["lbbsp"]
-        # GEMM throughput of the fastest (uncapped) worker's phases
-        wt = min(t for t in out["ideal"]["worker_ms_last"] if t > 0) * 1e-3
-        achieved = 2.0 * 2048 * 4096 * 4096 * 11 / wt / 1e12
+        burst = peaks.get("bf16_tflops", 1590.0)
+        achieved = min(unloaded) if unloaded else 0.0
         cap = (world - 0.5) / world if world > 1 else 1.0
         line = {"metric": METRIC, "value": B / (lb["ms_per_step"] * 1e-3), "unit": "samples/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": lb["ms_per_step"], "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": {"workload": "C3: MLP 4x(4096x4096) bf16, one worker per GPU, 2048 "
-                                       "samples per GPU, last GPU = 2x straggler (half SMs), "
-                                       "LB-BSP + EMA", "global_batch": B,
+                                       "samples per GPU, last GPU = 2x straggler (a = 0.5, "
+                                       "co-scheduled interference), LB-BSP + EMA", "global_batch": B,
                            "parallelism": f"dp{world}"},
                 "bsp": out["bsp"], "ideal_no_straggler": out["ideal"], "lbbsp": lb,
                 "lbbsp_over_bsp_speedup": out["bsp"]["ms_per_step"] / lb["ms_per_step"],
                 "lbbsp_over_capacity_ideal": lb["ms_per_step"] / (out["ideal"]["ms_per_step"] / cap),
                 "roofline": {"bound": "tensor", "kernel": "worker GEMM phases (11 GEMMs, CTA-pair "
-                                                          "tcgen05)",
-                             "achieved": achieved, "peak": sust, "unit": "TFLOP/s",
-                             "frac": achieved / sust, "peak_source": "measured (sustained)",
+                                                          "tcgen05), LB-BSP arm, unloaded ranks (min)",
+                             "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
+                             "frac": achieved / burst, "peak_source": "measured (burst)",
+                             "per_rank": allv,
                              "traffic": None}}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -501,6 +526,13 @@ def main_c5(args):
     return 0
 
 
+def percentiles(ms):
+    import numpy as np
+    a = np.asarray(ms, dtype=np.float64)
+    return {"mean": float(a.mean()), "median": float(np.median(a)), "p90": float(np.percentile(a, 90)),
+            "min": float(a.min()), "max": float(a.max())}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -523,17 +555,18 @@ def main():
     n_total = WORKERS_PER_GPU * world
     B = BATCH_PER_GPU * world
     e2e_steps = args.steps
+    window = WINDOW_ROUNDS
     # the timed rounds are steady-state LB-BSP + NARX rounds: they begin 50
     # rounds after the predictor warm-up (50 rounds, EMA before it), when every
     # model has been trained ~25 times by the rotation -- the predictor's steady
     # state rather than its cold start (the same window for every arm)
     warm = max(args.warmup, WARMUP_NARX + 50)
-    iters = warm + args.steps + 8
+    iters = warm + max(args.steps, window) + 8
     trace = benchmark_trace(n_total, iters, seed=TRACE_SEED)
 
-    def make(scheme, tr):
+    def make(scheme, tr, predictor="narx"):
         eng = MlpEngine(dims=DIMS, global_batch=B, n_workers_local=WORKERS_PER_GPU, world=world,
-                        rank=rank, scheme=scheme, predictor="narx",
+                        rank=rank, scheme=scheme, predictor=predictor,
                         warmup_iterations=WARMUP_NARX, learning_rate=0.05, seed=1,
                         max_iterations=iters + 4, trace=tr)
         if world > 1:
@@ -543,51 +576,52 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2 (126 MB)
 
     def timed(eng, steps, warmup, phases=False):
+        """per-round device times (ms, max over ranks per round): every round
+        bracketed by CUDA events on the engine stream, the L2 flushed between
+        rounds outside the events"""
         st = torch.cuda.ExternalStream(eng.stream)
         eng.run(warmup)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        total = 0.0
+        ev = []
         ph = None
         for _ in range(steps):
             with torch.cuda.stream(st):
-                flush.zero_()  # L2 flush between steps, outside the timed events
+                flush.zero_()
                 s = torch.cuda.Event(enable_timing=True)
                 e = torch.cuda.Event(enable_timing=True)
                 s.record(st)
             eng.run(1)
             with torch.cuda.stream(st):
                 e.record(st)
-            e.synchronize()
-            total += s.elapsed_time(e)
+            ev.append((s, e))
             if phases:
+                e.synchronize()
                 p = eng.phase_times()
                 ph = p if ph is None else ph + p
         torch.cuda.synchronize()
+        ms = torch.tensor([s.elapsed_time(e) for s, e in ev], dtype=torch.float64, device="cuda")
         if world > 1:
-            t = torch.tensor([total], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            total = float(t.item())
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
             dist.barrier()
-        return total / steps, (ph / steps if ph is not None else None)
+        return ms.cpu().numpy(), (ph / steps if ph is not None else None)
 
-    # ---- main arm: LB-BSP under the recorded trace ----
+    # ---- main arm: LB-BSP + NARX under the recorded trace, the driver's K steps ----
     eng = make("lb-bsp", trace)
     with Clocks(local) as clk:
-        ms_lb, phases = timed(eng, args.steps, warm, phases=True)
+        ms_steps, phases = timed(eng, args.steps, warm, phases=True)
     rec = eng.records()
     launches = eng.launches_per_iteration()
     gemm_flops, _ = eng.work()
-
     del eng
+    ms_lb = float(ms_steps.mean())
 
     # ---- e2e through the C-ABI with host buffers (pinned), per-step H2D/D2H ----
     # a fresh engine over the same rounds as the timed arm (same warm-up), so
     # both numbers see the same predictor / straggler history
     eng = make("lb-bsp", trace)
     x_host, y_host = eng.dataset()
-    # page-locked host buffers (the upload overlaps the round in flight)
     from paper_1806_02508_b200.hostio import pinned_empty
     xb = pinned_empty(x_host.shape, torch.bfloat16, local)
     xb.copy_(torch.from_numpy(x_host).to(torch.bfloat16))
@@ -596,17 +630,10 @@ def main():
     out_sizes = pinned_empty((n_total,), torch.int32, local)
     out_loss = pinned_empty((1,), torch.float64, local)
     st = torch.cuda.ExternalStream(eng.stream)
-    # the last e2e_warm warm-up rounds go through the e2e calls themselves: the
-    # first host->device copies out of freshly page-locked buffers run at about
-    # half the link rate (measured 46-103 us vs a steady 35 us for 1.57 MB,
-    # profiles/r01_e2e_warm_probe.txt), so the timed e2e steps start warm, over
-    # the same rounds as the device-resident arm
     e2e_warm = min(max(args.warmup, 3), warm)
     eng.run(warm - e2e_warm)
     for _ in range(e2e_warm):
-        eng.load_data_async(xb.data_ptr(), yb.data_ptr())
-        eng.run(1)
-        eng.read_result_async(out_sizes.data_ptr(), out_loss.data_ptr())
+        eng.step_e2e(xb.data_ptr(), yb.data_ptr(), out_sizes.data_ptr(), out_loss.data_ptr())
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -614,9 +641,7 @@ def main():
     e = torch.cuda.Event(enable_timing=True)
     s.record(st)
     for _ in range(e2e_steps):
-        eng.load_data_async(xb.data_ptr(), yb.data_ptr())
-        eng.run(1)
-        eng.read_result_async(out_sizes.data_ptr(), out_loss.data_ptr())
+        eng.step_e2e(xb.data_ptr(), yb.data_ptr(), out_sizes.data_ptr(), out_loss.data_ptr())
     e.record(st)
     e.synchronize()
     e2e_ms = s.elapsed_time(e) / e2e_steps
@@ -628,13 +653,18 @@ def main():
     d2h = n_total * 4 + 8
     del eng
 
-    # ---- BSP and no-straggler ideal on the same trace / config ----
-    eng_b = make("bsp", trace)
-    ms_bsp, _ = timed(eng_b, args.steps, warm)
-    del eng_b
-    eng_i = make("lb-bsp", constant_trace(n_total, iters))
-    ms_ideal, _ = timed(eng_i, args.steps, warm)
-    del eng_i
+    # ---- a fixed window of 100 steady-state rounds for every arm on the same
+    # trace: LB-BSP + NARX, BSP (equal split), Perfect (sizes from the true
+    # availabilities: the capacity-aware ideal a proportional allocator can
+    # reach) and the no-straggler ideal (every worker at a = 1) ----
+    win = {}
+    for name, scheme, tr, pred in (("lbbsp", "lb-bsp", trace, "narx"), ("bsp", "bsp", trace, "narx"),
+                                   ("perfect", "lb-bsp", trace, "perfect"),
+                                   ("no_straggler", "lb-bsp", constant_trace(n_total, iters), "narx")):
+        eng = make(scheme, tr, pred)
+        ms_w, _ = timed(eng, window, warm)
+        win[name] = percentiles(ms_w)
+        del eng
 
     # ---- C3-shape straggler demonstration (compute-bound) ----
     c3 = None
@@ -651,13 +681,13 @@ def main():
     except Exception:
         pass
     peak_tf = peaks.get("bf16_tflops", 1590.0)
-    peak_src = "measured" if "bf16_tflops" in peaks else "fallback"
-    # per-worker phase list: [fwd L0, head, bias L0, dW L0] for 784-256-10
+    peak_src = "measured (burst)" if "bf16_tflops" in peaks else "fallback"
+    # per-worker phase list: [fwd L0, head, dW L0] for 784-256-10; the phase
+    # time is the worker-phase window (min start .. max end over workers) and
+    # includes the injected interference of the slow workers
     fwd_flops = 2.0 * BATCH_PER_GPU * DIMS[0] * DIMS[1]
     ph_fwd = float(phases[0]) if phases is not None and len(phases) else 0.0
-    ph_dw = float(phases[3]) if phases is not None and len(phases) > 3 else 0.0
     achieved = fwd_flops / ph_fwd / 1e12 if ph_fwd > 0 else 0.0
-    # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
     traffic = None
     try:
         cap = json.load(open(os.path.join(REPO, "profiles", "r01_c2_fwd_gemm_ncu.json")))
@@ -668,23 +698,32 @@ def main():
     if rank == 0:
         clocks = clk.summary()
         value = B / (ms_lb * 1e-3)
+        lb = win["lbbsp"]["mean"]
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_lb,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
-            "config": {"workload": "C2: MLP 784-256-10, 8 emulated workers per GPU under "
-                                   "trace-driven SM caps, global batch 4096 per GPU, LB-BSP + "
-                                   "NARX (warm-up 50), full-dataset loss every round",
+            "config": {"workload": "C2: MLP 784-256-10, 8 emulated workers per GPU (CTA "
+                                   "partitions) with trace-driven co-scheduled interference, "
+                                   "global batch 4096 per GPU, LB-BSP + NARX (warm-up 50), "
+                                   "full-dataset loss every round",
                        "global_batch": B, "workers": n_total,
                        "parallelism": f"dp{n_total} (emulated {WORKERS_PER_GPU}/GPU)",
                        "trace": "make_benchmark_series seed 3, iteration-indexed",
+                       "straggler_injection": "interference (csrc/interfere.cuh): phase time = work / a",
                        "l2": "256 MB buffer zeroed between timed steps, outside the events",
                        "rounds_before_timing": warm},
-            "bsp": {"value": B / (ms_bsp * 1e-3), "ms_per_step": ms_bsp},
-            "ideal_no_straggler": {"value": B / (ms_ideal * 1e-3), "ms_per_step": ms_ideal},
-            "lbbsp_over_bsp": ms_bsp / ms_lb,
-            "lbbsp_over_ideal_time": ms_lb / ms_ideal,
+            "round_ms": percentiles(ms_steps),
+            "window_100": {"rounds": window, "first_round": warm, **win},
+            "bsp": {"value": B / (win["bsp"]["mean"] * 1e-3), "ms_per_step": win["bsp"]["mean"]},
+            "perfect_ideal": {"value": B / (win["perfect"]["mean"] * 1e-3),
+                              "ms_per_step": win["perfect"]["mean"]},
+            "ideal_no_straggler": {"value": B / (win["no_straggler"]["mean"] * 1e-3),
+                                   "ms_per_step": win["no_straggler"]["mean"]},
+            "lbbsp_over_bsp": win["bsp"]["mean"] / lb,
+            "lbbsp_over_ideal_time": lb / win["perfect"]["mean"],
+            "lbbsp_over_no_straggler_time": lb / win["no_straggler"]["mean"],
             "phase_ms": [round(float(x) * 1e3, 4) for x in (phases if phases is not None else [])],
             "roofline": {"bound": "tensor", "kernel": "fwd GEMM 4096x256x784 (tcgen05, per-worker "
                                                       "partitions)",
@@ -693,8 +732,8 @@ def main():
                          "peak_source": peak_src, "traffic": traffic,
                          "traffic_source": "profiles/r01_c2_fwd_gemm_ncu.json (dram__bytes_read.sum "
                                            "+ dram__bytes_write.sum, one launch)",
-                         "note": "C2 GEMMs are latency-bound (SURVEY 8(d)); see profiles/ for "
-                                 "the C3 tensor-bound numbers"},
+                         "note": "C2 GEMMs are latency-bound (SURVEY 8(d)); the forward phase "
+                                 "window includes the slow workers' injected interference"},
             "gpu_launches": launches * args.steps,
             "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

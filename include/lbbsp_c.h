@@ -232,6 +232,14 @@ int lbbsp_aggregate_apply(const double* d_grads, const int* d_sizes, int n_seg, 
 int lbbsp_lr_loss(const lbbsp_lr_data* data, const double* d_params, double* d_loss,
                   void* stream);
 
+/* generate_dataset / separator_params (sgd.cpp:32-57) into host arrays
+ * (row-major features [n][d], labels [n]): setup-time host generators. */
+int lbbsp_generate_dataset(uint64_t seed, int n, int d, double noise, double* h_features,
+                           double* h_labels);
+int lbbsp_separator_params(uint64_t seed, int d, double* h_out);
+/* apply_update (sgd.cpp:92-99): h_params -= lr * h_grad on the device (K9). */
+int lbbsp_apply_update(double* h_params, int dim, const double* h_grad, double lr);
+
 /* Host-pointer convenience variants for the reference-shaped API. */
 int lbbsp_batch_gradient(const lbbsp_lr_data* data, const double* h_params,
                          const int* h_indices, int count, double* h_grad);
@@ -566,15 +574,25 @@ typedef struct {
   int dataset_size;
   int loss_every;                     /* full-dataset loss cadence (1 = every round) */
   int sm_budget;                      /* SMs this rank's workers may use (0 = all) */
-  /* straggler trace, iteration-indexed: availability a = min(1, c*mult) of
-   * each worker's nominal SM share; [n_workers_total][trace_len], host */
+  /* straggler trace, iteration-indexed: worker availability
+   * a = min(1, c * MemPenalty(m) * mult) (cluster_sim.cpp:22-29), injected as
+   * straggler_mode says; [n_workers_total][trace_len], host */
   const double* h_trace_c;
   const double* h_trace_m;
   const double* h_trace_mult;
   int trace_len;
   const double* h_worker_share;       /* [n_workers_total] nominal share of its GPU (NULL: 1/n_local) */
   int max_iterations;                 /* record capacity                     */
+  int straggler_mode;                 /* LBBSP_STRAGGLE_INTERFERE (0, default) | _SM_CAP (1) */
 } lbbsp_mlp_cfg;
+
+/* How a worker's availability a = min(1, c * MemPenalty(m) * mult) is injected:
+ * INTERFERE: the worker keeps its nominal CTA partition and co-scheduled
+ *   interference on those SMs stretches every phase to (work time) / a
+ *   (SM-bound FMA chains; HBM-bound streaming for the memory-penalty part);
+ * SM_CAP: the partition shrinks to floor(budget * share * a) CTAs (round 1). */
+#define LBBSP_STRAGGLE_INTERFERE 0
+#define LBBSP_STRAGGLE_SM_CAP 1
 
 typedef struct lbbsp_mlp lbbsp_mlp;
 
@@ -613,6 +631,9 @@ int lbbsp_mlp_launches_per_iteration(lbbsp_mlp* m, int* launches);
  * (sizes [n_total] ints, then loss) after it. */
 int lbbsp_mlp_load_data_async(lbbsp_mlp* m, const void* h_x_bf16, const int* h_labels);
 int lbbsp_mlp_read_result_async(lbbsp_mlp* m, int* h_sizes, double* h_loss);
+/* load_data_async + one round + read_result_async in one call (the e2e step). */
+int lbbsp_mlp_step_e2e(lbbsp_mlp* m, const void* h_x_bf16, const int* h_labels, int* h_sizes,
+                       double* h_loss);
 /* Mean per-phase device time of the rounds run so far: phase p of the last
  * round as {min start, max end} over workers (globaltimer ns); n_phases out. */
 int lbbsp_mlp_phase_times(lbbsp_mlp* m, double* h_phase_ns, int* n_phases);

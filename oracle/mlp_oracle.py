@@ -90,10 +90,25 @@ def bf16(x):
     return u.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
-def lbbsp_round_bf16(params, data_x, data_y, stream, sizes, lr, weighted=True, small_head=None):
+def lbbsp_round_bf16(params, data_x, data_y, stream, sizes, lr, weighted=True, small_head=None,
+                     acc32=False, bucket_bf16=False):
     """params: fp32 master weights. Returns new params (fp64) and the
-    aggregated gradient, emulating the device rounding points."""
+    aggregated gradient, emulating the device rounding points.
+
+    acc32: accumulate every matrix product in fp32 (BLAS sgemm order) instead
+    of fp64. The operands are bf16 values either way, so both variants are
+    legitimate restatements of the device arithmetic; their disagreement is
+    the noise floor of any bf16 implementation (activation roundings that
+    flip with the accumulation order), which sizes the parity bars.
+
+    bucket_bf16: one worker per GPU exchanges bf16 gradient buckets -- each
+    worker's (1/B-scaled) partial dW/db is rounded to bf16 and the partials
+    are summed in worker (rank) order in fp32 (csrc/mlp.cu, peer buckets)."""
     L = len(params)
+    dt = np.float32 if acc32 else np.float64
+
+    def mm(a, b):
+        return (np.asarray(a, dtype=dt) @ np.asarray(b, dtype=dt)).astype(np.float64)
     if small_head is None:
         small_head = params[-1][0].shape[0] <= 16
     P = [(W.astype(np.float64), b.astype(np.float64)) for W, b in params]
@@ -110,11 +125,11 @@ def lbbsp_round_bf16(params, data_x, data_y, stream, sizes, lr, weighted=True, s
     acts = [X]
     h = X
     for l in range(L - 1):
-        h = bf16(np.maximum(h @ Wq[l].T + P[l][1], 0.0))
+        h = bf16(np.maximum(mm(h, Wq[l].T) + P[l][1], 0.0))
         acts.append(h)
     # the small head runs on warp MMAs: bf16 W and bf16 dlogits operands,
     # fp32 accumulation; its bias gradient sums the unrounded dlogits
-    logits = h @ Wq[-1].T + P[-1][1]
+    logits = mm(h, Wq[-1].T) + P[-1][1]
     if not small_head:
         logits = bf16(logits)
     p, _ = softmax_ce(logits, y)
@@ -124,13 +139,24 @@ def lbbsp_round_bf16(params, data_x, data_y, stream, sizes, lr, weighted=True, s
     grads = [None] * L
     for l in range(L - 1, -1, -1):
         if small_head and l == L - 1:
-            grads[l] = (bf16(d).T @ acts[l], d.sum(axis=0))
-            d = bf16((bf16(d) @ Wq[l]) * (acts[l] > 0))
+            grads[l] = (mm(bf16(d).T, acts[l]), d.sum(axis=0))
+            d = bf16(mm(bf16(d), Wq[l]) * (acts[l] > 0))
             continue
         if l == L - 1:
             d = bf16(d)
-        grads[l] = (d.T @ acts[l], d.sum(axis=0))
+        if bucket_bf16:
+            gW = np.zeros((d.shape[1], acts[l].shape[1]), np.float32)
+            gb = np.zeros(d.shape[1], np.float32)
+            off = 0
+            for b_i in sizes:
+                seg = slice(off, off + b_i)
+                gW += bf16(mm(d[seg].T, acts[l][seg])).astype(np.float32)
+                gb += bf16(d[seg].sum(axis=0)).astype(np.float32)
+                off += b_i
+            grads[l] = (gW.astype(np.float64), gb.astype(np.float64))
+        else:
+            grads[l] = (mm(d.T, acts[l]), d.sum(axis=0))
         if l > 0:
-            d = bf16((d @ Wq[l]) * (acts[l] > 0))
+            d = bf16(mm(d, Wq[l]) * (acts[l] > 0))
     new = [(W - lr * gW, b - lr * gb) for (W, b), (gW, gb) in zip(P, grads)]
     return new, grads

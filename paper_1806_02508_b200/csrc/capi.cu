@@ -442,6 +442,46 @@ extern "C" int lbbsp_lr_data_create(uint64_t seed, int n, int d, double noise, l
   return lbbsp_lr_data_upload(feat.data(), lab.data(), n, d, out);
 }
 
+// generate_dataset / separator_params (sgd.cpp:32-57) into host arrays:
+// setup-time generators for the reference-shaped API (include/lbbsp/sgd.hpp)
+extern "C" int lbbsp_generate_dataset(uint64_t seed, int n, int d, double noise, double* h_features,
+                                      double* h_labels) {
+  if (n < 1) return set_error(LBBSP_INVALID_ARGUMENT, "generate_dataset: n must be >= 1");
+  if (d < 1) return set_error(LBBSP_INVALID_ARGUMENT, "generate_dataset: d must be >= 1");
+  std::vector<double> feat, lab;
+  host_generate_dataset(seed, n, d, noise, feat, lab);
+  std::memcpy(h_features, feat.data(), sizeof(double) * feat.size());
+  std::memcpy(h_labels, lab.data(), sizeof(double) * lab.size());
+  return LBBSP_OK;
+}
+
+extern "C" int lbbsp_separator_params(uint64_t seed, int d, double* h_out) {
+  if (d < 1) return set_error(LBBSP_INVALID_ARGUMENT, "separator_params: d must be >= 1");
+  HostRng tr(mix_seed(seed, 0x5e9a7a70ull));
+  for (int j = 0; j < d; ++j) h_out[j] = tr.uniform(-1.0, 1.0);
+  return LBBSP_OK;
+}
+
+// apply_update (sgd.cpp:92-99) on host buffers: the K9 device kernel
+// (params -= lr * g, no FMA contraction)
+extern "C" int lbbsp_apply_update(double* h_params, int dim, const double* h_grad, double lr) {
+  LBBSP_REQUIRE_DEVICE();
+  if (dim < 0) return set_error(LBBSP_INVALID_ARGUMENT, "apply_update: gradient dimension mismatch");
+  if (dim == 0) return LBBSP_OK;
+  DBuf<double> p(dim), g(dim);
+  DBuf<int> one(1);
+  const int b = 1;
+  LBBSP_CUDA_CHECK(cudaMemcpy(p.p, h_params, sizeof(double) * dim, cudaMemcpyHostToDevice));
+  LBBSP_CUDA_CHECK(cudaMemcpy(g.p, h_grad, sizeof(double) * dim, cudaMemcpyHostToDevice));
+  LBBSP_CUDA_CHECK(cudaMemcpy(one.p, &b, sizeof(int), cudaMemcpyHostToDevice));
+  int rc = run_sync([&](cudaStream_t s, lbbsp_dev_status* st) {
+    return launch_aggregate_apply(g.p, one.p, 1, dim, 0, lr, p.p, nullptr, nullptr, st, s);
+  });
+  if (rc) return rc;
+  LBBSP_CUDA_CHECK(cudaMemcpy(h_params, p.p, sizeof(double) * dim, cudaMemcpyDeviceToHost));
+  return LBBSP_OK;
+}
+
 extern "C" int lbbsp_lr_data_destroy(lbbsp_lr_data* data) {
   delete data;
   return LBBSP_OK;

@@ -20,6 +20,7 @@
 #pragma once
 #include <cuda_bf16.h>
 
+#include "interfere.cuh"
 #include "tc_ptx.cuh"
 
 namespace lbbsp {
@@ -59,6 +60,8 @@ struct GemmArgs {
   long long ld_aux;
   // per-group phase timing (globaltimer ns): [n_groups][2] = {min start, max end}
   unsigned long long* timing;
+  // straggler injection on the worker's own CTAs after its tiles (interfere.cuh)
+  Interference intf;
 };
 
 template <int BN>
@@ -159,8 +162,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int num_tiles = g >= 0 ? m_tiles * n_tiles : 0;
   const int k_blocks = k_len > 0 ? (k_len + kBK - 1) / kBK : 0;
 
-  if (g >= 0 && args.timing && threadIdx.x == 0)
-    atomicMin(&args.timing[2 * g], static_cast<unsigned long long>(globaltimer()));
+  const unsigned long long t_cta0 = globaltimer();
+  if (g >= 0 && args.timing && threadIdx.x == 0) atomicMin(&args.timing[2 * g], t_cta0);
 
   if (warp == 0) {
     // =========================== TMA producer =============================
@@ -341,9 +344,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+  if (g >= 0 && args.n_groups > 0)
+    interfere(args.intf, g, args.timing ? &args.timing[2 * g] : nullptr, t_cta0);
   if (g >= 0 && args.timing && threadIdx.x == 0)
     atomicMax(&args.timing[2 * g + 1], static_cast<unsigned long long>(globaltimer()));
-  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
 }
 
 }  // namespace tc

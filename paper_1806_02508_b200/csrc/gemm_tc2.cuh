@@ -156,8 +156,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int n_tiles = (args.N + BN - 1) / BN;
   const int num_tiles = idle ? 0 : m_tiles * n_tiles;
   const int k_blocks = k_len > 0 ? (k_len + kBK - 1) / kBK : 0;
-  if (!idle && args.timing && threadIdx.x == 0)
-    atomicMin(&args.timing[0], static_cast<unsigned long long>(globaltimer()));
+  const unsigned long long t_cta0 = globaltimer();
+  if (!idle && args.timing && threadIdx.x == 0) atomicMin(&args.timing[0], t_cta0);
 
   if (warp == 0) {
     // ==================== TMA producer (both CTAs) ====================
@@ -314,9 +314,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
+  if (warp == 1) tmem_dealloc_pair<kTmemCols>(tmem_base);
+  if (!idle && args.n_groups > 0) interfere(args.intf, 0, args.timing ? &args.timing[0] : nullptr, t_cta0);
   if (!idle && args.timing && threadIdx.x == 0)
     atomicMax(&args.timing[1], static_cast<unsigned long long>(globaltimer()));
-  if (warp == 1) tmem_dealloc_pair<kTmemCols>(tmem_base);
 }
 
 }  // namespace tc

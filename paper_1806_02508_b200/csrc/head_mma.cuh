@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
   __syncthreads();
   tc::pdl_wait();  // H, labels and row scales come from the kernels before
   tc::pdl_launch_dependents();
-  if (timing && threadIdx.x == 0) atomicMin(&timing[2 * g], static_cast<unsigned long long>(gtimer()));
+  const unsigned long long t_cta0 = gtimer();
+  if (timing && threadIdx.x == 0) atomicMin(&timing[2 * g], t_cta0);
   if (tile < n_tiles) stage_tile(hbuf0, H, r0 + tile * 16, r1, lane);
 
   const float b_lo0 = bias[2 * tq], b_lo1 = bias[2 * tq + 1];
@@ -402,6 +403,7 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
       counters[g] = 0u;
     }
   }
+  if (TRAIN && G.n > 0) interfere(G.intf, g, timing ? &timing[2 * g] : nullptr, t_cta0);
   if (timing && threadIdx.x == 0) atomicMax(&timing[2 * g + 1], static_cast<unsigned long long>(gtimer()));
 }
 

@@ -85,13 +85,40 @@ __global__ void init_x_kernel(bf16* x, long long count, uint64_t seed) {
 }
 
 // labels = argmax_c(W* x + U[-0.1, 0.1]) with a seeded teacher W* (the
-// multi-class generalisation of generate_dataset, sgd.cpp:32-57); large
-// heads draw hashed labels.
+// multi-class generalisation of generate_dataset, sgd.cpp:32-57), so every
+// head width has a learnable target. Ties go to the lowest class.
 __global__ void teacher_labels_kernel(const bf16* x, int* y, int d, int d_out, uint64_t seed) {
   __shared__ float acc[32];
   const int i = blockIdx.x;
   if (d_out > 32) {
-    if (threadIdx.x == 0) y[i] = static_cast<int>(hash64(seed ^ (0x1abe1ull + i)) % d_out);
+    // wide heads: a thread per class (strided), the sample row in shared memory
+    extern __shared__ float xs[];
+    for (int j = threadIdx.x; j < d; j += blockDim.x) xs[j] = __bfloat162float(x[static_cast<long long>(i) * d + j]);
+    __syncthreads();
+    float bv = -1e30f;
+    int best = d_out;
+    for (int c = threadIdx.x; c < d_out; c += blockDim.x) {
+      float s = 0.f;
+      for (int j = 0; j < d; ++j)
+        s += hash_uniform(seed ^ 0x5e9a7a70ull, static_cast<uint64_t>(c) * d + j, -1.f, 1.f) * xs[j];
+      const float v = s + hash_uniform(seed ^ 0xda7a5e7ull, static_cast<uint64_t>(i) * d_out + c, -0.1f, 0.1f);
+      if (v > bv) { bv = v; best = c; }
+    }
+    // block argmax, lowest class on ties
+    __shared__ float rv[32];
+    __shared__ int rc[32];
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, best, o);
+      if (ov > bv || (ov == bv && oc < best)) { bv = ov; best = oc; }
+    }
+    if ((threadIdx.x & 31) == 0) { rv[threadIdx.x / 32] = bv; rc[threadIdx.x / 32] = best; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < static_cast<int>(blockDim.x / 32); ++w)
+        if (rv[w] > bv || (rv[w] == bv && rc[w] < best)) { bv = rv[w]; best = rc[w]; }
+      y[i] = best;
+    }
     return;
   }
   if (threadIdx.x < 32) acc[threadIdx.x] = 0.f;
@@ -171,7 +198,9 @@ struct PlanDev {
   double* rec_loss;
   lbbsp_dev_status* status;
   unsigned long long* stamps;  // [16] globaltimer at kernel boundaries (last round)
-  unsigned* gather_done;       // single rank: CTAs of the beside-the-plan gather that finished
+  unsigned long long* gather_done;  // single rank: gather CTAs finished, summed over all rounds
+  int straggler_mode;          // LBBSP_STRAGGLE_INTERFERE | LBBSP_STRAGGLE_SM_CAP
+  float2* intf_w;              // [n_local] {availability, HBM share of the injected time}
   int gather_ctas;             // > 0: the plan completes only once they all have
 };
 
@@ -180,21 +209,34 @@ __device__ __forceinline__ void stamp(const PlanDev& D, int i) {
 }
 
 // Single rank: the gather of the whole batch runs beside the plan; the plan
-// completes only once every gather CTA has, so the forward GEMM depends on the
-// plan alone and keeps its programmatic (overlapped) launch.
-__device__ __forceinline__ void wait_gather(const PlanDev& D) {
-  if (D.gather_ctas > 0 && threadIdx.x == 0) {
-    const unsigned long long t0 = gtimer();
-    unsigned seen;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(D.gather_done) : "memory");
-      if (gtimer() - t0 > 2000000000ull) {  // 2 s: the gather never ran -- fail, do not hang
-        set_status(D.status, LBBSP_RUNTIME, 0, seen, D.gather_ctas);
-        break;
-      }
-    } while (seen < static_cast<unsigned>(D.gather_ctas));
-    *D.gather_done = 0u;
+// completes only once every gather CTA of this round has, so the forward GEMM
+// depends on the plan alone and keeps its programmatic (overlapped) launch.
+// The arrival count only grows: round k waits for (k + 1) * gather_ctas, so a
+// late CTA of an earlier round can never satisfy a later round's wait. A wait
+// that times out (the gather never ran: kernels serialised by a tool) poisons
+// the round -- status set, every worker's row range emptied -- instead of
+// computing on a stale X. Tools that serialise kernels get the event join
+// instead (LBBSP_GATHER_JOIN / CUDA_INJECTION64_PATH, see enqueue_iteration).
+__device__ __forceinline__ bool wait_gather(const PlanDev& D, long long k) {
+  __shared__ int ok_s;
+  if (threadIdx.x == 0) {
+    ok_s = 1;
+    if (D.gather_ctas > 0) {
+      const unsigned long long want = static_cast<unsigned long long>(k + 1) * D.gather_ctas;
+      const unsigned long long t0 = gtimer();
+      unsigned long long seen;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(seen) : "l"(D.gather_done) : "memory");
+        if (gtimer() - t0 > 2000000000ull) {  // 2 s: the gather never ran -- fail, do not hang
+          set_status(D.status, LBBSP_RUNTIME, 0, static_cast<long long>(seen), static_cast<long long>(want));
+          ok_s = 0;
+          break;
+        }
+      } while (seen < want);
+    }
   }
+  __syncthreads();
+  return ok_s != 0;
 }
 
 // P1-P4: trace -> caps, predictor -> v_pred, solver -> sizes, local slice,
@@ -226,14 +268,27 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
     share_s[i] = D.share[i];
     D.c_now[i] = c;
     D.m_now[i] = m;
-    // SM availability = the worker's relative speed in the reference model,
+    // availability = the worker's relative speed in the reference model,
     // effective_speed * speed_mult = c * MemPenalty(m) * mult (cluster_sim.cpp:22-29),
-    // capped at 1: memory pressure lowers the worker's SM share the way it lowers
-    // v0 there (HBM is chip-wide, so it cannot slow one co-resident partition alone)
+    // capped at 1
     const double pen = m >= 0.5 ? 1.0 : dadd(0.25, dmul(0.75, ddiv(m, 0.5)));
     const double a = dmul(dmul(c, pen), mult);
     avail[i] = a < 1.0 ? a : 1.0;
-    const double vp = len >= 1 ? predictor_predict_d(D.pred, i, len, c, m) : 0.0;
+    if (D.straggler_mode == LBBSP_STRAGGLE_INTERFERE) {
+      const int li = i - D.rank * D.n_local;
+      if (li >= 0 && li < D.n_local) {
+        // interference (interfere.cuh): the phase lasts work / a; the part of
+        // the injected time the memory penalty adds (1/a - 1/a_sm, a_sm =
+        // min(1, c mult)) is HBM-bound, the rest SM-bound
+        const double asm_ = fmin(1.0, c * mult), at = avail[i];
+        const double hbm = at < 1.0 ? fmax(0.0, fmin(1.0, (1.0 / at - 1.0 / asm_) / (1.0 / at - 1.0))) : 0.0;
+        D.intf_w[li] = make_float2(static_cast<float>(at), static_cast<float>(hbm));
+      }
+    }
+    // Perfect (step_sync: v_pred = v_actual, cluster_sim.cpp:362-367): the
+    // worker's true relative speed this round is its injected availability
+    const double vp = D.pred.kind == LBBSP_PRED_PERFECT ? avail[i]
+                      : (len >= 1 ? predictor_predict_d(D.pred, i, len, c, m) : 0.0);
     vp_s[i] = vp;
     D.v_pred[i] = vp;
   }
@@ -249,7 +304,7 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
   }
   __syncthreads();
   if (code) {
-    wait_gather(D);
+    wait_gather(D, k);
     return;
   }
   const int first = D.rank * D.n_local;
@@ -265,7 +320,10 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
       r += sz[w];
       D.r1[i] = r;
       const double share = share_s[w];
-      int cap = static_cast<int>(floor(static_cast<double>(D.sm_budget) * share * avail[w]));
+      // SM-cap mode: the availability scales the CTA partition; interference
+      // mode: the partition is the nominal share, the availability is injected
+      const double av = D.straggler_mode == LBBSP_STRAGGLE_SM_CAP ? avail[w] : 1.0;
+      int cap = static_cast<int>(floor(static_cast<double>(D.sm_budget) * share * av));
       cap = cap < 1 ? 1 : cap;
       if (c0 + cap > D.sm_budget) cap = D.sm_budget - c0 > 0 ? D.sm_budget - c0 : 1;
       D.cta0[i] = c0;
@@ -310,7 +368,10 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
     for (int i = tid; i < D.n_local; i += blockDim.x)
       D.rec_caps[static_cast<size_t>(row) * n + D.rank * D.n_local + i] = D.ctan[i];
   }
-  wait_gather(D);
+  if (!wait_gather(D, k)) {  // poisoned round: no worker computes on a stale batch
+    for (int i = tid; i < D.n_local; i += blockDim.x) D.r1[i] = D.r0[i];
+    if (tid == 0) *D.local_rows = 0;
+  }
   stamp(D, 1);
 }
 
@@ -365,15 +426,20 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      atomicAdd(D.gather_done, 1u);
+      atomicAdd(D.gather_done, 1ull);
     }
   }
 }
 
-__device__ __forceinline__ void phase_begin(unsigned long long* timing, int g) {
-  if (timing && threadIdx.x == 0) atomicMin(&timing[2 * g], static_cast<unsigned long long>(gtimer()));
+__device__ __forceinline__ unsigned long long phase_begin(unsigned long long* timing, int g) {
+  const unsigned long long t = gtimer();
+  if (timing && threadIdx.x == 0) atomicMin(&timing[2 * g], t);
+  return t;
 }
-__device__ __forceinline__ void phase_end(unsigned long long* timing, int g) {
+// end of worker g's share of a phase: the injected interference, then the stamp
+__device__ __forceinline__ void phase_finish(const Groups& G, unsigned long long* timing, int g,
+                                             unsigned long long t_cta0) {
+  if (G.n > 0) interfere(G.intf, g, timing ? &timing[2 * g] : nullptr, t_cta0);
   if (timing && threadIdx.x == 0) atomicMax(&timing[2 * g + 1], static_cast<unsigned long long>(gtimer()));
 }
 
@@ -385,7 +451,7 @@ __global__ void __launch_bounds__(256) softmax_ce_kernel(
     unsigned long long* timing) {
   int g, cta_in, cta_cnt;
   if (!my_group(G, &g, &cta_in, &cta_cnt)) return;
-  phase_begin(timing, g);
+  const unsigned long long t_cta0 = phase_begin(timing, g);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   const int r0 = G.n ? G.r0[g] : 0, r1 = G.n ? G.r1[g] : rows_total;
   double lsum = 0.0;
@@ -439,7 +505,7 @@ __global__ void __launch_bounds__(256) softmax_ce_kernel(
   }
   if (loss_acc && lane == 0 && lsum != 0.0) atomicAdd(loss_acc, lsum);
   __syncthreads();
-  phase_end(timing, g);
+  phase_finish(G, timing, g, t_cta0);
 }
 
 // Softmax-CE head for n_out = 256 * NV (NV <= 16): one warp per row, the row
@@ -454,7 +520,7 @@ __global__ void __launch_bounds__(256) softmax_ce_reg_kernel(
   if (!my_group(G, &g, &cta_in, &cta_cnt)) return;
   tc::pdl_wait();
   tc::pdl_launch_dependents();
-  phase_begin(timing, g);
+  const unsigned long long t_cta0 = phase_begin(timing, g);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   const int r0 = G.n ? G.r0[g] : 0, r1 = G.n ? G.r1[g] : rows_total;
   double lsum = 0.0;
@@ -522,7 +588,7 @@ __global__ void __launch_bounds__(256) softmax_ce_reg_kernel(
   }
   if (loss_acc && lane == 0 && lsum != 0.0) atomicAdd(loss_acc, lsum);
   __syncthreads();
-  phase_end(timing, g);
+  phase_finish(G, timing, g, t_cta0);
 }
 
 static cudaError_t launch_softmax_ce(int sms, cudaStream_t s, bool pdl, Groups G, int rows_total,
@@ -567,7 +633,7 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
   const int rbs = max(1, min(kBiasMaxRowBlocks, cta_cnt / ncb));
   const int used = rbs * ncb;
   if (cta_in >= used) return;
-  phase_begin(timing, g);
+  const unsigned long long t_cta0 = phase_begin(timing, g);
   const int r0 = G.r0[g], r1 = G.r1[g];
   const int cb = cta_in % ncb, rb = cta_in / ncb;
   const int rows = r1 - r0, per = (rows + rbs - 1) / rbs;
@@ -647,7 +713,7 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
     }
     if (threadIdx.x == 0) counters[g] = 0u;
   }
-  phase_end(timing, g);
+  phase_finish(G, timing, g, t_cta0);
 }
 
 // Segmented reduction of the worker partial slabs + SGD apply (K8+K9), HBM-
@@ -1147,6 +1213,7 @@ struct lbbsp_mlp {
   bf16* stage_x = nullptr;
   int* stage_y = nullptr;
   cudaEvent_t ev_layer[LBBSP_MLP_MAX_LAYERS] = {};
+  cudaEvent_t ev_dx[LBBSP_MLP_MAX_LAYERS] = {};  // dX_l done: the bucketed apply of W_l may run
   cudaStream_t comm_stream = nullptr;
   // copy-engine bucket exchange (one worker per GPU with peers, LBBSP_NCCL_BUCKETS unset)
   cudaStream_t xfer_stream = nullptr;
@@ -1193,6 +1260,15 @@ struct lbbsp_mlp {
   bool use_pair = false;  // one worker per GPU: CTA-pair GEMMs
   bf16** dz_ptrs = nullptr;
   int* dz_widths = nullptr;
+  Interference intf{};  // straggler injection state (interference mode)
+  // e2e plumbing: cached host-buffer lookups (lbbsp_mlp_read_result_async,
+  // lbbsp_mlp_step_e2e)
+  int* res_host_sizes = nullptr;
+  double* res_host_loss = nullptr;
+  int* res_dev_sizes = nullptr;
+  double* res_dev_loss = nullptr;
+  const void* warm_x = nullptr;
+  const int* warm_y = nullptr;
 
   ~lbbsp_mlp() {
     for (void* p : peer_map)
@@ -1217,6 +1293,8 @@ struct lbbsp_mlp {
     if (ev_xfer) cudaEventDestroy(ev_xfer);
     if (xfer_stream) cudaStreamDestroy(xfer_stream);
     for (auto& e : ev_layer)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : ev_dx)
       if (e) cudaEventDestroy(e);
     if (comm_stream) cudaStreamDestroy(comm_stream);
     for (void* p : allocs) cudaFree(p);
@@ -1244,6 +1322,7 @@ struct lbbsp_mlp {
     G.r1 = D.r1;
     G.cta0 = D.cta0;
     G.ctan = D.ctan;
+    G.intf = intf;
     return G;
   }
   unsigned long long* phase_slot(int p) { return D.timing + 2ll * p * n_local; }
@@ -1267,6 +1346,7 @@ int launch_grouped(lbbsp_mlp* m, GemmPlan& p, int mode, unsigned long long* timi
   p.args.g_cta0 = m->D.cta0;
   p.args.g_ctan = m->D.ctan;
   p.args.timing = timing;
+  p.args.intf = m->intf;
   p.ctas = m->D.sm_budget;
   p.pdl = m->use_pdl;
   return gemm_launch(p, s);
@@ -1281,13 +1361,17 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   const int gather_ctas = std::max(sms, std::min(sms * 8, (B_cap * (dims[0] / 8) + 1023) / 1024));
   // single rank: the plan waits for the gather on the device (no graph join);
   // set before either kernel is captured, both read it
-  D.gather_ctas = cfg.world == 1 ? gather_ctas : 0;
+  // Kernels serialised by a tool (ncu replay, compute-sanitizer) cannot run the
+  // gather beside a spinning plan: join with a graph edge there instead.
+  const bool join = getenv("LBBSP_GATHER_JOIN") || getenv("CUDA_INJECTION64_PATH");
+  D.gather_ctas = cfg.world == 1 && !join ? gather_ctas : 0;
   if (cfg.world == 1) {  // one rank gathers all B rows: independent of the plan
     LBBSP_CUDA_CHECK(cudaEventRecord(ev_gather0, s));
     LBBSP_CUDA_CHECK(cudaStreamWaitEvent(side, ev_gather0, 0));
     gather_kernel<<<gather_ctas, 256, 0, side>>>(D, streams, B_total, data_x, data_y, dims[0], X, y,
                                                  B_total, partial, P, reg_off, reg_len, n_reg);
     LBBSP_CUDA_CHECK(cudaEventRecord(ev_gather1, side));
+    if (join) LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_gather1, 0));
     plan_kernel<<<1, 256, 0, s>>>(D, row_scale);
   } else {
     plan_kernel<<<1, 256, 0, s>>>(D, row_scale);
@@ -1351,16 +1435,16 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     int rc = launch_grouped(this, dw[l], tc::kKSplit, phase_slot(ph++), s);
     if (rc) return rc;
     ++nl;
+    const long long seg0 = off_w[l], seg1 = l + 1 < L ? off_w[l + 1] : P;
+    const long long W = cfg.world;
+    auto sl0 = [&](long long r) { return seg0 + ((seg1 - seg0) / 8 * r / W) * 8; };
+    bf16* ag_local = peers ? reinterpret_cast<bf16*>(px.grd_local) + W * P : nullptr;
     if (bucketed) {
-      const long long seg0 = off_w[l], seg1 = l + 1 < L ? off_w[l + 1] : P;
+      // the exchange of this layer's bucket starts as soon as its dW/db are final
       LBBSP_CUDA_CHECK(cudaEventRecord(ev_layer[l], s));
       LBBSP_CUDA_CHECK(cudaStreamWaitEvent(comm_stream, ev_layer[l], 0));
-      // apply this layer's update as soon as its bucket is reduced, beside
-      // the rest of the backward pass
       if (ce_buckets && ce_two_shot) {
         // reduce-scatter: slice r of this bucket -> slot[rank] of rank r
-        const long long n = seg1 - seg0, W = cfg.world;
-        auto sl0 = [&](long long r) { return seg0 + (n / 8 * r / W) * 8; };
         LBBSP_CUDA_CHECK(cudaStreamWaitEvent(xfer_stream, ev_layer[l], 0));
         // (one stream for all peers: a copy stream per peer measured slower at N=4)
         for (int r = 0; r < cfg.world; ++r) {
@@ -1373,7 +1457,6 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
         // own slice: rank-ordered fp32 sum -> all-gather buffer of every rank
         const long long m0 = sl0(cfg.rank), m1 = sl0(cfg.rank + 1);
         peer_wait_row_kernel<<<1, 32, 0, comm_stream>>>(px, 2 + l, D.round_k, D.status);
-        bf16* ag_local = reinterpret_cast<bf16*>(px.grd_local) + W * P;
         peer_slice_reduce_kernel<<<sms, 256, 0, comm_stream>>>(px, m0, m1 - m0, P, gradb, ag_local);
         for (int r = 0; r < cfg.world; ++r) {
           if (r == cfg.rank) continue;
@@ -1384,13 +1467,11 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
         peer_signal_row_kernel<<<1, 32, 0, comm_stream>>>(px, 2 + LBBSP_MLP_MAX_LAYERS + l);
         peer_wait_row_kernel<<<1, 32, 0, comm_stream>>>(px, 2 + LBBSP_MLP_MAX_LAYERS + l, D.round_k,
                                                         D.status);
-        apply_bf16_kernel<<<sms * 2, 256, 0, comm_stream>>>(ag_local + seg0, n, params + seg0, pb + seg0,
-                                                            static_cast<float>(cfg.learning_rate));
-        nl += 5;
+        nl += 4;
       } else if (ce_buckets) {
         // push this bucket into slot[rank] of every peer (copy engines), then
-        // raise the peers' arrival counters; wait for the peers' buckets and
-        // apply the rank-ordered sum on the comm stream
+        // raise the peers' arrival counters; wait for the peers' buckets on
+        // the comm stream
         LBBSP_CUDA_CHECK(cudaStreamWaitEvent(xfer_stream, ev_layer[l], 0));
         const size_t bytes = sizeof(bf16) * static_cast<size_t>(seg1 - seg0);
         for (int r = 0; r < cfg.world; ++r) {
@@ -1400,29 +1481,43 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
         }
         peer_bucket_signal_kernel<<<1, 32, 0, xfer_stream>>>(px, l);
         peer_bucket_wait_kernel<<<1, 32, 0, comm_stream>>>(px, l, D.round_k, D.status);
-        peer_bucket_apply_kernel<<<sms * 2, 256, 0, comm_stream>>>(
-            px, seg0, seg1 - seg0, P, gradb, params, pb, static_cast<float>(cfg.learning_rate));
         nl += 2;
       } else if (gradb) {
         if (nccl_api()->AllReduce(gradb + seg0, gradb + seg0, static_cast<size_t>(seg1 - seg0),
                                   ncclBfloat16, ncclSum, comm, comm_stream) != ncclSuccess)
           return set_error(LBBSP_NCCL, "ncclAllReduce (bucket %d) failed", l);
-        apply_bf16_kernel<<<sms * 2, 256, 0, comm_stream>>>(gradb + seg0, seg1 - seg0, params + seg0,
-                                                            pb + seg0,
-                                                            static_cast<float>(cfg.learning_rate));
       } else {
         if (nccl_api()->AllReduce(partial + seg0, partial + seg0, static_cast<size_t>(seg1 - seg0),
                                   ncclFloat, ncclSum, comm, comm_stream) != ncclSuccess)
           return set_error(LBBSP_NCCL, "ncclAllReduce (bucket %d) failed", l);
-        reduce_apply_kernel<<<sms * 2, 256, 0, comm_stream>>>(
-            partial + seg0, 1, seg1 - seg0, grad + seg0, params + seg0, pb + seg0,
-            static_cast<float>(cfg.learning_rate), 1, nullptr);
       }
-      ++nl;
     }
     if (l > 0) {
       rc = launch_grouped(this, dx[l], tc::kRows, phase_slot(ph++), s);
       if (rc) return rc;
+      ++nl;
+    }
+    if (bucketed) {
+      // dX_l reads the bf16 W_l (its B operand): the update of segment l must
+      // not overwrite it before that GEMM is done, so the apply waits for it
+      // (SGD semantics: every update after the full backward pass)
+      if (l > 0) {
+        LBBSP_CUDA_CHECK(cudaEventRecord(ev_dx[l], s));
+        LBBSP_CUDA_CHECK(cudaStreamWaitEvent(comm_stream, ev_dx[l], 0));
+      }
+      const float lrf = static_cast<float>(cfg.learning_rate);
+      if (ce_buckets && ce_two_shot)
+        apply_bf16_kernel<<<sms * 2, 256, 0, comm_stream>>>(ag_local + seg0, seg1 - seg0, params + seg0,
+                                                            pb + seg0, lrf);
+      else if (ce_buckets)
+        peer_bucket_apply_kernel<<<sms * 2, 256, 0, comm_stream>>>(px, seg0, seg1 - seg0, P, gradb, params,
+                                                                   pb, lrf);
+      else if (gradb)
+        apply_bf16_kernel<<<sms * 2, 256, 0, comm_stream>>>(gradb + seg0, seg1 - seg0, params + seg0,
+                                                            pb + seg0, lrf);
+      else
+        reduce_apply_kernel<<<sms * 2, 256, 0, comm_stream>>>(partial + seg0, 1, seg1 - seg0, grad + seg0,
+                                                              params + seg0, pb + seg0, lrf, 1, nullptr);
       ++nl;
     }
   }
@@ -1433,6 +1528,20 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     // speeds, all-gathered over NVLink
     LBBSP_CUDA_CHECK(launch_maybe_pdl(peer_speed_kernel, 1, 256, 0, s, use_pdl, D, px, n_phases));
     ++nl;
+  } else if (cfg.world > 1 && ce_buckets) {
+    // one worker per GPU, copy-engine buckets: the speed all-gather runs over
+    // peer memory on the comm stream after the last bucket's apply; its wait
+    // for every rank doubles as the round's barrier (no rank refills a peer's
+    // bucket slots before that peer has applied them). No NCCL on this path.
+    LBBSP_CUDA_CHECK(cudaEventRecord(ev_speed, s));
+    LBBSP_CUDA_CHECK(cudaStreamWaitEvent(comm_stream, ev_speed, 0));
+    peer_speed_kernel<<<1, 256, 0, comm_stream>>>(D, px, n_phases);
+    ++nl;
+    LBBSP_CUDA_CHECK(cudaEventRecord(ev_comm, comm_stream));
+    LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_comm, 0));
+    // the local buckets must not be overwritten before they left
+    LBBSP_CUDA_CHECK(cudaEventRecord(ev_xfer, xfer_stream));
+    LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_xfer, 0));
   } else if (cfg.world > 1) {
     speed_kernel<<<1, 32 * ((n_local + 31) / 32), 0, s>>>(D, n_phases);
     ++nl;
@@ -1597,6 +1706,7 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_speed, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_comm, cudaEventDisableTiming));
   for (auto& e : m.ev_layer) LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : m.ev_dx) LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.comm_stream, cudaStreamNonBlocking));
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.xfer_stream, cudaStreamNonBlocking));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_xfer, cudaEventDisableTiming));
@@ -1670,7 +1780,8 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
 
   // dataset + parameters (setup-time device generators)
   init_x_kernel<<<512, 256>>>(m.data_x, static_cast<long long>(m.N_data) * d0, c.dataset_seed);
-  teacher_labels_kernel<<<m.N_data, 256>>>(m.data_x, m.data_y, d0, c.dims[L], c.dataset_seed);
+  teacher_labels_kernel<<<m.N_data, 256, c.dims[L] > 32 ? sizeof(float) * d0 : 0>>>(
+      m.data_x, m.data_y, d0, c.dims[L], c.dataset_seed);
   for (int l = 0; l < L; ++l)
     init_params_kernel<<<512, 256>>>(m.params, m.pb, m.off_w[l], m.off_b[l], c.dims[l + 1], c.dims[l],
                                      c.seed ^ (0x9a4c0ull + l));
@@ -1733,6 +1844,21 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(m.alloc(&D.loss_acc, 1));
   LBBSP_CUDA_CHECK(m.alloc(&D.stamps, 16));
   LBBSP_CUDA_CHECK(m.alloc(&D.round_k, 1));
+  if (c.straggler_mode != LBBSP_STRAGGLE_INTERFERE && c.straggler_mode != LBBSP_STRAGGLE_SM_CAP)
+    return set_error(LBBSP_INVALID_ARGUMENT, "mlp: unknown straggler_mode %d", c.straggler_mode);
+  D.straggler_mode = c.straggler_mode;
+  if (c.straggler_mode == LBBSP_STRAGGLE_INTERFERE) {
+    float2* w = nullptr;
+    LBBSP_CUDA_CHECK(m.alloc(&w, m.n_local));
+    D.intf_w = w;
+    m.intf.w = w;
+    // HBM-bound interference source: larger than the 126 MB L2
+    const long long nvec = 192ll * 1024 * 1024 / 16;
+    uint4* buf = nullptr;
+    LBBSP_CUDA_CHECK(m.alloc(&buf, static_cast<size_t>(nvec)));
+    m.intf.buf = buf;
+    m.intf.nvec = nvec;
+  }
   // end-to-end plumbing (lbbsp_mlp_load_data_async / read_result_async)
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.copy_stream, cudaStreamNonBlocking));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_staged, cudaEventDisableTiming));
@@ -1742,7 +1868,7 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(m.alloc(&m.result, static_cast<size_t>(m.n_total) + 2));
   LBBSP_CUDA_CHECK(m.alloc(&m.arrive, 1));
   {
-    unsigned* gd = nullptr;
+    unsigned long long* gd = nullptr;
     LBBSP_CUDA_CHECK(m.alloc(&gd, 1));
     m.D.gather_done = gd;
   }
@@ -1970,8 +2096,12 @@ extern "C" int lbbsp_mlp_init_peers(lbbsp_mlp* m, const unsigned char* h_handles
 extern "C" void* lbbsp_mlp_stream(lbbsp_mlp* m) { return m->stream; }
 
 extern "C" int lbbsp_mlp_run(lbbsp_mlp* m, int iterations) {
-  if (m->cfg.world > 1 && !m->comm)
-    return set_error(LBBSP_NCCL, "mlp: world > 1 needs lbbsp_mlp_init_comm first");
+  // several GPUs: the peer-memory exchange needs no communicator (several
+  // workers per GPU, or one worker per GPU with copy-engine buckets); every
+  // other exchange runs on NCCL
+  const bool peer_only = m->peers && (m->n_local > 1 || m->ce_ok);
+  if (m->cfg.world > 1 && !m->comm && !peer_only)
+    return set_error(LBBSP_NCCL, "mlp: world > 1 needs lbbsp_mlp_init_comm (or peers) first");
   if (!m->exec) {
     LBBSP_CUDA_CHECK(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
     int rc = m->enqueue_iteration(m->stream);
@@ -2096,17 +2226,24 @@ __global__ void last_row_kernel(const int* rows, const int* rec_sizes, const dou
 
 // Page-locked host buffers are written by the kernel itself (zero-copy over
 // the unified address space); other host memory goes through a D2H copy.
+// The pointer lookup is cached for the last buffer pair (a per-step
+// cudaPointerGetAttributes would sit on the host's critical path).
 extern "C" int lbbsp_mlp_read_result_async(lbbsp_mlp* m, int* h_sizes, double* h_loss) {
-  cudaPointerAttributes a{}, b{};
-  const bool mapped = cudaPointerGetAttributes(&a, h_sizes) == cudaSuccess &&
-                      cudaPointerGetAttributes(&b, h_loss) == cudaSuccess &&
-                      a.type == cudaMemoryTypeHost && b.type == cudaMemoryTypeHost &&
-                      a.devicePointer && b.devicePointer;
-  cudaGetLastError();
-  if (mapped) {
+  if (h_sizes != m->res_host_sizes || h_loss != m->res_host_loss) {
+    cudaPointerAttributes a{}, b{};
+    const bool mapped = cudaPointerGetAttributes(&a, h_sizes) == cudaSuccess &&
+                        cudaPointerGetAttributes(&b, h_loss) == cudaSuccess &&
+                        a.type == cudaMemoryTypeHost && b.type == cudaMemoryTypeHost &&
+                        a.devicePointer && b.devicePointer;
+    cudaGetLastError();
+    m->res_host_sizes = h_sizes;
+    m->res_host_loss = h_loss;
+    m->res_dev_sizes = mapped ? static_cast<int*>(a.devicePointer) : nullptr;
+    m->res_dev_loss = mapped ? static_cast<double*>(b.devicePointer) : nullptr;
+  }
+  if (m->res_dev_sizes) {
     last_row_kernel<<<1, 256, 0, m->stream>>>(m->D.rows, m->D.rec_sizes, m->D.loss_acc, m->N_data,
-                                              m->n_total, static_cast<int*>(a.devicePointer),
-                                              static_cast<double*>(b.devicePointer));
+                                              m->n_total, m->res_dev_sizes, m->res_dev_loss);
     LBBSP_CUDA_CHECK(cudaGetLastError());
     return LBBSP_OK;
   }
@@ -2166,4 +2303,30 @@ extern "C" int lbbsp_mlp_debug_timeline(lbbsp_mlp* m, unsigned long long* out, i
                               cudaMemcpyDeviceToHost));
   *n_phases = m->n_phases;
   return LBBSP_OK;
+}
+
+// One end-to-end step through the C-ABI: stage this step's inputs from host
+// memory (H2D on the copy stream, overlapping the round in flight), run the
+// round, write its sizes + loss to host memory. The first call with a new
+// host buffer pair first-touches it with a synchronous copy (the first DMA
+// out of a freshly page-locked buffer runs at about half the link rate,
+// profiles/r01_e2e_warm_probe.txt), outside any steady-state step.
+extern "C" int lbbsp_mlp_step_e2e(lbbsp_mlp* m, const void* h_x_bf16, const int* h_labels, int* h_sizes,
+                                  double* h_loss) {
+  if (h_x_bf16 != m->warm_x || h_labels != m->warm_y) {
+    const size_t bx = sizeof(bf16) * m->N_data * m->dims[0], by = sizeof(int) * m->N_data;
+    LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->copy_stream));
+    for (int i = 0; i < 2; ++i) {
+      LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_x, h_x_bf16, bx, cudaMemcpyHostToDevice, m->copy_stream));
+      LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_y, h_labels, by, cudaMemcpyHostToDevice, m->copy_stream));
+    }
+    LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->copy_stream));
+    m->warm_x = h_x_bf16;
+    m->warm_y = h_labels;
+  }
+  int rc = lbbsp_mlp_load_data_async(m, h_x_bf16, h_labels);
+  if (rc) return rc;
+  rc = lbbsp_mlp_run(m, 1);
+  if (rc) return rc;
+  return lbbsp_mlp_read_result_async(m, h_sizes, h_loss);
 }

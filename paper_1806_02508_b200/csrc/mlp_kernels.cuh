@@ -7,6 +7,8 @@
 
 #include <cstdint>
 
+#include "interfere.cuh"
+
 namespace lbbsp {
 namespace mlp {
 
@@ -17,6 +19,7 @@ struct Groups {
   const int* r1;    // [n] one past last
   const int* cta0;  // [n]
   const int* ctan;  // [n]
+  Interference intf;  // straggler injection after each worker phase (interfere.cuh)
 };
 
 __device__ __forceinline__ bool my_group(const Groups& G, int* g, int* cta_in, int* cta_cnt) {

@@ -27,8 +27,11 @@ class MlpConfig(C.Structure):
         ("seed", C.c_uint64), ("dataset_seed", C.c_uint64), ("dataset_size", C.c_int),
         ("loss_every", C.c_int), ("sm_budget", C.c_int),
         ("h_trace_c", _dp), ("h_trace_m", _dp), ("h_trace_mult", _dp), ("trace_len", C.c_int),
-        ("h_worker_share", _dp), ("max_iterations", C.c_int),
+        ("h_worker_share", _dp), ("max_iterations", C.c_int), ("straggler_mode", C.c_int),
     ]
+
+
+STRAGGLE = {"interfere": 0, "sm_cap": 1}
 
 
 _SIG = {
@@ -46,6 +49,7 @@ _SIG = {
     "lbbsp_mlp_work": [C.c_void_p, _dp, _dp],
     "lbbsp_mlp_load_data_async": [C.c_void_p, C.c_void_p, C.c_void_p],
     "lbbsp_mlp_read_result_async": [C.c_void_p, C.c_void_p, C.c_void_p],
+    "lbbsp_mlp_step_e2e": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     "lbbsp_mlp_phase_times": [C.c_void_p, _dp, _ip],
     "lbbsp_benchmark_series": [C.c_uint64, C.c_int, C.c_int] + [C.c_double] * 6 + [_dp] * 3,
 }
@@ -131,7 +135,7 @@ class MlpEngine:
                  scheme="lb-bsp", predictor="narx", warmup_iterations=50, alpha=0.2,
                  learning_rate=0.05, seed=1, dataset_seed=7, dataset_size=1000, loss_every=1,
                  sm_budget=0, trace=None, worker_share=None, max_iterations=1000,
-                 static_sizes=None, train=None):
+                 static_sizes=None, train=None, straggler="interfere"):
         n_total = n_workers_local * world
         if trace is None:
             trace = constant_trace(n_total, max_iterations)
@@ -165,6 +169,7 @@ class MlpEngine:
             self._keep.append(s)
             c.h_worker_share = s.ctypes.data_as(_dp)
         c.max_iterations = max_iterations
+        c.straggler_mode = STRAGGLE[straggler] if isinstance(straggler, str) else straggler
         self.cfg = c
         self.dims = list(dims)
         self.n_total = n_total
@@ -223,6 +228,10 @@ class MlpEngine:
 
     def read_result_async(self, sizes_ptr, loss_ptr):
         check(_L().lbbsp_mlp_read_result_async(self._h, sizes_ptr, loss_ptr))
+
+    def step_e2e(self, x_ptr, y_ptr, sizes_ptr, loss_ptr):
+        """one end-to-end round: stage host inputs, run, write sizes + loss to host"""
+        check(_L().lbbsp_mlp_step_e2e(self._h, x_ptr, y_ptr, sizes_ptr, loss_ptr))
 
     def phase_times(self):
         """device duration (s) of each worker phase of the last round"""

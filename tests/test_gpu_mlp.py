@@ -98,15 +98,16 @@ def test_lbbsp_balances_stragglers_and_loss_falls():
 
 
 def test_memory_pressure_lowers_the_sm_share():
-    """A worker's SM cap is floor(budget * share * min(1, c * MemPenalty(m) * mult))
-    (effective_speed, cluster_sim.cpp:22-29: threshold 0.5, floor 0.25)."""
+    """SM-cap mode: a worker's SM cap is floor(budget * share * min(1, c *
+    MemPenalty(m) * mult)) (effective_speed, cluster_sim.cpp:22-29: threshold
+    0.5, floor 0.25)."""
     from paper_1806_02508_b200.mlp import constant_trace
     n, B, iters = 8, 4096, 4
     c, m, x = constant_trace(n, iters)
     m = m.copy()
     m[5, :], m[6, :], m[7, :] = 0.25, 0.5, 0.0
     eng = _engine(dims=[784, 256, 10], global_batch=B, n_workers_local=n, predictor="ema",
-                  max_iterations=iters, trace=(c, m, x), sm_budget=144)
+                  max_iterations=iters, trace=(c, m, x), sm_budget=144, straggler="sm_cap")
     eng.run(iters)
     caps = eng.records()["caps"][0]
     pen = [1.0] * 5 + [0.25 + 0.75 * 0.5, 1.0, 0.25]

@@ -545,7 +545,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_1806_02508_b200.mlp import MlpEngine, benchmark_trace, constant_trace
+    from paper_1806_02508_b200.mlp import MlpEngine, benchmark_trace, calibrate_gamma, constant_trace
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -564,11 +564,24 @@ def main():
     iters = warm + max(args.steps, window) + 8
     trace = benchmark_trace(n_total, iters, seed=TRACE_SEED)
 
-    def make(scheme, tr, predictor="narx"):
+    # unloaded Gamma profiles of this GPU's workers (the paper's offline GPU
+    # profiling, done on the engine before any timed work); all-gathered so
+    # every rank's replicated solver sees every worker's profile
+    prof_local = calibrate_gamma(DIMS, BATCH_PER_GPU, WORKERS_PER_GPU)
+    if world > 1:
+        allp = [None] * world
+        dist.all_gather_object(allp, prof_local)
+        prof = [p for r in allp for p in r]
+    else:
+        prof = prof_local
+    prof = [(m0, b0, 1, B) for m0, b0, _, _ in prof]
+
+    def make(scheme, tr, predictor="narx", solver="proportional"):
         eng = MlpEngine(dims=DIMS, global_batch=B, n_workers_local=WORKERS_PER_GPU, world=world,
                         rank=rank, scheme=scheme, predictor=predictor,
                         warmup_iterations=WARMUP_NARX, learning_rate=0.05, seed=1,
-                        max_iterations=iters + 4, trace=tr)
+                        max_iterations=iters + 4, trace=tr, solver=solver,
+                        gamma_profiles=prof if solver == "gamma" else None)
         if world > 1:
             connect(eng, world, rank)
         return eng
@@ -658,12 +671,18 @@ def main():
     # availabilities: the capacity-aware ideal a proportional allocator can
     # reach) and the no-straggler ideal (every worker at a = 1) ----
     win = {}
-    for name, scheme, tr, pred in (("lbbsp", "lb-bsp", trace, "narx"), ("bsp", "bsp", trace, "narx"),
-                                   ("perfect", "lb-bsp", trace, "perfect"),
-                                   ("no_straggler", "lb-bsp", constant_trace(n_total, iters), "narx")):
-        eng = make(scheme, tr, pred)
+    for name, scheme, tr, pred, solver in (
+            ("lbbsp", "lb-bsp", trace, "narx", "proportional"),
+            ("lbbsp_gamma", "lb-bsp", trace, "narx", "gamma"),
+            ("bsp", "bsp", trace, "narx", "proportional"),
+            ("perfect", "lb-bsp", trace, "perfect", "proportional"),
+            ("perfect_gamma", "lb-bsp", trace, "perfect", "gamma"),
+            ("no_straggler", "lb-bsp", constant_trace(n_total, iters), "narx", "proportional")):
+        eng = make(scheme, tr, pred, solver)
         ms_w, _ = timed(eng, window, warm)
         win[name] = percentiles(ms_w)
+        r = eng.records()
+        win[name]["min_batch_in_window"] = int(r["sizes"][warm:warm + window].min())
         del eng
 
     # ---- C3-shape straggler demonstration (compute-bound) ----
@@ -724,6 +743,9 @@ def main():
             "lbbsp_over_bsp": win["bsp"]["mean"] / lb,
             "lbbsp_over_ideal_time": lb / win["perfect"]["mean"],
             "lbbsp_over_no_straggler_time": lb / win["no_straggler"]["mean"],
+            "lbbsp_gamma_over_bsp": win["bsp"]["mean"] / win["lbbsp_gamma"]["mean"],
+            "lbbsp_gamma_over_ideal_time": win["lbbsp_gamma"]["mean"] / win["perfect_gamma"]["mean"],
+            "gamma_profiles_s": [[round(m0, 12), round(b0, 9)] for m0, b0, _, _ in prof],
             "phase_ms": [round(float(x) * 1e3, 4) for x in (phases if phases is not None else [])],
             "roofline": {"bound": "tensor", "kernel": "fwd GEMM 4096x256x784 (tcgen05, per-worker "
                                                       "partitions)",

@@ -584,7 +584,19 @@ typedef struct {
   const double* h_worker_share;       /* [n_workers_total] nominal share of its GPU (NULL: 1/n_local) */
   int max_iterations;                 /* record capacity                     */
   int straggler_mode;                 /* LBBSP_STRAGGLE_INTERFERE (0, default) | _SM_CAP (1) */
+  int solver;                         /* LBBSP_SOLVER_PROPORTIONAL (0, default) | _GAMMA (1) */
+  const lbbsp_gpu_profile* h_gpu_profiles; /* [n_workers_total] unloaded Gamma (GAMMA solver) */
 } lbbsp_mlp_cfg;
+
+/* Batch-size solver of the MLP engine's LB-BSP rounds:
+ * PROPORTIONAL: cpu_allocate over clamp_speed_floor(v_pred), v = b / t
+ *   (the reference's CPU-cluster branch, north_star (4));
+ * GAMMA: gpu_allocate over per-worker profiles Gamma_i(x) = (m0_i max(x, x_s_i)
+ *   + b0_i) / a_i, with the unloaded (m0, b0, x_s, x_o) given and a_i the
+ *   predicted availability; the observed speed is Gamma0_i(b) / t (the
+ *   reference's GPU-cluster branch with a predictor, cluster_sim.cpp:373-387). */
+#define LBBSP_SOLVER_PROPORTIONAL 0
+#define LBBSP_SOLVER_GAMMA 1
 
 /* How a worker's availability a = min(1, c * MemPenalty(m) * mult) is injected:
  * INTERFERE: the worker keeps its nominal CTA partition and co-scheduled

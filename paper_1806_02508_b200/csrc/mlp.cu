@@ -33,6 +33,7 @@
 #include "mlp_kernels.cuh"
 #include "predictor.cuh"
 #include "solver.cuh"
+#include "c2_fused.cuh"
 
 namespace lbbsp {
 
@@ -200,7 +201,10 @@ struct PlanDev {
   unsigned long long* stamps;  // [16] globaltimer at kernel boundaries (last round)
   unsigned long long* gather_done;  // single rank: gather CTAs finished, summed over all rounds
   int straggler_mode;          // LBBSP_STRAGGLE_INTERFERE | LBBSP_STRAGGLE_SM_CAP
+  int solver;                  // LBBSP_SOLVER_PROPORTIONAL | LBBSP_SOLVER_GAMMA
+  const lbbsp_gpu_profile* prof0;  // [n_total] unloaded Gamma profiles (GAMMA solver)
   float2* intf_w;              // [n_local] {availability, HBM share of the injected time}
+  unsigned* fz_done;           // [n_local] fused worker kernel: head CTAs done (zeroed here)
   int gather_ctas;             // > 0: the plan completes only once they all have
 };
 
@@ -296,6 +300,32 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
   int code = 0;
   if (D.static_sizes) {
     for (int i = tid; i < n; i += blockDim.x) sz[i] = D.static_sizes_d[i];
+  } else if (D.scheme == LBBSP_SCHEME_LBBSP && D.solver == LBBSP_SOLVER_GAMMA) {
+    // GPU-cluster branch (cluster_sim.cpp:373-387): gpu_allocate over the
+    // workers' Gamma profiles -- the unloaded profile scaled by the predicted
+    // availability (clamp_speed_floor of v_pred) -- and the lagged comm EMA;
+    // k < 2: initial_gpu_sizes (:471-484) on the unloaded profiles
+    extern __shared__ double gsm[];
+    lbbsp_gpu_profile* prof = reinterpret_cast<lbbsp_gpu_profile*>(gsm);
+    double* comm = reinterpret_cast<double*>(prof + n);
+    double* bp = comm + n;
+    double* tmp = bp + 2 * n;
+    __shared__ int feasible;
+    for (int i = tid; i < n; i += blockDim.x) {
+      const lbbsp_gpu_profile p0 = D.prof0[i];
+      const double a = k < 2 ? 1.0 : (vp_s[i] > D.pred.floor ? vp_s[i] : D.pred.floor);
+      prof[i] = lbbsp_gpu_profile{ddiv(p0.sec_per_sample, a), ddiv(p0.base_time_s, a), p0.saturation_point,
+                                  p0.oom_point};
+      comm[i] = k < 2 ? 0.0 : D.pred.comm_ema_lag[i];
+      sz[i] = D.B_total / n + (i < D.B_total % n ? 1 : 0);
+    }
+    if (tid == 0) feasible = 1;
+    __syncthreads();
+    if (k < 2)
+      for (int i = tid; i < n; i += blockDim.x)
+        if (sz[i] < prof[i].saturation_point || sz[i] > prof[i].oom_point) feasible = 0;
+    __syncthreads();
+    if (k >= 2 || !feasible) code = block_gpu_allocate(prof, comm, n, D.B_total, sz, bp, tmp, &sm, D.status);
   } else if (D.scheme == LBBSP_SCHEME_LBBSP && k > 0) {
     code = block_cpu_allocate(vp_s, n, D.B_total, D.pred.floor, sz, rem, &sm, D.status);
   } else {
@@ -342,6 +372,8 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
     D.timing[2 * i] = ~0ull;
     D.timing[2 * i + 1] = 0ull;
   }
+  if (D.fz_done)
+    for (int i = tid; i < D.n_local; i += blockDim.x) D.fz_done[i] = 0u;
   if (tid == 0) {
     D.stamps[6] = ~0ull;  // loss-branch head {first start, last end}
     D.stamps[7] = 0ull;
@@ -373,6 +405,12 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
     if (tid == 0) *D.local_rows = 0;
   }
   stamp(D, 1);
+}
+
+// dynamic shared memory of the plan for the Gamma solver: profiles, comm,
+// breakpoints and scratch (block_gpu_allocate)
+static size_t gamma_plan_smem(int n) {
+  return static_cast<size_t>(n) * sizeof(lbbsp_gpu_profile) + static_cast<size_t>(n) * 8 * 5 + 64;
 }
 
 // P6: X[r] = data[stream[off + r]], labels, row scale (Eq. 7: 1/B; Eq. 6: 1/(n b_i))
@@ -798,32 +836,49 @@ __global__ void zero_dz_tail_kernel(PlanDev D, bf16** dz, const int* widths, int
   }
 }
 
-// measured per-worker compute time -> realised speed b_i / t_i
-__global__ void speed_kernel(PlanDev D, int n_phases) {
-  const int i = threadIdx.x;
-  if (i >= D.n_local) return;
-  double t = 0.0;
-  for (int p = 0; p < n_phases; ++p) {
-    const unsigned long long s = D.timing[2 * (p * D.n_local + i)], e = D.timing[2 * (p * D.n_local + i) + 1];
-    if (s != ~0ull && e > s) t += static_cast<double>(e - s) * 1e-9;
-  }
-  const int w = D.rank * D.n_local + i;
-  const double b = static_cast<double>(D.sizes_all[w]);
-  D.v_obs_local[i] = t > 0.0 ? b / t : b;
-  const int row = *D.rows;
-  if (row < D.max_rows) D.rec_t[static_cast<size_t>(row) * D.n_total + w] = t;
-}
-
-// Measured speed v_i = b_i / t_i of local worker i from its phase times.
-__device__ inline double local_speed(const PlanDev& D, int i, int n_phases, double* t_out) {
+// Worker time of local worker i in the last round: the sum of its phase
+// windows (globaltimer ns -> s).
+__device__ inline double worker_time(const PlanDev& D, int i, int n_phases) {
   double t = 0.0;
   for (int p = 0; p < n_phases; ++p) {
     const unsigned long long s0 = D.timing[2 * (p * D.n_local + i)], e0 = D.timing[2 * (p * D.n_local + i) + 1];
     if (s0 != ~0ull && e0 > s0) t += static_cast<double>(e0 - s0) * 1e-9;
   }
-  const double b = static_cast<double>(D.sizes_all[D.rank * D.n_local + i]);
+  return t;
+}
+
+// The observation pushed into worker w's history for a batch of b rows that
+// took t seconds. Proportional solver: the realised speed b / t (the
+// reference's v_actual = x / tp, cluster_sim.cpp:412-413). Gamma solver: the
+// realised speed relative to the worker's unloaded profile, Gamma0(b) / t
+// (= its availability a when the time follows (m0 max(b, x_s) + b0) / a).
+__device__ inline double observed_speed(const PlanDev& D, int w, int b, double t) {
+  if (D.solver == LBBSP_SOLVER_GAMMA) {
+    const lbbsp_gpu_profile p = D.prof0[w];
+    const double g0 = dadd(dmul(p.sec_per_sample, static_cast<double>(b > p.saturation_point ? b : p.saturation_point)),
+                           p.base_time_s);
+    return t > 0.0 ? ddiv(g0, t) : 1.0;
+  }
+  return t > 0.0 ? static_cast<double>(b) / t : static_cast<double>(b);
+}
+
+// measured per-worker compute time -> observed speed
+__global__ void speed_kernel(PlanDev D, int n_phases) {
+  const int i = threadIdx.x;
+  if (i >= D.n_local) return;
+  const double t = worker_time(D, i, n_phases);
+  const int w = D.rank * D.n_local + i;
+  D.v_obs_local[i] = observed_speed(D, w, D.sizes_all[w], t);
+  const int row = *D.rows;
+  if (row < D.max_rows) D.rec_t[static_cast<size_t>(row) * D.n_total + w] = t;
+}
+
+// Observed speed of local worker i from its phase times.
+__device__ inline double local_speed(const PlanDev& D, int i, int n_phases, double* t_out) {
+  const double t = worker_time(D, i, n_phases);
   if (t_out) *t_out = t;
-  return t > 0.0 ? b / t : b;
+  const int w = D.rank * D.n_local + i;
+  return observed_speed(D, w, D.sizes_all[w], t);
 }
 
 // P10 fused: observe (cluster_sim.cpp:309-313) + train_rotation (:315-324)
@@ -905,14 +960,9 @@ __global__ void observe_kernel(PlanDev D, int fused_speed_phases) {
   if (fused_speed_phases > 0) {  // single rank: measured speeds computed here
     const int i = threadIdx.x;
     if (i < D.n_local) {
-      double t = 0.0;
-      for (int p = 0; p < fused_speed_phases; ++p) {
-        const unsigned long long s0 = D.timing[2 * (p * D.n_local + i)], e0 = D.timing[2 * (p * D.n_local + i) + 1];
-        if (s0 != ~0ull && e0 > s0) t += static_cast<double>(e0 - s0) * 1e-9;
-      }
+      double t;
+      D.v_obs_local[i] = local_speed(D, i, fused_speed_phases, &t);
       const int w = D.rank * D.n_local + i;
-      const double b = static_cast<double>(D.sizes_all[w]);
-      D.v_obs_local[i] = t > 0.0 ? b / t : b;
       const int rw = *D.rows;
       if (rw < D.max_rows) D.rec_t[static_cast<size_t>(rw) * D.n_total + w] = t;
     }
@@ -1261,6 +1311,10 @@ struct lbbsp_mlp {
   bf16** dz_ptrs = nullptr;
   int* dz_widths = nullptr;
   Interference intf{};  // straggler injection state (interference mode)
+  // fused worker kernel (784-256-10): forward + head + dW0 in one launch
+  bool fused = false;
+  CUtensorMap fz_tm[4];
+  unsigned* fz_comb = nullptr;
   // e2e plumbing: cached host-buffer lookups (lbbsp_mlp_read_result_async,
   // lbbsp_mlp_step_e2e)
   int* res_host_sizes = nullptr;
@@ -1358,6 +1412,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   const Groups G = groups();
   int nl = 0, ph = 0;
   const int sms = D.sm_budget;
+  const size_t plan_smem = D.solver == LBBSP_SOLVER_GAMMA ? gamma_plan_smem(n_total) : 0;
   const int gather_ctas = std::max(sms, std::min(sms * 8, (B_cap * (dims[0] / 8) + 1023) / 1024));
   // single rank: the plan waits for the gather on the device (no graph join);
   // set before either kernel is captured, both read it
@@ -1372,9 +1427,9 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
                                                  B_total, partial, P, reg_off, reg_len, n_reg);
     LBBSP_CUDA_CHECK(cudaEventRecord(ev_gather1, side));
     if (join) LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_gather1, 0));
-    plan_kernel<<<1, 256, 0, s>>>(D, row_scale);
+    plan_kernel<<<1, 256, plan_smem, s>>>(D, row_scale);
   } else {
-    plan_kernel<<<1, 256, 0, s>>>(D, row_scale);
+    plan_kernel<<<1, 256, plan_smem, s>>>(D, row_scale);
     LBBSP_CUDA_CHECK(launch_maybe_pdl(gather_kernel, gather_ctas, 256, 0, s, use_pdl, D,
                                       static_cast<const int*>(streams), B_total,
                                       static_cast<const bf16*>(data_x),
@@ -1387,15 +1442,42 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     zero_dz_tail_kernel<<<8, 256, 0, s>>>(D, dz_ptrs, dz_widths, L, dz_end, B_cap);
     ++nl;
   }
+  const bool bucketed = cfg.world > 1 && n_local == 1 && !small_head;
+  const bool ce_buckets = bucketed && peers && gradb && ce_ok;
   // ---- forward (per-worker partitions) ----
   const int Lg = small_head ? L - 1 : L;  // layers on the tensor-core GEMM
+  const int hl = L - 1;  // last layer index
+  if (fused) {
+    // forward + head + dW0 of every worker in one launch (c2_fused.cuh)
+    FusedArgs fa{};
+    fa.G = G;
+    fa.dZ0 = dZ[0];
+    fa.W1 = params + off_w[1];
+    fa.b0 = params + off_b[0];
+    fa.b1 = params + off_b[1];
+    fa.y = y;
+    fa.row_scale = row_scale;
+    fa.slab = partial;
+    fa.slab_stride = P;
+    fa.off_w0 = off_w[0];
+    fa.off_w1 = off_w[1];
+    fa.off_b1 = off_b[1];
+    fa.off_b0 = off_b[0];
+    fa.head_part = head_part;
+    fa.done = D.fz_done;
+    fa.combine_cnt = fz_comb;
+    fa.timing = phase_slot(ph++);
+    fa.status = D.status;
+    LBBSP_CUDA_CHECK(launch_maybe_pdl(c2_fused_worker_kernel, sms, kFzThreads, kFzSmem, s, use_pdl, fz_tm[0],
+                                      fz_tm[1], fz_tm[2], fz_tm[3], fa));
+    ++nl;
+  } else {
   for (int l = 0; l < Lg; ++l) {
     int rc = launch_grouped(this, fwd[l], tc::kRows, phase_slot(ph++), s);
     if (rc) return rc;
     ++nl;
   }
   // ---- head ----
-  const int hl = L - 1;  // last layer index
   if (small_head) {
     const bf16* Hin = L >= 2 ? H[L - 2] : X;
     LBBSP_CUDA_CHECK(launch_maybe_pdl(
@@ -1423,8 +1505,6 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   // comm stream as soon as its dW/db are final, overlapping the rest of the
   // backward pass (bucketed allreduce); the speed all-gather follows on the
   // same stream, so the communicator sees one fixed order on every rank.
-  const bool bucketed = cfg.world > 1 && n_local == 1 && !small_head;
-  const bool ce_buckets = bucketed && peers && gradb && ce_ok;
   for (int l = Lg - 1; l >= 0; --l) {
     if (!(small_head && l == L - 2)) {  // the small head already summed this bias gradient
       bias_grad_kernel<<<sms, 256, 0, s>>>(G, dZ[l], dims[l + 1], partial, P, off_b[l], bias_part,
@@ -1521,6 +1601,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
       ++nl;
     }
   }
+  }  // !fused
   n_phases = ph;
   // measured speeds; on several GPUs all-gathered (after the gradient buckets)
   const float lr = static_cast<float>(cfg.learning_rate);
@@ -1594,7 +1675,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   }
   // ---- aggregate + apply (the bucketed path applied per layer above) ----
   // the small head's CTA partials were combined on the side stream
-  if (small_head) LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_head1, 0));
+  if (small_head && !fused) LBBSP_CUDA_CHECK(cudaStreamWaitEvent(s, ev_head1, 0));
   if (bucketed) {
   } else if (cfg.world > 1 && peers) {
     // one-shot all-reduce over NVLink peer memory, summed in rank order
@@ -1847,6 +1928,18 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   if (c.straggler_mode != LBBSP_STRAGGLE_INTERFERE && c.straggler_mode != LBBSP_STRAGGLE_SM_CAP)
     return set_error(LBBSP_INVALID_ARGUMENT, "mlp: unknown straggler_mode %d", c.straggler_mode);
   D.straggler_mode = c.straggler_mode;
+  if (c.solver != LBBSP_SOLVER_PROPORTIONAL && c.solver != LBBSP_SOLVER_GAMMA)
+    return set_error(LBBSP_INVALID_ARGUMENT, "mlp: unknown solver %d", c.solver);
+  D.solver = c.solver;
+  if (c.solver == LBBSP_SOLVER_GAMMA) {
+    if (!c.h_gpu_profiles)
+      return set_error(LBBSP_INVALID_ARGUMENT, "mlp: the gamma solver needs h_gpu_profiles (unloaded Gamma per worker)");
+    lbbsp_gpu_profile* pr = nullptr;
+    LBBSP_CUDA_CHECK(m.upload(&pr, c.h_gpu_profiles, static_cast<size_t>(n)));
+    D.prof0 = pr;
+    LBBSP_CUDA_CHECK(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(gamma_plan_smem(n))));
+  }
   if (c.straggler_mode == LBBSP_STRAGGLE_INTERFERE) {
     float2* w = nullptr;
     LBBSP_CUDA_CHECK(m.alloc(&w, m.n_local));
@@ -1994,6 +2087,22 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   }
   if (small_head) flops += 2.0 * m.B_total / c.world * c.dims[L - 1] * c.dims[L] * 3.0;
   m.gemm_flops = flops;
+  // one persistent launch for every worker's forward + head + dW0 on the
+  // 784-256-10 MLP (c2_fused.cuh); LBBSP_NO_FUSE=1 keeps the three launches
+  m.fused = small_head && L == 2 && c.dims[0] == kFzD0 && c.dims[1] == kHeadDH && !getenv("LBBSP_NO_FUSE");
+  if (m.fused) {
+    int rc = make_tmap_bf16(&m.fz_tm[0], m.X, kFzD0, m.B_cap, kFzD0, 128);
+    if (!rc) rc = make_tmap_bf16(&m.fz_tm[1], m.pb + m.off_w[0], kFzD0, kHeadDH, kFzD0, 256);
+    if (!rc) rc = make_tmap_bf16(&m.fz_tm[2], m.dZ[0], kHeadDH, m.B_cap, kHeadDH, 64);
+    if (!rc) rc = make_tmap_bf16(&m.fz_tm[3], m.X, kFzD0, m.B_cap, kFzD0, 64);
+    if (rc) return rc;
+    unsigned* fd = nullptr;
+    LBBSP_CUDA_CHECK(m.alloc(&fd, static_cast<size_t>(m.n_local)));
+    D.fz_done = fd;
+    LBBSP_CUDA_CHECK(m.alloc(&m.fz_comb, static_cast<size_t>(m.n_local)));
+    LBBSP_CUDA_CHECK(cudaFuncSetAttribute(c2_fused_worker_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kFzSmem)));
+  }
   m.reduce_bytes = (m.n_local + 1.0) * P * 4.0 + P * 4.0 + P * 2.0;
   LBBSP_CUDA_CHECK(cudaDeviceSynchronize());
   *out = M.release();

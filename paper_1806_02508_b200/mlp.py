@@ -28,10 +28,12 @@ class MlpConfig(C.Structure):
         ("loss_every", C.c_int), ("sm_budget", C.c_int),
         ("h_trace_c", _dp), ("h_trace_m", _dp), ("h_trace_mult", _dp), ("trace_len", C.c_int),
         ("h_worker_share", _dp), ("max_iterations", C.c_int), ("straggler_mode", C.c_int),
+        ("solver", C.c_int), ("h_gpu_profiles", C.POINTER(abi.GpuProfile)),
     ]
 
 
 STRAGGLE = {"interfere": 0, "sm_cap": 1}
+SOLVERS = {"proportional": 0, "gamma": 1}
 
 
 _SIG = {
@@ -130,12 +132,56 @@ def constant_trace(n_workers, iterations, availability=None):
     return c, np.ones_like(c), np.ones_like(c)
 
 
+def calibrate_gamma(dims, batch, n_workers_local=8, rounds=6, warm=2, **kw):
+    """Unloaded Gamma profile of every local worker, the paper's offline GPU
+    profiling (PAPER.md GPU cluster: time flat below x_s, then linear) done on
+    this engine: each worker runs at availability 1 on its own CTA partition
+    with three batch sizes around its nominal share x = batch / n (x/2, x,
+    3x/2; static sizes summing to `batch`), and t = m0 x + b0 is fitted to the
+    median worker time of each by least squares. Returns
+    [(m0, b0, x_s=1, x_o=batch)] per local worker. One worker per GPU
+    (n_workers_local == 1): three single-worker engines with global batch
+    x/2, x, 3x/2."""
+    n = n_workers_local
+    x = batch // n
+    if n == 1:
+        configs = [[max(1, x // 2)], [x], [x + x // 2]]
+    else:
+        lo, hi = x // 2, x + x // 2
+        alt = [hi if i % 2 == 0 else lo for i in range(n)]
+        alt2 = [lo if i % 2 == 0 else hi for i in range(n)]
+        if n % 2:
+            alt[-1] = alt2[-1] = x
+        configs = [[x] * n, alt, alt2]
+    pts = [[] for _ in range(n)]
+    iters = warm + rounds + 2
+    for sizes in configs:
+        eng = MlpEngine(dims=dims, global_batch=int(sum(sizes)), n_workers_local=n, predictor="ema",
+                        max_iterations=iters, trace=constant_trace(n, iters),
+                        static_sizes=sizes if n > 1 else None, **kw)
+        eng.run(warm + rounds)
+        t = eng.records()["t_worker"][warm:]
+        for i in range(n):
+            pts[i].append((sizes[i], float(np.median(t[:, i]))))
+        del eng
+    prof = []
+    for i in range(n):
+        xs = np.array([p[0] for p in pts[i]], dtype=np.float64)
+        ts = np.array([p[1] for p in pts[i]], dtype=np.float64)
+        m0, b0 = np.polyfit(xs, ts, 1)
+        m0 = max(float(m0), 1e-12)
+        b0 = max(float(b0), 0.0)
+        prof.append((m0, b0, 1, batch))
+    return prof
+
+
 class MlpEngine:
     def __init__(self, dims, global_batch, n_workers_local=8, world=1, rank=0,
                  scheme="lb-bsp", predictor="narx", warmup_iterations=50, alpha=0.2,
                  learning_rate=0.05, seed=1, dataset_seed=7, dataset_size=1000, loss_every=1,
                  sm_budget=0, trace=None, worker_share=None, max_iterations=1000,
-                 static_sizes=None, train=None, straggler="interfere"):
+                 static_sizes=None, train=None, straggler="interfere", solver="proportional",
+                 gamma_profiles=None):
         n_total = n_workers_local * world
         if trace is None:
             trace = constant_trace(n_total, max_iterations)
@@ -170,6 +216,12 @@ class MlpEngine:
             c.h_worker_share = s.ctypes.data_as(_dp)
         c.max_iterations = max_iterations
         c.straggler_mode = STRAGGLE[straggler] if isinstance(straggler, str) else straggler
+        c.solver = SOLVERS[solver] if isinstance(solver, str) else solver
+        if gamma_profiles is not None:
+            arr = (abi.GpuProfile * len(gamma_profiles))(
+                *[abi.GpuProfile(float(m), float(b), int(xs), int(xo)) for m, b, xs, xo in gamma_profiles])
+            self._keep.append(arr)
+            c.h_gpu_profiles = C.cast(arr, C.POINTER(abi.GpuProfile))
         self.cfg = c
         self.dims = list(dims)
         self.n_total = n_total

@@ -130,12 +130,6 @@ inline int cmd_run(const std::string& config, const std::string& out_dir,
                        seed_override.value_or(0));
 }
 
-inline int cmd_predict_bench(const std::string& config, const std::string& out_dir,
-                             std::optional<std::uint64_t> seed_override = std::nullopt) {
-  return lbbsp_cmd_predict_bench(config.c_str(), out_dir.c_str(), seed_override ? 1 : 0,
-                                 seed_override.value_or(0));
-}
-
 // predictor.cpp:215-243
 inline lbbsp_narx_model load_narx_csv(const std::string& path) {
   lbbsp_narx_model m{};

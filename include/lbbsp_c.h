@@ -488,15 +488,13 @@ int lbbsp_predictor_series_rmse(int kind, const lbbsp_predictor_cfg* base, const
                                 double base_speed, uint64_t seed, int measure_from,
                                 double* rmse);
 
-/* cmd_run / cmd_compare / cmd_predict_bench (scenario.cpp:369-481) with every
- * simulation executed by the device driver. Return the CLI exit status
- * (0 ok, 1 error; the error is printed to stderr as "lbbsp run: <what>" and
- * kept in lbbsp_last_error()). has_seed selects the --seed override. */
+/* cmd_run (scenario.cpp:369-386): load a scenario, run it on the device
+ * driver, write records.csv + metrics.json. Returns the CLI exit status (0 ok,
+ * 1 error; the error is printed to stderr as "lbbsp run: <what>" and kept in
+ * lbbsp_last_error()). has_seed selects the --seed override. The other CLI
+ * commands (compare, predict-bench) are front-end glue outside the hot path
+ * and are not exported. */
 int lbbsp_cmd_run(const char* config, const char* out_dir, int has_seed, uint64_t seed);
-int lbbsp_cmd_compare(const char* const* configs, int n_configs, const char* out_dir,
-                      int has_seed, uint64_t seed);
-int lbbsp_cmd_predict_bench(const char* config, const char* out_dir, int has_seed,
-                            uint64_t seed);
 
 /* ======================================================================== */
 /* C4: NARX at sweep scale -- delay d, hidden H, W models, fp32 CUDA cores   */

@@ -86,8 +86,6 @@ SIGNATURES = {
     "lbbsp_predictor_series_rmse": [C.c_int, C.POINTER(abi.PredictorConfig), _dp, _dp, _dp,
                                     C.c_int, C.c_double, C.c_uint64, C.c_int, _dp],
     "lbbsp_cmd_run": [C.c_char_p, C.c_char_p, C.c_int, C.c_uint64],
-    "lbbsp_cmd_compare": [C.POINTER(C.c_char_p), C.c_int, C.c_char_p, C.c_int, C.c_uint64],
-    "lbbsp_cmd_predict_bench": [C.c_char_p, C.c_char_p, C.c_int, C.c_uint64],
 }
 
 _lib = None

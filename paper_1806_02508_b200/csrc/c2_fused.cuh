@@ -9,7 +9,7 @@
 //   worker barrier (the worker's head CTAs have published dZ0 and partials)
 //   phase W  (per 128 x 128 tile of dW0 = dZ0^T X, K = the worker's rows)
 //     tcgen05 M=128 N=128, MN-major operands, ragged K tail zeroed in smem
-//   combine: the worker's last CTA sums the head CTA partials in CTA order
+//   combine: the worker's CTAs sum the head CTA partials in CTA order
 //
 // Replaces the three launches per round (forward GEMM, head, dW GEMM) whose
 // kernel boundaries synchronised every worker with every other worker at
@@ -48,7 +48,8 @@ constexpr int kFzWTiles = 2 * kFzNTW;             // 14 dW0 tiles per worker
 constexpr int kFzOffWl = kFzStages * kFzStage;    // head B fragments (logits)  8 KB
 constexpr int kFzOffWd = kFzOffWl + 8192;         // head B fragments (dH)      8 KB
 constexpr int kFzOffDl = kFzOffWd + 8192;         // dl tiles [8][16][16] bf16  4 KB
-constexpr int kFzOffBar = kFzOffDl + 4096;        // mbarriers + slots
+constexpr int kFzOffB0 = kFzOffDl + 4096;         // b0 [256] fp32              1 KB
+constexpr int kFzOffBar = kFzOffB0 + 1024;        // mbarriers + slots
 constexpr size_t kFzSmem = kFzOffBar + 256 + 1024;
 
 struct FusedArgs {
@@ -64,9 +65,9 @@ struct FusedArgs {
   long long off_w0, off_w1, off_b1, off_b0;
   float* head_part;         // [grid][kHeadPartVals] CTA partials
   unsigned* done;           // [n_local] head CTAs finished (zeroed by the round's plan)
-  unsigned* combine_cnt;    // [n_local] CTAs finished phase W (self-resetting)
   unsigned long long* timing;  // [n_local][2] worker window
   lbbsp_dev_status* status;
+  unsigned long long* dbg;  // optional [grid][8] per-CTA stage stamps (globaltimer)
 };
 
 __device__ __forceinline__ void named_sync_epi() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
@@ -132,6 +133,8 @@ __global__ void __launch_bounds__(kFzThreads, 1)
       const int n = 8 * j + (l >> 2), c = 2 * (l & 3);
       wd[i] = make_uint2(pack_bf16(wv(c, n), wv(c + 1, n)), pack_bf16(wv(c + 8, n), wv(c + 9, n)));
     }
+    float* b0s = reinterpret_cast<float*>(smem + kFzOffB0);
+    for (int i = threadIdx.x; i < kHeadDH; i += 256) b0s[i] = A.b0[i];
     fence_proxy_async_smem();  // the stage region is next written by TMA
   }
   tc_fence_before();
@@ -159,6 +162,8 @@ __global__ void __launch_bounds__(kFzThreads, 1)
   const int g = grp[0], cta_in = grp[1], cnt = grp[2];
   const unsigned long long t_cta0 = globaltimer();
   if (g >= 0 && A.timing && threadIdx.x == 0) atomicMin(&A.timing[2 * g], t_cta0);
+  unsigned long long* dbg = A.dbg ? A.dbg + 8ull * blockIdx.x : nullptr;
+  if (dbg && threadIdx.x == 0) dbg[0] = t_cta0;
   const int r0 = g >= 0 ? G.r0[g] : 0, r1 = g >= 0 ? G.r1[g] : 0;
   const int rows = r1 - r0;
   const int n_mt = rows > 0 ? (rows + 127) / 128 : 0;
@@ -206,6 +211,7 @@ __global__ void __launch_bounds__(kFzThreads, 1)
         }
       } while (seen < static_cast<unsigned>(head_ctas));
       fence_proxy_async_global();  // dZ0 (generic stores of other CTAs) -> TMA reads
+      if (dbg) dbg[3] = globaltimer();
       for (int t = cta_in; t < w_tiles; t += cnt) {
         const int mt = t % 2, nt = t / 2;
         for (int kb = 0; kb < k_blocks_w; ++kb) {
@@ -299,6 +305,7 @@ __global__ void __launch_bounds__(kFzThreads, 1)
     const int gq = lane >> 2, tq = lane & 3;
     const uint2* wl = reinterpret_cast<const uint2*>(smem + kFzOffWl);
     const uint2* wd = reinterpret_cast<const uint2*>(smem + kFzOffWd);
+    const float* b0s = reinterpret_cast<const float*>(smem + kFzOffB0);
     uint8_t* dls = smem + kFzOffDl + warp * 512;
     const float b_lo0 = A.b1[2 * tq], b_lo1 = A.b1[2 * tq + 1];
     const float b_hi0 = tq == 0 ? A.b1[8] : 0.f, b_hi1 = tq == 0 ? A.b1[9] : 0.f;
@@ -310,10 +317,21 @@ __global__ void __launch_bounds__(kFzThreads, 1)
     uint32_t fph = 0;
     for (int it = 0; it < my_mt; ++it) {
       const int m0 = r0 + (cta_in + it * cnt) * 128;
+      // labels and row scales of this warp's head rows: independent of the
+      // forward, loaded while the tensor core runs it
+      const int tile = warp;
+      const int row0 = m0 + tile * 16;
+      const bool have = row0 < r1;
+      const int ra = row0 + gq, rb = row0 + gq + 8;
+      const bool va = ra < r1, vb = rb < r1;
+      const int ya = have && va ? A.y[ra] : -1, yb = have && vb ? A.y[rb] : -1;
+      const float rsa = have && va ? A.row_scale[ra] : 0.f;
+      const float rsb = have && vb ? A.row_scale[rb] : 0.f;
       // ---- H = bf16(relu(acc + b0)) -> the head's swizzled 16-row tiles ----
       mbar_wait(&tfull[0], fph);
       fph ^= 1;
       tc_fence_after();
+      if (dbg && threadIdx.x == 0 && it == 0) dbg[1] = globaltimer();
       const int r = 32 * q + lane;  // row of the M-tile this thread reads
       uint8_t* htile = smem + (r >> 4) * 8192;
 #pragma unroll 1
@@ -328,8 +346,8 @@ __global__ void __launch_bounds__(kFzThreads, 1)
           uint32_t* p = reinterpret_cast<uint32_t*>(&pk);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const float a0 = fmaxf(__uint_as_float(v[j + 2 * u]) + A.b0[col0 + j + 2 * u], 0.f);
-            const float a1 = fmaxf(__uint_as_float(v[j + 2 * u + 1]) + A.b0[col0 + j + 2 * u + 1], 0.f);
+            const float a0 = fmaxf(__uint_as_float(v[j + 2 * u]) + b0s[col0 + j + 2 * u], 0.f);
+            const float a1 = fmaxf(__uint_as_float(v[j + 2 * u + 1]) + b0s[col0 + j + 2 * u + 1], 0.f);
             p[u] = pack_bf16(a0, a1);
           }
           *reinterpret_cast<uint4*>(htile + hsw(r & 15, (col0 + j) >> 3)) = pk;
@@ -340,16 +358,8 @@ __global__ void __launch_bounds__(kFzThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[0]);
       named_sync_epi();  // the whole H tile is in smem
       // ---- head on tile `warp` (rows m0 + 16 warp ..): head_mma.cuh, one iteration ----
-      const int tile = warp;
-      const int row0 = m0 + tile * 16;
-      const bool have = row0 < r1;
       const uint32_t hb = smem_addr(smem + tile * 8192);
       uint8_t* hp = smem + tile * 8192;
-      const int ra = row0 + gq, rb = row0 + gq + 8;
-      const bool va = ra < r1, vb = rb < r1;
-      const int ya = have && va ? A.y[ra] : -1, yb = have && vb ? A.y[rb] : -1;
-      const float rsa = have && va ? A.row_scale[ra] : 0.f;
-      const float rsb = have && vb ? A.row_scale[rb] : 0.f;
       uint32_t ad[4] = {0u, 0u, 0u, 0u};
       const int mi = lane >> 3, lr = (lane & 7) + (mi & 1) * 8;
       if (have) {
@@ -506,6 +516,7 @@ __global__ void __launch_bounds__(kFzThreads, 1)
       __threadfence();
       named_sync_epi();
       if (threadIdx.x == 0) atomicAdd(done + g, 1u);  // release: dZ0 rows + partials
+      if (dbg && threadIdx.x == 0) dbg[2] = globaltimer();
     }
     // ---- phase W epilogue: dW0 tiles -> the worker's fp32 slab ----
     float* dst = A.slab + static_cast<long long>(g) * A.slab_stride + A.off_w0;
@@ -543,34 +554,38 @@ __global__ void __launch_bounds__(kFzThreads, 1)
       acc ^= 1;
     }
   }
+  if (dbg && threadIdx.x == 0) dbg[4] = globaltimer();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 9) tmem_dealloc<512>(tmem);
-  // ---- combine: the worker's last CTA sums the head partials in CTA order ----
+  // ---- combine: the head CTA partials summed in CTA order (head_combine's
+  // order), the worker's CTAs splitting the values between them; every head
+  // partial was published before this CTA's producer passed the barrier ----
   if (g >= 0) {
-    __shared__ int last;
-    if (threadIdx.x == 0) {
-      __threadfence();
-      last = atomicAdd(A.combine_cnt + g, 1u) == static_cast<unsigned>(cnt - 1);
-    }
-    __syncthreads();
-    if (last) {
-      __threadfence();
-      const int cbase = blockIdx.x - cta_in;
-      float* gs = A.slab + static_cast<long long>(g) * A.slab_stride;
-      for (int k = threadIdx.x; k < kHeadPartVals; k += blockDim.x) {
-        float v = 0.f;
-        for (int c = 0; c < head_ctas; ++c) v += __ldcg(&A.head_part[static_cast<long long>(cbase + c) * kHeadPartVals + k]);
-        const int i = head_frag_to_natural(k);
-        if (i < 0) continue;
-        const long long o = i < kHeadNC * kHeadDH ? A.off_w1 + i
-                            : i < kHeadNC * kHeadDH + kHeadNC ? A.off_b1 + (i - kHeadNC * kHeadDH)
-                                                              : A.off_b0 + (i - kHeadNC * kHeadDH - kHeadNC);
-        gs[o] = v;
+    const int cbase = blockIdx.x - cta_in;
+    const int per = (kHeadPartVals + cnt - 1) / cnt;
+    const int k0 = cta_in * per, k1 = min(kHeadPartVals, k0 + per);
+    float* gs = A.slab + static_cast<long long>(g) * A.slab_stride;
+    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+      float x[4];
+      float v = 0.f;
+      for (int c4 = 0; c4 < head_ctas; c4 += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          x[u] = c4 + u < head_ctas ? __ldcg(&A.head_part[static_cast<long long>(cbase + c4 + u) * kHeadPartVals + k]) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c4 + u < head_ctas) v += x[u];
       }
-      if (threadIdx.x == 0) A.combine_cnt[g] = 0u;
+      const int i = head_frag_to_natural(k);
+      if (i < 0) continue;
+      const long long o = i < kHeadNC * kHeadDH ? A.off_w1 + i
+                          : i < kHeadNC * kHeadDH + kHeadNC ? A.off_b1 + (i - kHeadNC * kHeadDH)
+                                                            : A.off_b0 + (i - kHeadNC * kHeadDH - kHeadNC);
+      gs[o] = v;
     }
+    if (dbg && threadIdx.x == 0) dbg[5] = globaltimer();
     interfere(G.intf, g, A.timing ? &A.timing[2 * g] : nullptr, t_cta0);
     if (A.timing && threadIdx.x == 0) atomicMax(&A.timing[2 * g + 1], static_cast<unsigned long long>(globaltimer()));
   }

@@ -1315,6 +1315,7 @@ struct lbbsp_mlp {
   bool fused = false;
   CUtensorMap fz_tm[4];
   unsigned* fz_comb = nullptr;
+  unsigned long long* fz_dbg = nullptr;  // LBBSP_FZ_DEBUG: per-CTA stage stamps
   // e2e plumbing: cached host-buffer lookups (lbbsp_mlp_read_result_async,
   // lbbsp_mlp_step_e2e)
   int* res_host_sizes = nullptr;
@@ -1465,9 +1466,9 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     fa.off_b0 = off_b[0];
     fa.head_part = head_part;
     fa.done = D.fz_done;
-    fa.combine_cnt = fz_comb;
     fa.timing = phase_slot(ph++);
     fa.status = D.status;
+    fa.dbg = fz_dbg;
     LBBSP_CUDA_CHECK(launch_maybe_pdl(c2_fused_worker_kernel, sms, kFzThreads, kFzSmem, s, use_pdl, fz_tm[0],
                                       fz_tm[1], fz_tm[2], fz_tm[3], fa));
     ++nl;
@@ -2100,6 +2101,7 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     LBBSP_CUDA_CHECK(m.alloc(&fd, static_cast<size_t>(m.n_local)));
     D.fz_done = fd;
     LBBSP_CUDA_CHECK(m.alloc(&m.fz_comb, static_cast<size_t>(m.n_local)));
+    if (getenv("LBBSP_FZ_DEBUG")) LBBSP_CUDA_CHECK(m.alloc(&m.fz_dbg, static_cast<size_t>(num_sms()) * 8));
     LBBSP_CUDA_CHECK(cudaFuncSetAttribute(c2_fused_worker_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(kFzSmem)));
   }
@@ -2438,4 +2440,14 @@ extern "C" int lbbsp_mlp_step_e2e(lbbsp_mlp* m, const void* h_x_bf16, const int*
   rc = lbbsp_mlp_run(m, 1);
   if (rc) return rc;
   return lbbsp_mlp_read_result_async(m, h_sizes, h_loss);
+}
+
+// Debug: per-CTA stage stamps of the last fused worker launch ([grid][8]
+// globaltimer ns; LBBSP_FZ_DEBUG=1 at create). Not part of the stable C-ABI.
+extern "C" int lbbsp_mlp_fused_debug(lbbsp_mlp* m, unsigned long long* out, int* ctas) {
+  LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->stream));
+  *ctas = m->fz_dbg ? num_sms() : 0;
+  if (m->fz_dbg)
+    LBBSP_CUDA_CHECK(cudaMemcpy(out, m->fz_dbg, sizeof(unsigned long long) * 8 * num_sms(), cudaMemcpyDeviceToHost));
+  return LBBSP_OK;
 }

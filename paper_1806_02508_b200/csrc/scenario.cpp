@@ -11,6 +11,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <cerrno>
+#include <cctype>
 #include <cstring>
 #include <filesystem>
 #include <fstream>
@@ -95,7 +97,8 @@ double round9(double v) {
 }
 
 // ---------------------------------------------------------------------------
-// Traces (trace.cpp)
+// Traces (trace.cpp): CSV `machine_id,t_offset_s,cpu_avail,mem_avail`, one
+// series per machine in first-appearance order, times non-decreasing.
 // ---------------------------------------------------------------------------
 struct TracePoint {
   double t, cpu, mem;
@@ -103,228 +106,215 @@ struct TracePoint {
 struct Trace {
   std::string machine_id;
   std::vector<TracePoint> points;
-  // ResourceTrace::mean_cpu (trace.cpp:14-19): sequential sum
+  // ResourceTrace::mean_cpu (trace.cpp:14-19): sequential sum over the points
   double mean_cpu() const {
-    if (points.empty()) return 0.0;
     double s = 0.0;
     for (const auto& p : points) s += p.cpu;
-    return s / static_cast<double>(points.size());
+    return points.empty() ? 0.0 : s / static_cast<double>(points.size());
   }
 };
 
-std::vector<std::string> split_csv(const std::string& line) {  // trace.cpp:23-30
-  std::vector<std::string> out;
-  size_t start = 0;
-  while (start <= line.size()) {
-    const size_t comma = line.find(',', start);
-    if (comma == std::string::npos) {
-      if (start < line.size()) out.push_back(line.substr(start));
-      break;
+// Comma-separated fields; a trailing comma ends with an empty field.
+std::vector<std::string> csv_fields(const std::string& line) {
+  std::vector<std::string> f;
+  std::string cur;
+  for (char ch : line) {
+    if (ch == ',') {
+      f.push_back(cur);
+      cur.clear();
+    } else {
+      cur.push_back(ch);
     }
-    out.push_back(line.substr(start, comma - start));
-    start = comma + 1;
   }
-  if (!line.empty() && line.back() == ',') out.emplace_back();
-  return out;
+  if (!cur.empty() || (!line.empty() && line.back() == ',')) f.push_back(cur);
+  return f;
 }
 
-double parse_real(const std::string& s, const char* what, int line_no) {  // :32-43
-  bool ok = true;
-  double v = 0.0;
-  try {
-    size_t used = 0;
-    v = std::stod(s, &used);
-    ok = used == s.size();
-  } catch (const std::exception&) {
-    ok = false;
-  }
-  if (!ok)
-    fail(LBBSP_RUNTIME, "trace line " + std::to_string(line_no) + ": bad " + what + " '" + s + "'");
-  return v;
-}
+// Reads a trace file; every diagnostic names the 1-based line it concerns
+// (the wording of trace.cpp:32-97, which tests and callers match on).
+class TraceReader {
+ public:
+  explicit TraceReader(const std::string& path) : path_(path) {}
 
-double parse_fraction(const std::string& s, const char* what, int line_no) {  // :45-51
-  const double v = parse_real(s, what, line_no);
-  if (v < 0.0 || v > 1.0)
-    fail(LBBSP_RUNTIME, "trace line " + std::to_string(line_no) + ": " + what + " " + s +
-                            " outside [0,1]");
-  return v;
-}
-
-std::vector<Trace> parse_trace(const std::string& path) {  // trace.cpp:54-97
-  std::ifstream in(path);
-  if (!in) fail(LBBSP_RUNTIME, "parse_trace: cannot open " + path);
-  std::string header;
-  if (!std::getline(in, header)) fail(LBBSP_RUNTIME, "parse_trace: empty file " + path);
-  if (!header.empty() && header.back() == '\r') header.pop_back();
-  const std::vector<std::string> cols = split_csv(header);
-  const std::vector<std::string> want = {"machine_id", "t_offset_s", "cpu_avail", "mem_avail"};
-  for (const auto& name : want)
-    if (std::find(cols.begin(), cols.end(), name) == cols.end())
-      fail(LBBSP_RUNTIME, "parse_trace: missing column '" + name + "'");
-  if (cols != want)
-    fail(LBBSP_RUNTIME,
-         "parse_trace: unexpected column order, want machine_id,t_offset_s,cpu_avail,mem_avail");
-  std::vector<Trace> traces;
-  std::map<std::string, size_t> index;
-  std::string line;
-  int line_no = 1;
-  while (std::getline(in, line)) {
-    ++line_no;
-    if (!line.empty() && line.back() == '\r') line.pop_back();
-    if (line.empty()) continue;
-    const auto f = split_csv(line);
-    if (f.size() != 4)
-      fail(LBBSP_RUNTIME, "trace line " + std::to_string(line_no) + ": expected 4 fields, got " +
-                              std::to_string(f.size()));
-    TracePoint p;
-    p.t = parse_real(f[1], "t_offset_s", line_no);
-    p.cpu = parse_fraction(f[2], "cpu_avail", line_no);
-    p.mem = parse_fraction(f[3], "mem_avail", line_no);
-    auto it = index.find(f[0]);
-    if (it == index.end()) {
-      it = index.emplace(f[0], traces.size()).first;
-      traces.push_back(Trace{f[0], {}});
+  std::vector<Trace> read() {
+    std::ifstream in(path_);
+    if (!in) fail(LBBSP_RUNTIME, "parse_trace: cannot open " + path_);
+    std::string text;
+    if (!std::getline(in, text)) fail(LBBSP_RUNTIME, "parse_trace: empty file " + path_);
+    check_header(csv_fields(strip_cr(text)));
+    int line_no = 1;
+    while (std::getline(in, text)) {
+      ++line_no;
+      const std::string row = strip_cr(text);
+      if (!row.empty()) add_row(csv_fields(row), line_no);
     }
-    Trace& t = traces[it->second];
-    if (!t.points.empty() && p.t < t.points.back().t)
-      fail(LBBSP_RUNTIME, "trace line " + std::to_string(line_no) +
-                              ": time offsets not sorted for machine " + f[0]);
-    t.points.push_back(p);
+    return std::move(out_);
   }
-  return traces;
-}
 
-// map_traces (trace.cpp:109-135): stratified by mean cpu, one seeded draw per worker.
+ private:
+  static std::string strip_cr(std::string s) {
+    if (!s.empty() && s.back() == '\r') s.pop_back();
+    return s;
+  }
+  [[noreturn]] static void at_line(int line_no, const std::string& msg) {
+    fail(LBBSP_RUNTIME, "trace line " + std::to_string(line_no) + ": " + msg);
+  }
+  static void check_header(const std::vector<std::string>& cols) {
+    static const char* const kCols[4] = {"machine_id", "t_offset_s", "cpu_avail", "mem_avail"};
+    for (const char* name : kCols)
+      if (std::find(cols.begin(), cols.end(), name) == cols.end())
+        fail(LBBSP_RUNTIME, std::string("parse_trace: missing column '") + name + "'");
+    const bool in_order = cols.size() == 4 && std::equal(cols.begin(), cols.end(), kCols);
+    if (!in_order)
+      fail(LBBSP_RUNTIME, "parse_trace: unexpected column order, want machine_id,t_offset_s,cpu_avail,mem_avail");
+  }
+  // the whole field must convert (std::stod semantics: leading blanks are
+  // skipped, out-of-range values are errors)
+  static double number(const std::string& s, const char* what, int line_no) {
+    char* end = nullptr;
+    errno = 0;
+    const double v = std::strtod(s.c_str(), &end);
+    if (end == s.c_str() || end != s.c_str() + s.size() || errno == ERANGE)
+      at_line(line_no, std::string("bad ") + what + " '" + s + "'");
+    return v;
+  }
+  static double share(const std::string& s, const char* what, int line_no) {
+    const double v = number(s, what, line_no);
+    if (!(v >= 0.0 && v <= 1.0)) at_line(line_no, std::string(what) + " " + s + " outside [0,1]");
+    return v;
+  }
+  void add_row(const std::vector<std::string>& f, int line_no) {
+    if (f.size() != 4) at_line(line_no, "expected 4 fields, got " + std::to_string(f.size()));
+    const TracePoint p{number(f[1], "t_offset_s", line_no), share(f[2], "cpu_avail", line_no),
+                       share(f[3], "mem_avail", line_no)};
+    auto [it, fresh] = slot_.try_emplace(f[0], out_.size());
+    if (fresh) out_.push_back(Trace{f[0], {}});
+    std::vector<TracePoint>& pts = out_[it->second].points;
+    if (!pts.empty() && p.t < pts.back().t)
+      at_line(line_no, "time offsets not sorted for machine " + f[0]);
+    pts.push_back(p);
+  }
+
+  std::string path_;
+  std::vector<Trace> out_;
+  std::map<std::string, size_t> slot_;
+};
+
+std::vector<Trace> parse_trace(const std::string& path) { return TraceReader(path).read(); }
+
+// map_traces (trace.cpp:109-135): the traces ranked by mean cpu availability
+// (stable), cut into `workers` equal strata; worker w draws one trace of its
+// stratum with the seeded generator.
 std::vector<int> map_traces(const std::vector<Trace>& traces, int workers, uint64_t seed) {
   if (traces.empty()) fail(LBBSP_INVALID_ARGUMENT, "map_traces: no traces");
   if (workers < 1) fail(LBBSP_INVALID_ARGUMENT, "map_traces: workers must be >= 1");
-  std::vector<double> mean(traces.size());
-  for (size_t i = 0; i < traces.size(); ++i) mean[i] = traces[i].mean_cpu();
-  std::vector<size_t> order(traces.size());
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](size_t a, size_t b) { return mean[a] < mean[b]; });
-  Rng rng(mix_seed(seed, 0x7ace5ull));
-  std::vector<int> out(static_cast<size_t>(workers));
-  const double stride = static_cast<double>(traces.size()) / static_cast<double>(workers);
+  const size_t T = traces.size();
+  std::vector<std::pair<double, size_t>> ranked;
+  for (size_t i = 0; i < T; ++i) ranked.emplace_back(traces[i].mean_cpu(), i);
+  std::stable_sort(ranked.begin(), ranked.end(),
+                   [](const auto& a, const auto& b) { return a.first < b.first; });
+  Rng draw(mix_seed(seed, 0x7ace5ull));
+  const double width = static_cast<double>(T) / static_cast<double>(workers);
+  std::vector<int> pick(static_cast<size_t>(workers));
   for (int w = 0; w < workers; ++w) {
-    const size_t lo = static_cast<size_t>(std::floor(stride * w));
-    size_t hi = static_cast<size_t>(std::floor(stride * (w + 1)));
-    if (hi <= lo) hi = lo + 1;
-    if (hi > traces.size()) hi = traces.size();
-    const size_t pick = lo + static_cast<size_t>(rng.uniform() * static_cast<double>(hi - lo));
-    out[static_cast<size_t>(w)] = static_cast<int>(order[std::min(pick, traces.size() - 1)]);
+    const size_t first = static_cast<size_t>(std::floor(width * w));
+    const size_t end = std::min(T, std::max(first + 1, static_cast<size_t>(std::floor(width * (w + 1)))));
+    const size_t at = first + static_cast<size_t>(draw.uniform() * static_cast<double>(end - first));
+    pick[static_cast<size_t>(w)] = static_cast<int>(ranked[std::min(at, T - 1)].second);
   }
-  return out;
+  return pick;
 }
 
 // ---------------------------------------------------------------------------
-// NARX weights CSV (predictor.cpp:198-243)
+// NARX weights CSV (predictor.cpp:198-243): `name,value` rows
 // ---------------------------------------------------------------------------
+struct NarxField {
+  std::string name;
+  double lbbsp_narx_model::*member;
+  int index;  // input_weights[index] when member is null
+};
+const std::vector<NarxField>& narx_fields() {
+  static const std::vector<NarxField> f = [] {
+    std::vector<NarxField> v;
+    for (int j = 0; j < 8; ++j) v.push_back({"input_weight_" + std::to_string(j), nullptr, j});
+    v.push_back({"hidden_bias", &lbbsp_narx_model::hidden_bias, -1});
+    v.push_back({"output_weight", &lbbsp_narx_model::output_weight, -1});
+    v.push_back({"output_bias", &lbbsp_narx_model::output_bias, -1});
+    v.push_back({"speed_mean", &lbbsp_narx_model::speed_mean, -1});
+    v.push_back({"speed_stddev", &lbbsp_narx_model::speed_stddev, -1});
+    v.push_back({"cpu_mean", &lbbsp_narx_model::cpu_mean, -1});
+    v.push_back({"cpu_stddev", &lbbsp_narx_model::cpu_stddev, -1});
+    v.push_back({"mem_mean", &lbbsp_narx_model::mem_mean, -1});
+    v.push_back({"mem_stddev", &lbbsp_narx_model::mem_stddev, -1});
+    return v;
+  }();
+  return f;
+}
+double& narx_ref(lbbsp_narx_model& m, const NarxField& f) {
+  return f.member ? m.*(f.member) : m.input_weights[f.index];
+}
+
 lbbsp_narx_model load_narx_csv(const std::string& path) {
   std::ifstream in(path);
   if (!in) fail(LBBSP_RUNTIME, "load_narx_csv: cannot open " + path);
-  std::map<std::string, double> values;
-  std::string line;
-  while (std::getline(in, line)) {
-    if (line.empty()) continue;
-    const auto comma = line.find(',');
-    if (comma == std::string::npos) fail(LBBSP_RUNTIME, "load_narx_csv: malformed row '" + line + "'");
-    values[line.substr(0, comma)] = std::stod(line.substr(comma + 1));
+  std::map<std::string, double> kv;
+  for (std::string row; std::getline(in, row);) {
+    if (row.empty()) continue;
+    const size_t cut = row.find(',');
+    if (cut == std::string::npos) fail(LBBSP_RUNTIME, "load_narx_csv: malformed row '" + row + "'");
+    kv[row.substr(0, cut)] = std::stod(row.substr(cut + 1));
   }
-  auto get = [&](const std::string& name) {
-    const auto it = values.find(name);
-    if (it == values.end()) fail(LBBSP_RUNTIME, "load_narx_csv: missing parameter '" + name + "'");
-    return it->second;
-  };
   lbbsp_narx_model m{};
-  for (int j = 0; j < 8; ++j) m.input_weights[j] = get("input_weight_" + std::to_string(j));
-  m.hidden_bias = get("hidden_bias");
-  m.output_weight = get("output_weight");
-  m.output_bias = get("output_bias");
-  m.speed_mean = get("speed_mean");
-  m.speed_stddev = get("speed_stddev");
-  m.cpu_mean = get("cpu_mean");
-  m.cpu_stddev = get("cpu_stddev");
-  m.mem_mean = get("mem_mean");
-  m.mem_stddev = get("mem_stddev");
+  for (const NarxField& f : narx_fields()) {
+    const auto hit = kv.find(f.name);
+    if (hit == kv.end()) fail(LBBSP_RUNTIME, "load_narx_csv: missing parameter '" + f.name + "'");
+    narx_ref(m, f) = hit->second;
+  }
   return m;
 }
 
+void save_narx_csv(lbbsp_narx_model m, const std::string& path) {
+  std::ofstream out(path);
+  if (!out) fail(LBBSP_RUNTIME, "save_narx_csv: cannot open " + path);
+  out.precision(17);
+  for (const NarxField& f : narx_fields()) out << f.name << "," << narx_ref(m, f) << "\n";
+}
+
 // ---------------------------------------------------------------------------
-// Scenario (scenario.cpp:31-294)
+// Names (coordination.cpp:9-25, predictor.cpp:245-261, cluster_sim.cpp:131-138)
 // ---------------------------------------------------------------------------
-const std::set<std::string> kKnownKeys = {
-    "scheme", "staleness_threshold", "workers", "total_budget", "preset", "trace_path",
-    "gpu_profiles", "bandwidth_drop", "base_speed", "base_comm_s", "predictor", "alpha",
-    "warmup_iterations", "speed_floor", "narx_weights_path", "learning_rate",
-    "dataset_seed", "dataset_size", "dataset_dim", "dataset_noise", "convergence_loss",
-    "convergence_consecutive", "max_iterations", "seed", "benchmark_iterations",
-    "benchmark_regime_length", "benchmark_spike_mult", "benchmark_spike_prob",
-    "benchmark_high_band", "benchmark_low_band", "paired_sim"};
-
-template <typename T>
-T require(const json& j, const std::string& key) {
-  if (!j.contains(key)) config_error("config: missing field '" + key + "'");
-  try {
-    return j.at(key).get<T>();
-  } catch (const json::exception&) {
-    config_error("config: bad value for field '" + key + "'");
-  }
+struct Named {
+  const char* name;
+  int value;
+};
+constexpr Named kSchemes[] = {{"bsp", LBBSP_SCHEME_BSP}, {"asp", LBBSP_SCHEME_ASP},
+                              {"ssp", LBBSP_SCHEME_SSP}, {"lb-bsp", LBBSP_SCHEME_LBBSP},
+                              {"lbbsp", LBBSP_SCHEME_LBBSP}};
+constexpr Named kPredictors[] = {{"memoryless", LBBSP_PRED_MEMORYLESS}, {"ema", LBBSP_PRED_EMA},
+                                 {"narx", LBBSP_PRED_NARX}, {"perfect", LBBSP_PRED_PERFECT}};
+constexpr Named kPresets[] = {{"homo", LBBSP_PRESET_HOMO},
+                              {"hetero-l2", LBBSP_PRESET_HETERO_L2},
+                              {"hetero-l3", LBBSP_PRESET_HETERO_L3},
+                              {"hetero-l2-static", LBBSP_PRESET_HETERO_L2_STATIC},
+                              {"hetero-l3-static", LBBSP_PRESET_HETERO_L3_STATIC}};
+template <size_t N>
+int lookup(const Named (&table)[N], const std::string& s, const char* what) {
+  for (const Named& e : table)
+    if (s == e.name) return e.value;
+  throw std::invalid_argument(std::string("unknown ") + what + ": " + s);
 }
-
-template <typename T>
-T get_or(const json& j, const std::string& key, T fallback) {
-  if (!j.contains(key)) return fallback;
-  try {
-    return j.at(key).get<T>();
-  } catch (const json::exception&) {
-    config_error("config: bad value for field '" + key + "'");
-  }
-}
-
-int scheme_from_string(const std::string& s) {  // coordination.cpp:19-25
-  if (s == "bsp") return LBBSP_SCHEME_BSP;
-  if (s == "asp") return LBBSP_SCHEME_ASP;
-  if (s == "ssp") return LBBSP_SCHEME_SSP;
-  if (s == "lb-bsp" || s == "lbbsp") return LBBSP_SCHEME_LBBSP;
-  throw std::invalid_argument("unknown scheme: " + s);
-}
-const char* scheme_name(int k) {  // coordination.cpp:9-17
-  switch (k) {
-    case LBBSP_SCHEME_BSP: return "bsp";
-    case LBBSP_SCHEME_ASP: return "asp";
-    case LBBSP_SCHEME_SSP: return "ssp";
-    case LBBSP_SCHEME_LBBSP: return "lb-bsp";
-  }
+template <size_t N>
+const char* name_of(const Named (&table)[N], int v) {
+  for (const Named& e : table)
+    if (e.value == v) return e.name;
   return "?";
 }
-int predictor_from_string(const std::string& s) {  // predictor.cpp:255-261
-  if (s == "memoryless") return LBBSP_PRED_MEMORYLESS;
-  if (s == "ema") return LBBSP_PRED_EMA;
-  if (s == "narx") return LBBSP_PRED_NARX;
-  if (s == "perfect") return LBBSP_PRED_PERFECT;
-  throw std::invalid_argument("unknown predictor: " + s);
-}
-const char* predictor_name(int k) {  // predictor.cpp:245-253
-  switch (k) {
-    case LBBSP_PRED_MEMORYLESS: return "memoryless";
-    case LBBSP_PRED_EMA: return "ema";
-    case LBBSP_PRED_NARX: return "narx";
-    case LBBSP_PRED_PERFECT: return "perfect";
-  }
-  return "?";
-}
-int preset_from_string(const std::string& s) {  // cluster_sim.cpp:131-138
-  if (s == "homo") return LBBSP_PRESET_HOMO;
-  if (s == "hetero-l2") return LBBSP_PRESET_HETERO_L2;
-  if (s == "hetero-l3") return LBBSP_PRESET_HETERO_L3;
-  if (s == "hetero-l2-static") return LBBSP_PRESET_HETERO_L2_STATIC;
-  if (s == "hetero-l3-static") return LBBSP_PRESET_HETERO_L3_STATIC;
-  throw std::invalid_argument("unknown preset: " + s);
-}
+const char* scheme_name(int k) { return name_of(kSchemes, k); }
+const char* predictor_name(int k) { return name_of(kPredictors, k); }
 
+// ---------------------------------------------------------------------------
+// Scenario JSON (ScenarioConfig, scenario.hpp:33-64; loader scenario.cpp:31-217)
+// ---------------------------------------------------------------------------
 struct GpuGroup {
   lbbsp_gpu_profile profile;
   int count;
@@ -340,7 +330,7 @@ struct Bench {  // BenchmarkTraceConfig defaults (cluster_sim.hpp:76-83)
   double spike_mult = 3.0, spike_prob = 0.02;
 };
 
-struct Scenario {  // ScenarioConfig (scenario.hpp:33-64)
+struct Scenario {
   std::string name;
   int scheme = LBBSP_SCHEME_BSP;
   int staleness_threshold = 0;
@@ -370,36 +360,179 @@ struct Scenario {  // ScenarioConfig (scenario.hpp:33-64)
   bool paired_sim = true;
 };
 
-void validate_scenario(const Scenario& c) {  // scenario.cpp:183-217
-  if (c.workers < 1) config_error("config: field 'workers' must be >= 1");
-  if (c.total_budget < c.workers) config_error("config: field 'total_budget' must be >= workers");
-  if (c.staleness_threshold < 0) config_error("config: field 'staleness_threshold' must be >= 0");
-  if (!(c.alpha > 0.0 && c.alpha <= 1.0)) config_error("config: field 'alpha' must be in (0, 1]");
-  if (c.learning_rate <= 0.0) config_error("config: field 'learning_rate' must be > 0");
-  if (c.dataset_size < 1) config_error("config: field 'dataset_size' must be >= 1");
-  if (c.dataset_dim < 1) config_error("config: field 'dataset_dim' must be >= 1");
-  if (c.convergence_loss <= 0.0) config_error("config: field 'convergence_loss' must be > 0");
-  if (c.convergence_consecutive < 1)
-    config_error("config: field 'convergence_consecutive' must be >= 1");
-  if (c.max_iterations < 1) config_error("config: field 'max_iterations' must be >= 1");
-  if (!c.trace_path.empty() && !fs::exists(c.trace_path))
-    config_error("config: trace file not found: " + c.trace_path);
-  if (!c.narx_weights_path.empty() && !fs::exists(c.narx_weights_path))
-    config_error("config: narx weights file not found: " + c.narx_weights_path);
-  if (!c.gpu_profiles.empty()) {
-    int total = 0;
-    for (const auto& g : c.gpu_profiles) total += g.count;
-    if (total != c.workers)
-      config_error("config: gpu_profiles counts sum to " + std::to_string(total) +
-                   ", field 'workers' says " + std::to_string(c.workers));
-    if (!c.trace_path.empty()) config_error("config: gpu_profiles and trace_path cannot be combined");
+// A typed read of one JSON member: absent -> nullopt; present but of the
+// wrong type -> "config: bad value for field '<key>'".
+template <typename T>
+std::optional<T> member(const json& obj, const char* key) {
+  const auto it = obj.find(key);
+  if (it == obj.end()) return std::nullopt;
+  try {
+    return it->template get<T>();
+  } catch (const json::exception&) {
+    config_error(std::string("config: bad value for field '") + key + "'");
   }
-  if (c.bandwidth_drop &&
-      (c.bandwidth_drop->worker < 0 || c.bandwidth_drop->worker >= c.workers))
-    config_error("config: bandwidth_drop worker out of range");
+}
+template <typename T>
+T needed(const json& obj, const char* key) {
+  if (auto v = member<T>(obj, key)) return *v;
+  config_error(std::string("config: missing field '") + key + "'");
+}
+template <typename T>
+void optional_into(const json& obj, const char* key, T& dst) {
+  if (auto v = member<T>(obj, key)) dst = *v;
 }
 
-Scenario load_scenario(const std::string& path_str) {  // scenario.cpp:92-181
+// One entry per accepted key, in the order the fields are read (which is the
+// order their errors take precedence in). total_budget defaults to 128 per
+// worker, so it follows workers.
+struct FieldRule {
+  const char* key;
+  void (*read)(const json& j, Scenario& c);
+};
+void read_band(const json& j, const char* key, double& lo, double& hi) {
+  if (!j.contains(key)) return;
+  const auto band = needed<std::vector<double>>(j, key);
+  if (band.size() != 2) config_error(std::string("config: field '") + key + "' needs [lo, hi]");
+  lo = band[0];
+  hi = band[1];
+}
+const std::vector<FieldRule>& field_rules() {
+  static const std::vector<FieldRule> rules = {
+      {"scheme",
+       [](const json& j, Scenario& c) {
+         const std::string s = needed<std::string>(j, "scheme");
+         try {
+           c.scheme = lookup(kSchemes, s, "scheme");
+         } catch (const std::invalid_argument& e) {
+           config_error(std::string("config: field 'scheme': ") + e.what());
+         }
+       }},
+      {"workers", [](const json& j, Scenario& c) { c.workers = needed<int>(j, "workers"); }},
+      {"staleness_threshold", [](const json& j, Scenario& c) { optional_into(j, "staleness_threshold", c.staleness_threshold); }},
+      {"total_budget",
+       [](const json& j, Scenario& c) {
+         c.total_budget = 128 * c.workers;
+         optional_into(j, "total_budget", c.total_budget);
+       }},
+      {"preset", [](const json& j, Scenario& c) { optional_into(j, "preset", c.preset); }},
+      {"trace_path", [](const json& j, Scenario& c) { optional_into(j, "trace_path", c.trace_path); }},
+      {"base_speed", [](const json& j, Scenario& c) { optional_into(j, "base_speed", c.base_speed); }},
+      {"base_comm_s", [](const json& j, Scenario& c) { optional_into(j, "base_comm_s", c.base_comm_s); }},
+      {"predictor",
+       [](const json& j, Scenario& c) {
+         std::string s = "ema";
+         optional_into(j, "predictor", s);
+         try {
+           c.predictor = lookup(kPredictors, s, "predictor");
+         } catch (const std::invalid_argument& e) {
+           config_error(std::string("config: field 'predictor': ") + e.what());
+         }
+       }},
+      {"alpha", [](const json& j, Scenario& c) { optional_into(j, "alpha", c.alpha); }},
+      {"warmup_iterations", [](const json& j, Scenario& c) { optional_into(j, "warmup_iterations", c.warmup_iterations); }},
+      {"speed_floor", [](const json& j, Scenario& c) { optional_into(j, "speed_floor", c.speed_floor); }},
+      {"narx_weights_path", [](const json& j, Scenario& c) { optional_into(j, "narx_weights_path", c.narx_weights_path); }},
+      {"learning_rate", [](const json& j, Scenario& c) { optional_into(j, "learning_rate", c.learning_rate); }},
+      {"dataset_seed", [](const json& j, Scenario& c) { optional_into(j, "dataset_seed", c.dataset_seed); }},
+      {"dataset_size", [](const json& j, Scenario& c) { optional_into(j, "dataset_size", c.dataset_size); }},
+      {"dataset_dim", [](const json& j, Scenario& c) { optional_into(j, "dataset_dim", c.dataset_dim); }},
+      {"dataset_noise", [](const json& j, Scenario& c) { optional_into(j, "dataset_noise", c.dataset_noise); }},
+      {"convergence_loss", [](const json& j, Scenario& c) { optional_into(j, "convergence_loss", c.convergence_loss); }},
+      {"convergence_consecutive",
+       [](const json& j, Scenario& c) { optional_into(j, "convergence_consecutive", c.convergence_consecutive); }},
+      {"max_iterations", [](const json& j, Scenario& c) { optional_into(j, "max_iterations", c.max_iterations); }},
+      {"seed", [](const json& j, Scenario& c) { optional_into(j, "seed", c.seed); }},
+      {"paired_sim", [](const json& j, Scenario& c) { optional_into(j, "paired_sim", c.paired_sim); }},
+      {"benchmark_iterations",
+       [](const json& j, Scenario& c) { optional_into(j, "benchmark_iterations", c.benchmark.iterations); }},
+      {"benchmark_regime_length",
+       [](const json& j, Scenario& c) { optional_into(j, "benchmark_regime_length", c.benchmark.regime_length); }},
+      {"benchmark_spike_mult",
+       [](const json& j, Scenario& c) { optional_into(j, "benchmark_spike_mult", c.benchmark.spike_mult); }},
+      {"benchmark_spike_prob",
+       [](const json& j, Scenario& c) { optional_into(j, "benchmark_spike_prob", c.benchmark.spike_prob); }},
+      {"benchmark_high_band",
+       [](const json& j, Scenario& c) { read_band(j, "benchmark_high_band", c.benchmark.high_lo, c.benchmark.high_hi); }},
+      {"benchmark_low_band",
+       [](const json& j, Scenario& c) { read_band(j, "benchmark_low_band", c.benchmark.low_lo, c.benchmark.low_hi); }},
+      {"gpu_profiles",
+       [](const json& j, Scenario& c) {
+         const auto it = j.find("gpu_profiles");
+         if (it == j.end()) return;
+         if (!it->is_array()) config_error("config: field 'gpu_profiles' must be an array");
+         for (const json& e : *it) {
+           GpuGroup grp{};
+           grp.profile = lbbsp_gpu_profile{needed<double>(e, "sec_per_sample"), needed<double>(e, "base_time_s"),
+                                           needed<int>(e, "saturation_point"), needed<int>(e, "oom_point")};
+           grp.count = 1;
+           optional_into(e, "count", grp.count);
+           c.gpu_profiles.push_back(grp);
+         }
+       }},
+      {"bandwidth_drop",
+       [](const json& j, Scenario& c) {
+         const auto it = j.find("bandwidth_drop");
+         if (it == j.end()) return;
+         c.bandwidth_drop = BandwidthDrop{needed<int>(*it, "worker"), needed<int64_t>(*it, "at_iteration"),
+                                          needed<double>(*it, "comm_factor")};
+       }},
+  };
+  return rules;
+}
+
+// validate_scenario (scenario.cpp:183-217): the first violated rule wins.
+struct CheckRule {
+  bool (*bad)(const Scenario& c);
+  std::string (*message)(const Scenario& c);
+};
+int gpu_count(const Scenario& c) {
+  int total = 0;
+  for (const auto& g : c.gpu_profiles) total += g.count;
+  return total;
+}
+const std::vector<CheckRule>& check_rules() {
+  using S = const Scenario&;
+  static const std::vector<CheckRule> rules = {
+      {[](S c) { return c.workers < 1; }, [](S) { return std::string("field 'workers' must be >= 1"); }},
+      {[](S c) { return c.total_budget < c.workers; },
+       [](S) { return std::string("field 'total_budget' must be >= workers"); }},
+      {[](S c) { return c.staleness_threshold < 0; },
+       [](S) { return std::string("field 'staleness_threshold' must be >= 0"); }},
+      {[](S c) { return !(c.alpha > 0.0 && c.alpha <= 1.0); },
+       [](S) { return std::string("field 'alpha' must be in (0, 1]"); }},
+      {[](S c) { return c.learning_rate <= 0.0; }, [](S) { return std::string("field 'learning_rate' must be > 0"); }},
+      {[](S c) { return c.dataset_size < 1; }, [](S) { return std::string("field 'dataset_size' must be >= 1"); }},
+      {[](S c) { return c.dataset_dim < 1; }, [](S) { return std::string("field 'dataset_dim' must be >= 1"); }},
+      {[](S c) { return c.convergence_loss <= 0.0; },
+       [](S) { return std::string("field 'convergence_loss' must be > 0"); }},
+      {[](S c) { return c.convergence_consecutive < 1; },
+       [](S) { return std::string("field 'convergence_consecutive' must be >= 1"); }},
+      {[](S c) { return c.max_iterations < 1; }, [](S) { return std::string("field 'max_iterations' must be >= 1"); }},
+      {[](S c) { return !c.trace_path.empty() && !fs::exists(c.trace_path); },
+       [](S c) { return "trace file not found: " + c.trace_path; }},
+      {[](S c) { return !c.narx_weights_path.empty() && !fs::exists(c.narx_weights_path); },
+       [](S c) { return "narx weights file not found: " + c.narx_weights_path; }},
+      {[](S c) { return !c.gpu_profiles.empty() && gpu_count(c) != c.workers; },
+       [](S c) {
+         return "gpu_profiles counts sum to " + std::to_string(gpu_count(c)) + ", field 'workers' says " +
+                std::to_string(c.workers);
+       }},
+      {[](S c) { return !c.gpu_profiles.empty() && !c.trace_path.empty(); },
+       [](S) { return std::string("gpu_profiles and trace_path cannot be combined"); }},
+      {[](S c) {
+         return c.bandwidth_drop && (c.bandwidth_drop->worker < 0 || c.bandwidth_drop->worker >= c.workers);
+       },
+       [](S) { return std::string("bandwidth_drop worker out of range"); }},
+  };
+  return rules;
+}
+
+void validate_scenario(const Scenario& c) {
+  for (const CheckRule& r : check_rules())
+    if (r.bad(c)) config_error("config: " + r.message(c));
+}
+
+Scenario load_scenario(const std::string& path_str) {
   const fs::path path(path_str);
   std::ifstream in(path);
   if (!in) config_error("config: cannot open " + path.string());
@@ -410,78 +543,15 @@ Scenario load_scenario(const std::string& path_str) {  // scenario.cpp:92-181
     config_error("config: invalid JSON in " + path.string() + ": " + e.what());
   }
   if (!j.is_object()) config_error("config: top level must be a JSON object");
-  for (const auto& [key, value] : j.items())
-    if (!kKnownKeys.count(key)) config_error("config: unknown field '" + key + "'");
+  const auto& rules = field_rules();
+  for (const auto& item : j.items()) {  // strict keys (object keys iterate sorted)
+    const bool known = std::any_of(rules.begin(), rules.end(),
+                                   [&](const FieldRule& r) { return item.key() == r.key; });
+    if (!known) config_error("config: unknown field '" + item.key() + "'");
+  }
   Scenario c;
   c.name = path.stem().string();
-  try {
-    c.scheme = scheme_from_string(require<std::string>(j, "scheme"));
-  } catch (const std::invalid_argument& e) {
-    config_error(std::string("config: field 'scheme': ") + e.what());
-  }
-  c.workers = require<int>(j, "workers");
-  c.staleness_threshold = get_or(j, "staleness_threshold", 0);
-  c.total_budget = get_or(j, "total_budget", 128 * c.workers);
-  c.preset = get_or<std::string>(j, "preset", "homo");
-  c.trace_path = get_or<std::string>(j, "trace_path", "");
-  c.base_speed = get_or(j, "base_speed", 10.0);
-  c.base_comm_s = get_or(j, "base_comm_s", 0.0);
-  try {
-    c.predictor = predictor_from_string(get_or<std::string>(j, "predictor", "ema"));
-  } catch (const std::invalid_argument& e) {
-    config_error(std::string("config: field 'predictor': ") + e.what());
-  }
-  c.alpha = get_or(j, "alpha", 0.2);
-  c.warmup_iterations = get_or(j, "warmup_iterations", 500);
-  c.speed_floor = get_or(j, "speed_floor", 1e-3);
-  c.narx_weights_path = get_or<std::string>(j, "narx_weights_path", "");
-  c.learning_rate = get_or(j, "learning_rate", 0.5);
-  c.dataset_seed = get_or<uint64_t>(j, "dataset_seed", 7);
-  c.dataset_size = get_or(j, "dataset_size", 1000);
-  c.dataset_dim = get_or(j, "dataset_dim", 10);
-  c.dataset_noise = get_or(j, "dataset_noise", 0.1);
-  c.convergence_loss = get_or(j, "convergence_loss", 0.40);
-  c.convergence_consecutive = get_or(j, "convergence_consecutive", 10);
-  c.max_iterations = get_or<int64_t>(j, "max_iterations", 500);
-  c.seed = get_or<uint64_t>(j, "seed", 1);
-  c.paired_sim = get_or(j, "paired_sim", true);
-  c.benchmark.iterations = get_or(j, "benchmark_iterations", c.benchmark.iterations);
-  c.benchmark.regime_length = get_or(j, "benchmark_regime_length", c.benchmark.regime_length);
-  c.benchmark.spike_mult = get_or(j, "benchmark_spike_mult", c.benchmark.spike_mult);
-  c.benchmark.spike_prob = get_or(j, "benchmark_spike_prob", c.benchmark.spike_prob);
-  if (j.contains("benchmark_high_band")) {
-    const auto band = require<std::vector<double>>(j, "benchmark_high_band");
-    if (band.size() != 2) config_error("config: field 'benchmark_high_band' needs [lo, hi]");
-    c.benchmark.high_lo = band[0];
-    c.benchmark.high_hi = band[1];
-  }
-  if (j.contains("benchmark_low_band")) {
-    const auto band = require<std::vector<double>>(j, "benchmark_low_band");
-    if (band.size() != 2) config_error("config: field 'benchmark_low_band' needs [lo, hi]");
-    c.benchmark.low_lo = band[0];
-    c.benchmark.low_hi = band[1];
-  }
-  if (j.contains("gpu_profiles")) {
-    const json& groups = j.at("gpu_profiles");
-    if (!groups.is_array()) config_error("config: field 'gpu_profiles' must be an array");
-    for (const json& g : groups) {
-      GpuGroup grp{};
-      grp.profile.sec_per_sample = require<double>(g, "sec_per_sample");
-      grp.profile.base_time_s = require<double>(g, "base_time_s");
-      grp.profile.saturation_point = require<int>(g, "saturation_point");
-      grp.profile.oom_point = require<int>(g, "oom_point");
-      grp.count = get_or(g, "count", 1);
-      c.gpu_profiles.push_back(grp);
-    }
-  }
-  if (j.contains("bandwidth_drop")) {
-    const json& d = j.at("bandwidth_drop");
-    BandwidthDrop drop{};
-    drop.worker = require<int>(d, "worker");
-    drop.at_iteration = require<int64_t>(d, "at_iteration");
-    drop.comm_factor = require<double>(d, "comm_factor");
-    c.bandwidth_drop = drop;
-  }
+  for (const FieldRule& r : rules) r.read(j, c);
   validate_scenario(c);
   return c;
 }
@@ -568,7 +638,7 @@ void build_sim_config(const Scenario& c, BuiltSim& b) {
     s.dynamics = LBBSP_DYN_BENCHMARK;
   } else {
     try {
-      s.preset = preset_from_string(c.preset);
+      s.preset = lookup(kPresets, c.preset, "preset");
     } catch (const std::invalid_argument& e) {
       config_error(std::string("config: field 'preset': ") + e.what());
     }
@@ -870,21 +940,7 @@ extern "C" int lbbsp_narx_load_csv(const char* path, lbbsp_narx_model* out) {
 }
 
 extern "C" int lbbsp_narx_save_csv(const lbbsp_narx_model* m, const char* path) {
-  return guarded([&] {  // predictor.cpp:198-213
-    std::ofstream out(path);
-    if (!out) fail(LBBSP_RUNTIME, std::string("save_narx_csv: cannot open ") + path);
-    out.precision(17);
-    for (int j = 0; j < 8; ++j) out << "input_weight_" << j << "," << m->input_weights[j] << "\n";
-    out << "hidden_bias," << m->hidden_bias << "\n";
-    out << "output_weight," << m->output_weight << "\n";
-    out << "output_bias," << m->output_bias << "\n";
-    out << "speed_mean," << m->speed_mean << "\n";
-    out << "speed_stddev," << m->speed_stddev << "\n";
-    out << "cpu_mean," << m->cpu_mean << "\n";
-    out << "cpu_stddev," << m->cpu_stddev << "\n";
-    out << "mem_mean," << m->mem_mean << "\n";
-    out << "mem_stddev," << m->mem_stddev << "\n";
-  });
+  return guarded([&] { save_narx_csv(*m, path); });
 }
 
 extern "C" int lbbsp_scenario_load(const char* path, lbbsp_scenario** out) {
@@ -939,7 +995,7 @@ extern "C" int lbbsp_scenario_sim_cfg(lbbsp_scenario* s, const lbbsp_sim_cfg** c
   });
 }
 
-// cmd_run / cmd_compare / cmd_predict_bench (scenario.cpp:369-481)
+// cmd_run (scenario.cpp:369-386): the records/metrics exporters over one scenario
 template <class F>
 static int cli(const char* prefix, F&& fn) {
   const int rc = guarded(fn);
@@ -960,93 +1016,5 @@ extern "C" int lbbsp_cmd_run(const char* config, const char* out_dir, int has_se
     const lbbsp_metrics exported = compute_metrics(v, r.converged, c.warmup_iterations, true);
     write_metrics_json(exported, c.convergence_loss, c.convergence_consecutive,
                        c.warmup_iterations, (fs::path(out_dir) / "metrics.json").string());
-  });
-}
-
-extern "C" int lbbsp_cmd_compare(const char* const* configs, int n_configs, const char* out_dir,
-                                 int has_seed, uint64_t seed) {
-  return cli("lbbsp compare: ", [&] {
-    fs::create_directories(out_dir);
-    const std::string path = (fs::path(out_dir) / "comparison.csv").string();
-    std::ofstream out(path, std::ios::binary);
-    if (!out) fail(LBBSP_RUNTIME, "cannot open " + path);
-    out << "scenario,metric,value\n";
-    for (int i = 0; i < n_configs; ++i) {
-      Scenario c = load_scenario(configs[i]);
-      if (has_seed) c.seed = seed;
-      const SimRun r = run_scenario(c);
-      std::string row;
-      auto emit = [&](const char* metric, double value) {
-        row.clear();
-        row += c.name;
-        row += ',';
-        row += metric;
-        row += ',';
-        format_real(row, value);
-        row += '\n';
-        out << row;
-      };
-      emit("updates_to_convergence", static_cast<double>(r.metrics.updates_to_convergence));
-      emit("mean_per_update_time", r.metrics.mean_per_update_time);
-      emit("wastage", r.metrics.wastage);
-      emit("predictor_rmse", r.metrics.predictor_rmse);
-      emit("converged", r.metrics.converged ? 1.0 : 0.0);
-    }
-  });
-}
-
-extern "C" int lbbsp_cmd_predict_bench(const char* config, const char* out_dir, int has_seed,
-                                       uint64_t seed) {
-  return cli("lbbsp predict-bench: ", [&] {
-    Scenario c = load_scenario(config);
-    if (has_seed) c.seed = seed;
-    fs::create_directories(out_dir);
-    const Bench& bc = c.benchmark;
-    if (bc.iterations < 1 || bc.regime_length < 1)
-      fail(LBBSP_INVALID_ARGUMENT, "benchmark series: need iterations, regime >= 1");
-    std::vector<double> cpu(bc.iterations), mem(bc.iterations), mult(bc.iterations);
-    check(lbbsp_benchmark_series(c.seed, bc.iterations, bc.regime_length, bc.high_lo, bc.high_hi,
-                                 bc.low_lo, bc.low_hi, bc.spike_mult, bc.spike_prob, cpu.data(),
-                                 mem.data(), mult.data()));
-    lbbsp_predictor_cfg base{};
-    base.alpha = c.alpha;
-    base.warmup_iterations = c.warmup_iterations;
-    base.speed_floor = c.speed_floor;
-    base.train = default_train_cfg(c.warmup_iterations);
-    // paired runs always use the benchmark dynamics on a CPU cluster
-    Scenario paired_base = c;
-    paired_base.preset = "benchmark";
-    paired_base.trace_path.clear();
-    paired_base.gpu_profiles.clear();
-    paired_base.bandwidth_drop.reset();
-    double bsp_per_update = 0.0;
-    if (c.paired_sim) {
-      Scenario bsp = paired_base;
-      bsp.scheme = LBBSP_SCHEME_BSP;
-      bsp_per_update = run_scenario(bsp).metrics.mean_per_update_time;
-    }
-    const std::string path = (fs::path(out_dir) / "predict_bench.csv").string();
-    std::ofstream out(path, std::ios::binary);
-    if (!out) fail(LBBSP_RUNTIME, "cannot open " + path);
-    out << "predictor,rmse,normalized_per_update_time\n";
-    for (const int kind : {LBBSP_PRED_MEMORYLESS, LBBSP_PRED_EMA, LBBSP_PRED_NARX}) {
-      double rmse = 0.0;
-      check(lbbsp_predictor_series_rmse(kind, &base, cpu.data(), mem.data(), mult.data(),
-                                        bc.iterations, c.base_speed, mix_seed(c.seed, 0xbe11c4ull),
-                                        c.warmup_iterations, &rmse));
-      std::string row(predictor_name(kind));
-      row += ',';
-      format_real(row, rmse);
-      row += ',';
-      if (c.paired_sim) {
-        Scenario paired = paired_base;
-        paired.scheme = LBBSP_SCHEME_LBBSP;
-        paired.predictor = kind;
-        const double per_update = run_scenario(paired).metrics.mean_per_update_time;
-        format_real(row, per_update / bsp_per_update);
-      }
-      row += '\n';
-      out << row;
-    }
   });
 }

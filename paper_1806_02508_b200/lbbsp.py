@@ -705,17 +705,3 @@ def cmd_run(config, out_dir, seed_override: Optional[int] = None) -> int:
     """cmd_run (scenario.cpp:369-386); returns the CLI exit status."""
     h, s = _seed_args(seed_override)
     return lib().lbbsp_cmd_run(str(config).encode(), str(out_dir).encode(), h, C.c_uint64(s))
-
-
-def cmd_compare(configs, out_dir, seed_override: Optional[int] = None) -> int:
-    """cmd_compare (scenario.cpp:388-423)."""
-    h, s = _seed_args(seed_override)
-    arr = (C.c_char_p * max(len(configs), 1))(*[str(c).encode() for c in configs])
-    return lib().lbbsp_cmd_compare(arr, len(configs), str(out_dir).encode(), h, C.c_uint64(s))
-
-
-def cmd_predict_bench(config, out_dir, seed_override: Optional[int] = None) -> int:
-    """cmd_predict_bench (scenario.cpp:425-481)."""
-    h, s = _seed_args(seed_override)
-    return lib().lbbsp_cmd_predict_bench(str(config).encode(), str(out_dir).encode(), h,
-                                         C.c_uint64(s))

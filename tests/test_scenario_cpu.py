@@ -158,7 +158,8 @@ def test_exported_files_byte_identical(sg, orc, tmp_path, name):
 
 
 def test_compare_rows_match_reference(sg, orc, tmp_path):
-    """cmd_compare's rows come from the unrounded Simulation::run metrics."""
+    """The reference's comparison.csv rows (cmd_compare, scenario.cpp:388-423)
+    are the unrounded Simulation::run metrics, which compute_metrics gives."""
     rows = ["scenario,metric,value"]
     for name in sg["compare"]["configs"]:
         s = L.load_scenario(write_config(str(tmp_path), name, sg["configs"][name]))

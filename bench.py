@@ -590,15 +590,16 @@ def main():
 
     def timed(eng, steps, warmup, phases=False):
         """per-round device times (ms, max over ranks per round): every round
-        bracketed by CUDA events on the engine stream, the L2 flushed between
-        rounds outside the events"""
+        bracketed by CUDA events on the engine stream with the L2 flushed
+        between rounds outside the events; all rounds are enqueued before the
+        host waits (no host sync between rounds: the next round's launch is
+        queued behind the flush, as in a training loop)"""
         st = torch.cuda.ExternalStream(eng.stream)
         eng.run(warmup)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         ev = []
-        ph = None
         for _ in range(steps):
             with torch.cuda.stream(st):
                 flush.zero_()
@@ -609,16 +610,13 @@ def main():
             with torch.cuda.stream(st):
                 e.record(st)
             ev.append((s, e))
-            if phases:
-                e.synchronize()
-                p = eng.phase_times()
-                ph = p if ph is None else ph + p
         torch.cuda.synchronize()
         ms = torch.tensor([s.elapsed_time(e) for s, e in ev], dtype=torch.float64, device="cuda")
+        ph = eng.phase_times() if phases else None  # the last timed round
         if world > 1:
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
             dist.barrier()
-        return ms.cpu().numpy(), (ph / steps if ph is not None else None)
+        return ms.cpu().numpy(), ph
 
     # ---- main arm: LB-BSP + NARX under the recorded trace, the driver's K steps ----
     eng = make("lb-bsp", trace)
@@ -671,6 +669,7 @@ def main():
     # availabilities: the capacity-aware ideal a proportional allocator can
     # reach) and the no-straggler ideal (every worker at a = 1) ----
     win = {}
+    phases_unloaded = None
     for name, scheme, tr, pred, solver in (
             ("lbbsp", "lb-bsp", trace, "narx", "proportional"),
             ("lbbsp_gamma", "lb-bsp", trace, "narx", "gamma"),
@@ -679,7 +678,9 @@ def main():
             ("perfect_gamma", "lb-bsp", trace, "perfect", "gamma"),
             ("no_straggler", "lb-bsp", constant_trace(n_total, iters), "narx", "proportional")):
         eng = make(scheme, tr, pred, solver)
-        ms_w, _ = timed(eng, window, warm)
+        ms_w, ph_w = timed(eng, window, warm, phases=(name == "no_straggler"))
+        if ph_w is not None:
+            phases_unloaded = ph_w
         win[name] = percentiles(ms_w)
         r = eng.records()
         win[name]["min_batch_in_window"] = int(r["sizes"][warm:warm + window].min())
@@ -701,15 +702,18 @@ def main():
         pass
     peak_tf = peaks.get("bf16_tflops", 1590.0)
     peak_src = "measured (burst)" if "bf16_tflops" in peaks else "fallback"
-    # per-worker phase list: [fwd L0, head, dW L0] for 784-256-10; the phase
-    # time is the worker-phase window (min start .. max end over workers) and
-    # includes the injected interference of the slow workers
-    fwd_flops = 2.0 * BATCH_PER_GPU * DIMS[0] * DIMS[1]
-    ph_fwd = float(phases[0]) if phases is not None and len(phases) else 0.0
-    achieved = fwd_flops / ph_fwd / 1e12 if ph_fwd > 0 else 0.0
+    # the dominant kernel: the fused worker kernel (csrc/c2_fused.cuh), one
+    # launch = every worker's forward + head + dW0 over the GPU's 4096 rows,
+    # 818,176 flop per sample; its duration = the worker-phase
+    # window (first CTA start .. last CTA end, %globaltimer) of the
+    # no-straggler arm's last timed round (the straggler arms' windows hold
+    # the injected interference by design)
+    kern_flops = 818176.0 * BATCH_PER_GPU
+    ph_k = float(phases_unloaded[0]) if phases_unloaded is not None and len(phases_unloaded) else 0.0
+    achieved = kern_flops / ph_k / 1e12 if ph_k > 0 else 0.0
     traffic = None
     try:
-        cap = json.load(open(os.path.join(REPO, "profiles", "r01_c2_fwd_gemm_ncu.json")))
+        cap = json.load(open(os.path.join(REPO, "profiles", "r02_c2_fused_ncu.json")))
         traffic = int(cap["dram_bytes_read"]) + int(cap["dram_bytes_write"])
     except Exception:
         pass
@@ -747,15 +751,16 @@ def main():
             "lbbsp_gamma_over_ideal_time": win["lbbsp_gamma"]["mean"] / win["perfect_gamma"]["mean"],
             "gamma_profiles_s": [[round(m0, 12), round(b0, 9)] for m0, b0, _, _ in prof],
             "phase_ms": [round(float(x) * 1e3, 4) for x in (phases if phases is not None else [])],
-            "roofline": {"bound": "tensor", "kernel": "fwd GEMM 4096x256x784 (tcgen05, per-worker "
-                                                      "partitions)",
+            "roofline": {"bound": "tensor",
+                         "kernel": "c2_fused_worker_kernel: 8 workers' forward (tcgen05) + head + dW0 "
+                                   "(tcgen05), one launch per round",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf if peak_tf else None,
-                         "peak_source": peak_src, "traffic": traffic,
-                         "traffic_source": "profiles/r01_c2_fwd_gemm_ncu.json (dram__bytes_read.sum "
-                                           "+ dram__bytes_write.sum, one launch)",
-                         "note": "C2 GEMMs are latency-bound (SURVEY 8(d)); the forward phase "
-                                 "window includes the slow workers' injected interference"},
+                         "peak_source": peak_src, "duration_us": ph_k * 1e6,
+                         "flop_per_launch": kern_flops, "traffic": traffic,
+                         "traffic_source": "profiles/r02_c2_fused_ncu.json (dram__bytes_read.sum + "
+                                           "dram__bytes_write.sum, one launch)",
+                         "note": "C2 is latency-bound (SURVEY 8(d)): ~512 rows per worker"},
             "gpu_launches": launches * args.steps,
             "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

@@ -635,10 +635,10 @@ int lbbsp_mlp_dataset(lbbsp_mlp* m, void* h_x_bf16, int* h_labels);
 int lbbsp_mlp_launches_per_iteration(lbbsp_mlp* m, int* launches);
 /* End-to-end plumbing (async, pinned host buffers): replace the resident
  * dataset with host rows ([dataset_size][dims[0]] bf16 + labels) before the
- * next round -- the host->device copy runs on a copy stream into a staging
- * buffer, overlapping the round in flight, and the next round starts with a
- * device-to-device refresh -- and read back the newest round's record
- * (sizes [n_total] ints, then loss) after it. */
+ * next round -- the dataset is double-buffered: the host->device copy runs on
+ * a copy stream into the buffer the round in flight does not read, and the
+ * next round reads it -- and read back the newest round's record (sizes
+ * [n_total] ints, then loss) after it. */
 int lbbsp_mlp_load_data_async(lbbsp_mlp* m, const void* h_x_bf16, const int* h_labels);
 int lbbsp_mlp_read_result_async(lbbsp_mlp* m, int* h_sizes, double* h_loss);
 /* load_data_async + one round + read_result_async in one call (the e2e step). */

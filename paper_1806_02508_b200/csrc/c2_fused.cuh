@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(kFzThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[0]);
       named_sync_epi();  // the whole H tile is in smem
+      if (dbg && threadIdx.x == 0 && it == 0) dbg[6] = globaltimer();
       // ---- head on tile `warp` (rows m0 + 16 warp ..): head_mma.cuh, one iteration ----
       const uint32_t hb = smem_addr(smem + tile * 8192);
       uint8_t* hp = smem + tile * 8192;
@@ -479,6 +480,7 @@ __global__ void __launch_bounds__(kFzThreads, 1)
       // the producer may refill the stage region once every warp is done with it
       fence_proxy_async_smem();
       named_sync_epi();
+      if (dbg && threadIdx.x == 0 && it == 0) dbg[7] = globaltimer();
       if (threadIdx.x == 0) mbar_arrive(hdone);
     }
     if (my_mt > 0) {

@@ -1259,17 +1259,24 @@ struct lbbsp_mlp {
   cudaEvent_t ev_gather0 = nullptr, ev_gather1 = nullptr;
   cudaEvent_t ev_head0 = nullptr, ev_head1 = nullptr;  // head partial combine beside the backward
   cudaStream_t copy_stream = nullptr;  // e2e input staging (lbbsp_mlp_load_data_async)
-  cudaEvent_t ev_staged = nullptr, ev_refreshed = nullptr;
-  bf16* stage_x = nullptr;
-  int* stage_y = nullptr;
+  cudaEvent_t ev_staged = nullptr;
+  // the resident dataset is double-buffered: a round reads buffer `cur`
+  // while the next round's inputs are copied into the other one; one graph
+  // per buffer (the loss branch's tensor map is bound to the buffer)
+  bf16* data_xb[2] = {nullptr, nullptr};
+  int* data_yb[2] = {nullptr, nullptr};
+  int cur = 0;      // buffer the next round reads
+  int cap_buf = 0;  // buffer the graph being captured reads
+  cudaEvent_t ev_used[2] = {nullptr, nullptr};  // last round that read buffer b
   cudaEvent_t ev_layer[LBBSP_MLP_MAX_LAYERS] = {};
   cudaEvent_t ev_dx[LBBSP_MLP_MAX_LAYERS] = {};  // dX_l done: the bucketed apply of W_l may run
   cudaStream_t comm_stream = nullptr;
   // copy-engine bucket exchange (one worker per GPU with peers, LBBSP_NCCL_BUCKETS unset)
   cudaStream_t xfer_stream = nullptr;
   cudaEvent_t ev_xfer = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t execb[2] = {nullptr, nullptr};
+  cudaGraph_t graphb[2] = {nullptr, nullptr};
+  GemmPlan fwd_d0_alt;  // the dataset-loss forward of layer 0 over buffer 1
   ncclComm_t comm = nullptr;
   // NVLink peer exchange (lbbsp_mlp_init_peers): replaces the NCCL calls of
   // the several-workers-per-GPU path when set
@@ -1329,15 +1336,17 @@ struct lbbsp_mlp {
     for (void* p : peer_map)
       if (p && p != peer_buf) cudaIpcCloseMemHandle(p);
     if (peer_buf) cudaFree(peer_buf);
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
+    for (int b = 0; b < 2; ++b) {
+      if (execb[b]) cudaGraphExecDestroy(execb[b]);
+      if (graphb[b]) cudaGraphDestroy(graphb[b]);
+      if (ev_used[b]) cudaEventDestroy(ev_used[b]);
+    }
     if (comm && nccl_api()) nccl_api()->CommDestroy(comm);
     if (stream) cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_gather0) cudaEventDestroy(ev_gather0);
     if (ev_staged) cudaEventDestroy(ev_staged);
-    if (ev_refreshed) cudaEventDestroy(ev_refreshed);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ev_gather1) cudaEventDestroy(ev_gather1);
     if (ev_head0) cudaEventDestroy(ev_head0);
@@ -1410,6 +1419,8 @@ int launch_grouped(lbbsp_mlp* m, GemmPlan& p, int mode, unsigned long long* timi
 }  // namespace
 
 int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
+  const bf16* data_x = data_xb[cap_buf];
+  const int* data_y = data_yb[cap_buf];
   const Groups G = groups();
   int nl = 0, ph = 0;
   const int sms = D.sm_budget;
@@ -1699,9 +1710,10 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   // ---- full-dataset loss (step_sync P9, cluster_sim.cpp:445) ----
   if (D.loss_on) {
     for (int l = 0; l < Lg; ++l) {
-      fwd_d[l].ctas = std::min(fwd_d[l].ctas, sms) & ~1;
-      fwd_d[l].pdl = use_pdl;
-      int rc = gemm_launch(fwd_d[l], s);
+      GemmPlan& fp = (l == 0 && cap_buf == 1) ? fwd_d0_alt : fwd_d[l];
+      fp.ctas = std::min(fp.ctas, sms) & ~1;
+      fp.pdl = use_pdl;
+      int rc = gemm_launch(fp, s);
       if (rc) return rc;
       ++nl;
     }
@@ -1828,6 +1840,10 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   }
   LBBSP_CUDA_CHECK(m.alloc(&m.data_x, static_cast<size_t>(m.N_data) * d0));
   LBBSP_CUDA_CHECK(m.alloc(&m.data_y, m.N_data));
+  m.data_xb[0] = m.data_x;
+  m.data_yb[0] = m.data_y;
+  LBBSP_CUDA_CHECK(m.alloc(&m.data_xb[1], static_cast<size_t>(m.N_data) * d0));
+  LBBSP_CUDA_CHECK(m.alloc(&m.data_yb[1], m.N_data));
   LBBSP_CUDA_CHECK(m.alloc(&m.X, static_cast<size_t>(m.B_cap) * d0));
   LBBSP_CUDA_CHECK(m.alloc(&m.y, m.B_cap));
   LBBSP_CUDA_CHECK(m.alloc(&m.row_scale, m.B_cap));
@@ -1956,9 +1972,7 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   // end-to-end plumbing (lbbsp_mlp_load_data_async / read_result_async)
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.copy_stream, cudaStreamNonBlocking));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_staged, cudaEventDisableTiming));
-  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_refreshed, cudaEventDisableTiming));
-  LBBSP_CUDA_CHECK(m.alloc(&m.stage_x, static_cast<size_t>(m.N_data) * c.dims[0]));
-  LBBSP_CUDA_CHECK(m.alloc(&m.stage_y, static_cast<size_t>(m.N_data)));
+  for (auto& e : m.ev_used) LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(m.alloc(&m.result, static_cast<size_t>(m.n_total) + 2));
   LBBSP_CUDA_CHECK(m.alloc(&m.arrive, 1));
   {
@@ -2064,6 +2078,12 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     m.fwd_d[l].args.c_bf16 = last ? m.logits_d : m.Hd[l];
     m.fwd_d[l].args.ldc = dout;
     m.fwd_d[l].args.bias = m.params + m.off_b[l];
+    if (l == 0) {  // the same plan over the second dataset buffer
+      rc = gemm_plan(&m.fwd_d0_alt, m.data_xb[1], m.pb + m.off_w[l], m.N_data, dout, din, false, false,
+                     pr ? 256 : bn_d, epi, pr);
+      if (rc) return rc;
+      m.fwd_d0_alt.args = m.fwd_d[l].args;
+    }
     // dW_l = dZ_l^T A_l : M=dout, N=din, K=rows ; A = dZ_l [rows][dout] MN-major, B = A_l [rows][din] MN-major
     const int bn_w = env_bn("LBBSP_BN_DW", pick_bn(static_cast<double>(dout), din));
     const int bn_x = env_bn("LBBSP_BN_DX", pick_bn(rows_per_worker, din));
@@ -2163,7 +2183,8 @@ extern "C" int lbbsp_mlp_peer_handle(lbbsp_mlp* m, unsigned char h_handle[64]) {
 extern "C" int lbbsp_mlp_init_peers(lbbsp_mlp* m, const unsigned char* h_handles) {
   const int W = m->cfg.world, R = m->cfg.rank;
   if (!m->peer_buf) return set_error(LBBSP_LOGIC, "mlp: lbbsp_mlp_peer_handle first");
-  if (m->exec) return set_error(LBBSP_LOGIC, "mlp: peers must be set up before the first round");
+  if (m->execb[0] || m->execb[1])
+    return set_error(LBBSP_LOGIC, "mlp: peers must be set up before the first round");
   PeerDev& X = m->px;
   X.world = W;
   X.rank = R;
@@ -2213,16 +2234,21 @@ extern "C" int lbbsp_mlp_run(lbbsp_mlp* m, int iterations) {
   const bool peer_only = m->peers && (m->n_local > 1 || m->ce_ok);
   if (m->cfg.world > 1 && !m->comm && !peer_only)
     return set_error(LBBSP_NCCL, "mlp: world > 1 needs lbbsp_mlp_init_comm (or peers) first");
-  if (!m->exec) {
-    LBBSP_CUDA_CHECK(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
-    int rc = m->enqueue_iteration(m->stream);
-    cudaError_t e2 = cudaStreamEndCapture(m->stream, &m->graph);
-    if (rc) return rc;
-    LBBSP_CUDA_CHECK(e2);
-    // honour the side (observe / NARX) stream's higher priority inside the graph
-    LBBSP_CUDA_CHECK(cudaGraphInstantiate(&m->exec, m->graph, cudaGraphInstantiateFlagUseNodePriority));
+  for (int i = 0; i < iterations; ++i) {
+    const int b = m->cur;
+    if (!m->execb[b]) {
+      m->cap_buf = b;
+      LBBSP_CUDA_CHECK(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
+      int rc = m->enqueue_iteration(m->stream);
+      cudaError_t e2 = cudaStreamEndCapture(m->stream, &m->graphb[b]);
+      if (rc) return rc;
+      LBBSP_CUDA_CHECK(e2);
+      // honour the side (observe / NARX) stream's higher priority inside the graph
+      LBBSP_CUDA_CHECK(cudaGraphInstantiate(&m->execb[b], m->graphb[b], cudaGraphInstantiateFlagUseNodePriority));
+    }
+    LBBSP_CUDA_CHECK(cudaGraphLaunch(m->execb[b], m->stream));
+    LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_used[b], m->stream));
   }
-  for (int i = 0; i < iterations; ++i) LBBSP_CUDA_CHECK(cudaGraphLaunch(m->exec, m->stream));
   return LBBSP_OK;
 }
 
@@ -2284,8 +2310,10 @@ extern "C" int lbbsp_mlp_set_params(lbbsp_mlp* m, const float* h_params) {
 extern "C" int lbbsp_mlp_dataset(lbbsp_mlp* m, void* h_x_bf16, int* h_labels) {
   LBBSP_CUDA_CHECK(cudaDeviceSynchronize());
   if (h_x_bf16)
-    LBBSP_CUDA_CHECK(cudaMemcpy(h_x_bf16, m->data_x, sizeof(bf16) * m->N_data * m->dims[0], cudaMemcpyDeviceToHost));
-  if (h_labels) LBBSP_CUDA_CHECK(cudaMemcpy(h_labels, m->data_y, sizeof(int) * m->N_data, cudaMemcpyDeviceToHost));
+    LBBSP_CUDA_CHECK(cudaMemcpy(h_x_bf16, m->data_xb[m->cur], sizeof(bf16) * m->N_data * m->dims[0],
+                                cudaMemcpyDeviceToHost));
+  if (h_labels)
+    LBBSP_CUDA_CHECK(cudaMemcpy(h_labels, m->data_yb[m->cur], sizeof(int) * m->N_data, cudaMemcpyDeviceToHost));
   return LBBSP_OK;
 }
 
@@ -2294,34 +2322,20 @@ extern "C" int lbbsp_mlp_launches_per_iteration(lbbsp_mlp* m, int* launches) {
   return LBBSP_OK;
 }
 
-namespace {
-__global__ void refresh_kernel(const uint4* __restrict__ sx, uint4* __restrict__ dx, size_t nx,
-                               const int* __restrict__ sy, int* __restrict__ dy, int ny) {
-  for (size_t i = blockIdx.x * 256ull + threadIdx.x; i < nx; i += 256ull * gridDim.x) dx[i] = sx[i];
-  for (int i = blockIdx.x * 256 + threadIdx.x; i < ny; i += 256 * gridDim.x) dy[i] = sy[i];
-}
-
-}  // namespace
-
-// The host->device copy runs on a copy stream into a staging buffer, so it
-// overlaps the round still executing; the next round then starts with a
-// device-to-device refresh of the resident dataset (stream-ordered after the
-// previous round, which read it).
+// The next round's inputs go into the dataset buffer the round in flight
+// does not read: the host->device copy runs on the copy stream (overlapping
+// that round) once the last round that read the buffer is done, and the
+// next round -- the graph bound to that buffer -- waits for the copy. No
+// device-side copy sits on the round's critical path.
 extern "C" int lbbsp_mlp_load_data_async(lbbsp_mlp* m, const void* h_x_bf16, const int* h_labels) {
   const size_t bx = sizeof(bf16) * m->N_data * m->dims[0], by = sizeof(int) * m->N_data;
-  // staging buffers, copy stream and events are created with the engine (an
-  // allocation here would synchronise the device inside the caller's loop)
-  // staging is free once the previous refresh consumed it
-  LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->copy_stream, m->ev_refreshed, 0));
-  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_x, h_x_bf16, bx, cudaMemcpyHostToDevice, m->copy_stream));
-  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_y, h_labels, by, cudaMemcpyHostToDevice, m->copy_stream));
+  const int b = 1 - m->cur;
+  LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->copy_stream, m->ev_used[b], 0));
+  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_xb[b], h_x_bf16, bx, cudaMemcpyHostToDevice, m->copy_stream));
+  LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_yb[b], h_labels, by, cudaMemcpyHostToDevice, m->copy_stream));
   LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_staged, m->copy_stream));
   LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->stream, m->ev_staged, 0));
-  refresh_kernel<<<num_sms(), 256, 0, m->stream>>>(reinterpret_cast<const uint4*>(m->stage_x),
-                                                  reinterpret_cast<uint4*>(m->data_x), bx / 16,
-                                                  m->stage_y, m->data_y, m->N_data);
-  LBBSP_CUDA_CHECK(cudaGetLastError());
-  LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_refreshed, m->stream));
+  m->cur = b;
   return LBBSP_OK;
 }
 
@@ -2426,10 +2440,13 @@ extern "C" int lbbsp_mlp_step_e2e(lbbsp_mlp* m, const void* h_x_bf16, const int*
                                   double* h_loss) {
   if (h_x_bf16 != m->warm_x || h_labels != m->warm_y) {
     const size_t bx = sizeof(bf16) * m->N_data * m->dims[0], by = sizeof(int) * m->N_data;
+    // first-touch the new host buffers (into the idle dataset buffer; the
+    // step below overwrites it again)
+    LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->stream));
     LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->copy_stream));
     for (int i = 0; i < 2; ++i) {
-      LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_x, h_x_bf16, bx, cudaMemcpyHostToDevice, m->copy_stream));
-      LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->stage_y, h_labels, by, cudaMemcpyHostToDevice, m->copy_stream));
+      LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_xb[1 - m->cur], h_x_bf16, bx, cudaMemcpyHostToDevice, m->copy_stream));
+      LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_yb[1 - m->cur], h_labels, by, cudaMemcpyHostToDevice, m->copy_stream));
     }
     LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->copy_stream));
     m->warm_x = h_x_bf16;

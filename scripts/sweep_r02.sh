@@ -13,7 +13,7 @@ export LBBSP_BENCH_NO_C3=1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 1500 -c 300 --csv \
   --log-file $O/c2_launches.csv python bench.py --steps 20 --warmup 5 --no-cpu-baseline > $O/ncu_list.log 2>&1; st ncu_list $?
 unset LBBSP_BENCH_NO_C3
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:c2_fused --launch-skip 40 -c 1 \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:c2_fused --launch-skip 3 -c 1 \
   -o $O/c2_fused python scripts/sanitize_c2.py > $O/ncu_fused.log 2>&1; st ncu_fused $?
 ROUNDS=3 timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemm_bf16_tc2 --launch-skip 8 -c 11 \
   -o $O/c3_gemms python scripts/c3_one_gpu.py > $O/ncu_c3.log 2>&1; st ncu_c3 $?

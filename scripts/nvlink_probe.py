@@ -40,6 +40,9 @@ TX, RX = 138, 139  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX (KiB)
 
 def counters():
     vals = nv.nvmlDeviceGetFieldValues(h, [TX, RX])
+    if rank == 0 and not getattr(counters, "said", False):
+        print("nvml field returns", [int(v.nvmlReturn) for v in vals], flush=True)
+        counters.said = True
     return [int(v.value.ullVal) for v in vals]
 
 

@@ -34,6 +34,7 @@
 #include "predictor.cuh"
 #include "solver.cuh"
 #include "c2_fused.cuh"
+#include "c2_fused_pair.cuh"
 
 namespace lbbsp {
 
@@ -205,6 +206,7 @@ struct PlanDev {
   const lbbsp_gpu_profile* prof0;  // [n_total] unloaded Gamma profiles (GAMMA solver)
   float2* intf_w;              // [n_local] {availability, HBM share of the injected time}
   unsigned* fz_done;           // [n_local] fused worker kernel: head CTAs done (zeroed here)
+  int pair_caps;               // worker CTA partitions cluster-aligned (even) for the pair kernel
   int gather_ctas;             // > 0: the plan completes only once they all have
 };
 
@@ -355,6 +357,7 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
       const double av = D.straggler_mode == LBBSP_STRAGGLE_SM_CAP ? avail[w] : 1.0;
       int cap = static_cast<int>(floor(static_cast<double>(D.sm_budget) * share * av));
       cap = cap < 1 ? 1 : cap;
+      if (D.pair_caps) cap = cap < 2 ? 2 : (cap & ~1);  // (2,1,1) clusters
       if (c0 + cap > D.sm_budget) cap = D.sm_budget - c0 > 0 ? D.sm_budget - c0 : 1;
       D.cta0[i] = c0;
       D.ctan[i] = cap;
@@ -1320,7 +1323,8 @@ struct lbbsp_mlp {
   Interference intf{};  // straggler injection state (interference mode)
   // fused worker kernel (784-256-10): forward + head + dW0 in one launch
   bool fused = false;
-  CUtensorMap fz_tm[4];
+  bool fused_pair = false;  // the (2,1,1)-cluster variant (c2_fused_pair.cuh)
+  CUtensorMap fz_tm[5];
   unsigned* fz_comb = nullptr;
   unsigned long long* fz_dbg = nullptr;  // LBBSP_FZ_DEBUG: per-CTA stage stamps
   // e2e plumbing: cached host-buffer lookups (lbbsp_mlp_read_result_async,
@@ -1480,8 +1484,12 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     fa.timing = phase_slot(ph++);
     fa.status = D.status;
     fa.dbg = fz_dbg;
-    LBBSP_CUDA_CHECK(launch_maybe_pdl(c2_fused_worker_kernel, sms, kFzThreads, kFzSmem, s, use_pdl, fz_tm[0],
-                                      fz_tm[1], fz_tm[2], fz_tm[3], fa));
+    if (fused_pair)
+      LBBSP_CUDA_CHECK(launch_maybe_pdl(c2_pair_worker_kernel, sms & ~1, kFpThreads, kFpSmem, s, use_pdl,
+                                        fz_tm[0], fz_tm[4], fz_tm[2], fz_tm[3], fa));
+    else
+      LBBSP_CUDA_CHECK(launch_maybe_pdl(c2_fused_worker_kernel, sms, kFzThreads, kFzSmem, s, use_pdl, fz_tm[0],
+                                        fz_tm[1], fz_tm[2], fz_tm[3], fa));
     ++nl;
   } else {
   for (int l = 0; l < Lg; ++l) {
@@ -2116,14 +2124,20 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     if (!rc) rc = make_tmap_bf16(&m.fz_tm[1], m.pb + m.off_w[0], kFzD0, kHeadDH, kFzD0, 256);
     if (!rc) rc = make_tmap_bf16(&m.fz_tm[2], m.dZ[0], kHeadDH, m.B_cap, kHeadDH, 64);
     if (!rc) rc = make_tmap_bf16(&m.fz_tm[3], m.X, kFzD0, m.B_cap, kFzD0, 64);
+    if (!rc) rc = make_tmap_bf16(&m.fz_tm[4], m.pb + m.off_w[0], kFzD0, kHeadDH, kFzD0, 128);
     if (rc) return rc;
+    // the column-split pair kernel by default (LBBSP_FUSE_SINGLE=1: one CTA per tile)
+    m.fused_pair = !getenv("LBBSP_FUSE_SINGLE");
+    D.pair_caps = m.fused_pair ? 1 : 0;
     unsigned* fd = nullptr;
     LBBSP_CUDA_CHECK(m.alloc(&fd, static_cast<size_t>(m.n_local)));
     D.fz_done = fd;
     LBBSP_CUDA_CHECK(m.alloc(&m.fz_comb, static_cast<size_t>(m.n_local)));
-    if (getenv("LBBSP_FZ_DEBUG")) LBBSP_CUDA_CHECK(m.alloc(&m.fz_dbg, static_cast<size_t>(num_sms()) * 8));
+    if (getenv("LBBSP_FZ_DEBUG")) LBBSP_CUDA_CHECK(m.alloc(&m.fz_dbg, static_cast<size_t>(num_sms()) * 16));
     LBBSP_CUDA_CHECK(cudaFuncSetAttribute(c2_fused_worker_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(kFzSmem)));
+    LBBSP_CUDA_CHECK(cudaFuncSetAttribute(c2_pair_worker_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kFpSmem)));
   }
   m.reduce_bytes = (m.n_local + 1.0) * P * 4.0 + P * 4.0 + P * 2.0;
   LBBSP_CUDA_CHECK(cudaDeviceSynchronize());
@@ -2474,12 +2488,12 @@ extern "C" int lbbsp_mlp_step_e2e(lbbsp_mlp* m, const void* h_x_bf16, const int*
   return lbbsp_mlp_read_result_async(m, h_sizes, h_loss);
 }
 
-// Debug: per-CTA stage stamps of the last fused worker launch ([grid][8]
+// Debug: per-CTA stage stamps of the last fused worker launch ([grid][16]
 // globaltimer ns; LBBSP_FZ_DEBUG=1 at create). Not part of the stable C-ABI.
 extern "C" int lbbsp_mlp_fused_debug(lbbsp_mlp* m, unsigned long long* out, int* ctas) {
   LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->stream));
   *ctas = m->fz_dbg ? num_sms() : 0;
   if (m->fz_dbg)
-    LBBSP_CUDA_CHECK(cudaMemcpy(out, m->fz_dbg, sizeof(unsigned long long) * 8 * num_sms(), cudaMemcpyDeviceToHost));
+    LBBSP_CUDA_CHECK(cudaMemcpy(out, m->fz_dbg, sizeof(unsigned long long) * 16 * num_sms(), cudaMemcpyDeviceToHost));
   return LBBSP_OK;
 }

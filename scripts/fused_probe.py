@@ -6,10 +6,12 @@ import numpy as np
 import torch
 from paper_1806_02508_b200.mlp import MlpEngine, constant_trace
 
-for fuse in (True, False):
-    if fuse:
-        os.environ.pop("LBBSP_NO_FUSE", None)
-    else:
+for fuse in ("pair",):
+    os.environ.pop("LBBSP_NO_FUSE", None)
+    os.environ.pop("LBBSP_FUSE_SINGLE", None)
+    if fuse == "single":
+        os.environ["LBBSP_FUSE_SINGLE"] = "1"
+    elif not fuse:
         os.environ["LBBSP_NO_FUSE"] = "1"
     for static in ([512] * 8, None):
         eng = MlpEngine(dims=[784, 256, 10], global_batch=4096, n_workers_local=8, predictor="ema",
@@ -34,17 +36,18 @@ for fuse in (True, False):
 import ctypes as C
 from paper_1806_02508_b200.mlp import _L
 os.environ.pop("LBBSP_NO_FUSE", None)
+os.environ.pop("LBBSP_FUSE_SINGLE", None)
 os.environ["LBBSP_FZ_DEBUG"] = "1"
 eng = MlpEngine(dims=[784, 256, 10], global_batch=4096, n_workers_local=8, predictor="ema",
                 max_iterations=40, trace=constant_trace(8, 40), static_sizes=[512] * 8)
 eng.run(30)
-buf = np.zeros(148 * 8, np.uint64)
+buf = np.zeros(148 * 16, np.uint64)
 n = C.c_int()
 f = _L().lbbsp_mlp_fused_debug
 f.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]
 f(eng._h, buf.ctypes.data_as(C.c_void_p), C.byref(n))
-t = buf.reshape(148, 8).astype(np.int64)
+t = buf.reshape(148, 16).astype(np.int64)
 base = t[t[:, 0] > 0, 0].min()
 for c in range(0, 40):
     r = t[c]
-    print(c, [(int(x - base) if x > 0 else -1) for x in r[:8]])
+    print(c, [(int(x - base) if x > 0 else -1) for x in r[:11]])

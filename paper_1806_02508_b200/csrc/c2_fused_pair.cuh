@@ -22,7 +22,8 @@ namespace lbbsp {
 namespace mlp {
 
 constexpr int kFpThreads = 320;
-constexpr int kFpStages = 4;
+constexpr int kFpStages = 4;                       // phase W ring (stage region)
+constexpr int kFpStagesF = 6;                      // phase F ring: + 2 stages in the (idle) W staging region
 constexpr int kFpStage = 32 * 1024;                // A 128x64 + B 128x64 bf16
 constexpr int kFpPartVals = 2048 + 128 + 128;      // dW1 frag | db1 frag | db0 (own 128 cols)
 // dynamic smem layout (after 1024 alignment)
@@ -32,8 +33,11 @@ constexpr int kFpOffDl = kFpOffWd + 4096;          // dl tiles [8][16][16] bf16 
 constexpr int kFpOffB0 = kFpOffDl + 4096;          // b0 (own 128 cols) fp32          512 B
 constexpr int kFpOffXl = kFpOffB0 + 512;           // peer partial logits [2][8][32][8] f32  16 KB
 constexpr int kFpOffFlag = kFpOffXl + 16384;       // [8] peer arrival sequence numbers
-constexpr int kFpOffBar = kFpOffFlag + 64;         // mbarriers + slots
+constexpr int kFpOffEpi = (kFpOffFlag + 64 + 1023) / 1024 * 1024;  // phase-W tile staging [4][128][32] f32 SW128, 64 KB
+constexpr int kFpOffBar = kFpOffEpi + 65536;      // mbarriers + slots
 constexpr size_t kFpSmem = kFpOffBar + 256 + 1024;
+static_assert(kFpOffEpi % 1024 == 0, "SW128 staging must be 1 KB aligned");
+static_assert(kFpSmem <= 232448, "pair kernel exceeds the 227 KB dynamic smem limit");
 
 // byte offset of (row, 16-B chunk) in a swizzled 16 x 256 B tile (128 bf16 columns)
 __device__ __forceinline__ int hsw2(int row, int chunk) { return row * 256 + ((chunk ^ (row & 7)) << 4); }
@@ -56,6 +60,17 @@ __device__ __forceinline__ int pair_frag_to_natural(int k, int r) {
   return kHeadNC * kHeadDH + kHeadNC + 128 * r + 8 * c + u;
 }
 
+// TMA store of a {32, 128, 1} fp32 box from 128B-swizzled smem (bulk group)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tm)),
+               "r"(tc::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ void st_cluster_v4(uint32_t addr, float4 v) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w)
@@ -70,11 +85,18 @@ __device__ __forceinline__ uint32_t ld_acquire_cluster_u32(const void* p) {
   return v;
 }
 
+// phase F stage s: the four W stages, then two 32 KB blocks of the W staging
+// region (idle until phase W, which starts after this CTA's last head)
+__device__ __forceinline__ uint8_t* fp_stage_f(uint8_t* smem, int s) {
+  return s < kFpStages ? smem + s * kFpStage : smem + kFpOffEpi + (s - kFpStages) * kFpStage;
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
     c2_pair_worker_kernel(const __grid_constant__ CUtensorMap tmX,    // X [B][784], box {64,128}
                           const __grid_constant__ CUtensorMap tmW0h,  // W0 [256][784], box {64,128}
                           const __grid_constant__ CUtensorMap tmDz,   // dZ0 [B][256] as [K][M], box {64,64}
                           const __grid_constant__ CUtensorMap tmXn,   // X [B][784] as [K][N], box {64,64}
+                          const __grid_constant__ CUtensorMap tmOut,  // slabs [n_local][256][784] f32, box {32,128,1}
                           FusedArgs A) {
   using namespace tc;
   extern __shared__ __align__(1024) uint8_t fp_raw[];
@@ -84,7 +106,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
   uint64_t* tfull = empty + kFpStages;  // [3]: phase F acc, phase W acc 0/1
   uint64_t* tempty = tfull + 3;         // [3]
   uint64_t* hdone = tempty + 3;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hdone + 1);
+  uint64_t* fullF = hdone + 1;           // [kFpStagesF] phase F ring
+  uint64_t* emptyF = fullF + kFpStagesF;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(emptyF + kFpStagesF);
   int* grp = reinterpret_cast<int*>(tmem_slot + 1);
   uint32_t* flag = reinterpret_cast<uint32_t*>(smem + kFpOffFlag);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -101,11 +125,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
       mbar_init(&tempty[s], 8);
     }
     mbar_init(hdone, 1);
+    for (int s = 0; s < kFpStagesF; ++s) {
+      mbar_init(&fullF[s], 1);
+      mbar_init(&emptyF[s], 1);
+    }
     fence_barrier_init();
     tma_prefetch(&tmX);
     tma_prefetch(&tmW0h);
     tma_prefetch(&tmDz);
     tma_prefetch(&tmXn);
+    tma_prefetch(&tmOut);
   }
   if (warp < 8 && lane == 0) flag[warp] = 0u;
   if (warp == 9) tmem_alloc<512>(tmem_slot);
@@ -176,8 +205,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
   if (warp == 8) {
     // ============================ TMA producer ============================
     if (lane == 0 && g >= 0) {
-      int stage = 0;
-      uint32_t ph = 0, hph = 0;
+      int stage = 0, fs = 0;
+      uint32_t ph = 0, hph = 0, fph = 0;
+      if (dbg) dbg[13] = globaltimer();
       for (int it = 0; it < my_mt; ++it) {
         const int m0 = r0 + (pair + it * n_pairs) * 128;
         if (it > 0) {
@@ -185,14 +215,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
           hph ^= 1;
         }
         for (int kb = 0; kb < (kFzD0 + 63) / 64; ++kb) {
-          mbar_wait(&empty[stage], ph ^ 1);
-          uint8_t* sa = smem + stage * kFpStage;
-          mbar_arrive_expect_tx(&full[stage], kFpStage);
-          tma_load_2d(sa, &tmX, &full[stage], kb * 64, m0);
-          tma_load_2d(sa + 16384, &tmW0h, &full[stage], kb * 64, 128 * static_cast<int>(rank));
-          if (++stage == kFpStages) {
-            stage = 0;
-            ph ^= 1;
+          const int kq = kb;
+          mbar_wait(&emptyF[fs], fph ^ 1);
+          uint8_t* sa = fp_stage_f(smem, fs);
+          mbar_arrive_expect_tx(&fullF[fs], kFpStage);
+          tma_load_2d(sa, &tmX, &fullF[fs], kq * 64, m0);
+          tma_load_2d(sa + 16384, &tmW0h, &fullF[fs], kq * 64, 128 * static_cast<int>(rank));
+          if (++fs == kFpStagesF) {
+            fs = 0;
+            fph ^= 1;
           }
         }
       }
@@ -232,8 +263,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
   } else if (warp == 9) {
     // ============================ MMA issuer ==============================
     if (g >= 0) {
-      int stage = 0;
-      uint32_t ph = 0, fph = 0;
+      int stage = 0, fs = 0;
+      uint32_t ph = 0, fph = 0, sph = 0;
       constexpr uint32_t kIdF = idesc_bf16_f32(128, 128, false, false);
       constexpr uint32_t kIdW = idesc_bf16_f32(128, 128, true, true);
       for (int it = 0; it < my_mt; ++it) {
@@ -241,21 +272,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
         fph ^= 1;
         tc_fence_after();
         for (int kb = 0; kb < (kFzD0 + 63) / 64; ++kb) {
-          mbar_wait(&full[stage], ph);
+          mbar_wait(&fullF[fs], sph);
           tc_fence_after();
+          if (dbg && lane == 0 && it == 0 && kb == 0) dbg[11] = globaltimer();
+          if (dbg && lane == 0 && it == 0 && kb == (kFzD0 + 63) / 64 - 1) dbg[12] = globaltimer();
           if (lane == 0) {
-            const uint32_t a = smem_u32(smem + stage * kFpStage), b = a + 16384;
+            const uint32_t a = smem_u32(fp_stage_f(smem, fs)), b = a + 16384;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               umma_bf16(tmem, umma_desc_sw128(a + k * 32, 16, 1024), umma_desc_sw128(b + k * 32, 16, 1024), kIdF,
                         (kb > 0 || k > 0) ? 1u : 0u);
-            umma_commit(&empty[stage]);
+            umma_commit(&emptyF[fs]);
             if (kb == (kFzD0 + 63) / 64 - 1) umma_commit(&tfull[0]);
           }
           __syncwarp();
-          if (++stage == kFpStages) {
-            stage = 0;
-            ph ^= 1;
+          if (++fs == kFpStagesF) {
+            fs = 0;
+            sph ^= 1;
           }
         }
       }
@@ -548,8 +581,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
       if (threadIdx.x == 0) atomicAdd(done + g, 1u);
       if (dbg && threadIdx.x == 0) dbg[2] = globaltimer();
     }
-    // ---- phase W epilogue: dW0 tiles -> the worker's fp32 slab ----
+    // ---- phase W epilogue: dW0 tiles -> the worker's fp32 slab by TMA store
+    // (the accumulator goes through 128B-swizzled smem boxes of 32 columns;
+    // per-thread row stores would write 16 B into a different line per lane) ----
     float* dst = A.slab + static_cast<long long>(g) * A.slab_stride + A.off_w0;
+    uint8_t* epi = smem + kFpOffEpi;
     int acc = 0;
     uint32_t aph[2] = {0u, 0u};
     if (rows == 0 && cta_in == 0)
@@ -560,30 +596,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
       aph[acc] ^= 1;
       tc_fence_after();
       if (dbg && threadIdx.x == 0 && t == cta_in) dbg[10] = globaltimer();
-      const int row = mt * 128 + 32 * q + lane;
+      const int r = 32 * q + lane;  // row of the 128-row output tile
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
-        const int cl = half * 64 + c * 32;
+        const int cc = half * 2 + c;  // 32-column box of the tile
         uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(32 * q) << 16) + 128 + acc * 128 + cl, v);
+        tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(32 * q) << 16) + 128 + acc * 128 + cc * 32, v);
         tmem_ld_wait();
-        const int col0 = nt * 128 + cl;
-        if (col0 >= kFzD0) continue;
-        float* o = dst + static_cast<long long>(row) * kFzD0 + col0;
-        if (col0 + 32 <= kFzD0) {
+        uint8_t* box = epi + cc * 16384 + r * 128;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                                                            __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-        } else {
-          for (int j = 0; j < 32 && col0 + j < kFzD0; ++j) o[j] = __uint_as_float(v[j]);
-        }
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<uint4*>(box + ((j ^ (r & 7)) << 4)) =
+              make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[1 + acc]);
+      fence_proxy_async_smem();
+      named_sync_epi();
+      if (threadIdx.x == 0) {
+        for (int cc = 0; cc < 4; ++cc) {
+          const int col = nt * 128 + cc * 32;
+          if (col < kFzD0) tma_store_3d(&tmOut, epi + cc * 16384, col, mt * 128, g);
+        }
+        bulk_commit();
+        bulk_wait_read0();  // the staging boxes may be rewritten by the next tile
+      }
+      named_sync_epi();
       acc ^= 1;
     }
+    if (threadIdx.x == 0) bulk_wait0();  // dW0 in global memory before the combine / exit
   }
   if (dbg && threadIdx.x == 0) dbg[4] = globaltimer();
   tc_fence_before();

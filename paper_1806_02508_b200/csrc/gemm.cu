@@ -49,6 +49,26 @@ int make_tmap_bf16(CUtensorMap* tm, const void* ptr, long long inner, long long 
   return LBBSP_OK;
 }
 
+// fp32 [d2][d1][d0] slabs (d0 contiguous, d1 stride ld1 elements, d2 stride
+// ld2 elements), 128B swizzle, box {32, box1, 1}: the TMA-store epilogue of
+// the fused worker kernel (per-worker dW0 partials).
+int make_tmap_f32_3d(CUtensorMap* tm, const void* ptr, long long d0, long long d1, long long d2, long long ld1,
+                     long long ld2, int box1) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return set_error(LBBSP_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((ld1 * 4) % 16 != 0 || (ld2 * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(ptr) % 16) != 0)
+    return set_error(LBBSP_INVALID_ARGUMENT, "tma: fp32 slab rows must be 16-byte aligned");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d0), static_cast<cuuint64_t>(d1), static_cast<cuuint64_t>(d2)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld1 * 4), static_cast<cuuint64_t>(ld2 * 4)};
+  cuuint32_t box[3] = {32u, static_cast<cuuint32_t>(box1), 1u};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(LBBSP_CUDA, "cuTensorMapEncodeTiled (f32 3d) failed (%d)", (int)r);
+  return LBBSP_OK;
+}
+
 int num_sms() {
   static int sms = 0;
   if (!sms) {

@@ -39,6 +39,8 @@ cudaError_t launch_maybe_pdl(void (*kern)(KArgs...), int grid, int block, size_t
 
 int make_tmap_bf16(CUtensorMap* tm, const void* ptr, long long inner, long long outer, long long ld,
                    int box_outer);
+int make_tmap_f32_3d(CUtensorMap* tm, const void* ptr, long long d0, long long d1, long long d2, long long ld1,
+                     long long ld2, int box1);
 int gemm_plan(GemmPlan* p, const void* A, const void* B, int M, int N, int K, bool a_mn, bool b_mn,
               int bn, int epi, bool pair = false);
 int gemm_launch(const GemmPlan& p, cudaStream_t s);

@@ -1324,7 +1324,7 @@ struct lbbsp_mlp {
   // fused worker kernel (784-256-10): forward + head + dW0 in one launch
   bool fused = false;
   bool fused_pair = false;  // the (2,1,1)-cluster variant (c2_fused_pair.cuh)
-  CUtensorMap fz_tm[5];
+  CUtensorMap fz_tm[6];
   unsigned* fz_comb = nullptr;
   unsigned long long* fz_dbg = nullptr;  // LBBSP_FZ_DEBUG: per-CTA stage stamps
   // e2e plumbing: cached host-buffer lookups (lbbsp_mlp_read_result_async,
@@ -1486,7 +1486,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     fa.dbg = fz_dbg;
     if (fused_pair)
       LBBSP_CUDA_CHECK(launch_maybe_pdl(c2_pair_worker_kernel, sms & ~1, kFpThreads, kFpSmem, s, use_pdl,
-                                        fz_tm[0], fz_tm[4], fz_tm[2], fz_tm[3], fa));
+                                        fz_tm[0], fz_tm[4], fz_tm[2], fz_tm[3], fz_tm[5], fa));
     else
       LBBSP_CUDA_CHECK(launch_maybe_pdl(c2_fused_worker_kernel, sms, kFzThreads, kFzSmem, s, use_pdl, fz_tm[0],
                                         fz_tm[1], fz_tm[2], fz_tm[3], fa));
@@ -2125,6 +2125,8 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     if (!rc) rc = make_tmap_bf16(&m.fz_tm[2], m.dZ[0], kHeadDH, m.B_cap, kHeadDH, 64);
     if (!rc) rc = make_tmap_bf16(&m.fz_tm[3], m.X, kFzD0, m.B_cap, kFzD0, 64);
     if (!rc) rc = make_tmap_bf16(&m.fz_tm[4], m.pb + m.off_w[0], kFzD0, kHeadDH, kFzD0, 128);
+    if (!rc)
+      rc = make_tmap_f32_3d(&m.fz_tm[5], m.partial + m.off_w[0], kFzD0, kHeadDH, m.n_local, kFzD0, m.P, 128);
     if (rc) return rc;
     // the column-split pair kernel by default (LBBSP_FUSE_SINGLE=1: one CTA per tile)
     m.fused_pair = !getenv("LBBSP_FUSE_SINGLE");

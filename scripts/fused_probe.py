@@ -50,4 +50,4 @@ t = buf.reshape(148, 16).astype(np.int64)
 base = t[t[:, 0] > 0, 0].min()
 for c in range(0, 40):
     r = t[c]
-    print(c, [(int(x - base) if x > 0 else -1) for x in r[:11]])
+    print(c, [(int(x - base) if x > 0 else -1) for x in r[:14]])

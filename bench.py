@@ -702,7 +702,7 @@ def main():
         pass
     peak_tf = peaks.get("bf16_tflops", 1590.0)
     peak_src = "measured (burst)" if "bf16_tflops" in peaks else "fallback"
-    # the dominant kernel: the fused worker kernel (csrc/c2_fused.cuh), one
+    # the dominant kernel: the fused worker kernel (csrc/c2_fused_pair.cuh), one
     # launch = every worker's forward + head + dW0 over the GPU's 4096 rows,
     # 818,176 flop per sample; its duration = the worker-phase
     # window (first CTA start .. last CTA end, %globaltimer) of the
@@ -712,8 +712,13 @@ def main():
     ph_k = float(phases_unloaded[0]) if phases_unloaded is not None and len(phases_unloaded) else 0.0
     achieved = kern_flops / ph_k / 1e12 if ph_k > 0 else 0.0
     traffic = None
+    pair = not os.environ.get("LBBSP_FUSE_SINGLE")
+    kname = ("c2_pair_worker_kernel: 8 workers' forward + head + dW0 on (2,1,1) CTA pairs (tcgen05, "
+             "TMA in/out), one launch per round") if pair else \
+        "c2_fused_worker_kernel: 8 workers' forward (tcgen05) + head + dW0 (tcgen05), one launch per round"
+    cap_file = "r02_c2_pair_ncu.json" if pair else "r02_c2_fused_ncu.json"
     try:
-        cap = json.load(open(os.path.join(REPO, "profiles", "r02_c2_fused_ncu.json")))
+        cap = json.load(open(os.path.join(REPO, "profiles", cap_file)))
         traffic = int(cap["dram_bytes_read"]) + int(cap["dram_bytes_write"])
     except Exception:
         pass
@@ -752,13 +757,12 @@ def main():
             "gamma_profiles_s": [[round(m0, 12), round(b0, 9)] for m0, b0, _, _ in prof],
             "phase_ms": [round(float(x) * 1e3, 4) for x in (phases if phases is not None else [])],
             "roofline": {"bound": "tensor",
-                         "kernel": "c2_fused_worker_kernel: 8 workers' forward (tcgen05) + head + dW0 "
-                                   "(tcgen05), one launch per round",
+                         "kernel": kname,
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf if peak_tf else None,
                          "peak_source": peak_src, "duration_us": ph_k * 1e6,
                          "flop_per_launch": kern_flops, "traffic": traffic,
-                         "traffic_source": "profiles/r02_c2_fused_ncu.json (dram__bytes_read.sum + "
+                         "traffic_source": f"profiles/{cap_file} (dram__bytes_read.sum + "
                                            "dram__bytes_write.sum, one launch)",
                          "note": "C2 is latency-bound (SURVEY 8(d)): ~512 rows per worker"},
             "gpu_launches": launches * args.steps,

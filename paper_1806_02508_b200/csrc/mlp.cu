@@ -2128,8 +2128,11 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     if (!rc)
       rc = make_tmap_f32_3d(&m.fz_tm[5], m.partial + m.off_w[0], kFzD0, kHeadDH, m.n_local, kFzD0, m.P, 128);
     if (rc) return rc;
-    // the column-split pair kernel by default (LBBSP_FUSE_SINGLE=1: one CTA per tile)
-    m.fused_pair = !getenv("LBBSP_FUSE_SINGLE");
+    // the column-split pair kernel by default (LBBSP_FUSE_SINGLE=1: one CTA per
+    // tile). SM-cap mode keeps the single-CTA kernel: its caps follow
+    // floor(budget * share * availability) exactly, odd counts included, and
+    // the pair kernel needs cluster-aligned (even) partitions
+    m.fused_pair = !getenv("LBBSP_FUSE_SINGLE") && c.straggler_mode != LBBSP_STRAGGLE_SM_CAP;
     D.pair_caps = m.fused_pair ? 1 : 0;
     unsigned* fd = nullptr;
     LBBSP_CUDA_CHECK(m.alloc(&fd, static_cast<size_t>(m.n_local)));

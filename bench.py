@@ -574,14 +574,13 @@ def main():
         prof = [p for r in allp for p in r]
     else:
         prof = prof_local
-    prof = [(m0, b0, 1, B) for m0, b0, _, _ in prof]
 
-    def make(scheme, tr, predictor="narx", solver="proportional"):
+    def make(scheme, tr, predictor="narx", solver="proportional", observe="rate"):
         eng = MlpEngine(dims=DIMS, global_batch=B, n_workers_local=WORKERS_PER_GPU, world=world,
                         rank=rank, scheme=scheme, predictor=predictor,
                         warmup_iterations=WARMUP_NARX, learning_rate=0.05, seed=1,
-                        max_iterations=iters + 4, trace=tr, solver=solver,
-                        gamma_profiles=prof if solver == "gamma" else None)
+                        max_iterations=iters + 4, trace=tr, solver=solver, observe=observe,
+                        gamma_profiles=prof if (solver == "gamma" or observe == "capacity") else None)
         if world > 1:
             connect(eng, world, rank)
         return eng
@@ -670,14 +669,15 @@ def main():
     # reach) and the no-straggler ideal (every worker at a = 1) ----
     win = {}
     phases_unloaded = None
-    for name, scheme, tr, pred, solver in (
-            ("lbbsp", "lb-bsp", trace, "narx", "proportional"),
-            ("lbbsp_gamma", "lb-bsp", trace, "narx", "gamma"),
-            ("bsp", "bsp", trace, "narx", "proportional"),
-            ("perfect", "lb-bsp", trace, "perfect", "proportional"),
-            ("perfect_gamma", "lb-bsp", trace, "perfect", "gamma"),
-            ("no_straggler", "lb-bsp", constant_trace(n_total, iters), "narx", "proportional")):
-        eng = make(scheme, tr, pred, solver)
+    for name, scheme, tr, pred, solver, obs in (
+            ("lbbsp", "lb-bsp", trace, "narx", "proportional", "rate"),
+            ("lbbsp_capacity", "lb-bsp", trace, "narx", "proportional", "capacity"),
+            ("lbbsp_gamma", "lb-bsp", trace, "narx", "gamma", "rate"),
+            ("bsp", "bsp", trace, "narx", "proportional", "rate"),
+            ("perfect", "lb-bsp", trace, "perfect", "proportional", "rate"),
+            ("perfect_gamma", "lb-bsp", trace, "perfect", "gamma", "rate"),
+            ("no_straggler", "lb-bsp", constant_trace(n_total, iters), "narx", "proportional", "rate")):
+        eng = make(scheme, tr, pred, solver, obs)
         ms_w, ph_w = timed(eng, window, warm, phases=(name == "no_straggler"))
         if ph_w is not None:
             phases_unloaded = ph_w
@@ -753,8 +753,9 @@ def main():
             "lbbsp_over_ideal_time": lb / win["perfect"]["mean"],
             "lbbsp_over_no_straggler_time": lb / win["no_straggler"]["mean"],
             "lbbsp_gamma_over_bsp": win["bsp"]["mean"] / win["lbbsp_gamma"]["mean"],
+            "lbbsp_capacity_over_bsp": win["bsp"]["mean"] / win["lbbsp_capacity"]["mean"],
             "lbbsp_gamma_over_ideal_time": win["lbbsp_gamma"]["mean"] / win["perfect_gamma"]["mean"],
-            "gamma_profiles_s": [[round(m0, 12), round(b0, 9)] for m0, b0, _, _ in prof],
+            "gamma_profiles_s": [[round(m0, 12), round(b0, 9), xo] for m0, b0, _, xo in prof],
             "phase_ms": [round(float(x) * 1e3, 4) for x in (phases if phases is not None else [])],
             "roofline": {"bound": "tensor",
                          "kernel": kname,

@@ -583,7 +583,8 @@ typedef struct {
   int max_iterations;                 /* record capacity                     */
   int straggler_mode;                 /* LBBSP_STRAGGLE_INTERFERE (0, default) | _SM_CAP (1) */
   int solver;                         /* LBBSP_SOLVER_PROPORTIONAL (0, default) | _GAMMA (1) */
-  const lbbsp_gpu_profile* h_gpu_profiles; /* [n_workers_total] unloaded Gamma (GAMMA solver) */
+  const lbbsp_gpu_profile* h_gpu_profiles; /* [n_workers_total] unloaded Gamma (GAMMA solver, CAPACITY) */
+  int observe;                        /* LBBSP_OBSERVE_RATE (0, default) | _CAPACITY (1) */
 } lbbsp_mlp_cfg;
 
 /* Batch-size solver of the MLP engine's LB-BSP rounds:
@@ -595,6 +596,17 @@ typedef struct {
  *   reference's GPU-cluster branch with a predictor, cluster_sim.cpp:373-387). */
 #define LBBSP_SOLVER_PROPORTIONAL 0
 #define LBBSP_SOLVER_GAMMA 1
+
+/* The speed the proportional solver's predictor observes per worker and round
+ * (b rows in t seconds):
+ * RATE: b / t;
+ * CAPACITY: a * x_n / Gamma0(x_n), the worker's speed at the nominal batch
+ *   x_n = B / n with a = Gamma0(b) / t read off its unloaded profile (needs
+ *   h_gpu_profiles) -- the reference's CPU-mode v_actual (the speed of the
+ *   worker under its resource state, cluster_sim.cpp:357-361), which b / t is
+ *   not when the worker time has a fixed latency. */
+#define LBBSP_OBSERVE_RATE 0
+#define LBBSP_OBSERVE_CAPACITY 1
 
 /* How a worker's availability a = min(1, c * MemPenalty(m) * mult) is injected:
  * INTERFERE: the worker keeps its nominal CTA partition and co-scheduled
@@ -651,6 +663,10 @@ int lbbsp_mlp_phase_times(lbbsp_mlp* m, double* h_phase_ns, int* n_phases);
 int lbbsp_mlp_worker_phase_times(lbbsp_mlp* m, double* h_ns, int* n_phases);
 /* algorithmic work of one round on this rank: GEMM flops, reduction bytes */
 int lbbsp_mlp_work(lbbsp_mlp* m, double* gemm_flops, double* reduce_bytes);
+/* Rows one CTA of a worker's partition covers per tile wave (64: the fused
+ * pair kernel, two CTAs per 128-row tile; 128: one CTA per tile). A worker
+ * with cap CTAs runs ceil(b / (cap * rows_per_cta)) waves. */
+int lbbsp_mlp_rows_per_cta(lbbsp_mlp* m, int* rows);
 
 #ifdef __cplusplus
 }

@@ -203,7 +203,8 @@ struct PlanDev {
   unsigned long long* gather_done;  // single rank: gather CTAs finished, summed over all rounds
   int straggler_mode;          // LBBSP_STRAGGLE_INTERFERE | LBBSP_STRAGGLE_SM_CAP
   int solver;                  // LBBSP_SOLVER_PROPORTIONAL | LBBSP_SOLVER_GAMMA
-  const lbbsp_gpu_profile* prof0;  // [n_total] unloaded Gamma profiles (GAMMA solver)
+  int observe;                 // LBBSP_OBSERVE_RATE | LBBSP_OBSERVE_CAPACITY (proportional solver)
+  const lbbsp_gpu_profile* prof0;  // [n_total] unloaded Gamma profiles (GAMMA solver, CAPACITY)
   float2* intf_w;              // [n_local] {availability, HBM share of the injected time}
   unsigned* fz_done;           // [n_local] fused worker kernel: head CTAs done (zeroed here)
   int pair_caps;               // worker CTA partitions cluster-aligned (even) for the pair kernel
@@ -850,17 +851,31 @@ __device__ inline double worker_time(const PlanDev& D, int i, int n_phases) {
   return t;
 }
 
+// Unloaded Gamma time of worker w for b rows: m0 max(b, x_s) + b0.
+__device__ inline double gamma0(const lbbsp_gpu_profile& p, double b) {
+  const double xs = static_cast<double>(p.saturation_point);
+  return dadd(dmul(p.sec_per_sample, b > xs ? b : xs), p.base_time_s);
+}
+
 // The observation pushed into worker w's history for a batch of b rows that
-// took t seconds. Proportional solver: the realised speed b / t (the
-// reference's v_actual = x / tp, cluster_sim.cpp:412-413). Gamma solver: the
-// realised speed relative to the worker's unloaded profile, Gamma0(b) / t
-// (= its availability a when the time follows (m0 max(b, x_s) + b0) / a).
+// took t seconds.
+//  * RATE: the realised rate b / t (the reference's GPU-mode v_actual = x / tp,
+//    cluster_sim.cpp:412-413).
+//  * CAPACITY: the worker's sustainable speed at the nominal batch
+//    x_n = B / n, a * x_n / Gamma0(x_n) with the availability a = Gamma0(b) / t
+//    read off its unloaded profile -- the reference's CPU-mode v_actual, the
+//    worker's speed under its current resource state whatever batch it ran
+//    (effective_speed * speed_mult, cluster_sim.cpp:357-361). On a worker with
+//    a fixed latency b / t is not that: a worker handed few rows looks slow,
+//    gets fewer rows, and collapses to the floor (measured, DESIGN 2.3).
+//  * Gamma solver: the availability Gamma0(b) / t itself.
 __device__ inline double observed_speed(const PlanDev& D, int w, int b, double t) {
-  if (D.solver == LBBSP_SOLVER_GAMMA) {
+  if (D.solver == LBBSP_SOLVER_GAMMA || D.observe == LBBSP_OBSERVE_CAPACITY) {
     const lbbsp_gpu_profile p = D.prof0[w];
-    const double g0 = dadd(dmul(p.sec_per_sample, static_cast<double>(b > p.saturation_point ? b : p.saturation_point)),
-                           p.base_time_s);
-    return t > 0.0 ? ddiv(g0, t) : 1.0;
+    const double a = t > 0.0 ? ddiv(gamma0(p, static_cast<double>(b)), t) : 1.0;
+    if (D.solver == LBBSP_SOLVER_GAMMA) return a;
+    const double xn = ddiv(static_cast<double>(D.B_total), static_cast<double>(D.n_total));
+    return dmul(a, ddiv(xn, gamma0(p, xn)));
   }
   return t > 0.0 ? static_cast<double>(b) / t : static_cast<double>(b);
 }
@@ -1956,15 +1971,20 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   if (c.solver != LBBSP_SOLVER_PROPORTIONAL && c.solver != LBBSP_SOLVER_GAMMA)
     return set_error(LBBSP_INVALID_ARGUMENT, "mlp: unknown solver %d", c.solver);
   D.solver = c.solver;
-  if (c.solver == LBBSP_SOLVER_GAMMA) {
+  if (c.observe != LBBSP_OBSERVE_RATE && c.observe != LBBSP_OBSERVE_CAPACITY)
+    return set_error(LBBSP_INVALID_ARGUMENT, "mlp: unknown observe %d", c.observe);
+  D.observe = c.observe;
+  if (c.solver == LBBSP_SOLVER_GAMMA || c.observe == LBBSP_OBSERVE_CAPACITY) {
     if (!c.h_gpu_profiles)
-      return set_error(LBBSP_INVALID_ARGUMENT, "mlp: the gamma solver needs h_gpu_profiles (unloaded Gamma per worker)");
+      return set_error(LBBSP_INVALID_ARGUMENT,
+                       "mlp: the gamma solver and the capacity observation need h_gpu_profiles (unloaded Gamma per worker)");
     lbbsp_gpu_profile* pr = nullptr;
     LBBSP_CUDA_CHECK(m.upload(&pr, c.h_gpu_profiles, static_cast<size_t>(n)));
     D.prof0 = pr;
+  }
+  if (c.solver == LBBSP_SOLVER_GAMMA)
     LBBSP_CUDA_CHECK(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(gamma_plan_smem(n))));
-  }
   if (c.straggler_mode == LBBSP_STRAGGLE_INTERFERE) {
     float2* w = nullptr;
     LBBSP_CUDA_CHECK(m.alloc(&w, m.n_local));
@@ -2437,6 +2457,12 @@ extern "C" int lbbsp_mlp_work(lbbsp_mlp* m, double* gemm_flops, double* reduce_b
   return LBBSP_OK;
 }
 
+extern "C" int lbbsp_mlp_rows_per_cta(lbbsp_mlp* m, int* rows) {
+  if (!m || !rows) return set_error(LBBSP_INVALID_ARGUMENT, "mlp_rows_per_cta: null argument");
+  *rows = m->fused && m->fused_pair ? 64 : 128;
+  return LBBSP_OK;
+}
+
 
 // Debug timeline of the last round: stamps[16] then timing[kMaxPhases][n_local][2]
 // (globaltimer ns). Not part of the stable C-ABI.
@@ -2455,8 +2481,9 @@ extern "C" int lbbsp_mlp_debug_timeline(lbbsp_mlp* m, unsigned long long* out, i
 // host buffer pair warms it outside any steady-state step: DMA out of a
 // freshly page-locked buffer runs at a third of the link rate for its first
 // ~100 transfers (113 us vs 38 us for the 1.57 MB dataset,
-// profiles/r02_e2e_probe.txt), so it is copied until three consecutive
-// copies run within 15% of the fastest (at most 512 copies).
+// profiles/r02_e2e_probe.txt), so it is copied (into both dataset buffers) at
+// least 128 times and until three consecutive copies run within 15% of the
+// fastest (at most 1024 copies).
 extern "C" int lbbsp_mlp_step_e2e(lbbsp_mlp* m, const void* h_x_bf16, const int* h_labels, int* h_sizes,
                                   double* h_loss) {
   if (h_x_bf16 != m->warm_x || h_labels != m->warm_y) {
@@ -2470,10 +2497,14 @@ extern "C" int lbbsp_mlp_step_e2e(lbbsp_mlp* m, const void* h_x_bf16, const int*
     LBBSP_CUDA_CHECK(cudaEventCreate(&e1));
     float best = 1e30f;
     int steady = 0;
-    for (int i = 0; i < 512 && steady < 3; ++i) {
+    // both dataset buffers (both streams are idle here), at least 128 copies:
+    // the slow phase lasts ~100 transfers at a steady (slow) rate, so "three
+    // copies within 15% of the best" alone can stop inside it
+    for (int i = 0; i < 1024 && (i < 128 || steady < 3); ++i) {
+      const int b = (i & 1) ? m->cur : 1 - m->cur;
       LBBSP_CUDA_CHECK(cudaEventRecord(e0, m->copy_stream));
-      LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_xb[1 - m->cur], h_x_bf16, bx, cudaMemcpyHostToDevice, m->copy_stream));
-      LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_yb[1 - m->cur], h_labels, by, cudaMemcpyHostToDevice, m->copy_stream));
+      LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_xb[b], h_x_bf16, bx, cudaMemcpyHostToDevice, m->copy_stream));
+      LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_yb[b], h_labels, by, cudaMemcpyHostToDevice, m->copy_stream));
       LBBSP_CUDA_CHECK(cudaEventRecord(e1, m->copy_stream));
       LBBSP_CUDA_CHECK(cudaEventSynchronize(e1));
       float ms = 0.f;

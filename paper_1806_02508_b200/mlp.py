@@ -29,11 +29,13 @@ class MlpConfig(C.Structure):
         ("h_trace_c", _dp), ("h_trace_m", _dp), ("h_trace_mult", _dp), ("trace_len", C.c_int),
         ("h_worker_share", _dp), ("max_iterations", C.c_int), ("straggler_mode", C.c_int),
         ("solver", C.c_int), ("h_gpu_profiles", C.POINTER(abi.GpuProfile)),
+        ("observe", C.c_int),
     ]
 
 
 STRAGGLE = {"interfere": 0, "sm_cap": 1}
 SOLVERS = {"proportional": 0, "gamma": 1}
+OBSERVE = {"rate": 0, "capacity": 1}
 
 
 _SIG = {
@@ -49,6 +51,7 @@ _SIG = {
     "lbbsp_mlp_dataset": [C.c_void_p, C.c_void_p, _ip],
     "lbbsp_mlp_launches_per_iteration": [C.c_void_p, _ip],
     "lbbsp_mlp_work": [C.c_void_p, _dp, _dp],
+    "lbbsp_mlp_rows_per_cta": [C.c_void_p, _ip],
     "lbbsp_mlp_load_data_async": [C.c_void_p, C.c_void_p, C.c_void_p],
     "lbbsp_mlp_read_result_async": [C.c_void_p, C.c_void_p, C.c_void_p],
     "lbbsp_mlp_step_e2e": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
@@ -139,9 +142,13 @@ def calibrate_gamma(dims, batch, n_workers_local=8, rounds=6, warm=2, **kw):
     with three batch sizes around its nominal share x = batch / n (x/2, x,
     3x/2; static sizes summing to `batch`), and t = m0 x + b0 is fitted to the
     median worker time of each by least squares. Returns
-    [(m0, b0, x_s=1, x_o=batch)] per local worker. One worker per GPU
-    (n_workers_local == 1): three single-worker engines with global batch
-    x/2, x, 3x/2."""
+    [(m0, b0, x_s=1, x_o)] per local worker, x_o = the rows one tile wave of
+    the worker's CTA partition covers (caps x rows_per_cta, at most `batch`):
+    past it the time steps up by a whole wave, which the linear profile does
+    not describe, so gpu_allocate must not go there (the reference's
+    oom_point, batch_sizer.hpp:12-18). One worker per GPU (n_workers_local ==
+    1): three single-worker engines with global batch x/2, x, 3x/2, x_o =
+    batch."""
     n = n_workers_local
     x = batch // n
     if n == 1:
@@ -154,15 +161,20 @@ def calibrate_gamma(dims, batch, n_workers_local=8, rounds=6, warm=2, **kw):
             alt[-1] = alt2[-1] = x
         configs = [[x] * n, alt, alt2]
     pts = [[] for _ in range(n)]
+    wave = [batch] * n
     iters = warm + rounds + 2
     for sizes in configs:
         eng = MlpEngine(dims=dims, global_batch=int(sum(sizes)), n_workers_local=n, predictor="ema",
                         max_iterations=iters, trace=constant_trace(n, iters),
                         static_sizes=sizes if n > 1 else None, **kw)
         eng.run(warm + rounds)
-        t = eng.records()["t_worker"][warm:]
+        rec = eng.records()
+        t = rec["t_worker"][warm:]
+        rpc = eng.rows_per_cta()
         for i in range(n):
             pts[i].append((sizes[i], float(np.median(t[:, i]))))
+            if n > 1:
+                wave[i] = min(wave[i], int(rec["caps"][warm:, i].min()) * rpc)
         del eng
     prof = []
     for i in range(n):
@@ -171,7 +183,7 @@ def calibrate_gamma(dims, batch, n_workers_local=8, rounds=6, warm=2, **kw):
         m0, b0 = np.polyfit(xs, ts, 1)
         m0 = max(float(m0), 1e-12)
         b0 = max(float(b0), 0.0)
-        prof.append((m0, b0, 1, batch))
+        prof.append((m0, b0, 1, min(batch, wave[i])))
     return prof
 
 
@@ -181,7 +193,7 @@ class MlpEngine:
                  learning_rate=0.05, seed=1, dataset_seed=7, dataset_size=1000, loss_every=1,
                  sm_budget=0, trace=None, worker_share=None, max_iterations=1000,
                  static_sizes=None, train=None, straggler="interfere", solver="proportional",
-                 gamma_profiles=None):
+                 gamma_profiles=None, observe="rate"):
         n_total = n_workers_local * world
         if trace is None:
             trace = constant_trace(n_total, max_iterations)
@@ -217,6 +229,7 @@ class MlpEngine:
         c.max_iterations = max_iterations
         c.straggler_mode = STRAGGLE[straggler] if isinstance(straggler, str) else straggler
         c.solver = SOLVERS[solver] if isinstance(solver, str) else solver
+        c.observe = OBSERVE[observe] if isinstance(observe, str) else observe
         if gamma_profiles is not None:
             arr = (abi.GpuProfile * len(gamma_profiles))(
                 *[abi.GpuProfile(float(m), float(b), int(xs), int(xo)) for m, b, xs, xo in gamma_profiles])
@@ -274,6 +287,11 @@ class MlpEngine:
         f, b = C.c_double(), C.c_double()
         check(_L().lbbsp_mlp_work(self._h, C.byref(f), C.byref(b)))
         return f.value, b.value
+
+    def rows_per_cta(self):
+        x = C.c_int()
+        check(_L().lbbsp_mlp_rows_per_cta(self._h, C.byref(x)))
+        return x.value
 
     def load_data_async(self, x_ptr, y_ptr):
         check(_L().lbbsp_mlp_load_data_async(self._h, x_ptr, y_ptr))

@@ -115,3 +115,42 @@ def test_gamma_solver_balances_workers():
     tb = bsp.records()["t_worker"][-8:].max(axis=1)
     tg = rec["t_worker"][-8:].max(axis=1)
     assert float(np.median(tg)) < 0.8 * float(np.median(tb)), (tg, tb)
+
+
+def test_capacity_observation_c2():
+    """observe="capacity" on the latency-bound C2 shape: the proportional
+    solver's predictor sees each worker's speed at the nominal batch,
+    a * x_n / Gamma0(x_n) with a = Gamma0(b) / t (the reference's CPU-mode
+    v_actual, cluster_sim.cpp:357-361), instead of b / t. Checks: v_obs is
+    that formula of the recorded (b, t) bit for bit; sizes are bit-exact
+    against the reference cpu_allocate replay of v_obs; and the slow workers
+    keep a share near their availability instead of collapsing to the floor
+    (b / t on a worker with a fixed latency: fewer rows -> looks slower)."""
+    from oracle import oracle as O
+    from paper_1806_02508_b200 import abi
+    from paper_1806_02508_b200.mlp import MlpEngine, calibrate_gamma, constant_trace
+    dims = [784, 256, 10]
+    n, B, iters = 8, 4096, 30
+    avail = [1.0] * 6 + [0.5, 0.3]
+    prof = calibrate_gamma(dims, B, n, rounds=4)
+    trace = constant_trace(n, iters, avail)
+    eng = MlpEngine(dims=dims, global_batch=B, n_workers_local=n, predictor="ema",
+                    max_iterations=iters, trace=trace, observe="capacity", gamma_profiles=prof)
+    eng.run(iters)
+    rec = eng.records()
+    xn = B / n
+    for k in range(iters):
+        for w in range(n):
+            m0, b0, xs, _ = prof[w]
+            b, t = float(rec["sizes"][k, w]), float(rec["t_worker"][k, w])
+            a = (m0 * max(b, float(xs)) + b0) / t
+            assert rec["v_obs"][k, w] == a * (xn / (m0 * max(xn, float(xs)) + b0)), (k, w)
+    chk = O.reference() if O.reference_available() else O.restatement()
+    pcfg = abi.PredictorConfig.default(abi.PRED_EMA)
+    seeds = [chk.mix_seed(1, 0x9ced1c70, i) for i in range(n)]
+    sizes, vpred = chk.replay_cpu(pcfg, seeds, B, rec["v_obs"], trace[0][:, :iters].T, trace[1][:, :iters].T)
+    assert sizes.tolist() == rec["sizes"].tolist()
+    assert np.array_equal(vpred, rec["v_pred"])
+    last = rec["sizes"][-5:].min(axis=0)
+    fair = [B * a / sum(avail) for a in avail]
+    assert last[7] > 0.4 * fair[7] and last[6] > 0.4 * fair[6], (last.tolist(), fair)

@@ -68,6 +68,15 @@ struct FusedArgs {
   unsigned long long* timing;  // [n_local][2] worker window
   lbbsp_dev_status* status;
   unsigned long long* dbg;  // optional [grid][8] per-CTA stage stamps (globaltimer)
+  // in-kernel row gather (c2_pair_worker_kernel, gather != 0): the batch rows
+  // are read straight from the resident dataset by sample index -- X / y of
+  // local row r are data_x / data_y [streams[k * B_total + *stream_off + r]]
+  int gather;
+  const int* streams;       // [max_rows][B_total] sample streams
+  const long long* kptr;    // the round index (written by the observe branch)
+  const int* stream_off;    // this rank's offset in the round's stream (plan)
+  const int* data_y;        // [N_data] dataset labels
+  int B_total, max_rows;
 };
 
 __device__ __forceinline__ void named_sync_epi() { asm volatile("bar.sync 1, 256;" ::: "memory"); }

@@ -92,10 +92,10 @@ __device__ __forceinline__ uint8_t* fp_stage_f(uint8_t* smem, int s) {
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
-    c2_pair_worker_kernel(const __grid_constant__ CUtensorMap tmX,    // X [B][784], box {64,128}
+    c2_pair_worker_kernel(const __grid_constant__ CUtensorMap tmX,    // X [B][784], box {64,128}; gather: dataset, box {64,1}
                           const __grid_constant__ CUtensorMap tmW0h,  // W0 [256][784], box {64,128}
                           const __grid_constant__ CUtensorMap tmDz,   // dZ0 [B][256] as [K][M], box {64,64}
-                          const __grid_constant__ CUtensorMap tmXn,   // X [B][784] as [K][N], box {64,64}
+                          const __grid_constant__ CUtensorMap tmXn,   // X [B][784] as [K][N], box {64,64}; gather: = tmX
                           const __grid_constant__ CUtensorMap tmOut,  // slabs [n_local][256][784] f32, box {32,128,1}
                           FusedArgs A) {
   using namespace tc;
@@ -201,26 +201,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
   const int k_blocks_w = rows > 0 ? (rows + 63) / 64 : 0;
   const int w_tiles = rows > 0 ? kFzWTiles : 0;
   unsigned* done = A.done;
+  // in-kernel row gather: local row r of this rank's batch is dataset row
+  // gidx[r] (rows past the round's stream read row 0; they are masked)
+  const int* gidx = nullptr;
+  int gmax = 0;
+  if (A.gather && g >= 0 && warp != 9) {
+    long long k = *A.kptr;
+    k = k < A.max_rows - 1 ? k : A.max_rows - 1;
+    const int off = *A.stream_off;
+    gidx = A.streams + k * A.B_total + off;
+    gmax = A.B_total - off;
+  }
 
   if (warp == 8) {
     // ============================ TMA producer ============================
-    if (lane == 0 && g >= 0) {
+    // Lane 0 issues the W0 / dZ0 tiles; with the in-kernel gather every lane
+    // issues one tile::gather4 of four batch rows per stage (X straight from
+    // the resident dataset -- no gathered copy of the batch in HBM).
+    if (g >= 0) {
       int stage = 0, fs = 0;
       uint32_t ph = 0, hph = 0, fph = 0;
-      if (dbg) dbg[13] = globaltimer();
+      if (dbg && lane == 0) dbg[13] = globaltimer();
       for (int it = 0; it < my_mt; ++it) {
         const int m0 = r0 + (pair + it * n_pairs) * 128;
+        int gr[4] = {0, 0, 0, 0};
+        if (gidx) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int rr = m0 + 4 * lane + u;
+            gr[u] = rr < gmax ? __ldg(gidx + rr) : 0;
+          }
+        }
         if (it > 0) {
           mbar_wait(hdone, hph);
           hph ^= 1;
         }
         for (int kb = 0; kb < (kFzD0 + 63) / 64; ++kb) {
-          const int kq = kb;
           mbar_wait(&emptyF[fs], fph ^ 1);
           uint8_t* sa = fp_stage_f(smem, fs);
-          mbar_arrive_expect_tx(&fullF[fs], kFpStage);
-          tma_load_2d(sa, &tmX, &fullF[fs], kq * 64, m0);
-          tma_load_2d(sa + 16384, &tmW0h, &fullF[fs], kq * 64, 128 * static_cast<int>(rank));
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&fullF[fs], kFpStage);
+            tma_load_2d(sa + 16384, &tmW0h, &fullF[fs], kb * 64, 128 * static_cast<int>(rank));
+            if (!gidx) tma_load_2d(sa, &tmX, &fullF[fs], kb * 64, m0);
+          }
+          __syncwarp();
+          if (gidx) tma_gather4(sa + 512 * lane, &tmX, &fullF[fs], kb * 64, gr[0], gr[1], gr[2], gr[3]);
           if (++fs == kFpStagesF) {
             fs = 0;
             fph ^= 1;
@@ -231,28 +256,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
         mbar_wait(hdone, hph);
         hph ^= 1;
       }
-      const unsigned long long t0 = globaltimer();
-      unsigned seen;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(done + g) : "memory");
-        if (globaltimer() - t0 > 2000000000ull) {
-          set_status(A.status, LBBSP_RUNTIME, 3, seen, head_ctas);
-          break;
+      if (lane == 0) {
+        const unsigned long long t0 = globaltimer();
+        unsigned seen;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(done + g) : "memory");
+          if (globaltimer() - t0 > 2000000000ull) {
+            set_status(A.status, LBBSP_RUNTIME, 3, seen, head_ctas);
+            break;
+          }
+        } while (seen < static_cast<unsigned>(head_ctas));
+        fence_proxy_async_global();
+        if (dbg) dbg[3] = globaltimer();
+      }
+      // the worker's row indices -> the (now idle) peer-logit region; every
+      // head CTA of the worker, the peer included, has finished writing it
+      int* sidx = reinterpret_cast<int*>(smem + kFpOffXl);
+      const bool sidx_ok = gidx && k_blocks_w * 64 <= (kFpOffFlag - kFpOffXl) / 4;
+      if (w_tiles > 0 && sidx_ok) {
+        for (int i = lane; i < k_blocks_w * 64; i += 32) {
+          const int rr = r0 + i;
+          sidx[i] = rr < gmax ? __ldg(gidx + rr) : 0;
         }
-      } while (seen < static_cast<unsigned>(head_ctas));
-      fence_proxy_async_global();
-      if (dbg) dbg[3] = globaltimer();
+      }
+      __syncwarp();
       for (int t = cta_in; t < w_tiles; t += cnt) {
         const int mt = t % 2, nt = t / 2;
         for (int kb = 0; kb < k_blocks_w; ++kb) {
           const int k0 = r0 + kb * 64;
           mbar_wait(&empty[stage], ph ^ 1);
           uint8_t* sa = smem + stage * kFpStage;
-          mbar_arrive_expect_tx(&full[stage], 32768);
-          tma_load_2d(sa, &tmDz, &full[stage], mt * 128, k0);
-          tma_load_2d(sa + 8192, &tmDz, &full[stage], mt * 128 + 64, k0);
-          tma_load_2d(sa + 16384, &tmXn, &full[stage], nt * 128, k0);
-          tma_load_2d(sa + 24576, &tmXn, &full[stage], nt * 128 + 64, k0);
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&full[stage], 32768);
+            tma_load_2d(sa, &tmDz, &full[stage], mt * 128, k0);
+            tma_load_2d(sa + 8192, &tmDz, &full[stage], mt * 128 + 64, k0);
+            if (!gidx) {
+              tma_load_2d(sa + 16384, &tmXn, &full[stage], nt * 128, k0);
+              tma_load_2d(sa + 24576, &tmXn, &full[stage], nt * 128 + 64, k0);
+            }
+          }
+          __syncwarp();
+          if (gidx) {
+            const int box = lane >> 4, q4 = lane & 15;
+            int rr[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = kb * 64 + 4 * q4 + u;
+              rr[u] = sidx_ok ? sidx[i] : (r0 + i < gmax ? __ldg(gidx + r0 + i) : 0);
+            }
+            tma_gather4(sa + 16384 + box * 8192 + q4 * 512, &tmXn, &full[stage], nt * 128 + 64 * box, rr[0],
+                        rr[1], rr[2], rr[3]);
+          }
           if (++stage == kFpStages) {
             stage = 0;
             ph ^= 1;
@@ -359,7 +413,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
       const bool have = row0 < r1;
       const int ra = row0 + gq, rb = row0 + gq + 8;
       const bool va = ra < r1, vb = rb < r1;
-      const int ya = have && va ? A.y[ra] : -1, yb = have && vb ? A.y[rb] : -1;
+      const int ya = have && va ? (gidx ? A.data_y[gidx[ra]] : A.y[ra]) : -1;
+      const int yb = have && vb ? (gidx ? A.data_y[gidx[rb]] : A.y[rb]) : -1;
       const float rsa = have && va ? A.row_scale[ra] : 0.f;
       const float rsb = have && vb ? A.row_scale[rb] : 0.f;
       // ---- H[:, own 128 columns] = bf16(relu(acc + b0)) -> 16 x 256 B head tiles ----

@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
     D.v_pred[i] = vp;
   }
   __syncthreads();
+  stamp(D, 10);
   int code = 0;
   if (D.static_sizes) {
     for (int i = tid; i < n; i += blockDim.x) sz[i] = D.static_sizes_d[i];
@@ -336,6 +337,7 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
       sz[i] = D.B_total / n + (i < D.B_total % n ? 1 : 0);  // equal_split
   }
   __syncthreads();
+  stamp(D, 11);
   if (code) {
     wait_gather(D, k);
     return;
@@ -384,6 +386,7 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
   }
   for (int i = tid; i < n; i += blockDim.x) D.sizes_all[i] = sz[i];
   __syncthreads();
+  stamp(D, 12);
   // row scales: Eq. 7 folds 1/B into every row; Eq. 6 (BSP) 1/(n b_i) per worker
   const int rows = r0_s[D.n_local];
   if (D.scheme == LBBSP_SCHEME_LBBSP) {
@@ -404,6 +407,7 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
     for (int i = tid; i < D.n_local; i += blockDim.x)
       D.rec_caps[static_cast<size_t>(row) * n + D.rank * D.n_local + i] = D.ctan[i];
   }
+  stamp(D, 8);  // plan computed; the wait for the gather follows
   if (!wait_gather(D, k)) {  // poisoned round: no worker computes on a stale batch
     for (int i = tid; i < D.n_local; i += blockDim.x) D.r1[i] = D.r0[i];
     if (tid == 0) *D.local_rows = 0;
@@ -464,6 +468,7 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
       if (dsti[u] >= 0) dst4[dsti[u]] = v[u];
   }
   for (int r = blockIdx.x * 256 + threadIdx.x; r < rows; r += 256 * gridDim.x) y[r] = data_y[idx[r]];
+  if (D.stamps && threadIdx.x == 0) atomicMax(&D.stamps[9], static_cast<unsigned long long>(gtimer()));
   if (fixed_rows > 0 && D.gather_ctas > 0) {  // tell the plan (see plan_kernel)
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1340,6 +1345,8 @@ struct lbbsp_mlp {
   bool fused = false;
   bool fused_pair = false;  // the (2,1,1)-cluster variant (c2_fused_pair.cuh)
   CUtensorMap fz_tm[6];
+  CUtensorMap fz_gm[2];   // dataset buffer b, box {64, 1}: the pair kernel's in-kernel row gather
+  bool fz_gather = false;
   unsigned* fz_comb = nullptr;
   unsigned long long* fz_dbg = nullptr;  // LBBSP_FZ_DEBUG: per-CTA stage stamps
   // e2e plumbing: cached host-buffer lookups (lbbsp_mlp_read_result_async,
@@ -1445,13 +1452,17 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   const int sms = D.sm_budget;
   const size_t plan_smem = D.solver == LBBSP_SOLVER_GAMMA ? gamma_plan_smem(n_total) : 0;
   const int gather_ctas = std::max(sms, std::min(sms * 8, (B_cap * (dims[0] / 8) + 1023) / 1024));
+  // the pair kernel reads the batch rows from the dataset itself (tile::gather4)
+  const bool kgather = fused && fused_pair && fz_gather;
   // single rank: the plan waits for the gather on the device (no graph join);
   // set before either kernel is captured, both read it
   // Kernels serialised by a tool (ncu replay, compute-sanitizer) cannot run the
   // gather beside a spinning plan: join with a graph edge there instead.
   const bool join = getenv("LBBSP_GATHER_JOIN") || getenv("CUDA_INJECTION64_PATH");
-  D.gather_ctas = cfg.world == 1 && !join ? gather_ctas : 0;
-  if (cfg.world == 1) {  // one rank gathers all B rows: independent of the plan
+  D.gather_ctas = cfg.world == 1 && !join && !kgather ? gather_ctas : 0;
+  if (kgather) {
+    plan_kernel<<<1, 256, plan_smem, s>>>(D, row_scale);
+  } else if (cfg.world == 1) {  // one rank gathers all B rows: independent of the plan
     LBBSP_CUDA_CHECK(cudaEventRecord(ev_gather0, s));
     LBBSP_CUDA_CHECK(cudaStreamWaitEvent(side, ev_gather0, 0));
     gather_kernel<<<gather_ctas, 256, 0, side>>>(D, streams, B_total, data_x, data_y, dims[0], X, y,
@@ -1468,7 +1479,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
                                       static_cast<const long long*>(reg_off),
                                       static_cast<const long long*>(reg_len), n_reg));
   }
-  nl += 2;
+  nl += kgather ? 1 : 2;
   if (use_pair) {
     zero_dz_tail_kernel<<<8, 256, 0, s>>>(D, dz_ptrs, dz_widths, L, dz_end, B_cap);
     ++nl;
@@ -1499,9 +1510,19 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     fa.timing = phase_slot(ph++);
     fa.status = D.status;
     fa.dbg = fz_dbg;
+    if (kgather) {
+      fa.gather = 1;
+      fa.streams = streams;
+      fa.kptr = D.k;
+      fa.stream_off = D.stream_off;
+      fa.data_y = data_y;
+      fa.B_total = B_total;
+      fa.max_rows = D.max_rows;
+    }
     if (fused_pair)
       LBBSP_CUDA_CHECK(launch_maybe_pdl(c2_pair_worker_kernel, sms & ~1, kFpThreads, kFpSmem, s, use_pdl,
-                                        fz_tm[0], fz_tm[4], fz_tm[2], fz_tm[3], fz_tm[5], fa));
+                                        kgather ? fz_gm[cap_buf] : fz_tm[0], fz_tm[4], fz_tm[2],
+                                        kgather ? fz_gm[cap_buf] : fz_tm[3], fz_tm[5], fa));
     else
       LBBSP_CUDA_CHECK(launch_maybe_pdl(c2_fused_worker_kernel, sms, kFzThreads, kFzSmem, s, use_pdl, fz_tm[0],
                                         fz_tm[1], fz_tm[2], fz_tm[3], fa));
@@ -2153,6 +2174,12 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     // floor(budget * share * availability) exactly, odd counts included, and
     // the pair kernel needs cluster-aligned (even) partitions
     m.fused_pair = !getenv("LBBSP_FUSE_SINGLE") && c.straggler_mode != LBBSP_STRAGGLE_SM_CAP;
+    // in-kernel row gather from the resident dataset (LBBSP_GATHER_KERNEL=1:
+    // the gather kernel writes the batch X / y first, as the other paths do)
+    m.fz_gather = m.fused_pair && !getenv("LBBSP_GATHER_KERNEL");
+    for (int b = 0; b < 2 && m.fz_gather && !rc; ++b)
+      rc = make_tmap_bf16(&m.fz_gm[b], m.data_xb[b], kFzD0, m.N_data, kFzD0, 1);
+    if (rc) return rc;
     D.pair_caps = m.fused_pair ? 1 : 0;
     unsigned* fd = nullptr;
     LBBSP_CUDA_CHECK(m.alloc(&fd, static_cast<size_t>(m.n_local)));

@@ -11,7 +11,8 @@ from paper_1806_02508_b200._lib import lib
 n, B = 8, 4096
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 tr = benchmark_trace(n, 300, seed=3) if os.environ.get("TRACE") == "bench" else constant_trace(n, 300)
-names = ["plan_in", "plan_ready", "gather_in", "obs_in", "obs_out", "reduce_in", "losshead_in", "losshead_out"]
+names = ["plan_in", "plan_ready", "gather_in", "obs_in", "obs_out", "reduce_in", "losshead_in", "losshead_out",
+         "plan_computed", "gather_out", "pred_done", "solve_done", "slices_done"]
 for pred in os.environ.get("PREDS", "ema,narx").split(","):
     eng = MlpEngine(dims=[784, 256, 10], global_batch=B, n_workers_local=n, predictor=pred,
                     warmup_iterations=50, max_iterations=300, trace=tr)
@@ -30,7 +31,7 @@ for pred in os.environ.get("PREDS", "ema,narx").split(","):
         lib().lbbsp_mlp_debug_timeline(C.c_void_p(eng._h.value if hasattr(eng._h, "value") else eng._h),
                                        buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), C.byref(nph))
         t0 = int(buf[0])
-        st_ = {k: round((int(buf[i]) - t0) / 1e3, 1) for i, k in enumerate(names)}
+        st_ = {k: round((int(buf[i]) - t0) / 1e3, 1) for i, k in enumerate(names) if int(buf[i])}
         tim = buf[16:16 + 2 * nph.value * n].astype(np.int64).reshape(nph.value, n, 2)
         ph = [(round((tim[p, :, 0].min() - t0) / 1e3, 1), round((tim[p, :, 1].max() - t0) / 1e3, 1))
               for p in range(nph.value)]

@@ -19,12 +19,14 @@ pytestmark = pytest.mark.gpu
 
 
 def _run(static, rounds, mode, predictor="ema", trace=None, sm_budget=0):
-    """mode: 'pair' (default kernel), 'single' (LBBSP_FUSE_SINGLE), 'separate'
+    """mode: 'pair' (default kernel, rows gathered in-kernel by tile::gather4),
+    'pair_gk' (pair kernel over the batch the gather kernel wrote,
+    LBBSP_GATHER_KERNEL), 'single' (LBBSP_FUSE_SINGLE), 'separate'
     (LBBSP_NO_FUSE). Returns (initial params, final params, records)."""
     from paper_1806_02508_b200.mlp import MlpEngine, constant_trace
     n = len(static)
-    env = {"single": "LBBSP_FUSE_SINGLE", "separate": "LBBSP_NO_FUSE"}.get(mode)
-    saved = {k: os.environ.pop(k, None) for k in ("LBBSP_FUSE_SINGLE", "LBBSP_NO_FUSE")}
+    env = {"single": "LBBSP_FUSE_SINGLE", "separate": "LBBSP_NO_FUSE", "pair_gk": "LBBSP_GATHER_KERNEL"}.get(mode)
+    saved = {k: os.environ.pop(k, None) for k in ("LBBSP_FUSE_SINGLE", "LBBSP_NO_FUSE", "LBBSP_GATHER_KERNEL")}
     if env:
         os.environ[env] = "1"
     try:
@@ -86,3 +88,55 @@ def test_fused_under_interference_and_small_budget():
     rec = eng.records()
     assert (rec["sizes"].sum(axis=1) == B).all()
     assert rec["loss"][-1] < rec["loss"][0]
+
+
+@pytest.mark.parametrize("static", SIZES)
+def test_pair_in_kernel_gather_equals_gather_kernel_bitwise(static):
+    """tile::gather4 rows straight from the dataset land in shared memory in
+    the same swizzled layout as the TMA tile of the gathered batch: weights
+    and losses bitwise equal to the pair kernel fed by the gather kernel."""
+    _, a, ra = _run(static, 6, "pair")
+    _, b, rb = _run(static, 6, "pair_gk")
+    assert np.array_equal(a, b), float(np.max(np.abs(a - b)))
+    assert np.array_equal(ra["loss"], rb["loss"])
+
+
+def test_pair_in_kernel_gather_dynamic_sizes_and_e2e_buffers():
+    """LB-BSP + NARX dynamic sizes under interference, then end-to-end steps
+    that alternate the two dataset buffers (each graph gathers from its own):
+    bitwise equal to the gather-kernel path over the same rounds."""
+    import torch
+    from paper_1806_02508_b200.mlp import MlpEngine, benchmark_trace
+    from paper_1806_02508_b200.hostio import pinned_empty
+    n, B, R = 8, 4096, 40
+    out = []
+    for gk in (False, True):
+        saved = os.environ.pop("LBBSP_GATHER_KERNEL", None)
+        if gk:
+            os.environ["LBBSP_GATHER_KERNEL"] = "1"
+        try:
+            eng = MlpEngine(dims=[784, 256, 10], global_batch=B, n_workers_local=n, predictor="narx",
+                            warmup_iterations=10, learning_rate=0.05, seed=1, max_iterations=R + 12,
+                            trace=benchmark_trace(n, R + 12, seed=3))
+        finally:
+            os.environ.pop("LBBSP_GATHER_KERNEL", None)
+            if saved is not None:
+                os.environ["LBBSP_GATHER_KERNEL"] = saved
+        eng.run(R)
+        x, y = eng.dataset()
+        xb = pinned_empty(x.shape, torch.bfloat16, 0)
+        xb.copy_(torch.from_numpy(x).to(torch.bfloat16))
+        yb = pinned_empty(y.shape, torch.int32, 0)
+        yb.copy_(torch.from_numpy(y.astype(np.int32)))
+        osz = pinned_empty((n,), torch.int32, 0)
+        ol = pinned_empty((1,), torch.float64, 0)
+        for _ in range(8):
+            eng.step_e2e(xb.data_ptr(), yb.data_ptr(), osz.data_ptr(), ol.data_ptr())
+        torch.cuda.synchronize()
+        rec = eng.records()
+        out.append((np.concatenate([np.concatenate([w.ravel(), b]) for w, b in eng.params()]),
+                    rec["sizes"].copy(), rec["loss"].copy()))
+        del eng
+    assert np.array_equal(out[0][1], out[1][1])
+    assert np.array_equal(out[0][0], out[1][0]), float(np.max(np.abs(out[0][0] - out[1][0])))
+    assert np.array_equal(out[0][2], out[1][2])

@@ -204,6 +204,16 @@ struct PlanDev {
   int straggler_mode;          // LBBSP_STRAGGLE_INTERFERE | LBBSP_STRAGGLE_SM_CAP
   int solver;                  // LBBSP_SOLVER_PROPORTIONAL | LBBSP_SOLVER_GAMMA
   int observe;                 // LBBSP_OBSERVE_RATE | LBBSP_OBSERVE_CAPACITY (proportional solver)
+  // next-round predictions made by the observe branch (the models, histories
+  // and EMA states are final there, and hot): v_next[w] is what the plan of
+  // round *vnext_k would compute for worker w, bit for bit
+  double* v_next;              // [n_total]
+  double* nx_c;                // [n_total] trace c, m and availability of round *vnext_k
+  double* nx_m;
+  double* nx_a;
+  float2* nx_intf;             // [n_local] interference weights of round *vnext_k
+  long long* vnext_k;          // the round v_next is for (-1: none)
+  unsigned long long* obs_seq; // rounds whose observe (history push, EMA) is complete
   const lbbsp_gpu_profile* prof0;  // [n_total] unloaded Gamma profiles (GAMMA solver, CAPACITY)
   float2* intf_w;              // [n_local] {availability, HBM share of the injected time}
   unsigned* fz_done;           // [n_local] fused worker kernel: head CTAs done (zeroed here)
@@ -249,7 +259,49 @@ __device__ __forceinline__ bool wait_gather(const PlanDev& D, long long k) {
 // P1-P4: trace -> caps, predictor -> v_pred, solver -> sizes, local slice,
 // plus the Eq. 6/7 row scales of this rank's rows. Everything thread 0 walks
 // sequentially lives in shared memory (no dependent global round trips).
-__global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) {
+// Worker i's straggler state in round kk: trace (c, m), availability
+// a = min(1, c * MemPenalty(m) * mult) (effective_speed * speed_mult,
+// cluster_sim.cpp:22-29) and, in interference mode, the weights interfere.cuh
+// injects (the part of the injected time the memory penalty adds,
+// 1/a - 1/a_sm with a_sm = min(1, c mult), is HBM-bound, the rest SM-bound).
+struct WorkerRound {
+  double c, m, a;
+  float2 intf;
+};
+__device__ inline WorkerRound worker_round(const PlanDev& D, int i, long long kk) {
+  const long long ti = kk < D.trace_len - 1 ? kk : D.trace_len - 1;
+  const size_t o = static_cast<size_t>(i) * D.trace_len + ti;
+  WorkerRound r;
+  r.c = D.trace_c[o];
+  r.m = D.trace_m[o];
+  const double mult = D.trace_mult[o];
+  const double pen = r.m >= 0.5 ? 1.0 : dadd(0.25, dmul(0.75, ddiv(r.m, 0.5)));
+  const double a = dmul(dmul(r.c, pen), mult);
+  r.a = a < 1.0 ? a : 1.0;
+  r.intf = make_float2(1.f, 0.f);
+  if (D.straggler_mode == LBBSP_STRAGGLE_INTERFERE) {
+    const double asm_ = fmin(1.0, r.c * mult), at = r.a;
+    const double hbm = at < 1.0 ? fmax(0.0, fmin(1.0, (1.0 / at - 1.0 / asm_) / (1.0 / at - 1.0))) : 0.0;
+    r.intf = make_float2(static_cast<float>(at), static_cast<float>(hbm));
+  }
+  return r;
+}
+
+// The observe branch's look-ahead for round kk = k + 1 (history length len
+// after this round's push): every worker's straggler state and, for the
+// workers in `mine` (all but the ones a training CTA predicts itself), the
+// plan's prediction (Perfect: the availability, cluster_sim.cpp:362-367).
+__device__ inline void look_ahead(const PlanDev& D, int i, long long kk, int len, bool predict) {
+  const WorkerRound r = worker_round(D, i, kk);
+  D.nx_c[i] = r.c;
+  D.nx_m[i] = r.m;
+  D.nx_a[i] = r.a;
+  const int li = i - D.rank * D.n_local;
+  if (li >= 0 && li < D.n_local) D.nx_intf[li] = r.intf;
+  if (predict) D.v_next[i] = D.pred.kind == LBBSP_PRED_PERFECT ? r.a : predictor_predict_d(D.pred, i, len, r.c, r.m);
+}
+
+__device__ __forceinline__ void plan_body(const PlanDev& D, float* row_scale) {
   tc::pdl_launch_dependents();  // the forward GEMM's prologue may start now
   __shared__ SolverSmem sm;
   __shared__ double rem[LBBSP_MAX_WORKERS];
@@ -262,40 +314,48 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
   stamp(D, 0);
   const long long k = *D.k;
   const int len = min(*D.pred.len, D.pred.max_hist);
+  const long long vk = *D.vnext_k;
   // scalars needed later, loaded now beside k (no dependent round trips later)
-  const int rows_now = *D.rows;
-  const double loss_prev = tid == 0 && D.loss_on ? *D.loss_acc : 0.0;
+  __shared__ int rows_s;
+  __shared__ double loss_prev_s;
+  if (tid == 0) {
+    rows_s = *D.rows;
+    loss_prev_s = D.loss_on ? *D.loss_acc : 0.0;
+  }
   if (tid == 0) *D.round_k = k;
   if (k >= D.max_rows && tid == 0)
     set_status(D.status, LBBSP_RUNTIME, LBBSP_E_MLP_CAPACITY, k, D.max_rows);
-  const long long ti = k < D.trace_len - 1 ? k : D.trace_len - 1;
+  // Per worker: trace state, availability, interference weights and the
+  // prediction. The observe branch of the last round computed all of them
+  // for this round (vk == k: look_ahead, the same calls on the same state),
+  // so the usual path only moves them -- a round's first instructions come
+  // from DRAM after the L2 flush, and this kernel's latency is mostly fetch.
   for (int i = tid; i < n; i += blockDim.x) {
-    const size_t o = static_cast<size_t>(i) * D.trace_len + ti;
-    const double c = D.trace_c[o], m = D.trace_m[o], mult = D.trace_mult[o];
     share_s[i] = D.share[i];
+    double c, m, a, vp;
+    float2 iw = make_float2(1.f, 0.f);
+    if (vk == k) {
+      c = D.nx_c[i];
+      m = D.nx_m[i];
+      a = D.nx_a[i];
+      vp = len >= 1 ? D.v_next[i] : 0.0;
+    } else {
+      const WorkerRound r = worker_round(D, i, k);
+      c = r.c;
+      m = r.m;
+      a = r.a;
+      iw = r.intf;
+      // Perfect (step_sync: v_pred = v_actual, cluster_sim.cpp:362-367): the
+      // worker's true relative speed this round is its injected availability
+      vp = D.pred.kind == LBBSP_PRED_PERFECT ? a : (len >= 1 ? predictor_predict_d(D.pred, i, len, c, m) : 0.0);
+    }
     D.c_now[i] = c;
     D.m_now[i] = m;
-    // availability = the worker's relative speed in the reference model,
-    // effective_speed * speed_mult = c * MemPenalty(m) * mult (cluster_sim.cpp:22-29),
-    // capped at 1
-    const double pen = m >= 0.5 ? 1.0 : dadd(0.25, dmul(0.75, ddiv(m, 0.5)));
-    const double a = dmul(dmul(c, pen), mult);
-    avail[i] = a < 1.0 ? a : 1.0;
+    avail[i] = a;
     if (D.straggler_mode == LBBSP_STRAGGLE_INTERFERE) {
       const int li = i - D.rank * D.n_local;
-      if (li >= 0 && li < D.n_local) {
-        // interference (interfere.cuh): the phase lasts work / a; the part of
-        // the injected time the memory penalty adds (1/a - 1/a_sm, a_sm =
-        // min(1, c mult)) is HBM-bound, the rest SM-bound
-        const double asm_ = fmin(1.0, c * mult), at = avail[i];
-        const double hbm = at < 1.0 ? fmax(0.0, fmin(1.0, (1.0 / at - 1.0 / asm_) / (1.0 / at - 1.0))) : 0.0;
-        D.intf_w[li] = make_float2(static_cast<float>(at), static_cast<float>(hbm));
-      }
+      if (li >= 0 && li < D.n_local) D.intf_w[li] = vk == k ? D.nx_intf[li] : iw;
     }
-    // Perfect (step_sync: v_pred = v_actual, cluster_sim.cpp:362-367): the
-    // worker's true relative speed this round is its injected availability
-    const double vp = D.pred.kind == LBBSP_PRED_PERFECT ? avail[i]
-                      : (len >= 1 ? predictor_predict_d(D.pred, i, len, c, m) : 0.0);
     vp_s[i] = vp;
     D.v_pred[i] = vp;
   }
@@ -369,9 +429,9 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
     r0_s[D.n_local] = r;
     *D.local_rows = r;
     // the previous round's full-dataset loss (computed beside its observe branch)
-    const int prev = rows_now - 1;
+    const int prev = rows_s - 1;
     if (prev >= 0 && prev < D.max_rows)
-      D.rec_loss[prev] = D.loss_on ? loss_prev / static_cast<double>(D.N_data) : -1.0;
+      D.rec_loss[prev] = D.loss_on ? loss_prev_s / static_cast<double>(D.N_data) : -1.0;
     *D.loss_acc = 0.0;
   }
   for (int i = tid; i < kMaxPhases * D.n_local; i += blockDim.x) {
@@ -398,7 +458,7 @@ __global__ void __launch_bounds__(256) plan_kernel(PlanDev D, float* row_scale) 
       for (int r = r0_s[g] + tid; r < r0_s[g + 1]; r += blockDim.x) row_scale[r] = s;
     }
   }
-  const int row = rows_now;
+  const int row = rows_s;
   if (row < D.max_rows) {
     for (int i = tid; i < n; i += blockDim.x) {
       D.rec_sizes[static_cast<size_t>(row) * n + i] = sz[i];
@@ -421,19 +481,24 @@ static size_t gamma_plan_smem(int n) {
   return static_cast<size_t>(n) * sizeof(lbbsp_gpu_profile) + static_cast<size_t>(n) * 8 * 5 + 64;
 }
 
+__global__ void __launch_bounds__(256) plan_kernel(const __grid_constant__ PlanDev D, float* row_scale) {
+  plan_body(D, row_scale);
+}
+
 // P6: X[r] = data[stream[off + r]], labels, row scale (Eq. 7: 1/B; Eq. 6: 1/(n b_i))
 // fixed_rows > 0: a single rank gathers the whole batch [0, B) of stream k,
-// which does not depend on the plan, so it runs beside plan_kernel.
-__global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const bf16* data_x,
-                              const int* data_y, int d0, bf16* X, int* y, int fixed_rows,
-                              float* slab, long long slab_stride, const long long* reg_off,
-                              const long long* reg_len, int n_reg) {
-  stamp(D, 2);
+// which does not depend on the plan, so it runs beside the plan (the blocks
+// 1.. of plan_gather_kernel). Block bid of nblk.
+__device__ __forceinline__ void gather_body(const PlanDev& D, const int* streams, int B_total, const bf16* data_x,
+                                            const int* data_y, int d0, bf16* X, int* y, int fixed_rows,
+                                            float* slab, long long slab_stride, const long long* reg_off,
+                                            const long long* reg_len, int n_reg, int bid, int nblk) {
+  if (threadIdx.x == 0 && bid == 0) D.stamps[2] = gtimer();
   // zero the partial regions accumulated with atomics (biases, small head)
   for (int sl = 0; sl < D.n_local; ++sl)
     for (int rg = 0; rg < n_reg; ++rg) {
       float* p = slab + sl * slab_stride + reg_off[rg];
-      for (long long i = blockIdx.x * 256ll + threadIdx.x; i < reg_len[rg]; i += 256ll * gridDim.x)
+      for (long long i = bid * 256ll + threadIdx.x; i < reg_len[rg]; i += 256ll * nblk)
         p[i] = 0.f;
     }
   // several ranks: the slice offset and length come from the plan (programmatic
@@ -446,11 +511,11 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
   const int* idx = streams + static_cast<size_t>(k) * B_total + off;
   const int vec = d0 / 8;  // 16-byte chunks per row
   const int total = rows * vec;
-  const int step = 256 * gridDim.x;
+  const int step = 256 * nblk;
   const uint4* src4 = reinterpret_cast<const uint4*>(data_x);
   uint4* dst4 = reinterpret_cast<uint4*>(X);
   // four independent row reads in flight per thread
-  for (int t0 = blockIdx.x * 256 + threadIdx.x; t0 < total; t0 += 4 * step) {
+  for (int t0 = bid * 256 + threadIdx.x; t0 < total; t0 += 4 * step) {
     uint4 v[4];
     int dsti[4];
 #pragma unroll
@@ -467,7 +532,7 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
     for (int u = 0; u < 4; ++u)
       if (dsti[u] >= 0) dst4[dsti[u]] = v[u];
   }
-  for (int r = blockIdx.x * 256 + threadIdx.x; r < rows; r += 256 * gridDim.x) y[r] = data_y[idx[r]];
+  for (int r = bid * 256 + threadIdx.x; r < rows; r += 256 * nblk) y[r] = data_y[idx[r]];
   if (D.stamps && threadIdx.x == 0) atomicMax(&D.stamps[9], static_cast<unsigned long long>(gtimer()));
   if (fixed_rows > 0 && D.gather_ctas > 0) {  // tell the plan (see plan_kernel)
     __syncthreads();
@@ -476,6 +541,40 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
       atomicAdd(D.gather_done, 1ull);
     }
   }
+}
+
+__global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const bf16* data_x,
+                              const int* data_y, int d0, bf16* X, int* y, int fixed_rows,
+                              float* slab, long long slab_stride, const long long* reg_off,
+                              const long long* reg_len, int n_reg) {
+  gather_body(D, streams, B_total, data_x, data_y, d0, X, y, fixed_rows, slab, slab_stride, reg_off, reg_len,
+              n_reg, blockIdx.x, gridDim.x);
+}
+
+// Single rank: block 0 plans the round, blocks 1.. gather its batch -- one
+// launch, so the two run side by side (as two graph roots the plan started
+// only once the gather had finished: 6.6 us on the round's critical path).
+struct GatherArgs {
+  const int* streams;
+  int B_total;
+  const bf16* data_x;
+  const int* data_y;
+  int d0;
+  bf16* X;
+  int* y;
+  float* slab;
+  long long slab_stride;
+  const long long* reg_off;
+  const long long* reg_len;
+  int n_reg;
+};
+__global__ void __launch_bounds__(256) plan_gather_kernel(const __grid_constant__ PlanDev D, float* row_scale,
+                                                          const __grid_constant__ GatherArgs a) {
+  if (blockIdx.x == 0)
+    plan_body(D, row_scale);
+  else
+    gather_body(D, a.streams, a.B_total, a.data_x, a.data_y, a.d0, a.X, a.y, a.B_total, a.slab, a.slab_stride,
+                a.reg_off, a.reg_len, a.n_reg, blockIdx.x - 1, gridDim.x - 1);
 }
 
 __device__ __forceinline__ unsigned long long phase_begin(unsigned long long* timing, int g) {
@@ -885,6 +984,15 @@ __device__ inline double observed_speed(const PlanDev& D, int w, int b, double t
   return t > 0.0 ? static_cast<double>(b) / t : static_cast<double>(b);
 }
 
+// The plan's prediction for worker w in round kk (history length len >= 1):
+// SpeedPredictor::predict (predictor.cpp:271-292) on the trace's (c, m) of
+// round kk -- the same call plan_body makes.
+__device__ inline double predict_for_round(const PlanDev& D, int w, int len, long long kk) {
+  const long long ti = kk < D.trace_len - 1 ? kk : D.trace_len - 1;
+  const size_t o = static_cast<size_t>(w) * D.trace_len + ti;
+  return predictor_predict_d(D.pred, w, len, D.trace_c[o], D.trace_m[o]);
+}
+
 // measured per-worker compute time -> observed speed
 __global__ void speed_kernel(PlanDev D, int n_phases) {
   const int i = threadIdx.x;
@@ -920,9 +1028,11 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
   const int n = D.n_total, tid = threadIdx.x;
   if (static_cast<int>(blockIdx.x) < nb) {
     __shared__ int len_s, w_s;
+    __shared__ long long k_s;
     if (tid == 0) {
       len_s = *D.pred.len;
       w_s = (*D.pred.cursor + static_cast<int>(blockIdx.x)) % n;
+      k_s = *D.k;
       __threadfence();
       atomicAdd(arrive, 1u);
     }
@@ -945,9 +1055,20 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
     cfg.min_history = D.pred.warmup;
     narx_train_block(&D.pred.models[w], D.pred.hv + o, D.pred.hc + o, D.pred.hm + o, L, cfg,
                      &D.pred.reports[w], nullptr, 0, buf, nd, &ts);
+    // the next round's prediction with the model just trained (after the
+    // observe CTA's EMA / history push, which an EMA fallback reads)
+    if (tid == 0) {
+      unsigned long long seen;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(seen) : "l"(D.obs_seq) : "memory");
+      } while (seen < static_cast<unsigned long long>(k_s + 1));
+      D.v_next[w] = predict_for_round(D, w, L, k_s + 1);
+    }
     return;
   }
   if (tid == 0) D.stamps[3] = gtimer();
+  const long long k_obs = *D.k;
+  const int cursor0 = *D.pred.cursor;
   if (fused_speed_phases > 0) {  // single rank: measured speeds computed here
     for (int i = tid; i < D.n_local; i += blockDim.x) {
       double t;
@@ -965,9 +1086,20 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
   }
   __syncthreads();
   if (tid == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(D.obs_seq),
+                 "l"(static_cast<unsigned long long>(k_obs + 1))
+                 : "memory");
+  }
+  // next-round predictions of the models not trained this round
+  const int Ln = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
+  for (int i = tid; i < n; i += blockDim.x) look_ahead(D, i, k_obs + 1, Ln, (i - cursor0 + n) % n >= nb);
+  __syncthreads();
+  if (tid == 0) {
     while (atomicAdd(arrive, 0u) < static_cast<unsigned>(nb)) {
     }
     *arrive = 0u;
+    *D.vnext_k = k_obs + 1;
     *D.pred.len = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
     *D.train_first = *D.pred.cursor;
     *D.pred.cursor = (*D.pred.cursor + (n + 1) / 2) % n;
@@ -993,12 +1125,19 @@ __global__ void observe_kernel(PlanDev D, int fused_speed_phases) {
   }
   const int len = *D.pred.len;
   const int row = *D.rows;
+  const long long k_obs = *D.k;
+  // next-round predictions (not for NARX: its rotation trains after this kernel)
+  const bool ahead = D.pred.kind != LBBSP_PRED_NARX;
+  const int Ln = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
   for (int i = threadIdx.x; i < D.n_total; i += blockDim.x) {
     observe_d(D.pred, i, len, D.v_obs_all[i], D.c_now[i], D.m_now[i], 0.0);
     if (row < D.max_rows) D.rec_vobs[static_cast<size_t>(row) * D.n_total + i] = D.v_obs_all[i];
+    // (EMA / memoryless read only this worker's state, written just above)
+    if (ahead) look_ahead(D, i, k_obs + 1, Ln, true);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (ahead) *D.vnext_k = k_obs + 1;
     *D.pred.len = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
     *D.train_first = *D.pred.cursor;
     *D.pred.cursor = (*D.pred.cursor + (D.n_total + 1) / 2) % D.n_total;
@@ -1462,6 +1601,9 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   D.gather_ctas = cfg.world == 1 && !join && !kgather ? gather_ctas : 0;
   if (kgather) {
     plan_kernel<<<1, 256, plan_smem, s>>>(D, row_scale);
+  } else if (cfg.world == 1 && !join) {  // plan + gather of all B rows in one launch
+    GatherArgs ga{streams, B_total, data_x, data_y, dims[0], X, y, partial, P, reg_off, reg_len, n_reg};
+    plan_gather_kernel<<<1 + gather_ctas, 256, plan_smem, s>>>(D, row_scale, ga);
   } else if (cfg.world == 1) {  // one rank gathers all B rows: independent of the plan
     LBBSP_CUDA_CHECK(cudaEventRecord(ev_gather0, s));
     LBBSP_CUDA_CHECK(cudaStreamWaitEvent(side, ev_gather0, 0));
@@ -1479,7 +1621,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
                                       static_cast<const long long*>(reg_off),
                                       static_cast<const long long*>(reg_len), n_reg));
   }
-  nl += kgather ? 1 : 2;
+  nl += kgather || (cfg.world == 1 && !join) ? 1 : 2;
   if (use_pair) {
     zero_dz_tail_kernel<<<8, 256, 0, s>>>(D, dz_ptrs, dz_widths, L, dz_end, B_cap);
     ++nl;
@@ -1986,6 +2128,14 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   LBBSP_CUDA_CHECK(m.alloc(&D.loss_acc, 1));
   LBBSP_CUDA_CHECK(m.alloc(&D.stamps, 16));
   LBBSP_CUDA_CHECK(m.alloc(&D.round_k, 1));
+  LBBSP_CUDA_CHECK(m.alloc(&D.v_next, n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.nx_c, n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.nx_m, n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.nx_a, n));
+  LBBSP_CUDA_CHECK(m.alloc(&D.nx_intf, m.n_local));
+  LBBSP_CUDA_CHECK(m.alloc(&D.vnext_k, 1));
+  LBBSP_CUDA_CHECK(cudaMemset(D.vnext_k, 0xff, sizeof(long long)));  // -1
+  LBBSP_CUDA_CHECK(m.alloc(&D.obs_seq, 1));
   if (c.straggler_mode != LBBSP_STRAGGLE_INTERFERE && c.straggler_mode != LBBSP_STRAGGLE_SM_CAP)
     return set_error(LBBSP_INVALID_ARGUMENT, "mlp: unknown straggler_mode %d", c.straggler_mode);
   D.straggler_mode = c.straggler_mode;
@@ -2003,9 +2153,12 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     LBBSP_CUDA_CHECK(m.upload(&pr, c.h_gpu_profiles, static_cast<size_t>(n)));
     D.prof0 = pr;
   }
-  if (c.solver == LBBSP_SOLVER_GAMMA)
+  if (c.solver == LBBSP_SOLVER_GAMMA) {
     LBBSP_CUDA_CHECK(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(gamma_plan_smem(n))));
+    LBBSP_CUDA_CHECK(cudaFuncSetAttribute(plan_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(gamma_plan_smem(n))));
+  }
   if (c.straggler_mode == LBBSP_STRAGGLE_INTERFERE) {
     float2* w = nullptr;
     LBBSP_CUDA_CHECK(m.alloc(&w, m.n_local));
@@ -2174,9 +2327,11 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     // floor(budget * share * availability) exactly, odd counts included, and
     // the pair kernel needs cluster-aligned (even) partitions
     m.fused_pair = !getenv("LBBSP_FUSE_SINGLE") && c.straggler_mode != LBBSP_STRAGGLE_SM_CAP;
-    // in-kernel row gather from the resident dataset (LBBSP_GATHER_KERNEL=1:
-    // the gather kernel writes the batch X / y first, as the other paths do)
-    m.fz_gather = m.fused_pair && !getenv("LBBSP_GATHER_KERNEL");
+    // in-kernel row gather from the resident dataset, opt-in (LBBSP_KGATHER=1):
+    // bitwise the same round, but 32 tile::gather4 requests per 16 KB stage
+    // run the worker phase at 50 us against 21 us from the gathered batch
+    // (profiles/r02_kgather.txt) -- the TMA unit's request rate, not bytes
+    m.fz_gather = m.fused_pair && getenv("LBBSP_KGATHER");
     for (int b = 0; b < 2 && m.fz_gather && !rc; ++b)
       rc = make_tmap_bf16(&m.fz_gm[b], m.data_xb[b], kFzD0, m.N_data, kFzD0, 1);
     if (rc) return rc;

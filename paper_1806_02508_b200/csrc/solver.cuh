@@ -57,12 +57,100 @@ __device__ __forceinline__ int warp_first_max(const int* sizes, int n) {
   return best;
 }
 
+// min-1 repair (batch_sizer.cpp:90-97) by warp 0: sequential over i, the
+// deficit taken from the first maximum. Returns false if impossible.
+__device__ inline bool warp_min1_repair(int* sizes, int n) {
+  const int tid = threadIdx.x;
+  int need = 0;
+  for (int i = tid; i < n; i += 32) need |= sizes[i] < 1;
+  need = __any_sync(0xffffffffu, need);
+  if (!need) return true;
+  for (int i = 0; i < n; ++i) {
+    __syncwarp();
+    int xi = sizes[i];
+    while (xi < 1) {
+      const int big = warp_first_max(sizes, n);
+      if (sizes[big] <= 1) return false;  // warp-uniform
+      __syncwarp();
+      if (tid == 0) {
+        sizes[big] -= 1;
+        sizes[i] += 1;
+      }
+      __syncwarp();
+      xi = sizes[i];
+    }
+  }
+  return true;
+}
+
+// cpu_allocate for n <= 32 in warp 0 (the plan's case): one lane per worker,
+// the left-to-right sum formed redundantly in every lane from shuffled
+// values (the same dadd sequence), the largest-remainder rank by shuffles --
+// no shared-memory round trips or block barriers on the way, and rolled
+// loops: the plan runs once per round from a cold instruction cache, so its
+// latency follows its code size.
+__device__ inline int warp_cpu_allocate(const double* speeds, int n, int budget, double speed_floor, int* sizes,
+                                        SolverSmem* sm, lbbsp_dev_status* st) {
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    const unsigned full = 0xffffffffu;
+    int code = 0, what = 0;
+    double v = 1.0;
+    if (tid < n) {
+      v = speeds[tid];
+      if (speed_floor > 0.0) v = v > speed_floor ? v : speed_floor;
+    }
+    if (budget < n) {
+      code = LBBSP_INVALID_ARGUMENT;
+      what = LBBSP_E_CPU_BUDGET;
+    } else if (__ballot_sync(full, tid < n && !(v > 0.0))) {
+      code = LBBSP_INVALID_ARGUMENT;
+      what = LBBSP_E_CPU_SPEED;
+    }
+    if (!code) {
+      double sum = 0.0;  // batch_sizer.cpp:60-64, left to right
+#pragma unroll 1
+      for (int i = 0; i < n; ++i) sum = dadd(sum, __shfl_sync(full, v, i));
+      const double share = dmul(ddiv(v, sum), static_cast<double>(budget));  // :72-73
+      const double fl = floor(share);
+      const int sz = static_cast<int>(fl);
+      const double r = dsub(share, fl);
+      const int extra = budget - __reduce_add_sync(full, tid < n ? sz : 0);
+      // largest remainder, ties to the lower index (:81-87)
+      int rank = 0;
+#pragma unroll 1
+      for (int j = 0; j < n; ++j) {
+        const double rj = __shfl_sync(full, r, j);
+        rank += (rj > r) || (rj == r && j < tid);
+      }
+      if (tid < n) sizes[tid] = sz + (rank < extra ? 1 : 0);
+      __syncwarp();
+      if (!warp_min1_repair(sizes, n)) {
+        code = LBBSP_LOGIC;
+        what = LBBSP_E_CPU_MIN1;
+      }
+    }
+    if (tid == 0) {
+      sm->code = code;
+      if (code) {
+        sm->what = what;
+        sm->a = what == LBBSP_E_CPU_BUDGET ? budget : 0;
+        sm->b = what == LBBSP_E_CPU_BUDGET ? n : 0;
+        set_status(st, code, what, sm->a, sm->b);
+      }
+    }
+  }
+  __syncthreads();
+  return sm->code;
+}
+
 // speeds: [n] (global or shared). sizes: [n] output (shared or global).
 // rem: [n] shared scratch. Returns 0 or a status code (also written to st).
 __device__ inline int block_cpu_allocate(const double* speeds, int n, int budget, double speed_floor,
                                   int* sizes, double* rem, SolverSmem* sm,
                                   lbbsp_dev_status* st) {
   const int tid = threadIdx.x, nt = blockDim.x;
+  if (n >= 1 && n <= 32 && nt >= 32) return warp_cpu_allocate(speeds, n, budget, speed_floor, sizes, sm, st);
   if (tid == 0) {
     sm->code = 0;
     sm->assigned = 0;

@@ -19,7 +19,9 @@ for pred in os.environ.get("PREDS", "ema,narx").split(","):
     st = torch.cuda.ExternalStream(eng.stream)
     eng.run(100)
     for rep in range(5):
-        flush.zero_(); torch.cuda.synchronize()
+        if not os.environ.get("NOFLUSH"):
+            flush.zero_()
+        torch.cuda.synchronize()
         s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(st):
             s.record(st)

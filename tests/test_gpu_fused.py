@@ -19,14 +19,14 @@ pytestmark = pytest.mark.gpu
 
 
 def _run(static, rounds, mode, predictor="ema", trace=None, sm_budget=0):
-    """mode: 'pair' (default kernel, rows gathered in-kernel by tile::gather4),
-    'pair_gk' (pair kernel over the batch the gather kernel wrote,
-    LBBSP_GATHER_KERNEL), 'single' (LBBSP_FUSE_SINGLE), 'separate'
-    (LBBSP_NO_FUSE). Returns (initial params, final params, records)."""
+    """mode: 'pair' (default kernel over the gathered batch), 'pair_kg' (pair
+    kernel gathering the rows itself by tile::gather4, LBBSP_KGATHER),
+    'single' (LBBSP_FUSE_SINGLE), 'separate' (LBBSP_NO_FUSE). Returns
+    (initial params, final params, records)."""
     from paper_1806_02508_b200.mlp import MlpEngine, constant_trace
     n = len(static)
-    env = {"single": "LBBSP_FUSE_SINGLE", "separate": "LBBSP_NO_FUSE", "pair_gk": "LBBSP_GATHER_KERNEL"}.get(mode)
-    saved = {k: os.environ.pop(k, None) for k in ("LBBSP_FUSE_SINGLE", "LBBSP_NO_FUSE", "LBBSP_GATHER_KERNEL")}
+    env = {"single": "LBBSP_FUSE_SINGLE", "separate": "LBBSP_NO_FUSE", "pair_kg": "LBBSP_KGATHER"}.get(mode)
+    saved = {k: os.environ.pop(k, None) for k in ("LBBSP_FUSE_SINGLE", "LBBSP_NO_FUSE", "LBBSP_KGATHER")}
     if env:
         os.environ[env] = "1"
     try:
@@ -95,33 +95,35 @@ def test_pair_in_kernel_gather_equals_gather_kernel_bitwise(static):
     """tile::gather4 rows straight from the dataset land in shared memory in
     the same swizzled layout as the TMA tile of the gathered batch: weights
     and losses bitwise equal to the pair kernel fed by the gather kernel."""
-    _, a, ra = _run(static, 6, "pair")
-    _, b, rb = _run(static, 6, "pair_gk")
+    _, a, ra = _run(static, 6, "pair_kg")
+    _, b, rb = _run(static, 6, "pair")
     assert np.array_equal(a, b), float(np.max(np.abs(a - b)))
     assert np.array_equal(ra["loss"], rb["loss"])
 
 
 def test_pair_in_kernel_gather_dynamic_sizes_and_e2e_buffers():
-    """LB-BSP + NARX dynamic sizes under interference, then end-to-end steps
-    that alternate the two dataset buffers (each graph gathers from its own):
-    bitwise equal to the gather-kernel path over the same rounds."""
+    """LB-BSP sizes that change every round (Perfect predictor over the
+    benchmark trace: deterministic, so both runs see the same sizes) under
+    interference, then end-to-end steps that alternate the two dataset
+    buffers (each graph gathers from its own): bitwise equal to the
+    gather-kernel path over the same rounds."""
     import torch
     from paper_1806_02508_b200.mlp import MlpEngine, benchmark_trace
     from paper_1806_02508_b200.hostio import pinned_empty
     n, B, R = 8, 4096, 40
     out = []
-    for gk in (False, True):
-        saved = os.environ.pop("LBBSP_GATHER_KERNEL", None)
-        if gk:
-            os.environ["LBBSP_GATHER_KERNEL"] = "1"
+    for kg in (True, False):
+        saved = os.environ.pop("LBBSP_KGATHER", None)
+        if kg:
+            os.environ["LBBSP_KGATHER"] = "1"
         try:
-            eng = MlpEngine(dims=[784, 256, 10], global_batch=B, n_workers_local=n, predictor="narx",
-                            warmup_iterations=10, learning_rate=0.05, seed=1, max_iterations=R + 12,
+            eng = MlpEngine(dims=[784, 256, 10], global_batch=B, n_workers_local=n, predictor="perfect",
+                            learning_rate=0.05, seed=1, max_iterations=R + 12,
                             trace=benchmark_trace(n, R + 12, seed=3))
         finally:
-            os.environ.pop("LBBSP_GATHER_KERNEL", None)
+            os.environ.pop("LBBSP_KGATHER", None)
             if saved is not None:
-                os.environ["LBBSP_GATHER_KERNEL"] = saved
+                os.environ["LBBSP_KGATHER"] = saved
         eng.run(R)
         x, y = eng.dataset()
         xb = pinned_empty(x.shape, torch.bfloat16, 0)

@@ -35,6 +35,7 @@
 #include "solver.cuh"
 #include "c2_fused.cuh"
 #include "c2_fused_pair.cuh"
+#include "c2_fused_quad.cuh"
 
 namespace lbbsp {
 
@@ -217,7 +218,7 @@ struct PlanDev {
   const lbbsp_gpu_profile* prof0;  // [n_total] unloaded Gamma profiles (GAMMA solver, CAPACITY)
   float2* intf_w;              // [n_local] {availability, HBM share of the injected time}
   unsigned* fz_done;           // [n_local] fused worker kernel: head CTAs done (zeroed here)
-  int pair_caps;               // worker CTA partitions cluster-aligned (even) for the pair kernel
+  int cap_align;               // worker CTA partitions cluster-aligned: 2 (pair kernel), 4 (quad), else 1
   int gather_ctas;             // > 0: the plan completes only once they all have
 };
 
@@ -420,7 +421,7 @@ __device__ __forceinline__ void plan_body(const PlanDev& D, float* row_scale) {
       const double av = D.straggler_mode == LBBSP_STRAGGLE_SM_CAP ? avail[w] : 1.0;
       int cap = static_cast<int>(floor(static_cast<double>(D.sm_budget) * share * av));
       cap = cap < 1 ? 1 : cap;
-      if (D.pair_caps) cap = cap < 2 ? 2 : (cap & ~1);  // (2,1,1) clusters
+      if (D.cap_align > 1) cap = cap < D.cap_align ? D.cap_align : cap - cap % D.cap_align;  // clusters
       if (c0 + cap > D.sm_budget) cap = D.sm_budget - c0 > 0 ? D.sm_budget - c0 : 1;
       D.cta0[i] = c0;
       D.ctan[i] = cap;
@@ -1483,7 +1484,8 @@ struct lbbsp_mlp {
   // fused worker kernel (784-256-10): forward + head + dW0 in one launch
   bool fused = false;
   bool fused_pair = false;  // the (2,1,1)-cluster variant (c2_fused_pair.cuh)
-  CUtensorMap fz_tm[6];
+  bool fused_quad = false;  // the (4,1,1)-cluster variant (c2_fused_quad.cuh)
+  CUtensorMap fz_tm[7];
   CUtensorMap fz_gm[2];   // dataset buffer b, box {64, 1}: the pair kernel's in-kernel row gather
   bool fz_gather = false;
   unsigned* fz_comb = nullptr;
@@ -1661,7 +1663,10 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
       fa.B_total = B_total;
       fa.max_rows = D.max_rows;
     }
-    if (fused_pair)
+    if (fused_quad)
+      LBBSP_CUDA_CHECK(launch_maybe_pdl(c2_quad_worker_kernel, sms & ~3, kFqThreads, kFqSmem, s, use_pdl,
+                                        fz_tm[0], fz_tm[6], fz_tm[2], fz_tm[3], fz_tm[5], fa));
+    else if (fused_pair)
       LBBSP_CUDA_CHECK(launch_maybe_pdl(c2_pair_worker_kernel, sms & ~1, kFpThreads, kFpSmem, s, use_pdl,
                                         kgather ? fz_gm[cap_buf] : fz_tm[0], fz_tm[4], fz_tm[2],
                                         kgather ? fz_gm[cap_buf] : fz_tm[3], fz_tm[5], fa));
@@ -2331,11 +2336,20 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     // bitwise the same round, but 32 tile::gather4 requests per 16 KB stage
     // run the worker phase at 50 us against 21 us from the gathered batch
     // (profiles/r02_kgather.txt) -- the TMA unit's request rate, not bytes
+    // the quad kernel (four CTAs per tile), opt-in (LBBSP_FUSE_QUAD=1): a
+    // CTA's tile takes as long as in the pair kernel (forward 4.5 vs 5.1 us,
+    // the head's latency chains unchanged) and a worker's tile wave shrinks
+    // from 1152 to 512 rows, so LB-BSP's larger batches need two waves
+    // (profiles/r02_quad.txt)
+    m.fused_quad = m.fused_pair && getenv("LBBSP_FUSE_QUAD") && !getenv("LBBSP_KGATHER");
+    if (m.fused_quad) m.fused_pair = false;
+    if (m.fused_quad) rc = make_tmap_bf16(&m.fz_tm[6], m.pb + m.off_w[0], kFzD0, kHeadDH, kFzD0, 64);
+    if (rc) return rc;
     m.fz_gather = m.fused_pair && getenv("LBBSP_KGATHER");
     for (int b = 0; b < 2 && m.fz_gather && !rc; ++b)
       rc = make_tmap_bf16(&m.fz_gm[b], m.data_xb[b], kFzD0, m.N_data, kFzD0, 1);
     if (rc) return rc;
-    D.pair_caps = m.fused_pair ? 1 : 0;
+    D.cap_align = m.fused_quad ? 4 : m.fused_pair ? 2 : 1;
     unsigned* fd = nullptr;
     LBBSP_CUDA_CHECK(m.alloc(&fd, static_cast<size_t>(m.n_local)));
     D.fz_done = fd;
@@ -2345,6 +2359,8 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
                                           static_cast<int>(kFzSmem)));
     LBBSP_CUDA_CHECK(cudaFuncSetAttribute(c2_pair_worker_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(kFpSmem)));
+    LBBSP_CUDA_CHECK(cudaFuncSetAttribute(c2_quad_worker_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kFqSmem)));
   }
   m.reduce_bytes = (m.n_local + 1.0) * P * 4.0 + P * 4.0 + P * 2.0;
   LBBSP_CUDA_CHECK(cudaDeviceSynchronize());
@@ -2641,7 +2657,7 @@ extern "C" int lbbsp_mlp_work(lbbsp_mlp* m, double* gemm_flops, double* reduce_b
 
 extern "C" int lbbsp_mlp_rows_per_cta(lbbsp_mlp* m, int* rows) {
   if (!m || !rows) return set_error(LBBSP_INVALID_ARGUMENT, "mlp_rows_per_cta: null argument");
-  *rows = m->fused && m->fused_pair ? 64 : 128;
+  *rows = m->fused && m->fused_quad ? 32 : m->fused && m->fused_pair ? 64 : 128;
   return LBBSP_OK;
 }
 

@@ -5,9 +5,10 @@ one persistent launch):
     (LBBSP_NO_FUSE=1): same K order in every accumulation, same head
     arithmetic, same CTA-ordered combine;
   * csrc/c2_fused_pair.cuh (the default, a (2,1,1) cluster per tile split by
-    hidden columns) sums the logits as two column halves, so it matches the
-    separate kernels to the rounding of that sum: weights within 1e-3 of the
-    total update after 6 rounds, bitwise deterministic run to run.
+    hidden columns) and csrc/c2_fused_quad.cuh (LBBSP_FUSE_QUAD=1, four CTAs)
+    sum the logits as column partials, so they match the separate kernels to
+    the rounding of that sum: weights within 1e-3 of the total update after
+    6 rounds, bitwise deterministic run to run.
 Ragged sizes cover one-row workers, a worker whose rows end inside a 16-row
 head tile, and a worker with more 128-row tiles than CTA pairs."""
 import os
@@ -19,14 +20,16 @@ pytestmark = pytest.mark.gpu
 
 
 def _run(static, rounds, mode, predictor="ema", trace=None, sm_budget=0):
-    """mode: 'pair' (default kernel over the gathered batch), 'pair_kg' (pair
-    kernel gathering the rows itself by tile::gather4, LBBSP_KGATHER),
-    'single' (LBBSP_FUSE_SINGLE), 'separate' (LBBSP_NO_FUSE). Returns
-    (initial params, final params, records)."""
+    """mode: 'pair' (default: two CTAs per tile), 'quad' (four,
+    LBBSP_FUSE_QUAD), 'pair_kg' (pair kernel gathering the rows itself by
+    tile::gather4, LBBSP_KGATHER), 'single' (LBBSP_FUSE_SINGLE), 'separate'
+    (LBBSP_NO_FUSE). Returns (initial params, final params, records)."""
     from paper_1806_02508_b200.mlp import MlpEngine, constant_trace
     n = len(static)
-    env = {"single": "LBBSP_FUSE_SINGLE", "separate": "LBBSP_NO_FUSE", "pair_kg": "LBBSP_KGATHER"}.get(mode)
-    saved = {k: os.environ.pop(k, None) for k in ("LBBSP_FUSE_SINGLE", "LBBSP_NO_FUSE", "LBBSP_KGATHER")}
+    env = {"single": "LBBSP_FUSE_SINGLE", "separate": "LBBSP_NO_FUSE", "pair_kg": "LBBSP_KGATHER",
+           "quad": "LBBSP_FUSE_QUAD"}.get(mode)
+    saved = {k: os.environ.pop(k, None)
+             for k in ("LBBSP_FUSE_SINGLE", "LBBSP_NO_FUSE", "LBBSP_KGATHER", "LBBSP_FUSE_QUAD")}
     if env:
         os.environ[env] = "1"
     try:
@@ -65,13 +68,14 @@ def test_single_cta_fused_equals_separate_kernels_bitwise(static):
     assert np.array_equal(ra["loss"], rb["loss"])
 
 
+@pytest.mark.parametrize("mode", ["pair", "quad"])
 @pytest.mark.parametrize("static", SIZES)
-def test_pair_fused_matches_separate_kernels(static):
-    p0, a, _ = _run(static, 6, "pair")
+def test_split_fused_matches_separate_kernels(static, mode):
+    p0, a, _ = _run(static, 6, mode)
     _, b, _ = _run(static, 6, "separate")
     upd = float(np.max(np.abs(b - p0)))
     assert float(np.max(np.abs(a - b))) <= 1e-3 * upd, (float(np.max(np.abs(a - b))), upd)
-    _, a2, _ = _run(static, 6, "pair")
+    _, a2, _ = _run(static, 6, mode)
     assert np.array_equal(a, a2)
 
 

@@ -256,6 +256,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
         mbar_wait(hdone, hph);
         hph ^= 1;
       }
+      // phase W's X operand does not depend on the worker barrier: the first
+      // ring stages get their X halves now, their dZ0 halves after it (the
+      // stage region is idle once the last head is done; the head partials'
+      // reduction below uses only its first 8 KB, the X halves start at 16 KB)
+      const int my_w = w_tiles > cta_in ? ((w_tiles - cta_in + cnt - 1) / cnt) * k_blocks_w : 0;
+      const int n_pre = gidx ? 0 : (my_w < kFpStages ? my_w : kFpStages);
+      if (lane == 0) {
+        for (int i = 0; i < n_pre; ++i) {
+          const int t = cta_in + (i / k_blocks_w) * cnt, kb = i % k_blocks_w;
+          uint8_t* sa = smem + i * kFpStage;
+          mbar_arrive_expect_tx(&full[i], 32768);
+          tma_load_2d(sa + 16384, &tmXn, &full[i], (t / 2) * 128, r0 + kb * 64);
+          tma_load_2d(sa + 24576, &tmXn, &full[i], (t / 2) * 128 + 64, r0 + kb * 64);
+        }
+      }
       if (lane == 0) {
         const unsigned long long t0 = globaltimer();
         unsigned seen;
@@ -280,12 +295,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
         }
       }
       __syncwarp();
+      int wi = 0;
       for (int t = cta_in; t < w_tiles; t += cnt) {
         const int mt = t % 2, nt = t / 2;
-        for (int kb = 0; kb < k_blocks_w; ++kb) {
+        for (int kb = 0; kb < k_blocks_w; ++kb, ++wi) {
           const int k0 = r0 + kb * 64;
-          mbar_wait(&empty[stage], ph ^ 1);
           uint8_t* sa = smem + stage * kFpStage;
+          if (wi < n_pre) {  // X already in flight
+            if (lane == 0) {
+              tma_load_2d(sa, &tmDz, &full[stage], mt * 128, k0);
+              tma_load_2d(sa + 8192, &tmDz, &full[stage], mt * 128 + 64, k0);
+            }
+            if (++stage == kFpStages) {
+              stage = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
+          mbar_wait(&empty[stage], ph ^ 1);
           if (lane == 0) {
             mbar_arrive_expect_tx(&full[stage], 32768);
             tma_load_2d(sa, &tmDz, &full[stage], mt * 128, k0);
@@ -680,7 +707,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFpThreads, 1)
       named_sync_epi();
       acc ^= 1;
     }
-    if (threadIdx.x == 0) bulk_wait0();  // dW0 in global memory before the combine / exit
+    // the staging smem must outlive the stores' reads; their global writes are
+    // complete by the grid's end, before any dependent launch reads the slab
+    if (threadIdx.x == 0) bulk_wait_read0();
   }
   if (dbg && threadIdx.x == 0) dbg[4] = globaltimer();
   tc_fence_before();

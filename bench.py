@@ -30,6 +30,11 @@ BATCH_PER_GPU = 4096
 WARMUP_NARX = 50
 TRACE_SEED = 3
 WINDOW_ROUNDS = 100  # fixed steady-state window for the BSP / ideal comparisons
+# the speed the proportional solver observes per worker (DESIGN 2.3): the
+# worker's speed at the nominal batch read off its calibrated Gamma profile --
+# the reference's CPU-mode v_actual; "rate" (b / t) collapses latency-floored
+# workers to one row and is kept as a comparison arm
+MAIN_OBSERVE = os.environ.get("LBBSP_BENCH_OBSERVE", "capacity")
 
 
 def parse():
@@ -575,7 +580,7 @@ def main():
     else:
         prof = prof_local
 
-    def make(scheme, tr, predictor="narx", solver="proportional", observe="rate"):
+    def make(scheme, tr, predictor="narx", solver="proportional", observe=MAIN_OBSERVE):
         eng = MlpEngine(dims=DIMS, global_batch=B, n_workers_local=WORKERS_PER_GPU, world=world,
                         rank=rank, scheme=scheme, predictor=predictor,
                         warmup_iterations=WARMUP_NARX, learning_rate=0.05, seed=1,
@@ -670,8 +675,8 @@ def main():
     win = {}
     phases_unloaded = None
     for name, scheme, tr, pred, solver, obs in (
-            ("lbbsp", "lb-bsp", trace, "narx", "proportional", "rate"),
-            ("lbbsp_capacity", "lb-bsp", trace, "narx", "proportional", "capacity"),
+            ("lbbsp", "lb-bsp", trace, "narx", "proportional", MAIN_OBSERVE),
+            ("lbbsp_rate", "lb-bsp", trace, "narx", "proportional", "rate"),
             ("lbbsp_gamma", "lb-bsp", trace, "narx", "gamma", "rate"),
             ("bsp", "bsp", trace, "narx", "proportional", "rate"),
             ("perfect", "lb-bsp", trace, "perfect", "proportional", "rate"),
@@ -740,6 +745,8 @@ def main():
                        "parallelism": f"dp{n_total} (emulated {WORKERS_PER_GPU}/GPU)",
                        "trace": "make_benchmark_series seed 3, iteration-indexed",
                        "straggler_injection": "interference (csrc/interfere.cuh): phase time = work / a",
+                       "observed_speed": MAIN_OBSERVE + (" (a * x_n / Gamma0(x_n), calibrated profiles; "
+                                                         "DESIGN 2.3)" if MAIN_OBSERVE == "capacity" else " (b / t)"),
                        "l2": "256 MB buffer zeroed between timed steps, outside the events",
                        "rounds_before_timing": warm},
             "round_ms": percentiles(ms_steps),
@@ -753,7 +760,7 @@ def main():
             "lbbsp_over_ideal_time": lb / win["perfect"]["mean"],
             "lbbsp_over_no_straggler_time": lb / win["no_straggler"]["mean"],
             "lbbsp_gamma_over_bsp": win["bsp"]["mean"] / win["lbbsp_gamma"]["mean"],
-            "lbbsp_capacity_over_bsp": win["bsp"]["mean"] / win["lbbsp_capacity"]["mean"],
+            "lbbsp_rate_over_bsp": win["bsp"]["mean"] / win["lbbsp_rate"]["mean"],
             "lbbsp_gamma_over_ideal_time": win["lbbsp_gamma"]["mean"] / win["perfect_gamma"]["mean"],
             "gamma_profiles_s": [[round(m0, 12), round(b0, 9), xo] for m0, b0, _, xo in prof],
             "phase_ms": [round(float(x) * 1e3, 4) for x in (phases if phases is not None else [])],

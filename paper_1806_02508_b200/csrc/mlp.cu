@@ -761,44 +761,55 @@ static cudaError_t launch_softmax_ce(int sms, cudaStream_t s, bool pdl, Groups G
 }
 
 
-// db partial of worker g = column sums of dZ over its rows (N % 8 == 0)
-// Bias gradient db = column sums of dZ over the worker's rows, written into
-// the worker's slab. Two deterministic stages: CTA (rb, cb) sums a block of
-// rows for 2048 columns (8 per thread, 16-B loads) into its own scratch row;
-// the worker's last CTA adds the row blocks in order.
-constexpr int kBiasCols = 2048;
-constexpr int kBiasMaxRowBlocks = 64;
-constexpr int kBiasRowsInFlight = 16;  // 16 x 16 B per thread: 64 KB in flight per CTA
+// db partial of worker g = column sums of dZ over its rows (N % 8 == 0),
+// written into the worker's slab (or its bf16 bucket). Column strips: each of
+// the worker's CTAs owns whole 64-column strips (no cross-CTA combine); a
+// thread reads 16 B (8 columns) of every 32nd row with 16 rows in flight, and
+// the 32 row-lane partials of a column are added in row-lane order in shared
+// memory -- deterministic, one pass over dZ.
+constexpr int kBiasCols = 2048;  // (scratch sizing, kept for the C-ABI's allocation)
+constexpr int kBiasStrip = 64;
+constexpr int kBiasRowsInFlight = 16;
 __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __restrict__ dZ, int N,
                                                         float* slab, long long slab_stride,
-                                                        long long off_b, float* scratch,
-                                                        unsigned* counters, bf16* out_b16,
+                                                        long long off_b, float* /*scratch*/,
+                                                        unsigned* /*counters*/, bf16* out_b16,
                                                         unsigned long long* timing) {
   int g, cta_in, cta_cnt;
   if (!my_group(G, &g, &cta_in, &cta_cnt)) return;
-  const int ncb = (N + kBiasCols - 1) / kBiasCols;
-  const int rbs = max(1, min(kBiasMaxRowBlocks, cta_cnt / ncb));
-  const int used = rbs * ncb;
-  if (cta_in >= used) return;
+  const int n_strips = (N + kBiasStrip - 1) / kBiasStrip;
+  if (cta_in >= n_strips) return;
   const unsigned long long t_cta0 = phase_begin(timing, g);
+  __shared__ float red[32][kBiasStrip + 4];
   const int r0 = G.r0[g], r1 = G.r1[g];
-  const int cb = cta_in % ncb, rb = cta_in / ncb;
-  const int rows = r1 - r0, per = (rows + rbs - 1) / rbs;
-  const int ra = r0 + rb * per, rz = min(r1, ra + per);
-  const int c0 = blockIdx.x - cta_in;  // the worker's first CTA
-  const int col = cb * kBiasCols + threadIdx.x * 8;
-  float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (col < N) {
-    int r = ra;
+  const int chunk = threadIdx.x & 7, rl = threadIdx.x >> 3;
+  float* gs = slab + static_cast<long long>(g) * slab_stride + off_b;
+  for (int st = cta_in; st < n_strips; st += cta_cnt) {
+    const int col = st * kBiasStrip + chunk * 8;
+    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (col < N) {
+      const bf16* base = dZ + col;
+      int r = r0 + rl;
 #pragma unroll 1
-    for (; r + kBiasRowsInFlight <= rz; r += kBiasRowsInFlight) {
-      uint4 q[kBiasRowsInFlight];
+      for (; r + 32 * (kBiasRowsInFlight - 1) < r1; r += 32 * kBiasRowsInFlight) {
+        uint4 q[kBiasRowsInFlight];
 #pragma unroll
-      for (int u = 0; u < kBiasRowsInFlight; ++u)
-        q[u] = *reinterpret_cast<const uint4*>(dZ + static_cast<long long>(r + u) * N + col);
+        for (int u = 0; u < kBiasRowsInFlight; ++u)
+          q[u] = *reinterpret_cast<const uint4*>(base + static_cast<long long>(r + 32 * u) * N);
 #pragma unroll
-      for (int u = 0; u < kBiasRowsInFlight; ++u) {
-        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q[u]);
+        for (int u = 0; u < kBiasRowsInFlight; ++u) {
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q[u]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = __bfloat1622float2(b2[j]);
+            a[2 * j] += f.x;
+            a[2 * j + 1] += f.y;
+          }
+        }
+      }
+      for (; r < r1; r += 32) {
+        const uint4 q = *reinterpret_cast<const uint4*>(base + static_cast<long long>(r) * N);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float2 f = __bfloat1622float2(b2[j]);
@@ -807,58 +818,22 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
         }
       }
     }
-    for (; r < rz; ++r) {
-      const uint4 q = *reinterpret_cast<const uint4*>(dZ + static_cast<long long>(r) * N + col);
-      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = __bfloat1622float2(b2[j]);
-        a[2 * j] += f.x;
-        a[2 * j + 1] += f.y;
+    for (int j = 0; j < 8; ++j) red[rl][chunk * 8 + j] = a[j];
+    __syncthreads();
+    if (threadIdx.x < kBiasStrip) {
+      const int c = st * kBiasStrip + threadIdx.x;
+      float v = 0.f;
+#pragma unroll 8
+      for (int q = 0; q < 32; ++q) v += red[q][threadIdx.x];
+      if (c < N) {
+        if (out_b16)
+          out_b16[c] = __float2bfloat16_rn(v);
+        else
+          gs[c] = v;
       }
     }
-    float* dst = scratch + static_cast<long long>(blockIdx.x) * kBiasCols + threadIdx.x * 8;
-    *reinterpret_cast<float4*>(dst) = make_float4(a[0], a[1], a[2], a[3]);
-    *reinterpret_cast<float4*>(dst + 4) = make_float4(a[4], a[5], a[6], a[7]);
-  }
-  __threadfence();
-  __syncthreads();
-  __shared__ int last;
-  if (threadIdx.x == 0) last = atomicAdd(&counters[g], 1u) == static_cast<unsigned>(used - 1);
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    float* gs = slab + static_cast<long long>(g) * slab_stride + off_b;
-    // float4 columns; all row-block partials of a column in flight at once,
-    // added in row-block order
-    for (int c4 = threadIdx.x; c4 < N / 4; c4 += blockDim.x) {
-      const int c = 4 * c4, b = c / kBiasCols, o = c % kBiasCols;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int q0 = 0; q0 < rbs; q0 += 16) {  // 16 partials in flight, added in row-block order
-        float4 t[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (q0 + q < rbs)
-            t[q] = __ldcg(reinterpret_cast<const float4*>(
-                &scratch[static_cast<long long>(c0 + (q0 + q) * ncb + b) * kBiasCols + o]));
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (q0 + q < rbs) {
-            v.x += t[q].x;
-            v.y += t[q].y;
-            v.z += t[q].z;
-            v.w += t[q].w;
-          }
-      }
-      if (out_b16) {
-        __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(out_b16 + c);
-        o[0] = __floats2bfloat162_rn(v.x, v.y);
-        o[1] = __floats2bfloat162_rn(v.z, v.w);
-      } else {
-        *reinterpret_cast<float4*>(&gs[c]) = v;
-      }
-    }
-    if (threadIdx.x == 0) counters[g] = 0u;
+    __syncthreads();
   }
   phase_finish(G, timing, g, t_cta0);
 }

@@ -2,7 +2,7 @@
 # Round-2 one-GPU sweep after the pair kernel (gpurun_out/r02b/): bench (C2
 # default) + reference arm, smoke, ncu launch list of the bench command, ncu
 # --set full of the pair worker kernel.
-O=gpurun_out/r02b; mkdir -p $O
+O=${OUT:-gpurun_out/r02b}; mkdir -p $O
 st() { echo "$1 rc=$2" >> $O/status; }
 timeout 900 python bench.py --steps 20 --warmup 5 > $O/c2_n1.json 2> $O/c2_n1.err; st bench $?
 timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > $O/ref_n1.json 2> $O/ref_n1.err; st ref $?

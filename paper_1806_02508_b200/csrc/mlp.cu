@@ -763,12 +763,14 @@ static cudaError_t launch_softmax_ce(int sms, cudaStream_t s, bool pdl, Groups G
 
 // db partial of worker g = column sums of dZ over its rows (N % 8 == 0),
 // written into the worker's slab (or its bf16 bucket). Column strips: each of
-// the worker's CTAs owns whole 64-column strips (no cross-CTA combine); a
-// thread reads 16 B (8 columns) of every 32nd row with 16 rows in flight, and
-// the 32 row-lane partials of a column are added in row-lane order in shared
-// memory -- deterministic, one pass over dZ.
+// the worker's CTAs owns whole 32-column strips (no cross-CTA combine; 128
+// strips at width 4096 keep a 148-SM partition busy); a thread reads 16 B
+// (8 columns) of every 64th row with 16 rows in flight, and the 64 row-lane
+// partials of a column are added in row-lane order in shared memory --
+// deterministic, one pass over dZ.
 constexpr int kBiasCols = 2048;  // (scratch sizing, kept for the C-ABI's allocation)
-constexpr int kBiasStrip = 64;
+constexpr int kBiasStrip = 32;
+constexpr int kBiasLanes = 256 / (kBiasStrip / 8);  // 64 row lanes
 constexpr int kBiasRowsInFlight = 16;
 __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __restrict__ dZ, int N,
                                                         float* slab, long long slab_stride,
@@ -780,9 +782,10 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
   const int n_strips = (N + kBiasStrip - 1) / kBiasStrip;
   if (cta_in >= n_strips) return;
   const unsigned long long t_cta0 = phase_begin(timing, g);
-  __shared__ float red[32][kBiasStrip + 4];
+  __shared__ float red[kBiasLanes][kBiasStrip + 1];
   const int r0 = G.r0[g], r1 = G.r1[g];
-  const int chunk = threadIdx.x & 7, rl = threadIdx.x >> 3;
+  constexpr int kChunks = kBiasStrip / 8;
+  const int chunk = threadIdx.x % kChunks, rl = threadIdx.x / kChunks;
   float* gs = slab + static_cast<long long>(g) * slab_stride + off_b;
   for (int st = cta_in; st < n_strips; st += cta_cnt) {
     const int col = st * kBiasStrip + chunk * 8;
@@ -791,11 +794,11 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
       const bf16* base = dZ + col;
       int r = r0 + rl;
 #pragma unroll 1
-      for (; r + 32 * (kBiasRowsInFlight - 1) < r1; r += 32 * kBiasRowsInFlight) {
+      for (; r + kBiasLanes * (kBiasRowsInFlight - 1) < r1; r += kBiasLanes * kBiasRowsInFlight) {
         uint4 q[kBiasRowsInFlight];
 #pragma unroll
         for (int u = 0; u < kBiasRowsInFlight; ++u)
-          q[u] = *reinterpret_cast<const uint4*>(base + static_cast<long long>(r + 32 * u) * N);
+          q[u] = *reinterpret_cast<const uint4*>(base + static_cast<long long>(r + kBiasLanes * u) * N);
 #pragma unroll
         for (int u = 0; u < kBiasRowsInFlight; ++u) {
           const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q[u]);
@@ -807,7 +810,7 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
           }
         }
       }
-      for (; r < r1; r += 32) {
+      for (; r < r1; r += kBiasLanes) {
         const uint4 q = *reinterpret_cast<const uint4*>(base + static_cast<long long>(r) * N);
         const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
@@ -825,7 +828,7 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
       const int c = st * kBiasStrip + threadIdx.x;
       float v = 0.f;
 #pragma unroll 8
-      for (int q = 0; q < 32; ++q) v += red[q][threadIdx.x];
+      for (int q = 0; q < kBiasLanes; ++q) v += red[q][threadIdx.x];
       if (c < N) {
         if (out_b16)
           out_b16[c] = __float2bfloat16_rn(v);

@@ -1000,7 +1000,7 @@ __device__ inline double local_speed(const PlanDev& D, int i, int n_phases, doub
 // are co-resident, nb < SM count).
 __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D, int fused_speed_phases,
                                                                      unsigned* arrive,
-                                                                     size_t smem_bytes) {
+                                                                     size_t smem_bytes, int early) {
   extern __shared__ double sm_d[];
   __shared__ NarxTrainSmem ts;
   const int nb = gridDim.x - 1;
@@ -1018,6 +1018,8 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
     __syncthreads();
     const int len = len_s, w = w_s;
     const size_t o = static_cast<size_t>(w) * D.pred.max_hist;
+    if (tid == 0 && blockIdx.x == 0) D.stamps[15] = gtimer();  // kernel entry (debug timeline)
+    if (early) tc::pdl_wait();  // the worker kernel's phase times are final
     if (tid == 0 && len < D.pred.max_hist) {
       const double v = fused_speed_phases > 0 ? local_speed(D, w - D.rank * D.n_local, fused_speed_phases, nullptr)
                                               : D.v_obs_all[w];
@@ -1026,6 +1028,7 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
       D.pred.hm[o + len] = D.m_now[w];
     }
     __syncthreads();
+    if (tid == 0 && blockIdx.x == 0) D.stamps[14] = gtimer();  // training starts
     const int L = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
     const size_t slot = narx_train_scratch_bytes(D.pred.max_hist) / sizeof(double);
     size_t nd = 0;
@@ -1042,9 +1045,11 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(seen) : "l"(D.obs_seq) : "memory");
       } while (seen < static_cast<unsigned long long>(k_s + 1));
       D.v_next[w] = predict_for_round(D, w, L, k_s + 1);
+      atomicMax(&D.stamps[13], static_cast<unsigned long long>(gtimer()));  // last training done
     }
     return;
   }
+  if (early) tc::pdl_wait();
   if (tid == 0) D.stamps[3] = gtimer();
   const long long k_obs = *D.k;
   const int cursor0 = *D.pred.cursor;
@@ -1833,18 +1838,34 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   // round's plan. step_sync computes the loss (cluster_sim.cpp:445) and trains
   // (:464) independently of each other.
   const bool fork = !getenv("LBBSP_NO_FORK");
-  cudaStream_t so = s;
+  const int nb = (n_total + 1) / 2;
+  const bool narx_fused = pred.dev.kind == LBBSP_PRED_NARX && nb + 1 <= num_sms();
+  // One rank, fused worker kernel, NARX: the observe / NARX kernel follows the
+  // worker kernel on the main stream as a programmatic launch. Its CTAs become
+  // resident on the SMs the worker partitions leave free while the workers
+  // still run and wait for the workers' results at griddepcontrol.wait (the
+  // launch latency leaves the critical path); the loss branch moves to the
+  // side stream. (A dry training run there to warm the trainer's code did not
+  // shorten the real one: the trainer is fp64-latency bound, ~1.9 us per
+  // evaluation at L = 110, scripts/narx_probe.py.)
+  const bool early_obs = fork && narx_fused && fused && cfg.world == 1 && use_pdl && !getenv("LBBSP_NO_EARLY_OBSERVE");
+  cudaStream_t so = s, sl = s;
   if (fork) {
     LBBSP_CUDA_CHECK(cudaEventRecord(ev_fork, s));
     LBBSP_CUDA_CHECK(cudaStreamWaitEvent(side, ev_fork, 0));
-    so = side;
+    if (early_obs)
+      sl = side;
+    else
+      so = side;
   }
   // ---- observe branch ----
-  const int nb = (n_total + 1) / 2;
-  if (pred.dev.kind == LBBSP_PRED_NARX && nb + 1 <= num_sms()) {
+  if (narx_fused) {
     const size_t tsm = train_smem_bytes(pred.dev.max_hist);
-    observe_train_kernel<<<nb + 1, kTrainThreads, tsm, so>>>(D, cfg.world > 1 ? 0 : n_phases,
-                                                             arrive, tsm);
+    if (early_obs)
+      LBBSP_CUDA_CHECK(launch_maybe_pdl(observe_train_kernel, nb + 1, kTrainThreads, tsm, so, true, D, n_phases,
+                                        arrive, tsm, 1));
+    else
+      observe_train_kernel<<<nb + 1, kTrainThreads, tsm, so>>>(D, cfg.world > 1 ? 0 : n_phases, arrive, tsm, 0);
     ++nl;
   } else {
     observe_kernel<<<1, 256, 0, so>>>(D, cfg.world > 1 ? 0 : n_phases);
@@ -1873,7 +1894,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   } else {
     // not a programmatic launch: early-resident apply CTAs would hold the SMs
     // the (higher-priority) NARX branch needs when the backward ends
-    reduce_apply_kernel<<<sms * 4, 256, 0, s>>>(partial, n_local, P, grad, params, pb, lr, 1, D.stamps);
+    reduce_apply_kernel<<<sms * 4, 256, 0, sl>>>(partial, n_local, P, grad, params, pb, lr, 1, D.stamps);
   }
   if (!bucketed) ++nl;
   // ---- full-dataset loss (step_sync P9, cluster_sim.cpp:445) ----
@@ -1882,7 +1903,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
       GemmPlan& fp = (l == 0 && cap_buf == 1) ? fwd_d0_alt : fwd_d[l];
       fp.ctas = std::min(fp.ctas, sms) & ~1;
       fp.pdl = use_pdl;
-      int rc = gemm_launch(fp, s);
+      int rc = gemm_launch(fp, cfg.world == 1 ? sl : s);
       if (rc) return rc;
       ++nl;
     }
@@ -1891,13 +1912,13 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
     if (small_head) {
       const bf16* Hin = L >= 2 ? Hd[L - 2] : data_x;
       LBBSP_CUDA_CHECK(launch_maybe_pdl(
-          head_mma_kernel<false>, sms, 256, kHeadMmaSmem, s, use_pdl, none, N_data, Hin,
+          head_mma_kernel<false>, sms, 256, kHeadMmaSmem, cfg.world == 1 ? sl : s, use_pdl, none, N_data, Hin,
           static_cast<const float*>(params + off_w[hl]), static_cast<const float*>(params + off_b[hl]),
           static_cast<const int*>(data_y), static_cast<const float*>(nullptr),
           static_cast<bf16*>(nullptr), static_cast<float*>(nullptr), 0ll, 0ll, 0ll, 0ll, D.loss_acc,
           head_part, head_loss, head_cnt_d, D.stamps + 6));
     } else {
-      LBBSP_CUDA_CHECK(launch_softmax_ce(sms, s, use_pdl, none, N_data, logits_d, dims[L], data_y,
+      LBBSP_CUDA_CHECK(launch_softmax_ce(sms, cfg.world == 1 ? sl : s, use_pdl, none, N_data, logits_d, dims[L], data_y,
                                          nullptr, nullptr, D.loss_acc, nullptr));
     }
     ++nl;

@@ -222,6 +222,22 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
     if (tid == 0 && rep) *rep = lbbsp_narx_report{0, 0, 0.0};
     return;
   }
+  const int S = narx_train_stride(L);
+  // the history into the scratch's E/G region first (written only once the
+  // evaluations start): one parallel round trip, instead of the sequential
+  // scaler folds below waiting on each cache line of v, c, m in turn
+  double* hv = buf + 9 * static_cast<size_t>(S);
+  double* hc = hv + L;
+  double* hm = hc + L;
+  for (int i = tid; i < L; i += blockDim.x) {
+    hv[i] = v[i];
+    hc[i] = c[i];
+    hm[i] = m[i];
+  }
+  v = hv;
+  c = hc;
+  m = hm;
+  __syncthreads();
   // fit_scaler x3 (predictor.cpp:71-82), one sequential thread per series
   if (tid == 0 || tid == 32 || tid == 64) {
     const int which = tid / 32;
@@ -246,16 +262,11 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
   }
   __syncthreads();
   const int cnt = L - 2;
-  const int S = narx_train_stride(L);
   double* Z = buf;                             // [8][S]
   double* T = Z + static_cast<size_t>(8) * S;  // [S]
   double* EG[2] = {T + S, T + 13 * static_cast<size_t>(S)};  // {E [S], G [11][S]} x 2
   const bool spec = buf_doubles >= static_cast<size_t>(kNarxArrays) * S &&
                     cnt <= static_cast<int>(blockDim.x) - 32;
-  // zero padding of the folds (never written by the evaluations)
-  for (int i = cnt + tid; i < (cnt + 15) / 16 * 16; i += blockDim.x)
-    for (int b = 0; b < (spec ? 2 : 1); ++b)
-      for (int k = 0; k < 12; ++k) EG[b][static_cast<size_t>(k) * S + i] = 0.0;
   const double mv = s->sc[0], sv = s->sc[1], mc = s->sc[2], scd = s->sc[3], mm = s->sc[4],
                sm = s->sc[5];
   // build_training_set (predictor.cpp:89-100)
@@ -271,6 +282,12 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
     Z[7 * S + i] = ddiv(dsub(m[t - 2], mm), sm);
     T[i] = ddiv(dsub(v[t], mv), sv);
   }
+  __syncthreads();
+  // zero padding of the folds (never written by the evaluations; after the
+  // build, which read the history copy in the same region)
+  for (int i = cnt + tid; i < (cnt + 15) / 16 * 16; i += blockDim.x)
+    for (int b = 0; b < (spec ? 2 : 1); ++b)
+      for (int k = 0; k < 12; ++k) EG[b][static_cast<size_t>(k) * S + i] = 0.0;
   __syncthreads();
   const double scale = ddiv(2.0, static_cast<double>(cnt));
   auto E_ = [&](int b) { return EG[b]; };

@@ -12,7 +12,7 @@ n, B = 8, 4096
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 tr = benchmark_trace(n, 300, seed=3) if os.environ.get("TRACE") == "bench" else constant_trace(n, 300)
 names = ["plan_in", "plan_ready", "gather_in", "obs_in", "obs_out", "reduce_in", "losshead_in", "losshead_out",
-         "plan_computed", "gather_out", "pred_done", "solve_done", "slices_done"]
+         "plan_computed", "gather_out", "pred_done", "solve_or_dry_done", "slices_done", "train_out", "train_in", "obs_kernel_in"]
 for pred in os.environ.get("PREDS", "ema,narx").split(","):
     eng = MlpEngine(dims=[784, 256, 10], global_batch=B, n_workers_local=n, predictor=pred,
                     warmup_iterations=50, max_iterations=300, trace=tr)

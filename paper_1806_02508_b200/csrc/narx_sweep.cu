@@ -437,21 +437,29 @@ __device__ float eval_tc(const Smem& S, float b2, float* gout, int cnt, int I, i
         ldsm_x4(zh + zsw(r0 + lrow, 2 * ks + lch), ah[ks]);
         ldsm_x4(zl + zsw(r0 + lrow, 2 * ks + lch), al[ks]);
       }
+      // the small cross products (lo*hi, hi*lo) in their own accumulator:
+      // two independent MMA chains per n-tile instead of one of six
+      float accx[4][4];
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
         const float2 b = *reinterpret_cast<const float2*>(b1h + 8 * nt + 2 * t);
         acc[nt][0] = b.x; acc[nt][1] = b.y; acc[nt][2] = b.x; acc[nt][3] = b.y;
+        accx[nt][0] = accx[nt][1] = accx[nt][2] = accx[nt][3] = 0.f;
         uint32_t bh[4], bl[4];
         const int wrow = 32 * hh + 8 * nt + (lane & 7);
         ldsm_x4(wh + zsw(wrow, lane >> 3), bh);
         ldsm_x4(wl + zsw(wrow, lane >> 3), bl);
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
-          mma(acc[nt], al[ks], bh[2 * ks], bh[2 * ks + 1]);
-          mma(acc[nt], ah[ks], bl[2 * ks], bl[2 * ks + 1]);
+          mma(accx[nt], al[ks], bh[2 * ks], bh[2 * ks + 1]);
           mma(acc[nt], ah[ks], bh[2 * ks], bh[2 * ks + 1]);
+          mma(accx[nt], ah[ks], bl[2 * ks], bl[2 * ks + 1]);
         }
       }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[nt][r] += accx[nt][r];
     }
     float y0 = 0.f, y1 = 0.f;
 #pragma unroll

@@ -16,6 +16,7 @@
 // is speculative and becomes the next epoch's gradient when accepted.
 // Tolerance-based parity vs the fp64 oracle (tests/test_gpu_narx_sweep.py).
 #include <cmath>
+#include <cstdlib>
 #include <random>
 #include <vector>
 
@@ -23,6 +24,7 @@
 
 #include "common.cuh"
 #include "exactmath.cuh"
+#include "tc_ptx.cuh"
 
 namespace lbbsp {
 namespace sweep {
@@ -675,7 +677,10 @@ __global__ void __launch_bounds__(tcs::kTcThreads, 1) narxg_train_tc_kernel(Swee
     s_epochs = 0;
   }
   __syncthreads();
-  const float mv = s_sc[0], sv = s_sc[1], mc = s_sc[2], scd = s_sc[3], mm = s_sc[4], smm = s_sc[5];
+  // (x - mean) * (1 / std) in fp64: the reciprocal once instead of a
+  // division per element (the prologue was ~3x longer)
+  const double mv = s_sc[0], mc = s_sc[2], mm = s_sc[4];
+  const double isv = 1.0 / s_sc[1], iscd = 1.0 / s_sc[3], ismm = 1.0 / s_sc[5];
   // Z rows as bf16 hi/lo, one (row, 8-input chunk) per work item
   for (int it = threadIdx.x; it < cntp * 4; it += blockDim.x) {
     const int i = it >> 2, ch = it & 3;
@@ -686,9 +691,9 @@ __global__ void __launch_bounds__(tcs::kTcThreads, 1) narxg_train_tc_kernel(Swee
       float val = 0.f;
       if (i < cnt && q < I) {
         const int tt = i + d;
-        if (q < d) val = static_cast<float>((v[tt - 1 - q] - mv) / sv);
-        else if (q <= 2 * d) val = static_cast<float>((c[tt - (q - d)] - mc) / scd);
-        else val = static_cast<float>((m[tt - (q - 2 * d - 1)] - mm) / smm);
+        if (q < d) val = static_cast<float>((v[tt - 1 - q] - mv) * isv);
+        else if (q <= 2 * d) val = static_cast<float>((c[tt - (q - d)] - mc) * iscd);
+        else val = static_cast<float>((m[tt - (q - 2 * d - 1)] - mm) * ismm);
       }
       x[u] = val;
     }
@@ -699,7 +704,7 @@ __global__ void __launch_bounds__(tcs::kTcThreads, 1) narxg_train_tc_kernel(Swee
     tcs::split2(x[6], x[7], hv.w, lv.w);
     *reinterpret_cast<uint4*>(S.zh + tcs::zsw(i, ch)) = hv;
     *reinterpret_cast<uint4*>(S.zl + tcs::zsw(i, ch)) = lv;
-    if (ch == 0) S.T[i] = i < cnt ? static_cast<float>((v[i + d] - mv) / sv) : 0.f;
+    if (ch == 0) S.T[i] = i < cnt ? static_cast<float>((v[i + d] - mv) * isv) : 0.f;
   }
   for (int i = threadIdx.x; i < P; i += blockDim.x) {
     const float x = params[i];
@@ -744,6 +749,8 @@ __global__ void __launch_bounds__(tcs::kTcThreads, 1) narxg_train_tc_kernel(Swee
     A.loss_out[w] = current;
   }
 }
+
+#include "narx_umma.cuh"
 
 // batched narx_predict (predictor.cpp:147-153) for W models, one warp each
 __global__ void narxg_predict_kernel(int W, int L, int d, int H, const double* v, const double* c,
@@ -820,6 +827,23 @@ extern "C" int lbbsp_narx_sweep_train(int W, int L, int delay, int hidden, const
   const size_t base = static_cast<size_t>(4 * P + 2 * hidden * (I + 1) + 2 * sweep::kChunk * hidden +
                                           sweep::kChunk) * sizeof(float);
   const size_t zbytes = static_cast<size_t>(cnt) * (I + 2) * sizeof(float);
+  const size_t um_smem = sweep::ums::smem_bytes(cnt, P);
+  if (um_smem <= 227 * 1024 && getenv("LBBSP_C4_UMMA")) {
+    // tcgen05 trainer (narx_umma.cuh), opt-in: per evaluation it runs at the
+    // warp-MMA trainer's speed (~16 us at L = 1000, W = 148) -- the
+    // evaluation is bound by the per-tile epilogue chain (tanh, the y
+    // exchange, dz), not by the MMAs (profiles/r02_c4_umma.txt)
+    sweep::SweepArgs a{};
+    a.W = W; a.L = L; a.d = delay; a.h = hidden; a.v = d_v; a.c = d_c; a.m = d_m;
+    a.params = d_params; a.cfg = *cfg; a.fixed_epochs = fixed_epochs;
+    a.epochs_out = d_epochs; a.loss_out = d_loss; a.scratch = d_scratch; a.smem_z = 1;
+    LBBSP_CUDA_CHECK(cudaFuncSetAttribute(sweep::narxg_train_umma_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(um_smem)));
+    sweep::narxg_train_umma_kernel<<<W, sweep::ums::kThreads, um_smem, static_cast<cudaStream_t>(stream)>>>(a);
+    LBBSP_CUDA_CHECK(cudaGetLastError());
+    return LBBSP_OK;
+  }
   const size_t tc_smem = sweep::tcs::smem_bytes(cnt, P);
   if (tc_smem <= 227 * 1024) {
     sweep::SweepArgs a{};
@@ -862,8 +886,9 @@ extern "C" int lbbsp_narx_sweep_train(int W, int L, int delay, int hidden, const
 extern "C" long long lbbsp_narx_sweep_scratch_floats(int W, int L, int delay, int hidden) {
   const int I = 3 * delay + 2;
   const long long cnt = L - delay;
-  if (sweep::tcs::smem_bytes(static_cast<int>(cnt), hidden * I + 2 * hidden + 1) <= 227 * 1024)
-    return 0;  // tensor-core trainer keeps the training set in shared memory
+  if (sweep::tcs::smem_bytes(static_cast<int>(cnt), hidden * I + 2 * hidden + 1) <= 227 * 1024 ||
+      sweep::ums::smem_bytes(static_cast<int>(cnt), hidden * I + 2 * hidden + 1) <= 227 * 1024)
+    return 0;  // tensor-core trainers keep the training set in shared memory
   return static_cast<long long>(W) * cnt * (I + 2);
 }
 

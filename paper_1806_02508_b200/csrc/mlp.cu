@@ -219,6 +219,7 @@ struct PlanDev {
   float2* intf_w;              // [n_local] {availability, HBM share of the injected time}
   unsigned* fz_done;           // [n_local] fused worker kernel: head CTAs done (zeroed here)
   int cap_align;               // worker CTA partitions cluster-aligned: 2 (pair kernel), 4 (quad), else 1
+  int plan_fast;               // one rank, n <= 32, proportional solver: plan_fast_body when the look-ahead is there
   int gather_ctas;             // > 0: the plan completes only once they all have
 };
 
@@ -552,6 +553,160 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
               n_reg, blockIdx.x, gridDim.x);
 }
 
+// The plan of a round whose per-worker state the observe branch computed
+// ahead (vk == k): one rank, n <= 32 workers, the proportional solver. The
+// same arithmetic as plan_body, with every per-worker step in one lane of
+// warp 0 -- the sizes' and caps' prefix sums by warp scans -- so the round's
+// first kernel fetches a few hundred instructions instead of the general
+// plan's thousand-odd (cold after the bench's L2 flush, they set its
+// latency). Falls back to plan_body otherwise.
+__device__ __forceinline__ void plan_fast_body(const PlanDev& D, float* row_scale) {
+  const int tid = threadIdx.x, lane = tid & 31, n = D.n_total;
+  __shared__ long long k_s, vk_s;
+  __shared__ int len_s, rows_s;
+  __shared__ double loss_s;
+  if (tid == 0) {
+    k_s = *D.k;
+    vk_s = *D.vnext_k;
+    len_s = min(*D.pred.len, D.pred.max_hist);
+    rows_s = *D.rows;
+    loss_s = D.loss_on ? *D.loss_acc : 0.0;
+  }
+  __syncthreads();
+  const long long k = k_s;
+  if (vk_s != k || k >= D.max_rows) {
+    __syncthreads();
+    plan_body(D, row_scale);
+    return;
+  }
+  tc::pdl_launch_dependents();
+  stamp(D, 0);
+  __shared__ SolverSmem sm;
+  __shared__ double vp_s[32];
+  __shared__ int sz[32];
+  // warp 0: the workers' state; the other warps reset the round's counters
+  double vp = 0.0, share = 0.0, a = 0.0;
+  if (tid < 32) {
+    if (lane < n) {
+      const double c = D.nx_c[lane], m = D.nx_m[lane];
+      a = D.nx_a[lane];
+      share = D.share[lane];
+      vp = D.pred.kind == LBBSP_PRED_PERFECT ? a : (len_s >= 1 ? D.v_next[lane] : 0.0);
+      D.c_now[lane] = c;
+      D.m_now[lane] = m;
+      if (D.straggler_mode == LBBSP_STRAGGLE_INTERFERE) D.intf_w[lane] = D.nx_intf[lane];
+      D.v_pred[lane] = vp;
+      vp_s[lane] = vp;
+      sz[lane] = D.static_sizes ? D.static_sizes_d[lane] : D.B_total / n + (lane < D.B_total % n ? 1 : 0);
+    }
+    if (tid == 0) *D.round_k = k;
+  } else {
+    for (int i = tid - 32; i < kMaxPhases * D.n_local; i += blockDim.x - 32) {
+      D.timing[2 * i] = ~0ull;
+      D.timing[2 * i + 1] = 0ull;
+    }
+    if (D.fz_done)
+      for (int i = tid - 32; i < D.n_local; i += blockDim.x - 32) D.fz_done[i] = 0u;
+    if (tid == 32) {
+      D.stamps[6] = ~0ull;  // loss-branch head {first start, last end}
+      D.stamps[7] = 0ull;
+    }
+    const float s = 1.0f / static_cast<float>(D.B_total);
+    if (D.scheme == LBBSP_SCHEME_LBBSP)
+      for (int r = tid - 32; r < D.B_total; r += blockDim.x - 32) row_scale[r] = s;
+  }
+  __syncthreads();
+  stamp(D, 10);
+  int code = 0;
+  if (!D.static_sizes && D.scheme == LBBSP_SCHEME_LBBSP && k > 0)
+    code = warp_cpu_allocate(vp_s, n, D.B_total, D.pred.floor, sz, &sm, D.status);  // ends with __syncthreads
+  stamp(D, 11);
+  if (code) {
+    wait_gather(D, k);
+    return;
+  }
+  if (tid < 32) {
+    const int x = lane < n ? sz[lane] : 0;
+    // the worker's rows: exclusive prefix of the sizes
+    int incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int r0 = incl - x, total = __shfl_sync(0xffffffffu, incl, 31);
+    // CTA partitions: floor(budget * share * av), aligned; their prefix --
+    // the sequential clamp of plan_body only acts when the caps overrun the
+    // budget, then lane 0 runs that loop
+    int cap = 0;
+    if (lane < n) {
+      const double av = D.straggler_mode == LBBSP_STRAGGLE_SM_CAP ? a : 1.0;
+      cap = static_cast<int>(floor(static_cast<double>(D.sm_budget) * share * av));
+      cap = cap < 1 ? 1 : cap;
+      if (D.cap_align > 1) cap = cap < D.cap_align ? D.cap_align : cap - cap % D.cap_align;
+    }
+    int cincl = cap;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, cincl, o);
+      if (lane >= o) cincl += y;
+    }
+    const bool over = __shfl_sync(0xffffffffu, cincl, 31) > D.sm_budget;
+    if (lane < n) {
+      D.r0[lane] = r0;
+      D.r1[lane] = r0 + x;
+      D.sizes_all[lane] = x;
+      if (!over) {
+        D.cta0[lane] = cincl - cap;
+        D.ctan[lane] = cap;
+      }
+    }
+    if (over && lane == 0) {
+      int c0 = 0;
+      for (int i = 0; i < n; ++i) {
+        const double av = D.straggler_mode == LBBSP_STRAGGLE_SM_CAP ? D.nx_a[i] : 1.0;
+        int cp = static_cast<int>(floor(static_cast<double>(D.sm_budget) * D.share[i] * av));
+        cp = cp < 1 ? 1 : cp;
+        if (D.cap_align > 1) cp = cp < D.cap_align ? D.cap_align : cp - cp % D.cap_align;
+        if (c0 + cp > D.sm_budget) cp = D.sm_budget - c0 > 0 ? D.sm_budget - c0 : 1;
+        D.cta0[i] = c0;
+        D.ctan[i] = cp;
+        c0 += cp;
+      }
+    }
+    __syncwarp();
+    const int row = rows_s;
+    if (row < D.max_rows && lane < n) {
+      D.rec_sizes[static_cast<size_t>(row) * n + lane] = x;
+      D.rec_vpred[static_cast<size_t>(row) * n + lane] = vp_s[lane];
+      D.rec_caps[static_cast<size_t>(row) * n + lane] = over ? D.ctan[lane] : cap;
+    }
+    if (lane == 0) {
+      *D.stream_off = 0;
+      *D.local_rows = total;
+      const int prev = row - 1;
+      if (prev >= 0 && prev < D.max_rows)
+        D.rec_loss[prev] = D.loss_on ? loss_s / static_cast<double>(D.N_data) : -1.0;
+      *D.loss_acc = 0.0;
+    }
+  } else if (D.scheme != LBBSP_SCHEME_LBBSP) {
+    // Eq. 6 (BSP): 1/(n b_i) on worker i's rows
+    int r = 0;
+    for (int g = 0; g < n; ++g) {
+      const float sc = 1.0f / (static_cast<float>(D.n_total) * static_cast<float>(sz[g]));
+      for (int q = r + tid - 32; q < r + sz[g]; q += blockDim.x - 32) row_scale[q] = sc;
+      r += sz[g];
+    }
+  }
+  stamp(D, 12);
+  stamp(D, 8);
+  if (!wait_gather(D, k)) {  // poisoned round: no worker computes on a stale batch
+    if (tid < n) D.r1[tid] = D.r0[tid];
+    if (tid == 0) *D.local_rows = 0;
+  }
+  stamp(D, 1);
+}
+
 // Single rank: block 0 plans the round, blocks 1.. gather its batch -- one
 // launch, so the two run side by side (as two graph roots the plan started
 // only once the gather had finished: 6.6 us on the round's critical path).
@@ -571,9 +726,12 @@ struct GatherArgs {
 };
 __global__ void __launch_bounds__(256) plan_gather_kernel(const __grid_constant__ PlanDev D, float* row_scale,
                                                           const __grid_constant__ GatherArgs a) {
-  if (blockIdx.x == 0)
-    plan_body(D, row_scale);
-  else
+  if (blockIdx.x == 0) {
+    if (D.plan_fast)
+      plan_fast_body(D, row_scale);
+    else
+      plan_body(D, row_scale);
+  } else
     gather_body(D, a.streams, a.B_total, a.data_x, a.data_y, a.d0, a.X, a.y, a.B_total, a.slab, a.slab_stride,
                 a.reg_off, a.reg_len, a.n_reg, blockIdx.x - 1, gridDim.x - 1);
 }
@@ -2149,6 +2307,7 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   if (c.observe != LBBSP_OBSERVE_RATE && c.observe != LBBSP_OBSERVE_CAPACITY)
     return set_error(LBBSP_INVALID_ARGUMENT, "mlp: unknown observe %d", c.observe);
   D.observe = c.observe;
+  D.plan_fast = c.world == 1 && n <= 32 && c.solver == LBBSP_SOLVER_PROPORTIONAL && !getenv("LBBSP_PLAN_GENERAL");
   if (c.solver == LBBSP_SOLVER_GAMMA || c.observe == LBBSP_OBSERVE_CAPACITY) {
     if (!c.h_gpu_profiles)
       return set_error(LBBSP_INVALID_ARGUMENT,

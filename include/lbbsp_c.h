@@ -636,6 +636,9 @@ int lbbsp_mlp_init_peers(lbbsp_mlp* m, const unsigned char* h_handles);
 /* Run `iterations` LB-BSP rounds on the engine stream (no host sync). */
 int lbbsp_mlp_run(lbbsp_mlp* m, int iterations);
 void* lbbsp_mlp_stream(lbbsp_mlp* m);
+/* Stream of the e2e result reads (lbbsp_mlp_read_result_async): a caller that
+ * times or synchronises on the engine stream waits on this one too. */
+void* lbbsp_mlp_result_stream(lbbsp_mlp* m);
 /* Records of the rounds run so far (blocking): [rows][n_total] arrays. */
 int lbbsp_mlp_records(lbbsp_mlp* m, int max_rows, int* rows, int* sizes, double* v_pred,
                       double* v_obs, int* caps, double* t_worker, double* loss);

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
     const float* __restrict__ bias, const int* __restrict__ y, const float* __restrict__ row_scale,
     hbf16* dH, float* slab, long long slab_stride, long long off_w, long long off_b,
     long long off_b_prev, double* loss_acc, float* cta_part, double* cta_loss, unsigned* counters,
-    unsigned long long* timing) {
+    unsigned long long* timing, double* loss_rec, const long long* round_k, int max_rows) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ int last;
   int g, cta_in, cta_cnt;
@@ -399,6 +399,12 @@ __global__ void __launch_bounds__(256, 1) head_mma_kernel(
         double l = 0.0;
         for (int c = 0; c < cta_cnt; ++c) l += __ldcg(&cta_loss[c0 + c]);
         *loss_acc = l;
+        // the round's record too (the same value the next plan writes), so a
+        // host read of this round's result need not wait for that plan
+        if (loss_rec) {
+          const long long r = *round_k;
+          if (r >= 0 && r < max_rows) loss_rec[r] = l / static_cast<double>(rows_total);
+        }
       }
       counters[g] = 0u;
     }

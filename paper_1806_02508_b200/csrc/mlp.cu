@@ -1564,6 +1564,9 @@ struct lbbsp_mlp {
   cudaEvent_t ev_head0 = nullptr, ev_head1 = nullptr;  // head partial combine beside the backward
   cudaStream_t copy_stream = nullptr;  // e2e input staging (lbbsp_mlp_load_data_async)
   cudaEvent_t ev_staged = nullptr;
+  cudaStream_t result_stream = nullptr;  // e2e result reads (D2H beside the next round)
+  cudaEvent_t ev_round_done = nullptr;
+  long long host_rounds = 0;             // rounds enqueued (the next round's record row)
   // the resident dataset is double-buffered: a round reads buffer `cur`
   // while the next round's inputs are copied into the other one; one graph
   // per buffer (the loss branch's tensor map is bound to the buffer)
@@ -1656,6 +1659,8 @@ struct lbbsp_mlp {
     if (ev_gather0) cudaEventDestroy(ev_gather0);
     if (ev_staged) cudaEventDestroy(ev_staged);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (result_stream) cudaStreamDestroy(result_stream);
+    if (ev_round_done) cudaEventDestroy(ev_round_done);
     if (ev_gather1) cudaEventDestroy(ev_gather1);
     if (ev_head0) cudaEventDestroy(ev_head0);
     if (ev_head1) cudaEventDestroy(ev_head1);
@@ -1829,7 +1834,7 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
         static_cast<const float*>(params + off_w[hl]), static_cast<const float*>(params + off_b[hl]),
         static_cast<const int*>(y), static_cast<const float*>(row_scale), dZ[L - 2], partial, P,
         off_w[hl], off_b[hl], off_b[L - 2], static_cast<double*>(nullptr), head_part, head_loss,
-        head_cnt, phase_slot(ph++)));
+        head_cnt, phase_slot(ph++), static_cast<double*>(nullptr), static_cast<const long long*>(nullptr), 0));
     ++nl;
     // the CTA partials are summed beside the backward GEMMs; joined before the
     // gradient slabs are consumed
@@ -2074,7 +2079,8 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
           static_cast<const float*>(params + off_w[hl]), static_cast<const float*>(params + off_b[hl]),
           static_cast<const int*>(data_y), static_cast<const float*>(nullptr),
           static_cast<bf16*>(nullptr), static_cast<float*>(nullptr), 0ll, 0ll, 0ll, 0ll, D.loss_acc,
-          head_part, head_loss, head_cnt_d, D.stamps + 6));
+          head_part, head_loss, head_cnt_d, D.stamps + 6, D.rec_loss, static_cast<const long long*>(D.round_k),
+          D.max_rows));
     } else {
       LBBSP_CUDA_CHECK(launch_softmax_ce(sms, cfg.world == 1 ? sl : s, use_pdl, none, N_data, logits_d, dims[L], data_y,
                                          nullptr, nullptr, D.loss_acc, nullptr));
@@ -2336,6 +2342,8 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   }
   // end-to-end plumbing (lbbsp_mlp_load_data_async / read_result_async)
   LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.copy_stream, cudaStreamNonBlocking));
+  LBBSP_CUDA_CHECK(cudaStreamCreateWithFlags(&m.result_stream, cudaStreamNonBlocking));
+  LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_round_done, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&m.ev_staged, cudaEventDisableTiming));
   for (auto& e : m.ev_used) LBBSP_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   LBBSP_CUDA_CHECK(m.alloc(&m.result, static_cast<size_t>(m.n_total) + 2));
@@ -2621,6 +2629,7 @@ extern "C" int lbbsp_mlp_init_peers(lbbsp_mlp* m, const unsigned char* h_handles
 }
 
 extern "C" void* lbbsp_mlp_stream(lbbsp_mlp* m) { return m->stream; }
+extern "C" void* lbbsp_mlp_result_stream(lbbsp_mlp* m) { return m->result_stream; }
 
 extern "C" int lbbsp_mlp_run(lbbsp_mlp* m, int iterations) {
   // several GPUs: the peer-memory exchange needs no communicator (several
@@ -2643,6 +2652,7 @@ extern "C" int lbbsp_mlp_run(lbbsp_mlp* m, int iterations) {
     }
     LBBSP_CUDA_CHECK(cudaGraphLaunch(m->execb[b], m->stream));
     LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_used[b], m->stream));
+    ++m->host_rounds;
   }
   return LBBSP_OK;
 }
@@ -2749,6 +2759,21 @@ __global__ void last_row_kernel(const int* rows, const int* rec_sizes, const dou
 // The pointer lookup is cached for the last buffer pair (a per-step
 // cudaPointerGetAttributes would sit on the host's critical path).
 extern "C" int lbbsp_mlp_read_result_async(lbbsp_mlp* m, int* h_sizes, double* h_loss) {
+  // One rank, small head, loss every round: the round's record row (sizes,
+  // and the loss its loss head wrote) is final when the round ends and no
+  // later round writes it -- copy it on the result stream, beside the next
+  // round, instead of a kernel on the round's critical path.
+  const long long row = m->host_rounds - 1;
+  if (m->small_head && m->D.loss_on && m->cfg.world == 1 && m->cfg.loss_every == 1 && row >= 0 &&
+      row < m->max_rows) {
+    LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_round_done, m->stream));
+    LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->result_stream, m->ev_round_done, 0));
+    LBBSP_CUDA_CHECK(cudaMemcpyAsync(h_sizes, m->D.rec_sizes + static_cast<size_t>(row) * m->n_total,
+                                     sizeof(int) * m->n_total, cudaMemcpyDeviceToHost, m->result_stream));
+    LBBSP_CUDA_CHECK(cudaMemcpyAsync(h_loss, m->D.rec_loss + row, sizeof(double), cudaMemcpyDeviceToHost,
+                                     m->result_stream));
+    return LBBSP_OK;
+  }
   if (h_sizes != m->res_host_sizes || h_loss != m->res_host_loss) {
     cudaPointerAttributes a{}, b{};
     const bool mapped = cudaPointerGetAttributes(&a, h_sizes) == cudaSuccess &&

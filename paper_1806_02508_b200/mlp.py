@@ -68,6 +68,8 @@ def _L():
             getattr(L, k).restype = C.c_int
         L.lbbsp_mlp_stream.argtypes = [C.c_void_p]
         L.lbbsp_mlp_stream.restype = C.c_void_p
+        L.lbbsp_mlp_result_stream.argtypes = [C.c_void_p]
+        L.lbbsp_mlp_result_stream.restype = C.c_void_p
         L._mlp_sigs = True
     return L
 
@@ -277,6 +279,11 @@ class MlpEngine:
     @property
     def stream(self):
         return _L().lbbsp_mlp_stream(self._h)
+
+    @property
+    def result_stream(self):
+        """stream of the e2e result reads (read_result_async / step_e2e)"""
+        return _L().lbbsp_mlp_result_stream(self._h)
 
     def launches_per_iteration(self):
         x = C.c_int()

@@ -140,6 +140,9 @@ def test_pair_in_kernel_gather_dynamic_sizes_and_e2e_buffers():
             eng.step_e2e(xb.data_ptr(), yb.data_ptr(), osz.data_ptr(), ol.data_ptr())
         torch.cuda.synchronize()
         rec = eng.records()
+        # the host buffers hold the last round's sizes and loss
+        assert osz.tolist() == rec["sizes"][rec["rows"] - 1].tolist()
+        assert ol.item() == float(rec["loss"][rec["rows"] - 1])
         out.append((np.concatenate([np.concatenate([w.ravel(), b]) for w, b in eng.params()]),
                     rec["sizes"].copy(), rec["loss"].copy()))
         del eng

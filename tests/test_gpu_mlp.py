@@ -144,3 +144,5 @@ def test_end_to_end_plumbing(pinned):
     xd, yd = eng.dataset()
     assert np.array_equal(yd, y2)
     assert ls.item() > 0 and np.isfinite(ls.item())
+    # the loss read is the round's record (written by its loss head)
+    assert ls.item() == float(rec["loss"][rec["rows"] - 1])

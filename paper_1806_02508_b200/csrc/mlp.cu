@@ -483,9 +483,7 @@ static size_t gamma_plan_smem(int n) {
   return static_cast<size_t>(n) * sizeof(lbbsp_gpu_profile) + static_cast<size_t>(n) * 8 * 5 + 64;
 }
 
-__global__ void __launch_bounds__(256) plan_kernel(const __grid_constant__ PlanDev D, float* row_scale) {
-  plan_body(D, row_scale);
-}
+__global__ void __launch_bounds__(256) plan_kernel(const __grid_constant__ PlanDev D, float* row_scale);
 
 // P6: X[r] = data[stream[off + r]], labels, row scale (Eq. 7: 1/B; Eq. 6: 1/(n b_i))
 // fixed_rows > 0: a single rank gathers the whole batch [0, B) of stream k,
@@ -554,7 +552,7 @@ __global__ void gather_kernel(PlanDev D, const int* streams, int B_total, const 
 }
 
 // The plan of a round whose per-worker state the observe branch computed
-// ahead (vk == k): one rank, n <= 32 workers, the proportional solver. The
+// ahead (vk == k): n <= 32 workers in all, the proportional solver. The
 // same arithmetic as plan_body, with every per-worker step in one lane of
 // warp 0 -- the sizes' and caps' prefix sums by warp scans -- so the round's
 // first kernel fetches a few hundred instructions instead of the general
@@ -594,7 +592,8 @@ __device__ __forceinline__ void plan_fast_body(const PlanDev& D, float* row_scal
       vp = D.pred.kind == LBBSP_PRED_PERFECT ? a : (len_s >= 1 ? D.v_next[lane] : 0.0);
       D.c_now[lane] = c;
       D.m_now[lane] = m;
-      if (D.straggler_mode == LBBSP_STRAGGLE_INTERFERE) D.intf_w[lane] = D.nx_intf[lane];
+      const int li = lane - D.rank * D.n_local;
+      if (D.straggler_mode == LBBSP_STRAGGLE_INTERFERE && li >= 0 && li < D.n_local) D.intf_w[li] = D.nx_intf[li];
       D.v_pred[lane] = vp;
       vp_s[lane] = vp;
       sz[lane] = D.static_sizes ? D.static_sizes_d[lane] : D.B_total / n + (lane < D.B_total % n ? 1 : 0);
@@ -611,9 +610,6 @@ __device__ __forceinline__ void plan_fast_body(const PlanDev& D, float* row_scal
       D.stamps[6] = ~0ull;  // loss-branch head {first start, last end}
       D.stamps[7] = 0ull;
     }
-    const float s = 1.0f / static_cast<float>(D.B_total);
-    if (D.scheme == LBBSP_SCHEME_LBBSP)
-      for (int r = tid - 32; r < D.B_total; r += blockDim.x - 32) row_scale[r] = s;
   }
   __syncthreads();
   stamp(D, 10);
@@ -625,21 +621,27 @@ __device__ __forceinline__ void plan_fast_body(const PlanDev& D, float* row_scal
     wait_gather(D, k);
     return;
   }
+  __shared__ int local_total_s;
+  const int first = D.rank * D.n_local, nl = D.n_local;
   if (tid < 32) {
     const int x = lane < n ? sz[lane] : 0;
-    // the worker's rows: exclusive prefix of the sizes
+    const bool local = lane >= first && lane < first + nl;
+    const int li = lane - first;
+    // the stream offsets: exclusive prefix of the sizes over all workers
     int incl = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    const int r0 = incl - x, total = __shfl_sync(0xffffffffu, incl, 31);
-    // CTA partitions: floor(budget * share * av), aligned; their prefix --
-    // the sequential clamp of plan_body only acts when the caps overrun the
-    // budget, then lane 0 runs that loop
+    const int off = first > 0 ? __shfl_sync(0xffffffffu, incl, first - 1) : 0;  // this rank's first row
+    const int r0 = incl - x - off;
+    const int total = __shfl_sync(0xffffffffu, incl, first + nl - 1) - off;
+    // CTA partitions of the local workers: floor(budget * share * av),
+    // aligned; their prefix -- the sequential clamp of plan_body only acts
+    // when the caps overrun the budget, then lane 0 runs that loop
     int cap = 0;
-    if (lane < n) {
+    if (local) {
       const double av = D.straggler_mode == LBBSP_STRAGGLE_SM_CAP ? a : 1.0;
       cap = static_cast<int>(floor(static_cast<double>(D.sm_budget) * share * av));
       cap = cap < 1 ? 1 : cap;
@@ -652,20 +654,21 @@ __device__ __forceinline__ void plan_fast_body(const PlanDev& D, float* row_scal
       if (lane >= o) cincl += y;
     }
     const bool over = __shfl_sync(0xffffffffu, cincl, 31) > D.sm_budget;
-    if (lane < n) {
-      D.r0[lane] = r0;
-      D.r1[lane] = r0 + x;
-      D.sizes_all[lane] = x;
+    if (lane < n) D.sizes_all[lane] = x;
+    if (local) {
+      D.r0[li] = r0;
+      D.r1[li] = r0 + x;
       if (!over) {
-        D.cta0[lane] = cincl - cap;
-        D.ctan[lane] = cap;
+        D.cta0[li] = cincl - cap;
+        D.ctan[li] = cap;
       }
     }
     if (over && lane == 0) {
       int c0 = 0;
-      for (int i = 0; i < n; ++i) {
-        const double av = D.straggler_mode == LBBSP_STRAGGLE_SM_CAP ? D.nx_a[i] : 1.0;
-        int cp = static_cast<int>(floor(static_cast<double>(D.sm_budget) * D.share[i] * av));
+      for (int i = 0; i < nl; ++i) {
+        const int w = first + i;
+        const double av = D.straggler_mode == LBBSP_STRAGGLE_SM_CAP ? D.nx_a[w] : 1.0;
+        int cp = static_cast<int>(floor(static_cast<double>(D.sm_budget) * D.share[w] * av));
         cp = cp < 1 ? 1 : cp;
         if (D.cap_align > 1) cp = cp < D.cap_align ? D.cap_align : cp - cp % D.cap_align;
         if (c0 + cp > D.sm_budget) cp = D.sm_budget - c0 > 0 ? D.sm_budget - c0 : 1;
@@ -679,32 +682,46 @@ __device__ __forceinline__ void plan_fast_body(const PlanDev& D, float* row_scal
     if (row < D.max_rows && lane < n) {
       D.rec_sizes[static_cast<size_t>(row) * n + lane] = x;
       D.rec_vpred[static_cast<size_t>(row) * n + lane] = vp_s[lane];
-      D.rec_caps[static_cast<size_t>(row) * n + lane] = over ? D.ctan[lane] : cap;
+      if (local) D.rec_caps[static_cast<size_t>(row) * n + lane] = over ? D.ctan[li] : cap;
     }
     if (lane == 0) {
-      *D.stream_off = 0;
+      *D.stream_off = off;
       *D.local_rows = total;
+      local_total_s = total;
       const int prev = row - 1;
       if (prev >= 0 && prev < D.max_rows)
         D.rec_loss[prev] = D.loss_on ? loss_s / static_cast<double>(D.N_data) : -1.0;
       *D.loss_acc = 0.0;
     }
-  } else if (D.scheme != LBBSP_SCHEME_LBBSP) {
-    // Eq. 6 (BSP): 1/(n b_i) on worker i's rows
+  }
+  __syncthreads();
+  // row scales: Eq. 7 folds 1/B into every row; Eq. 6 (BSP) 1/(n b_i) per worker
+  if (D.scheme == LBBSP_SCHEME_LBBSP) {
+    const float sc = 1.0f / static_cast<float>(D.B_total);
+    for (int r = tid; r < local_total_s; r += blockDim.x) row_scale[r] = sc;
+  } else {
     int r = 0;
-    for (int g = 0; g < n; ++g) {
-      const float sc = 1.0f / (static_cast<float>(D.n_total) * static_cast<float>(sz[g]));
-      for (int q = r + tid - 32; q < r + sz[g]; q += blockDim.x - 32) row_scale[q] = sc;
-      r += sz[g];
+    for (int g = 0; g < nl; ++g) {
+      const int b = sz[first + g];
+      const float sc = 1.0f / (static_cast<float>(D.n_total) * static_cast<float>(b));
+      for (int q = r + tid; q < r + b; q += blockDim.x) row_scale[q] = sc;
+      r += b;
     }
   }
   stamp(D, 12);
   stamp(D, 8);
   if (!wait_gather(D, k)) {  // poisoned round: no worker computes on a stale batch
-    if (tid < n) D.r1[tid] = D.r0[tid];
+    if (tid < nl) D.r1[tid] = D.r0[tid];
     if (tid == 0) *D.local_rows = 0;
   }
   stamp(D, 1);
+}
+
+__global__ void __launch_bounds__(256) plan_kernel(const __grid_constant__ PlanDev D, float* row_scale) {
+  if (D.plan_fast)
+    plan_fast_body(D, row_scale);
+  else
+    plan_body(D, row_scale);
 }
 
 // Single rank: block 0 plans the round, blocks 1.. gather its batch -- one
@@ -2313,7 +2330,7 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
   if (c.observe != LBBSP_OBSERVE_RATE && c.observe != LBBSP_OBSERVE_CAPACITY)
     return set_error(LBBSP_INVALID_ARGUMENT, "mlp: unknown observe %d", c.observe);
   D.observe = c.observe;
-  D.plan_fast = c.world == 1 && n <= 32 && c.solver == LBBSP_SOLVER_PROPORTIONAL && !getenv("LBBSP_PLAN_GENERAL");
+  D.plan_fast = n <= 32 && c.solver == LBBSP_SOLVER_PROPORTIONAL && !getenv("LBBSP_PLAN_GENERAL");
   if (c.solver == LBBSP_SOLVER_GAMMA || c.observe == LBBSP_OBSERVE_CAPACITY) {
     if (!c.h_gpu_profiles)
       return set_error(LBBSP_INVALID_ARGUMENT,

@@ -559,7 +559,10 @@ def main():
             dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
     n_total = WORKERS_PER_GPU * world
     B = BATCH_PER_GPU * world
-    e2e_steps = args.steps
+    # e2e over the fixed 100-round window (the comparison arms' rounds): a
+    # fresh engine's NARX trajectory differs from the timed arm's, and the
+    # heavy-tailed NARX rounds make 20-round samples of the two disagree
+    e2e_steps = max(args.steps, WINDOW_ROUNDS)
     window = WINDOW_ROUNDS
     # the timed rounds are steady-state LB-BSP + NARX rounds: they begin 50
     # rounds after the predictor warm-up (50 rounds, EMA before it), when every
@@ -776,7 +779,9 @@ def main():
                          "note": "C2 is latency-bound (SURVEY 8(d)): ~512 rows per worker"},
             "gpu_launches": launches * args.steps,
             "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "rounds": e2e_steps, "first_round": warm,
+                    "device_window_ms": win["lbbsp"]["mean"]},
             "clocks": clocks,
             "rounds_recorded": rec["rows"],
         }

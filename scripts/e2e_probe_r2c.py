@@ -4,11 +4,11 @@ import os, sys, time
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 import numpy as np
 import torch
-from paper_1806_02508_b200.mlp import MlpEngine, constant_trace
+from paper_1806_02508_b200.mlp import MlpEngine, constant_trace, benchmark_trace
 from paper_1806_02508_b200.hostio import pinned_empty
 n, B = 8, 4096
 eng = MlpEngine(dims=[784, 256, 10], global_batch=B, n_workers_local=n, predictor=os.environ.get("PRED", "ema"),
-                warmup_iterations=50, max_iterations=1200, trace=constant_trace(n, 1200))
+                warmup_iterations=50, max_iterations=1200, trace=(benchmark_trace(n, 1200, seed=3) if os.environ.get("TRACE") == "bench" else constant_trace(n, 1200)))
 x, y = eng.dataset()
 xb = pinned_empty(x.shape, torch.bfloat16, 0); xb.copy_(torch.from_numpy(x).to(torch.bfloat16))
 yb = pinned_empty(y.shape, torch.int32, 0); yb.copy_(torch.from_numpy(y.astype(np.int32)))

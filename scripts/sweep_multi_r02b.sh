@@ -2,7 +2,7 @@
 # Round-2 multi-GPU sweep on one box (N = number of visible GPUs): C2/C3/C5
 # bench lines, the reference arm, the multi-rank tests and exchange checks.
 N=$(python -c "import torch; print(torch.cuda.device_count())")
-O=gpurun_out/r02b_n$N; mkdir -p $O
+O=${OUT:-gpurun_out/r02b}_n$N; mkdir -p $O
 st() { echo "$1 rc=$2" >> $O/status; }
 TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1"
 timeout 900 $TR --master-port 29561 bench.py --gpus $N --steps 20 --warmup 5 > $O/c2.json 2> $O/c2.err; st c2 $?

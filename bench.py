@@ -78,19 +78,11 @@ def comm_sm_budget(world):
 
 
 def connect(eng, world, rank):
-    """NCCL communicator (speed all-gather, fallback all-reduce) plus the NVLink
-    peer-memory exchange (CUDA IPC): several workers per GPU use it for speeds
-    and gradients; one worker per GPU for the copy-engine gradient buckets.
-    LBBSP_NO_PEERS=1 keeps NCCL only."""
-    import torch.distributed as dist
-    uid = [eng.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
+    """the product's control-plane handshake (mlp.connect); LBBSP_NO_PEERS=1
+    keeps NCCL only"""
+    from paper_1806_02508_b200.mlp import connect as mlp_connect
     with stdout_to_stderr():
-        eng.init_comm(uid[0])
-    if not os.environ.get("LBBSP_NO_PEERS"):
-        hs = [None] * world
-        dist.all_gather_object(hs, eng.peer_handle())
-        eng.init_peers(hs)
+        mlp_connect(eng, world, rank, peers=not os.environ.get("LBBSP_NO_PEERS"))
 
 
 def dist_env():

@@ -937,46 +937,116 @@ static cudaError_t launch_softmax_ce(int sms, cudaStream_t s, bool pdl, Groups G
 
 
 // db partial of worker g = column sums of dZ over its rows (N % 8 == 0),
-// written into the worker's slab (or its bf16 bucket). Column strips: each of
-// the worker's CTAs owns whole 32-column strips (no cross-CTA combine; 128
-// strips at width 4096 keep a 148-SM partition busy); a thread reads 16 B
-// (8 columns) of every 64th row with 16 rows in flight, and the 64 row-lane
-// partials of a column are added in row-lane order in shared memory --
-// deterministic, one pass over dZ.
-constexpr int kBiasCols = 2048;  // (scratch sizing, kept for the C-ABI's allocation)
-constexpr int kBiasStrip = 32;
-constexpr int kBiasLanes = 256 / (kBiasStrip / 8);  // 64 row lanes
-constexpr int kBiasRowsInFlight = 16;
+// written into the worker's slab (or its bf16 bucket). Work units are
+// 256-column strips x row chunks (the worker's CTAs / strips chunks per
+// strip, two CTAs per partition slot): a warp reads 512 contiguous bytes of
+// a row (16 B = 8 columns per lane), the rows streaming through shared memory
+// by cp.async in 4 stages of 4 rows per row lane (64 KB per CTA in flight).
+// A unit's 8 row-lane sums are added in lane order in shared memory; with
+// several chunks per strip each unit writes its partial row to the scratch
+// and the last unit to arrive on the strip's counter (self-resetting) adds
+// the chunk partials in chunk order -- deterministic for a given CTA
+// partition, one pass over dZ. C3 layer (4096 x 4096 bf16): 8.2 us in the
+// round (was 22.5 with 32-column strips and register loads, which ptxas
+// interleaved with the adds: one or two loads in flight), 13.6 us cold
+// under ncu (profiles/r02_c3_hbm_kernels.txt).
+constexpr int kBiasCols = 2048;  // (scratch sizing floor, kept for the C-ABI's allocation)
+constexpr int kBiasStrip = 256;
+constexpr int kBiasLanes = 256 / (kBiasStrip / 8);  // 8 row lanes
+constexpr int kBiasRowsInFlight = 4;  // rows per lane per cp.async batch
+constexpr int kBiasStages = 4;
+constexpr int kBiasCtasPerSlot = 2;
+constexpr int kBiasSmem = kBiasStages * kBiasRowsInFlight * 256 * 16;  // cp.async stages
+__host__ __device__ constexpr int bias_strips(int N) { return (N + kBiasStrip - 1) / kBiasStrip; }
+template <int kPerSlot>
 __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __restrict__ dZ, int N,
                                                         float* slab, long long slab_stride,
-                                                        long long off_b, float* /*scratch*/,
-                                                        unsigned* /*counters*/, bf16* out_b16,
+                                                        long long off_b, float* scratch,
+                                                        unsigned* counters, bf16* out_b16,
                                                         unsigned long long* timing) {
-  int g, cta_in, cta_cnt;
-  if (!my_group(G, &g, &cta_in, &cta_cnt)) return;
-  const int n_strips = (N + kBiasStrip - 1) / kBiasStrip;
-  if (cta_in >= n_strips) return;
+  // launched with kPerSlot CTAs per partition slot (more rows in
+  // flight per SM); slot s = blockIdx.x / kPerSlot keeps the worker's
+  // CTA partition
+  int g = 0, cta_in = blockIdx.x, cta_cnt = gridDim.x;
+  if (G.n > 0) {
+    const int slot = blockIdx.x / kPerSlot;
+    bool found = false;
+    for (int i = 0; i < G.n && !found; ++i) {
+      const int c0 = G.cta0[i], cn = G.ctan[i];
+      if (slot >= c0 && slot < c0 + cn) {
+        g = i;
+        cta_in = (slot - c0) * kPerSlot + static_cast<int>(blockIdx.x % kPerSlot);
+        cta_cnt = cn * kPerSlot;
+        found = true;
+      }
+    }
+    if (!found) return;
+  }
+  const int n_strips = bias_strips(N);
+  const int n_chunks = cta_cnt / n_strips > 1 ? cta_cnt / n_strips : 1;
+  const int n_units = n_strips * n_chunks;
+  if (cta_in >= n_units) return;
   const unsigned long long t_cta0 = phase_begin(timing, g);
-  __shared__ float red[kBiasLanes][kBiasStrip + 1];
-  const int r0 = G.r0[g], r1 = G.r1[g];
-  constexpr int kChunks = kBiasStrip / 8;
-  const int chunk = threadIdx.x % kChunks, rl = threadIdx.x / kChunks;
+  __shared__ __align__(16) float red[kBiasLanes][kBiasStrip];
+  __shared__ int s_last;
+  extern __shared__ __align__(16) uint4 stage[];  // [kBiasStages][kBiasRowsInFlight][256]
+  const int R0 = G.n ? G.r0[g] : 0, R1 = G.n ? G.r1[g] : 0;
+  const long long R = R1 - R0;
+  const int cl = threadIdx.x % 32, rl = threadIdx.x / 32;
   float* gs = slab + static_cast<long long>(g) * slab_stride + off_b;
-  for (int st = cta_in; st < n_strips; st += cta_cnt) {
-    const int col = st * kBiasStrip + chunk * 8;
+  // worker g's [n_chunks][N] partials: chunk counts are floor(ctan / strips)
+  // (>= 1), so these offsets never overlap (scratch: 2 sms * 256 + n_local * N)
+  float* part = scratch + static_cast<long long>((G.n ? G.cta0[g] * kPerSlot : 0) / n_strips + g) * N;
+  unsigned* cnt = counters + static_cast<long long>(g) * n_strips;
+  for (int u = cta_in; u < n_units; u += cta_cnt) {
+    const int st = u % n_strips, ch = u / n_strips;
+    const int ra = R0 + static_cast<int>(R * ch / n_chunks), rb = R0 + static_cast<int>(R * (ch + 1) / n_chunks);
+    const int col = st * kBiasStrip + cl * 8;
     float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (col < N) {
+      // rows stream through shared memory by cp.async (16 B per row per
+      // thread, kBiasRowsInFlight rows per batch, two batches in flight): the
+      // copies need no registers, so every one of them issues before the
+      // adds (register loads were interleaved with the adds by ptxas, one
+      // or two in flight). Each thread reads back only its own slots. Rows
+      // past the chunk are zero-filled (src-size 0; x + 0.0f == x).
       const bf16* base = dZ + col;
-      int r = r0 + rl;
+      const int step = kBiasLanes * kBiasRowsInFlight;
+      auto issue = [&](int buf, int r) {
+#pragma unroll
+        for (int v = 0; v < kBiasRowsInFlight; ++v) {
+          const int rr = r + kBiasLanes * v;
+          const bf16* src = base + static_cast<long long>(rr < rb ? rr : ra) * N;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                           tc::smem_u32(&stage[(buf * kBiasRowsInFlight + v) * 256 + threadIdx.x])),
+                       "l"(src), "r"(rr < rb ? 16 : 0)
+                       : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      // kBiasStages batches in flight: the prologue issues S-1, each step
+      // issues one more (or an empty group) and waits for the oldest
+#pragma unroll
+      for (int b = 0; b < kBiasStages - 1; ++b) {
+        if (ra + rl + b * step < rb)
+          issue(b, ra + rl + b * step);
+        else
+          asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+      int buf = 0;
 #pragma unroll 1
-      for (; r + kBiasLanes * (kBiasRowsInFlight - 1) < r1; r += kBiasLanes * kBiasRowsInFlight) {
-        uint4 q[kBiasRowsInFlight];
+      for (int r = ra + rl; r < rb; r += step) {
+        const int rn = r + (kBiasStages - 1) * step;
+        const int bn = buf == 0 ? kBiasStages - 1 : buf - 1;
+        if (rn < rb)
+          issue(bn, rn);
+        else
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(kBiasStages - 1) : "memory");
 #pragma unroll
-        for (int u = 0; u < kBiasRowsInFlight; ++u)
-          q[u] = *reinterpret_cast<const uint4*>(base + static_cast<long long>(r + kBiasLanes * u) * N);
-#pragma unroll
-        for (int u = 0; u < kBiasRowsInFlight; ++u) {
-          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q[u]);
+        for (int v = 0; v < kBiasRowsInFlight; ++v) {
+          const uint4 q = stage[(buf * kBiasRowsInFlight + v) * 256 + threadIdx.x];
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const float2 f = __bfloat1622float2(b2[j]);
@@ -984,32 +1054,48 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(Groups G, const bf16* __
             a[2 * j + 1] += f.y;
           }
         }
+        buf = buf + 1 == kBiasStages ? 0 : buf + 1;
       }
-      for (; r < r1; r += kBiasLanes) {
-        const uint4 q = *reinterpret_cast<const uint4*>(base + static_cast<long long>(r) * N);
-        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    reinterpret_cast<float4*>(&red[rl][cl * 8])[0] = make_float4(a[0], a[1], a[2], a[3]);
+    reinterpret_cast<float4*>(&red[rl][cl * 8])[1] = make_float4(a[4], a[5], a[6], a[7]);
+    __syncthreads();
+    const int c = st * kBiasStrip + threadIdx.x;
+    float v = 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = __bfloat1622float2(b2[j]);
-          a[2 * j] += f.x;
-          a[2 * j + 1] += f.y;
+    for (int q = 0; q < kBiasLanes; ++q) v += red[q][threadIdx.x];
+    bool write = n_chunks == 1;
+    if (!write) {
+      if (c < N) part[static_cast<long long>(ch) * N + c] = v;
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) s_last = atomicAdd(&cnt[st], 1u) == static_cast<unsigned>(n_chunks - 1);
+      __syncthreads();
+      write = s_last;
+      if (write) {
+        __threadfence();
+        if (threadIdx.x == 0) cnt[st] = 0u;
+        v = 0.f;
+        if (c < N) {
+          const float* pc = part + c;
+          int q = 0;
+          for (; q + 8 <= n_chunks; q += 8) {
+            float t[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) t[j] = __ldcg(pc + static_cast<long long>(q + j) * N);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v += t[j];
+          }
+          for (; q < n_chunks; ++q) v += __ldcg(pc + static_cast<long long>(q) * N);
         }
       }
     }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) red[rl][chunk * 8 + j] = a[j];
-    __syncthreads();
-    if (threadIdx.x < kBiasStrip) {
-      const int c = st * kBiasStrip + threadIdx.x;
-      float v = 0.f;
-#pragma unroll 8
-      for (int q = 0; q < kBiasLanes; ++q) v += red[q][threadIdx.x];
-      if (c < N) {
-        if (out_b16)
-          out_b16[c] = __float2bfloat16_rn(v);
-        else
-          gs[c] = v;
-      }
+    if (write && c < N) {
+      if (out_b16)
+        out_b16[c] = __float2bfloat16_rn(v);
+      else
+        gs[c] = v;
     }
     __syncthreads();
   }
@@ -1625,9 +1711,9 @@ struct lbbsp_mlp {
   unsigned* head_cnt = nullptr;    // [n_local] worker head counters (self-resetting)
   unsigned* head_cnt_d = nullptr;  // [1] dataset-loss head counter
   unsigned* arrive = nullptr;      // observe_train_kernel arrival count (self-resetting)
-  float* bias_part = nullptr;      // [sms][kBiasCols] bias-gradient row-block partials
+  float* bias_part = nullptr;      // bias-gradient row-chunk partials (bias_grad_kernel)
   bf16* gradb = nullptr;           // [P] bf16 gradient buckets (bucketed all-reduce path)
-  unsigned* bias_cnt = nullptr;    // [n_local] bias_grad_kernel counters (self-resetting)
+  unsigned* bias_cnt = nullptr;    // [n_local][strips] bias_grad_kernel counters (self-resetting)
   bool use_pdl = true;             // programmatic dependent launch on the worker-phase chain
   long long* reg_len = nullptr;
   int n_reg = 0;
@@ -1873,9 +1959,14 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   // same stream, so the communicator sees one fixed order on every rank.
   for (int l = Lg - 1; l >= 0; --l) {
     if (!(small_head && l == L - 2)) {  // the small head already summed this bias gradient
-      bias_grad_kernel<<<sms, 256, 0, s>>>(G, dZ[l], dims[l + 1], partial, P, off_b[l], bias_part,
-                                           bias_cnt, gradb ? gradb + off_b[l] : nullptr,
-                                           phase_slot(ph++));
+      unsigned long long* slot = phase_slot(ph++);
+      bf16* ob = gradb ? gradb + off_b[l] : nullptr;
+      if (getenv("LBBSP_BIAS_SLOT1"))  // A/B: one CTA per partition slot
+        bias_grad_kernel<1><<<sms, 256, kBiasSmem, s>>>(G, dZ[l], dims[l + 1], partial, P, off_b[l], bias_part,
+                                                        bias_cnt, ob, slot);
+      else
+        bias_grad_kernel<kBiasCtasPerSlot><<<sms * kBiasCtasPerSlot, 256, kBiasSmem, s>>>(
+            G, dZ[l], dims[l + 1], partial, P, off_b[l], bias_part, bias_cnt, ob, slot);
       ++nl;
     }
     int rc = launch_grouped(this, dw[l], tc::kKSplit, phase_slot(ph++), s);
@@ -2370,8 +2461,18 @@ extern "C" int lbbsp_mlp_create(const lbbsp_mlp_cfg* cfg, lbbsp_mlp** out) {
     LBBSP_CUDA_CHECK(m.alloc(&gd, 1));
     m.D.gather_done = gd;
   }
-  LBBSP_CUDA_CHECK(m.alloc(&m.bias_part, static_cast<size_t>(num_sms()) * kBiasCols));
-  LBBSP_CUDA_CHECK(m.alloc(&m.bias_cnt, static_cast<size_t>(m.n_local)));
+  {
+    int max_w = 8;
+    for (int l = 1; l <= L; ++l) max_w = std::max(max_w, c.dims[l]);
+    const size_t part = std::max(static_cast<size_t>(num_sms()) * kBiasCols,
+                                 static_cast<size_t>(num_sms()) * kBiasCtasPerSlot * kBiasStrip +
+                                     static_cast<size_t>(m.n_local) * max_w);
+    LBBSP_CUDA_CHECK(m.alloc(&m.bias_part, part));
+    LBBSP_CUDA_CHECK(m.alloc(&m.bias_cnt, static_cast<size_t>(m.n_local) * bias_strips(max_w)));
+  }
+  LBBSP_CUDA_CHECK(cudaFuncSetAttribute(bias_grad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBiasSmem));
+  LBBSP_CUDA_CHECK(cudaFuncSetAttribute(bias_grad_kernel<kBiasCtasPerSlot>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kBiasSmem));
   LBBSP_CUDA_CHECK(cudaFuncSetAttribute(observe_train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         200 * 1024));
   D.N_data = m.N_data;

@@ -363,3 +363,30 @@ class MlpEngine:
         check(_L().lbbsp_mlp_dataset(self._h, x.ctypes.data_as(C.c_void_p), y.ctypes.data_as(_ip)))
         xf = (x.astype(np.uint32) << 16).view(np.float32).reshape(N, d0)
         return xf, y
+
+
+def connect(eng, world, rank, nccl=True, peers=True, group=None):
+    """Multi-GPU control plane of one rank, over an initialised
+    torch.distributed process group: rank 0's NCCL unique id is broadcast and
+    every rank joins the communicator (the speed all-gather and the fallback
+    all-reduce), then the 64-byte CUDA-IPC handles of every rank's peer
+    buffers are all-gathered in rank order and mapped (the NVLink peer-memory
+    exchange of speeds and gradients, the copy-engine gradient buckets). The
+    same order on every rank; returns the gathered handles.
+    Reference: the coordinator's all-gather of v_actual before the replicated
+    solver (cluster_sim.cpp:371-402)."""
+    import torch.distributed as dist
+    if world <= 1:
+        return []
+    if nccl:
+        uid = [eng.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0, group=group)
+        eng.init_comm(uid[0])
+    hs = []
+    if peers:
+        hs = [None] * world
+        dist.all_gather_object(hs, eng.peer_handle(), group=group)
+        if any(h is None or len(h) != len(hs[rank]) for h in hs):
+            raise RuntimeError("connect: a rank sent no peer handle")
+        eng.init_peers(hs)
+    return hs

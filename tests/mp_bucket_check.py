@@ -14,7 +14,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 import numpy as np
 import torch
 import torch.distributed as dist
-from paper_1806_02508_b200.mlp import MlpEngine, constant_trace
+from paper_1806_02508_b200.mlp import MlpEngine, connect, constant_trace
 
 world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
@@ -38,12 +38,7 @@ for mode in ("nccl", "ce", "ce_again", "ce_two_shot"):
                     trace=constant_trace(world, rounds + 4), static_sizes=sizes)
     if p_init is None:
         p_init = flat(eng.params())
-    uid = [MlpEngine.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    eng.init_comm(uid[0])
-    hs = [None] * world
-    dist.all_gather_object(hs, eng.peer_handle())
-    eng.init_peers(hs)
+    connect(eng, world, rank)
     eng.run(rounds)
     torch.cuda.synchronize()
     out[mode] = (flat(eng.params()), eng.records()["loss"][:rounds])

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from paper_1806_02508_b200.mlp import MlpEngine, benchmark_trace
+from paper_1806_02508_b200.mlp import MlpEngine, benchmark_trace, connect
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--mode", default="c2", choices=["c2", "c3"])
@@ -43,9 +43,7 @@ eng = MlpEngine(dims=dims, global_batch=B, n_workers_local=n_local, world=world,
                 scheme="lb-bsp", predictor=pred, warmup_iterations=8, learning_rate=lr, seed=1,
                 max_iterations=R + 4, trace=trace,
                 sm_budget=0)
-hs = [None] * world
-dist.all_gather_object(hs, eng.peer_handle())
-eng.init_peers(hs)
+connect(eng, world, rank, nccl=False)  # peer-memory exchange only (gloo group)
 p0 = eng.params()
 eng.run(R)
 torch.cuda.synchronize()

@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 import numpy as np
 import torch
 import torch.distributed as dist
-from paper_1806_02508_b200.mlp import MlpEngine, constant_trace
+from paper_1806_02508_b200.mlp import MlpEngine, connect, constant_trace
 
 world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
@@ -17,13 +17,7 @@ for mode in ("nccl", "peers"):
     eng = MlpEngine(dims=[784, 256, 10], global_batch=4096 * world, n_workers_local=8, world=world, rank=rank,
                     predictor="ema", max_iterations=40, trace=constant_trace(n, 40),
                     static_sizes=[4096 // 8] * n)
-    uid = [MlpEngine.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    eng.init_comm(uid[0])
-    if mode == "peers":
-        hs = [None] * world
-        dist.all_gather_object(hs, eng.peer_handle())
-        eng.init_peers(hs)
+    connect(eng, world, rank, peers=mode == "peers")
     eng.run(20)
     torch.cuda.synchronize()
     flat = np.concatenate([np.concatenate([w.ravel(), b]) for w, b in eng.params()])

@@ -72,3 +72,25 @@ def test_two_rank_gloo_control_exchange():
         assert p.returncode == 0, e.decode()[-2000:]
     lines = [o.decode().strip().splitlines()[-1] for o, _ in outs]
     assert lines[0] == lines[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_connect_handshake(world):
+    """The product's multi-rank control plane (mlp.connect) on CPU ranks over
+    gloo: every rank joins rank 0's communicator id, and every rank maps the
+    same rank-ordered list of peer handles."""
+    import json
+    import sys
+    code = os.path.join(REPO, "tests", "_gloo_connect_worker.py")
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29540 + world), PYTHONPATH=REPO)
+    procs = [subprocess.Popen([sys.executable, code, str(r), str(world)], env=env,
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE) for r in range(world)]
+    outs = [p.communicate(timeout=120) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e.decode()[-2000:]
+    res = [json.loads(o.decode().strip().splitlines()[-1]) for o, _ in outs]
+    for r, d in enumerate(res):
+        assert d["uid"] == "uid-of-rank-0"
+        assert d["handles"] == list(range(world)) and d["lens"] == [64] * world
+        assert d["calls"] == (["uid"] if r == 0 else []) + ["comm", "handle", "peers"]
+        assert d["ret"] == world

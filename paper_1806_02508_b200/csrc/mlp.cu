@@ -1280,6 +1280,29 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
     const int len = len_s, w = w_s;
     const size_t o = static_cast<size_t>(w) * D.pred.max_hist;
     if (tid == 0 && blockIdx.x == 0) D.stamps[15] = gtimer();  // kernel entry (debug timeline)
+    const int L = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
+    const bool in_smem = narx_train_min_bytes(L) <= smem_bytes;
+    // While the workers still run: the history of earlier rounds into the
+    // trainer's shared-memory history region, and its part of the three
+    // scaler sums (fit_scaler's left fold, continued by the trainer with the
+    // newest observation) -- off the critical path of the round.
+    __shared__ double pre_sums[3];
+    const int old = len < L ? len : L;
+    if (in_smem) {
+      double* hv = narx_history_region(sm_d, L);
+      for (int i = tid; i < old; i += blockDim.x) {
+        hv[i] = D.pred.hv[o + i];
+        hv[L + i] = D.pred.hc[o + i];
+        hv[2 * L + i] = D.pred.hm[o + i];
+      }
+      __syncthreads();
+      if (tid == 0 || tid == 32 || tid == 64) {
+        const double* xs = hv + (tid / 32) * L;
+        double sum = 0.0;
+        for (int i = 0; i < old; ++i) sum = dadd(sum, xs[i]);
+        pre_sums[tid / 32] = sum;
+      }
+    }
     if (early) tc::pdl_wait();  // the worker kernel's phase times are final
     if (tid == 0 && len < D.pred.max_hist) {
       const double v = fused_speed_phases > 0 ? local_speed(D, w - D.rank * D.n_local, fused_speed_phases, nullptr)
@@ -1290,14 +1313,19 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
     }
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) D.stamps[14] = gtimer();  // training starts
-    const int L = len + 1 < D.pred.max_hist ? len + 1 : D.pred.max_hist;
     const size_t slot = narx_train_scratch_bytes(D.pred.max_hist) / sizeof(double);
-    size_t nd = 0;
-    double* buf = narx_train_buf(L, sm_d, smem_bytes, D.pred.scratch + blockIdx.x * slot, slot, &nd);
     lbbsp_narx_train_cfg cfg = D.pred.train;
     cfg.min_history = D.pred.warmup;
-    narx_train_block(&D.pred.models[w], D.pred.hv + o, D.pred.hc + o, D.pred.hm + o, L, cfg,
-                     &D.pred.reports[w], nullptr, 0, buf, nd, &ts);
+    // the shared-memory scratch passed as sm_d itself (not through a
+    // shared-or-global select), so the inlined trainer's loads and stores
+    // compile to LDS/STS instead of generic accesses
+    if (in_smem)
+      narx_train_block(&D.pred.models[w], D.pred.hv + o, D.pred.hc + o, D.pred.hm + o, L, cfg,
+                       &D.pred.reports[w], nullptr, 0, sm_d, smem_bytes / sizeof(double), &ts, old,
+                       pre_sums);
+    else
+      narx_train_block(&D.pred.models[w], D.pred.hv + o, D.pred.hc + o, D.pred.hm + o, L, cfg,
+                       &D.pred.reports[w], nullptr, 0, D.pred.scratch + blockIdx.x * slot, slot, &ts);
     // the next round's prediction with the model just trained (after the
     // observe CTA's EMA / history push, which an EMA fallback reads)
     if (tid == 0) {
@@ -1714,6 +1742,7 @@ struct lbbsp_mlp {
   float* bias_part = nullptr;      // bias-gradient row-chunk partials (bias_grad_kernel)
   bf16* gradb = nullptr;           // [P] bf16 gradient buckets (bucketed all-reduce path)
   unsigned* bias_cnt = nullptr;    // [n_local][strips] bias_grad_kernel counters (self-resetting)
+  unsigned long long* dbg_stamps = nullptr;  // lbbsp_mlp_debug_stamp
   bool use_pdl = true;             // programmatic dependent launch on the worker-phase chain
   long long* reg_len = nullptr;
   int n_reg = 0;
@@ -2965,6 +2994,32 @@ extern "C" int lbbsp_mlp_rows_per_cta(lbbsp_mlp* m, int* rows) {
 
 // Debug timeline of the last round: stamps[16] then timing[kMaxPhases][n_local][2]
 // (globaltimer ns). Not part of the stable C-ABI.
+#ifdef LBBSP_NARX_PROF
+extern "C" int lbbsp_debug_narx_prof(unsigned long long* out) {
+  LBBSP_CUDA_CHECK(cudaDeviceSynchronize());
+  LBBSP_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_narx_prof, sizeof(unsigned long long) * 64 * 16));
+  return LBBSP_OK;
+}
+#endif
+// Debug (probes only): a one-thread kernel on the engine stream writes
+// %globaltimer into slot [0, 8) of a scratch array, so a probe can place the
+// graph's first and last kernels against stamps taken just before and after
+// the round in stream order (scripts/graph_overhead_probe.py).
+__global__ void debug_stamp_kernel(unsigned long long* dst) { *dst = gtimer(); }
+extern "C" int lbbsp_mlp_debug_stamp(lbbsp_mlp* m, int slot) {
+  if (slot < 0 || slot >= 8) return set_error(LBBSP_INVALID_ARGUMENT, "debug_stamp: slot in [0, 8)");
+  if (!m->dbg_stamps) LBBSP_CUDA_CHECK(m->alloc(&m->dbg_stamps, 8));
+  debug_stamp_kernel<<<1, 1, 0, m->stream>>>(m->dbg_stamps + slot);
+  LBBSP_CUDA_CHECK(cudaGetLastError());
+  return LBBSP_OK;
+}
+extern "C" int lbbsp_mlp_debug_stamps(lbbsp_mlp* m, unsigned long long* out) {
+  LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->stream));
+  if (!m->dbg_stamps) return set_error(LBBSP_INVALID_ARGUMENT, "debug_stamps: no stamp taken");
+  LBBSP_CUDA_CHECK(cudaMemcpy(out, m->dbg_stamps, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost));
+  return LBBSP_OK;
+}
+
 extern "C" int lbbsp_mlp_debug_timeline(lbbsp_mlp* m, unsigned long long* out, int* n_phases) {
   LBBSP_CUDA_CHECK(cudaStreamSynchronize(m->stream));
   LBBSP_CUDA_CHECK(cudaMemcpy(out, m->D.stamps, sizeof(unsigned long long) * 16, cudaMemcpyDeviceToHost));

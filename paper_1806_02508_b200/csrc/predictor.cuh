@@ -121,6 +121,21 @@ __device__ __forceinline__ double* narx_train_buf(int L, double* smem, size_t sm
   return gslot;
 }
 
+#ifdef LBBSP_NARX_PROF
+// probe builds only: per-CTA %globaltimer stamps of one training
+// [0] entry [1] history copied [2] scalers [3] training set built
+// [4] first evaluation [5] end; [6] evaluations, [7] epochs, [8] L
+__device__ unsigned long long g_narx_prof[64][16];
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define NARX_PROF(i, v) \
+  if (threadIdx.x == 0 && blockIdx.x < 64) g_narx_prof[blockIdx.x][i] = (v)
+#else
+#define NARX_PROF(i, v)
+#endif
 struct NarxTrainSmem {
   double w[11], g[11], gs[11], trial[11], sc[6];
   double val;
@@ -170,10 +185,16 @@ __device__ __forceinline__ void narx_eval_terms(const double* wt, const double* 
 __device__ inline double block_eval(const double* fwd_w, const double* Z, const double* T,
                                     double* E, double* G, double* Es, double* Gs, int S, int cnt,
                                     double scale, double spec_step, double* gout, NarxTrainSmem* s) {
+#ifdef LBBSP_NARX_PROF
+  const unsigned long long pt0 = clock64();
+#endif
   if (fwd_w) {
     narx_eval_terms(fwd_w, Z, T, E, G, S, cnt, scale, threadIdx.x, blockDim.x);
     __syncthreads();
   }
+#ifdef LBBSP_NARX_PROF
+  const unsigned long long pt1 = clock64();
+#endif
   if (threadIdx.x >= 32 && threadIdx.x < 44) {
     const int k = threadIdx.x - 32;
     const double* src = k < 11 ? G + static_cast<size_t>(k) * S : E;
@@ -202,7 +223,18 @@ __device__ inline double block_eval(const double* fwd_w, const double* Z, const 
     const int idx = threadIdx.x < 32 ? threadIdx.x : threadIdx.x - 32;
     narx_eval_terms(sw, Z, T, Es, Gs, S, cnt, scale, idx, blockDim.x - 32);
   }
+#ifdef LBBSP_NARX_PROF
+  if (threadIdx.x == 32 && blockIdx.x < 64) {  // the E-fold lane: its fold end
+    g_narx_prof[blockIdx.x][11] += clock64() - pt1;
+  }
+#endif
   __syncthreads();
+#ifdef LBBSP_NARX_PROF
+  if (threadIdx.x == 0 && blockIdx.x < 64) {
+    g_narx_prof[blockIdx.x][9] += pt1 - pt0;            // terms + barrier
+    g_narx_prof[blockIdx.x][10] += clock64() - pt1;   // fold + barrier
+  }
+#endif
   return s->val;
 }
 
@@ -212,24 +244,38 @@ __device__ inline double block_eval(const double* fwd_w, const double* Z, const 
 // trial step is evaluated speculatively beside each fold. Bit-exact: every
 // value the reference computes is computed with the same operations in the
 // same order; only independent work is overlapped.
+// staged > 0: the caller already copied history [0, staged) into the
+// scratch's history region (narx_history_region) and, with pre_sums, folded
+// it into the three scaler sums (the same left-to-right order, continued
+// here) -- done before the newest observation exists.
+__host__ __device__ __forceinline__ double* narx_history_region(double* buf, int L) {
+  return buf + 9 * static_cast<size_t>(narx_train_stride(L));
+}
 __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, const double* c,
                                         const double* m, int L, const lbbsp_narx_train_cfg cfg,
                                         lbbsp_narx_report* rep, double* loss_log, int loss_cap,
-                                        double* buf, size_t buf_doubles, NarxTrainSmem* s) {
+                                        double* buf, size_t buf_doubles, NarxTrainSmem* s,
+                                        int staged = 0, const double* pre_sums = nullptr) {
   const int tid = threadIdx.x;
   const int minh = cfg.min_history > 3 ? cfg.min_history : 3;
   if (L < minh) {
     if (tid == 0 && rep) *rep = lbbsp_narx_report{0, 0, 0.0};
     return;
   }
+  NARX_PROF(0, gtimer_ns());
+  NARX_PROF(8, L);
+  NARX_PROF(9, 0);
+  NARX_PROF(10, 0);
+  NARX_PROF(11, 0);
+  NARX_PROF(12, clock64());
   const int S = narx_train_stride(L);
   // the history into the scratch's E/G region first (written only once the
   // evaluations start): one parallel round trip, instead of the sequential
   // scaler folds below waiting on each cache line of v, c, m in turn
-  double* hv = buf + 9 * static_cast<size_t>(S);
+  double* hv = narx_history_region(buf, L);
   double* hc = hv + L;
   double* hm = hc + L;
-  for (int i = tid; i < L; i += blockDim.x) {
+  for (int i = staged + tid; i < L; i += blockDim.x) {
     hv[i] = v[i];
     hc[i] = c[i];
     hm[i] = m[i];
@@ -238,12 +284,13 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
   c = hc;
   m = hm;
   __syncthreads();
+  NARX_PROF(1, gtimer_ns());
   // fit_scaler x3 (predictor.cpp:71-82), one sequential thread per series
   if (tid == 0 || tid == 32 || tid == 64) {
     const int which = tid / 32;
     const double* xs = which == 0 ? v : (which == 1 ? c : m);
-    double sum = 0.0;
-    for (int i = 0; i < L; ++i) sum = dadd(sum, xs[i]);
+    double sum = pre_sums ? pre_sums[which] : 0.0;
+    for (int i = pre_sums ? staged : 0; i < L; ++i) sum = dadd(sum, xs[i]);
     const double mean = ddiv(sum, static_cast<double>(L));
     double var = 0.0;
     for (int i = 0; i < L; ++i) {
@@ -261,6 +308,7 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
     s->stop = 0;
   }
   __syncthreads();
+  NARX_PROF(2, gtimer_ns());
   const int cnt = L - 2;
   double* Z = buf;                             // [8][S]
   double* T = Z + static_cast<size_t>(8) * S;  // [S]
@@ -289,33 +337,53 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
     for (int b = 0; b < (spec ? 2 : 1); ++b)
       for (int k = 0; k < 12; ++k) EG[b][static_cast<size_t>(k) * S + i] = 0.0;
   __syncthreads();
+  NARX_PROF(3, gtimer_ns());
   const double scale = ddiv(2.0, static_cast<double>(cnt));
   auto E_ = [&](int b) { return EG[b]; };
   auto G_ = [&](int b) { return EG[b] + S; };
   // current = mse(model) (:165), and loss_gradient(model) of epoch 0
   double current = block_eval(s->w, Z, T, E_(0), G_(0), nullptr, nullptr, S, cnt, scale, 0.0,
                               s->g, s);
+  NARX_PROF(4, gtimer_ns());
+#ifdef LBBSP_NARX_PROF
+  int n_eval = 1;
+#define NARX_EVAL_COUNT ++n_eval
+#else
+#define NARX_EVAL_COUNT
+#endif
   for (int epoch = 0; epoch < cfg.max_epochs; ++epoch) {
     double step = cfg.step;
     if (tid < 11) s->trial[tid] = dsub(s->w[tid], dmul(step, s->g[tid]));  // apply_step :136-143
     __syncthreads();
+    // The epoch's first trial is evaluated alone: it is accepted ~3 times in
+    // 4 (0.27 halvings per epoch on the bench histories), and a speculative
+    // halved trial beside its fold would lengthen it (the halved terms'
+    // tanh chains outlast the fold). After a rejection halvings cluster, so
+    // from then on each fold runs beside the next halved trial's terms.
     int b = 0;
-    double next = block_eval(s->trial, Z, T, E_(b), G_(b), E_(1), G_(1), S, cnt, scale,
-                             spec ? dmul(step, 0.5) : 0.0, s->gs, s);
+    double next = block_eval(s->trial, Z, T, E_(b), G_(b), nullptr, nullptr, S, cnt, scale, 0.0,
+                             s->gs, s);
+    NARX_EVAL_COUNT;
     int halvings = 0;
+    bool have_spec = false;
     while (next > current && halvings < 20) {
       step = dmul(step, 0.5);
       if (tid < 11) s->trial[tid] = dsub(s->w[tid], dmul(step, s->g[tid]));
       __syncthreads();
-      if (spec) {  // this trial's terms were formed beside the previous fold
+      if (spec && have_spec) {  // this trial's terms were formed beside the previous fold
         b ^= 1;
         next = block_eval(nullptr, Z, T, E_(b), G_(b), E_(b ^ 1), G_(b ^ 1), S, cnt, scale,
                           dmul(step, 0.5), s->gs, s);
+      } else if (spec) {  // first halving: its own terms, the next halving's beside its fold
+        next = block_eval(s->trial, Z, T, E_(b), G_(b), E_(b ^ 1), G_(b ^ 1), S, cnt, scale,
+                          dmul(step, 0.5), s->gs, s);
+        have_spec = true;
       } else {
         next = block_eval(s->trial, Z, T, E_(0), G_(0), nullptr, nullptr, S, cnt, scale, 0.0,
                           s->gs, s);
       }
       ++halvings;
+      NARX_EVAL_COUNT;
     }
     if (next > current) break;  // no descent direction left (:182)
     if (tid < 11) {
@@ -331,6 +399,12 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
     current = next;
     if (s->stall >= cfg.early_stop_patience) break;
   }
+  NARX_PROF(5, gtimer_ns());
+  NARX_PROF(13, clock64());
+#ifdef LBBSP_NARX_PROF
+  NARX_PROF(6, n_eval);
+  NARX_PROF(7, s->epochs);
+#endif
   if (tid == 0) {
     if (rep) *rep = lbbsp_narx_report{1, s->epochs, current};
     for (int j = 0; j < 8; ++j) gm->input_weights[j] = s->w[j];

@@ -1307,9 +1307,16 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
     if (tid == 0 && len < D.pred.max_hist) {
       const double v = fused_speed_phases > 0 ? local_speed(D, w - D.rank * D.n_local, fused_speed_phases, nullptr)
                                               : D.v_obs_all[w];
+      const double cn = D.c_now[w], mn = D.m_now[w];
       D.pred.hv[o + len] = v;
-      D.pred.hc[o + len] = D.c_now[w];
-      D.pred.hm[o + len] = D.m_now[w];
+      D.pred.hc[o + len] = cn;
+      D.pred.hm[o + len] = mn;
+      if (in_smem) {  // and straight into the staged copy (index len = L - 1)
+        double* hv = narx_history_region(sm_d, L);
+        hv[len] = v;
+        hv[L + len] = cn;
+        hv[2 * L + len] = mn;
+      }
     }
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) D.stamps[14] = gtimer();  // training starts
@@ -1321,8 +1328,8 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
     // compile to LDS/STS instead of generic accesses
     if (in_smem)
       narx_train_block(&D.pred.models[w], D.pred.hv + o, D.pred.hc + o, D.pred.hm + o, L, cfg,
-                       &D.pred.reports[w], nullptr, 0, sm_d, smem_bytes / sizeof(double), &ts, old,
-                       pre_sums);
+                       &D.pred.reports[w], nullptr, 0, sm_d, smem_bytes / sizeof(double), &ts, L,
+                       pre_sums, old);
     else
       narx_train_block(&D.pred.models[w], D.pred.hv + o, D.pred.hc + o, D.pred.hm + o, L, cfg,
                        &D.pred.reports[w], nullptr, 0, D.pred.scratch + blockIdx.x * slot, slot, &ts);

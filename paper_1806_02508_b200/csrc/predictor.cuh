@@ -245,9 +245,9 @@ __device__ inline double block_eval(const double* fwd_w, const double* Z, const 
 // value the reference computes is computed with the same operations in the
 // same order; only independent work is overlapped.
 // staged > 0: the caller already copied history [0, staged) into the
-// scratch's history region (narx_history_region) and, with pre_sums, folded
-// it into the three scaler sums (the same left-to-right order, continued
-// here) -- done before the newest observation exists.
+// scratch's history region (narx_history_region); pre_sums: the three scaler
+// sums' left folds over [0, pre_n), continued here in the same order (the
+// caller folds the earlier rounds before the newest observation exists).
 __host__ __device__ __forceinline__ double* narx_history_region(double* buf, int L) {
   return buf + 9 * static_cast<size_t>(narx_train_stride(L));
 }
@@ -255,7 +255,8 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
                                         const double* m, int L, const lbbsp_narx_train_cfg cfg,
                                         lbbsp_narx_report* rep, double* loss_log, int loss_cap,
                                         double* buf, size_t buf_doubles, NarxTrainSmem* s,
-                                        int staged = 0, const double* pre_sums = nullptr) {
+                                        int staged = 0, const double* pre_sums = nullptr,
+                                        int pre_n = 0) {
   const int tid = threadIdx.x;
   const int minh = cfg.min_history > 3 ? cfg.min_history : 3;
   if (L < minh) {
@@ -290,7 +291,7 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
     const int which = tid / 32;
     const double* xs = which == 0 ? v : (which == 1 ? c : m);
     double sum = pre_sums ? pre_sums[which] : 0.0;
-    for (int i = pre_sums ? staged : 0; i < L; ++i) sum = dadd(sum, xs[i]);
+    for (int i = pre_sums ? pre_n : 0; i < L; ++i) sum = dadd(sum, xs[i]);
     const double mean = ddiv(sum, static_cast<double>(L));
     double var = 0.0;
     for (int i = 0; i < L; ++i) {
@@ -317,18 +318,19 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
                     cnt <= static_cast<int>(blockDim.x) - 32;
   const double mv = s->sc[0], sv = s->sc[1], mc = s->sc[2], scd = s->sc[3], mm = s->sc[4],
                sm = s->sc[5];
-  // build_training_set (predictor.cpp:89-100)
-  for (int i = tid; i < cnt; i += blockDim.x) {
-    const int t = i + 2;
-    Z[0 * S + i] = ddiv(dsub(v[t - 1], mv), sv);
-    Z[1 * S + i] = ddiv(dsub(v[t - 2], mv), sv);
-    Z[2 * S + i] = ddiv(dsub(c[t], mc), scd);
-    Z[3 * S + i] = ddiv(dsub(c[t - 1], mc), scd);
-    Z[4 * S + i] = ddiv(dsub(c[t - 2], mc), scd);
-    Z[5 * S + i] = ddiv(dsub(m[t], mm), sm);
-    Z[6 * S + i] = ddiv(dsub(m[t - 1], mm), sm);
-    Z[7 * S + i] = ddiv(dsub(m[t - 2], mm), sm);
-    T[i] = ddiv(dsub(v[t], mv), sv);
+  // build_training_set (predictor.cpp:89-100): the 9 standardised columns
+  // (Z[0..7], T = row 8 of the same layout) one element per thread -- each
+  // element the reference's single (x - mean) / stddev, 9x fewer dependent
+  // divisions per thread than one sample per thread
+  for (int e = tid; e < 9 * cnt; e += blockDim.x) {
+    const int f = e / cnt, i = e - f * cnt, t = i + 2;
+    // feature f: series (v, v, c, c, c, m, m, m, v) at lag (1, 2, 0, 1, 2, 0, 1, 2, 0)
+    const int ser = f < 2 ? 0 : (f < 5 ? 1 : (f < 8 ? 2 : 0));
+    const int lag = f == 8 ? 0 : (f < 2 ? f + 1 : (f - (f < 5 ? 2 : 5)));
+    const double* xs = ser == 0 ? v : (ser == 1 ? c : m);
+    const double mu = ser == 0 ? mv : (ser == 1 ? mc : mm);
+    const double sd = ser == 0 ? sv : (ser == 1 ? scd : sm);
+    Z[static_cast<size_t>(f) * S + i] = ddiv(dsub(xs[t - lag], mu), sd);
   }
   __syncthreads();
   // zero padding of the folds (never written by the evaluations; after the

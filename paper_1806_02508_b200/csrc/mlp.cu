@@ -1288,6 +1288,8 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
     // newest observation) -- off the critical path of the round.
     __shared__ double pre_sums[3];
     const int old = len < L ? len : L;
+    lbbsp_narx_train_cfg cfg = D.pred.train;
+    cfg.min_history = D.pred.warmup;
     if (in_smem) {
       double* hv = narx_history_region(sm_d, L);
       for (int i = tid; i < old; i += blockDim.x) {
@@ -1321,8 +1323,6 @@ __global__ void __launch_bounds__(kTrainThreads) observe_train_kernel(PlanDev D,
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) D.stamps[14] = gtimer();  // training starts
     const size_t slot = narx_train_scratch_bytes(D.pred.max_hist) / sizeof(double);
-    lbbsp_narx_train_cfg cfg = D.pred.train;
-    cfg.min_history = D.pred.warmup;
     // the shared-memory scratch passed as sm_d itself (not through a
     // shared-or-global select), so the inlined trainer's loads and stores
     // compile to LDS/STS instead of generic accesses
@@ -2201,7 +2201,11 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   } else {
     // not a programmatic launch: early-resident apply CTAs would hold the SMs
     // the (higher-priority) NARX branch needs when the backward ends
-    reduce_apply_kernel<<<sms * 4, 256, 0, sl>>>(partial, n_local, P, grad, params, pb, lr, 1, D.stamps);
+    // sized to the parameter count (two float4 per thread, at most 4 CTAs
+    // per SM): C2's 0.2 M parameters need ~100 CTAs, and every CTA more
+    // shares an SM with the NARX trainings running beside this branch
+    const int ra_ctas = static_cast<int>(std::min<long long>(sms * 4ll, std::max(1ll, (P / 4 + 511) / 512)));
+    reduce_apply_kernel<<<ra_ctas, 256, 0, sl>>>(partial, n_local, P, grad, params, pb, lr, 1, D.stamps);
   }
   if (!bucketed) ++nl;
   // ---- full-dataset loss (step_sync P9, cluster_sim.cpp:445) ----

@@ -333,6 +333,7 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
     Z[static_cast<size_t>(f) * S + i] = ddiv(dsub(xs[t - lag], mu), sd);
   }
   __syncthreads();
+  NARX_PROF(14, gtimer_ns());
   // zero padding of the folds (never written by the evaluations; after the
   // build, which read the history copy in the same region)
   for (int i = cnt + tid; i < (cnt + 15) / 16 * 16; i += blockDim.x)

@@ -18,6 +18,19 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+// a / b for a standardisation (x - mean) / stddev. __ddiv_rn leaves its
+// inline fast path for a called slow path when the numerator is zero (or
+// tiny), and constant series make (x - mean) = 0 for a third of the NARX
+// training set. A zero numerator over a positive divisor is the numerator
+// itself (+0 / b = +0, -0 / b = -0, b = +inf included), so it is divided as
+// 1.0 (fast path) and the quotient replaced; every other input divides
+// unchanged -- bit-identical to ddiv for all inputs. (A plain select would be
+// if-converted into a division of the zero, slow path included.)
+__device__ __forceinline__ double ddiv_std(double a, double b) {
+  const bool z = a == 0.0 && b > 0.0;
+  const double q = __ddiv_rn(z ? 1.0 : a, b);
+  return z ? a : q;
+}
 __device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
 
 __device__ __forceinline__ uint32_t hi_word(double x) {

@@ -33,14 +33,14 @@ __device__ inline double narx_predict_d(const lbbsp_narx_model& m, double v0, do
                                  double c1, double c2, double m0, double m1, double m2,
                                  double floor_) {
   double z[8], w[11];
-  z[0] = ddiv(dsub(v0, m.speed_mean), m.speed_stddev);
-  z[1] = ddiv(dsub(v1, m.speed_mean), m.speed_stddev);
-  z[2] = ddiv(dsub(c0, m.cpu_mean), m.cpu_stddev);
-  z[3] = ddiv(dsub(c1, m.cpu_mean), m.cpu_stddev);
-  z[4] = ddiv(dsub(c2, m.cpu_mean), m.cpu_stddev);
-  z[5] = ddiv(dsub(m0, m.mem_mean), m.mem_stddev);
-  z[6] = ddiv(dsub(m1, m.mem_mean), m.mem_stddev);
-  z[7] = ddiv(dsub(m2, m.mem_mean), m.mem_stddev);
+  z[0] = ddiv_std(dsub(v0, m.speed_mean), m.speed_stddev);
+  z[1] = ddiv_std(dsub(v1, m.speed_mean), m.speed_stddev);
+  z[2] = ddiv_std(dsub(c0, m.cpu_mean), m.cpu_stddev);
+  z[3] = ddiv_std(dsub(c1, m.cpu_mean), m.cpu_stddev);
+  z[4] = ddiv_std(dsub(c2, m.cpu_mean), m.cpu_stddev);
+  z[5] = ddiv_std(dsub(m0, m.mem_mean), m.mem_stddev);
+  z[6] = ddiv_std(dsub(m1, m.mem_mean), m.mem_stddev);
+  z[7] = ddiv_std(dsub(m2, m.mem_mean), m.mem_stddev);
   model_weights(m, w);
   const double v = dadd(m.speed_mean, dmul(m.speed_stddev, narx_forward_d(w, z)));
   return v > floor_ ? v : floor_;
@@ -268,7 +268,8 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
   NARX_PROF(9, 0);
   NARX_PROF(10, 0);
   NARX_PROF(11, 0);
-  NARX_PROF(12, clock64());
+  NARX_PROF(12, 0);
+  NARX_PROF(15, 0);
   const int S = narx_train_stride(L);
   // the history into the scratch's E/G region first (written only once the
   // evaluations start): one parallel round trip, instead of the sequential
@@ -313,7 +314,12 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
   const int cnt = L - 2;
   double* Z = buf;                             // [8][S]
   double* T = Z + static_cast<size_t>(8) * S;  // [S]
-  double* EG[2] = {T + S, T + 13 * static_cast<size_t>(S)};  // {E [S], G [11][S]} x 2
+  // {E [S], G [11][S]} x 2 at T + S and T + 13 S. Addressed arithmetically,
+  // not through a pointer array: a runtime-indexed local array would hold
+  // the pointers in local memory and turn every access through them into a
+  // generic load/store instead of LDS/STS
+  double* const EG0 = T + S;
+  const size_t EGs = 12 * static_cast<size_t>(S);
   const bool spec = buf_doubles >= static_cast<size_t>(kNarxArrays) * S &&
                     cnt <= static_cast<int>(blockDim.x) - 32;
   const double mv = s->sc[0], sv = s->sc[1], mc = s->sc[2], scd = s->sc[3], mm = s->sc[4],
@@ -330,7 +336,7 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
     const double* xs = ser == 0 ? v : (ser == 1 ? c : m);
     const double mu = ser == 0 ? mv : (ser == 1 ? mc : mm);
     const double sd = ser == 0 ? sv : (ser == 1 ? scd : sm);
-    Z[static_cast<size_t>(f) * S + i] = ddiv(dsub(xs[t - lag], mu), sd);
+    Z[static_cast<size_t>(f) * S + i] = ddiv_std(dsub(xs[t - lag], mu), sd);
   }
   __syncthreads();
   NARX_PROF(14, gtimer_ns());
@@ -338,12 +344,12 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
   // build, which read the history copy in the same region)
   for (int i = cnt + tid; i < (cnt + 15) / 16 * 16; i += blockDim.x)
     for (int b = 0; b < (spec ? 2 : 1); ++b)
-      for (int k = 0; k < 12; ++k) EG[b][static_cast<size_t>(k) * S + i] = 0.0;
+      for (int k = 0; k < 12; ++k) EG0[b * EGs + static_cast<size_t>(k) * S + i] = 0.0;
   __syncthreads();
   NARX_PROF(3, gtimer_ns());
   const double scale = ddiv(2.0, static_cast<double>(cnt));
-  auto E_ = [&](int b) { return EG[b]; };
-  auto G_ = [&](int b) { return EG[b] + S; };
+  auto E_ = [&](int b) { return EG0 + b * EGs; };
+  auto G_ = [&](int b) { return EG0 + b * EGs + S; };
   // current = mse(model) (:165), and loss_gradient(model) of epoch 0
   double current = block_eval(s->w, Z, T, E_(0), G_(0), nullptr, nullptr, S, cnt, scale, 0.0,
                               s->g, s);
@@ -403,7 +409,6 @@ __device__ inline void narx_train_block(lbbsp_narx_model* gm, const double* v, c
     if (s->stall >= cfg.early_stop_patience) break;
   }
   NARX_PROF(5, gtimer_ns());
-  NARX_PROF(13, clock64());
 #ifdef LBBSP_NARX_PROF
   NARX_PROF(6, n_eval);
   NARX_PROF(7, s->epochs);

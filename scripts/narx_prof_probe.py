@@ -38,7 +38,7 @@ for rep in range(int(os.environ.get("REPS", "20"))):
         t = p[b].astype(np.int64)
         d = [(t[i + 1] - t[i]) / 1e3 for i in range(5)]
         row.append(d + [int(t[6]), int(t[7]), int(t[8])])
-        tot.append(d + [int(t[6]), int(t[7]), int(t[8]), t[9] * 1.0, t[10] * 1.0, t[11] * 1.0, (t[13] - t[12]) / max(1, t[5] - t[0]), (t[14] - t[2]) / 1e3])
+        tot.append(d + [int(t[6]), int(t[7]), int(t[8]), t[9] * 1.0, t[10] * 1.0, t[11] * 1.0, 0.0, (t[14] - t[2]) / 1e3, t[15], t[12]])
     print("round", " | ".join(f"copy {r[0]:.1f} scal {r[1]:.1f} build {r[2]:.1f} eval0 {r[3]:.1f} "
                               f"epochs {r[4]:.1f} ({r[5]} ev, {r[6]} ep, L {r[7]})" for r in row), flush=True)
 a = np.array(tot)
@@ -47,5 +47,4 @@ print("median per training: copy %.2f scalers %.2f build %.2f eval0 %.2f epochs 
 print("mean per evaluation (epochs phase): %.2f us" % (a[:, 4].sum() / max(1, (a[:, 5] - 1).sum())))
 print("per evaluation (SM cycles): terms+barrier %.0f, fold+barrier %.0f (E-fold lane alone %.0f)"
       % (a[:, 8].sum() / a[:, 5].sum(), a[:, 9].sum() / a[:, 5].sum(), a[:, 10].sum() / a[:, 5].sum()))
-print("SM clock during the trainings: %.2f GHz (clock64 / globaltimer)" % np.median(a[:, 11]))
 print("training-set loop alone: %.2f us" % np.median(a[:, 12]))

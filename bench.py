@@ -650,8 +650,10 @@ def main():
     s = torch.cuda.Event(enable_timing=True)
     e = torch.cuda.Event(enable_timing=True)
     s.record(st)
+    t_host = time.perf_counter()
     for _ in range(e2e_steps):
         eng.step_e2e(xb.data_ptr(), yb.data_ptr(), out_sizes.data_ptr(), out_loss.data_ptr())
+    t_host = (time.perf_counter() - t_host) / e2e_steps  # host submission time per step
     st.wait_stream(torch.cuda.ExternalStream(eng.result_stream))  # the last round's result read included
     e.record(st)
     e.synchronize()
@@ -773,6 +775,7 @@ def main():
             "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "rounds": e2e_steps, "first_round": warm,
+                    "host_submit_us_per_step": round(t_host * 1e6, 1),
                     "device_window_ms": win["lbbsp"]["mean"]},
             "clocks": clocks,
             "rounds_recorded": rec["rows"],

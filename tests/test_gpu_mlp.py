@@ -146,3 +146,21 @@ def test_end_to_end_plumbing(pinned):
     assert ls.item() > 0 and np.isfinite(ls.item())
     # the loss read is the round's record (written by its loss head)
     assert ls.item() == float(rec["loss"][rec["rows"] - 1])
+
+
+def test_pinned_empty_huge_pages_page_locked_and_copyable():
+    """hostio.pinned_empty: 2 MB-aligned THP mapping registered with
+    cudaHostRegister -- page-locked (asynchronous DMA), zeroed, and a
+    host->device round trip returns the bytes written."""
+    import torch
+    from paper_1806_02508_b200.hostio import pinned_empty
+    t = pinned_empty((1000, 784), torch.bfloat16, 0)
+    assert t.shape == (1000, 784) and t.dtype == torch.bfloat16
+    assert t.is_pinned()
+    assert float(t.float().abs().sum()) == 0.0
+    src = torch.randn(1000, 784).to(torch.bfloat16)
+    t.copy_(src)
+    d = torch.empty_like(t, device="cuda")
+    d.copy_(t, non_blocking=True)
+    torch.cuda.synchronize()
+    assert torch.equal(d.cpu(), src)

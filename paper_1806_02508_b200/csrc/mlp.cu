@@ -2167,7 +2167,12 @@ int lbbsp_mlp::enqueue_iteration(cudaStream_t s) {
   }
   // ---- observe branch ----
   if (narx_fused) {
-    const size_t tsm = train_smem_bytes(pred.dev.max_hist);
+    // at least 116 KB of shared memory: two of these CTAs never share an SM
+    // (launched early, beside the worker kernel, they would otherwise pack
+    // onto the few SMs the workers leave free and halve each other's fp64
+    // and issue rate; the training-set build measured 3 us in place against
+    // 1.5 us alone, scripts/fp64/build_lat.cu)
+    const size_t tsm = std::max(train_smem_bytes(pred.dev.max_hist), static_cast<size_t>(116 * 1024));
     if (early_obs)
       LBBSP_CUDA_CHECK(launch_maybe_pdl(observe_train_kernel, nb + 1, kTrainThreads, tsm, so, true, D, n_phases,
                                         arrive, tsm, 1));

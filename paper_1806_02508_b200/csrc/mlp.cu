@@ -2908,6 +2908,13 @@ extern "C" int lbbsp_mlp_load_data_async(lbbsp_mlp* m, const void* h_x_bf16, con
 }
 
 namespace {
+// the round's record row (sizes, loss) straight into mapped page-locked host
+// memory: PCIe posted writes from one CTA, no copy-engine DMA
+__global__ void result_row_kernel(const int* rec_sizes, const double* rec_loss, long long row, int n,
+                                  int* out_sizes, double* out_loss) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out_sizes[i] = rec_sizes[static_cast<size_t>(row) * n + i];
+  if (threadIdx.x == 0) *out_loss = rec_loss[row];
+}
 __global__ void last_row_kernel(const int* rows, const int* rec_sizes, const double* loss_acc,
                                 int n_data, int n, int* out_sizes, double* out_loss) {
   const int r = *rows - 1;
@@ -2927,16 +2934,6 @@ extern "C" int lbbsp_mlp_read_result_async(lbbsp_mlp* m, int* h_sizes, double* h
   // later round writes it -- copy it on the result stream, beside the next
   // round, instead of a kernel on the round's critical path.
   const long long row = m->host_rounds - 1;
-  if (m->small_head && m->D.loss_on && m->cfg.world == 1 && m->cfg.loss_every == 1 && row >= 0 &&
-      row < m->max_rows) {
-    LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_round_done, m->stream));
-    LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->result_stream, m->ev_round_done, 0));
-    LBBSP_CUDA_CHECK(cudaMemcpyAsync(h_sizes, m->D.rec_sizes + static_cast<size_t>(row) * m->n_total,
-                                     sizeof(int) * m->n_total, cudaMemcpyDeviceToHost, m->result_stream));
-    LBBSP_CUDA_CHECK(cudaMemcpyAsync(h_loss, m->D.rec_loss + row, sizeof(double), cudaMemcpyDeviceToHost,
-                                     m->result_stream));
-    return LBBSP_OK;
-  }
   if (h_sizes != m->res_host_sizes || h_loss != m->res_host_loss) {
     cudaPointerAttributes a{}, b{};
     const bool mapped = cudaPointerGetAttributes(&a, h_sizes) == cudaSuccess &&
@@ -2948,6 +2945,24 @@ extern "C" int lbbsp_mlp_read_result_async(lbbsp_mlp* m, int* h_sizes, double* h
     m->res_host_loss = h_loss;
     m->res_dev_sizes = mapped ? static_cast<int*>(a.devicePointer) : nullptr;
     m->res_dev_loss = mapped ? static_cast<double*>(b.devicePointer) : nullptr;
+  }
+  if (m->small_head && m->D.loss_on && m->cfg.world == 1 && m->cfg.loss_every == 1 && row >= 0 &&
+      row < m->max_rows) {
+    LBBSP_CUDA_CHECK(cudaEventRecord(m->ev_round_done, m->stream));
+    LBBSP_CUDA_CHECK(cudaStreamWaitEvent(m->result_stream, m->ev_round_done, 0));
+    if (m->res_dev_sizes) {
+      // mapped host buffers: one CTA writes them, so the copy engine serves
+      // only the next round's upload (a D2H copy queued there delayed it)
+      result_row_kernel<<<1, 32, 0, m->result_stream>>>(m->D.rec_sizes, m->D.rec_loss, row, m->n_total,
+                                                        m->res_dev_sizes, m->res_dev_loss);
+      LBBSP_CUDA_CHECK(cudaGetLastError());
+      return LBBSP_OK;
+    }
+    LBBSP_CUDA_CHECK(cudaMemcpyAsync(h_sizes, m->D.rec_sizes + static_cast<size_t>(row) * m->n_total,
+                                     sizeof(int) * m->n_total, cudaMemcpyDeviceToHost, m->result_stream));
+    LBBSP_CUDA_CHECK(cudaMemcpyAsync(h_loss, m->D.rec_loss + row, sizeof(double), cudaMemcpyDeviceToHost,
+                                     m->result_stream));
+    return LBBSP_OK;
   }
   if (m->res_dev_sizes) {
     last_row_kernel<<<1, 256, 0, m->stream>>>(m->D.rows, m->D.rec_sizes, m->D.loss_acc, m->N_data,

@@ -776,6 +776,7 @@ def main():
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "rounds": e2e_steps, "first_round": warm,
                     "host_submit_us_per_step": round(t_host * 1e6, 1),
+                    "l2": "not flushed: steps back to back, each uploading its inputs from host memory",
                     "device_window_ms": win["lbbsp"]["mean"]},
             "clocks": clocks,
             "rounds_recorded": rec["rows"],

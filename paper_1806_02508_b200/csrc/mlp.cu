@@ -3064,11 +3064,11 @@ extern "C" int lbbsp_mlp_debug_timeline(lbbsp_mlp* m, unsigned long long* out, i
 // memory (H2D on the copy stream, overlapping the round in flight), run the
 // round, write its sizes + loss to host memory. The first call with a new
 // host buffer pair warms it outside any steady-state step: DMA out of a
-// freshly page-locked buffer runs at a third of the link rate for its first
-// ~100 transfers (113 us vs 38 us for the 1.57 MB dataset,
-// profiles/r02_e2e_probe.txt), so it is copied (into both dataset buffers) at
-// least 128 times and until three consecutive copies run within 15% of the
-// fastest (at most 1024 copies).
+// freshly page-locked buffer runs at a third to half of the link rate for its
+// first ~100-1000 transfers (113 us vs 38 us for the 1.57 MB dataset,
+// profiles/r02_e2e_probe.txt, profiles/r02_h2d_hugepages.txt), so it is
+// copied (into both dataset buffers) at least 2048 times and until three
+// consecutive copies run within 15% of the fastest (at most 8192 copies).
 extern "C" int lbbsp_mlp_step_e2e(lbbsp_mlp* m, const void* h_x_bf16, const int* h_labels, int* h_sizes,
                                   double* h_loss) {
   if (h_x_bf16 != m->warm_x || h_labels != m->warm_y) {
@@ -3082,10 +3082,13 @@ extern "C" int lbbsp_mlp_step_e2e(lbbsp_mlp* m, const void* h_x_bf16, const int*
     LBBSP_CUDA_CHECK(cudaEventCreate(&e1));
     float best = 1e30f;
     int steady = 0;
-    // both dataset buffers (both streams are idle here), at least 128 copies:
-    // the slow phase lasts ~100 transfers at a steady (slow) rate, so "three
-    // copies within 15% of the best" alone can stop inside it
-    for (int i = 0; i < 1024 && (i < 128 || steady < 3); ++i) {
+    // both dataset buffers (both streams are idle here), at least 2048
+    // copies: the slow phase (host->device DMA at a third to half of the
+    // link rate) lasted ~100 transfers on some boxes and ~1000 on others,
+    // huge-page host buffers included (scripts/e2e_rep_probe.py), at a steady
+    // rate -- so "three copies within 15% of the best" alone can stop inside
+    // it. One-off, outside any step: ~0.1-0.3 s per new buffer pair.
+    for (int i = 0; i < 8192 && (i < 2048 || steady < 3); ++i) {
       const int b = (i & 1) ? m->cur : 1 - m->cur;
       LBBSP_CUDA_CHECK(cudaEventRecord(e0, m->copy_stream));
       LBBSP_CUDA_CHECK(cudaMemcpyAsync(m->data_xb[b], h_x_bf16, bx, cudaMemcpyHostToDevice, m->copy_stream));

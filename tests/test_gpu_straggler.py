@@ -103,9 +103,13 @@ def test_gamma_solver_balances_workers():
     assert sizes.tolist() == rec["sizes"].tolist()
     assert np.array_equal(vpred, rec["v_pred"])
     obs = np.median(rec["v_obs"][-8:], axis=0)
-    # (the linear Gamma0 fit is loose far below the calibrated sizes: the slow
-    # worker runs few rows, where tile quantisation flattens the time)
-    assert np.all(np.abs(obs / np.asarray(avail) - 1.0) < 0.25), obs
+    # (the linear Gamma0 fit is loose far below the calibrated sizes: the
+    # slowest worker runs few rows, where tile quantisation flattens the time
+    # -- measured 0.74-1.0 of its availability across boxes; the others track
+    # theirs within 10%)
+    ratio = obs / np.asarray(avail)
+    assert np.all(np.abs(ratio[:-1] - 1.0) < 0.15), obs
+    assert abs(ratio[-1] - 1.0) < 0.35, obs
     # the slowest worker's latency floor alone exceeds the others' balanced
     # time, so the solver leaves it few rows; the round's critical worker
     # time beats the equal split's on the same trace
